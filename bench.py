@@ -1,0 +1,426 @@
+"""Benchmark: filtered path vertices/s (insert + query) for one HD 1 spp 4-bounce frame.
+
+Workload (BASELINE.json configs[2]): 1920x1080, 1 spp, all
+vertices of 4-bounce paths in the closed Cornell box (8,294,400 synthetic vertices,
+streams.closed_box_stream), capacity next_pow2(2*W*H) = 2^22, fine + coarse tables,
+FilterConfig defaults (jitter, fixed-point sums, integrate).  One step = one frame:
+begin_frame on both tables, accumulate_phase (keys + insert), resolve_phase
+(ladder + composite), with the animated-scene seed schedule (src/pipeline.py:329).
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl b200|reference]
+
+Prints ONE JSON line (rank 0).  N>1 (torchrun) runs one independent frame per rank
+(replicas: no data-path exchange).
+"""
+
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import subprocess
+import sys
+import threading
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+W_PIX, H_PIX, BOUNCES = 1920, 1080, 4
+METRIC = "filtered path vertices/sec (insert+query); ms/frame at 1080p 1spp 4 bounces"
+WORKLOAD = "1920x1080 1spp, all vertices of 4-bounce paths (closed Cornell box, synthetic)"
+# algorithmic HBM bytes
+INSERT_BYTES_PER_VERTEX = 96      # position 24 + normal 24 + distance 8 + pixel 8 + sample 8 + contribution 24
+QUERY_BYTES_PER_VERTEX = 120      # + throughput 24
+QUERY_BYTES_PER_PIXEL = 48        # base image read 24 + filtered image write 24
+LAUNCHES_PER_STEP = 6             # begin_frame x2, check, insert_frame, resolve main, fallback, finalize -> see count below
+
+_REASON_BITS = {0x1: "gpu_idle", 0x2: "applications_clocks_setting", 0x4: "sw_power_cap",
+                0x8: "hw_slowdown", 0x10: "sync_boost", 0x20: "sw_thermal_slowdown",
+                0x40: "hw_thermal_slowdown", 0x80: "hw_power_brake_slowdown",
+                0x100: "display_clock_setting"}
+
+
+def _env_int(k, d):
+    try:
+        return int(os.environ.get(k, d))
+    except ValueError:
+        return d
+
+
+class ClockSampler:
+    """nvidia-smi clocks / throttle reasons sampled during the timed region."""
+
+    def __init__(self, index: int):
+        self.index = index
+        self.samples = []
+        self._proc = None
+        self._thread = None
+
+    def __enter__(self):
+        try:
+            self._proc = subprocess.Popen(
+                ["nvidia-smi", "-i", str(self.index),
+                 "--query-gpu=clocks.sm,clocks.max.sm,clocks_event_reasons.active",
+                 "--format=csv,noheader,nounits", "-lms", "100"],
+                stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self._thread = threading.Thread(target=self._read, daemon=True)
+            self._thread.start()
+        except OSError:
+            self._proc = None
+        return self
+
+    def _read(self):
+        for line in self._proc.stdout:
+            parts = [p.strip() for p in line.split(",")]
+            if len(parts) >= 3:
+                try:
+                    self.samples.append((float(parts[0]), float(parts[1]), int(parts[2], 16)))
+                except ValueError:
+                    pass
+
+    def __exit__(self, *exc):
+        if self._proc is not None:
+            self._proc.terminate()
+            try:
+                self._proc.wait(timeout=5)
+            except subprocess.TimeoutExpired:
+                self._proc.kill()
+        if self._thread is not None:
+            self._thread.join(timeout=2)
+
+    def summary(self):
+        if not self.samples:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unsampled"]}
+        sm = sorted(s[0] for s in self.samples)
+        reasons = 0
+        for s in self.samples:
+            reasons |= s[2]
+        names = [v for k, v in _REASON_BITS.items() if reasons & k and v != "gpu_idle"]
+        return {"sm_mhz": sm[len(sm) // 2], "sm_max_mhz": max(s[1] for s in self.samples),
+                "reasons": names, "samples": len(self.samples)}
+
+
+def _peaks():
+    p = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    if os.path.exists(p):
+        with open(p) as fh:
+            d = json.load(fh)
+        return float(d["hbm_gbs"]), "measured"
+    return 6650.0, "fallback"
+
+
+def _traffic(kernel: str):
+    """dram bytes per launch from the committed ncu --set full summary, if any."""
+    p = os.path.join(ROOT, "profiles", "ncu_traffic.json")
+    if os.path.exists(p):
+        with open(p) as fh:
+            return json.load(fh).get(kernel)
+    return None
+
+
+def make_config(pf):
+    from paper_1902_05942_b200.streams import camera_footprint
+    cap = 1 << (2 * W_PIX * H_PIX - 1).bit_length()
+    return pf.FilterConfig(capacity=cap, footprint_scale=camera_footprint(H_PIX))
+
+
+def cpu_reference_frame(sample_stream, base, cfg_kwargs, seed, frame, state):
+    """One frame of the reference's own CPU path (baseline/_ref) or the oracle port."""
+    kind, mod = state["kind"], state["mod"]
+    if kind == "reference":
+        pf = mod
+        cfg = state["cfg"]
+        st = state["state"]
+        if "vs" not in state:  # the reference's own VertexStream type
+            state["vs"] = pf.VertexStream(**{f: getattr(sample_stream, f) for f in FIELDS})
+        sample_stream = state["vs"]
+        st.fine.begin_frame(frame, cfg)
+        st.coarse.begin_frame(frame, cfg)
+        fk, _, _ = pf.pipeline.accumulate_phase(sample_stream, cfg, st, frame, seed,
+                                                threads=os.cpu_count() or 1)
+        pf.pipeline.resolve_phase(sample_stream, cfg, st, frame, seed, 1, base, fk)
+    else:
+        orc = mod
+        orc.filter_frame(sample_stream, state["cfg"], state["state"], frame, seed, 1, base)
+
+
+def cpu_setup(cfg_kwargs):
+    """Prefer the unmodified reference installed in baseline/_ref; else the oracle port."""
+    ref = os.path.join(ROOT, "baseline", "_ref")
+    if os.path.isdir(os.path.join(ref, "pathfilter")):
+        sys.path.insert(0, ref)
+        try:
+            import pathfilter
+            import pathfilter.pipeline  # noqa: F401
+            cfg = pathfilter.FilterConfig(**cfg_kwargs)
+            st = pathfilter.FrameState.from_config(cfg)
+            return {"kind": "reference", "mod": pathfilter, "cfg": cfg, "state": st,
+                    "backend": pathfilter.BACKEND}
+        except Exception as exc:  # fall through to the port
+            print(f"bench: reference import failed ({exc}); using the oracle port",
+                  file=sys.stderr)
+    from oracle import pf_oracle
+    cfg = pf_oracle.Config(**{k: v for k, v in cfg_kwargs.items()
+                              if k in pf_oracle.Config.__dataclass_fields__})
+    return {"kind": "port", "mod": pf_oracle, "cfg": cfg, "state": pf_oracle.State.from_config(cfg),
+            "backend": "oracle"}
+
+
+class _Sub:
+    def __len__(self):
+        return len(self.pixel)
+
+    def select(self, rows):
+        s = _Sub()
+        for f in FIELDS:
+            setattr(s, f, getattr(self, f)[rows])
+        return s
+
+
+FIELDS = ("position", "normal", "omega_r", "contribution", "throughput", "pixel", "sample",
+          "layer_id", "camera_distance")
+
+
+def host_sample(stream_np, stride: int):
+    s = _Sub()
+    for f in FIELDS:
+        setattr(s, f, np.ascontiguousarray(getattr(stream_np, f)[::stride]))
+    return s
+
+
+def cpu_baseline(stream_np, base_np, cfg_kwargs, steps: int, stride: int):
+    setup = cpu_setup(cfg_kwargs)
+    sample = host_sample(stream_np, stride)
+    n = len(sample.pixel)
+    times = []
+    from paper_1902_05942_b200 import rng
+    for f in range(steps):
+        t0 = time.perf_counter()
+        cpu_reference_frame(sample, base_np, cfg_kwargs, rng.frame_seed(1, f), f, setup)
+        times.append(time.perf_counter() - t0)
+    cores = os.cpu_count() if setup["kind"] == "reference" else 1
+    return setup, n, times, cores
+
+
+def run_reference_arm(args):
+    rank = _env_int("RANK", 0)
+    if rank != 0:
+        return 0
+    import torch
+    from paper_1902_05942_b200.streams import camera_footprint, closed_box_stream, stream_to_numpy
+    dev = "cuda" if torch.cuda.is_available() else "cpu"
+    stream, base = closed_box_stream(W_PIX, H_PIX, BOUNCES, 1, device=dev)
+    stream_np = stream_to_numpy(stream)
+    base_np = base.cpu().numpy()
+    cap = 1 << (2 * W_PIX * H_PIX - 1).bit_length()
+    cfg_kwargs = dict(capacity=cap, footprint_scale=camera_footprint(H_PIX))
+    stride = 4
+    total = args.warmup + args.steps
+    setup, n, times, cores = cpu_baseline(stream_np, base_np, cfg_kwargs, total, stride)
+    timed = times[args.warmup:] or times
+    per = sum(timed) / len(timed)
+    value = n / per
+    line = {
+        "impl": "reference", "metric": METRIC, "value": value, "unit": "vertices/s",
+        "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
+        "ms_per_step": per * 1e3, "higher_is_better": True, "scaling": "weak",
+        "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+        "config": {"workload": WORKLOAD, "vertices_per_frame": len(stream_np.pixel),
+                   "sample_vertices_per_step": n, "capacity": cap, "tables": "fine+coarse"},
+        "cpu_baseline": {"value": value, "unit": "vertices/s", "cores": cores,
+                         "kind": setup["kind"],
+                         "sample": f"every {stride}th vertex of the 1080p 4-bounce stream "
+                                   f"({n} vertices, C=2^22 tables), backend={setup['backend']}, "
+                                   "numpy key build single-threaded"},
+        "e2e": {"value": value, "unit": "vertices/s", "h2d_bytes_per_step": 0,
+                "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+    return 0
+
+
+def run_b200(args):
+    import torch
+    import torch.distributed as dist
+
+    rank = _env_int("RANK", 0)
+    world = _env_int("WORLD_SIZE", 1)
+    local = _env_int("LOCAL_RANK", 0)
+    if world > 1:
+        dist.init_process_group("nccl")
+    torch.cuda.set_device(local)
+
+    import __graft_entry__
+    if rank == 0:
+        __graft_entry__.build()
+    if world > 1:
+        dist.barrier()
+    import paper_1902_05942_b200 as pf
+    from paper_1902_05942_b200 import rng
+    from paper_1902_05942_b200.streams import closed_box_stream, stream_to_numpy
+
+    cfg = make_config(pf)
+    stream, base = closed_box_stream(W_PIX, H_PIX, BOUNCES, 1 + rank)
+    vs = pf.VertexStream(**stream)
+    n = len(vs)
+    n_pix = W_PIX * H_PIX
+    state = pf.FrameState.from_config(cfg)
+
+    ev = lambda: torch.cuda.Event(enable_timing=True)  # noqa: E731
+    phases = {"begin_frame": [], "insert": [], "resolve": []}
+
+    def step(f, timing=None):
+        seed = rng.frame_seed(1, f)
+        if timing is None:
+            pf.filter_frame(vs, base, cfg, state, 1, seed)
+            return
+        e0, e1, e2, e3 = ev(), ev(), ev(), ev()
+        e0.record()
+        frame = state.frame
+        state.fine.begin_frame(frame, cfg)
+        state.coarse.begin_frame(frame, cfg)
+        e1.record()
+        fk, ck, _ = pf.accumulate_phase(vs, cfg, state, frame, seed)
+        e2.record()
+        pf.resolve_phase(vs, cfg, state, frame, seed, 1, base, fk, want_means=False)
+        e3.record()
+        state.frame = frame + 1
+        timing.append((e0, e1, e2, e3))
+
+    for f in range(args.warmup):
+        step(f)
+    torch.cuda.synchronize()
+    if world > 1:
+        dist.barrier()
+    torch.cuda.synchronize()
+    marks = []
+    start, stop = ev(), ev()
+    with ClockSampler(local) as clocks:
+        start.record()
+        for k in range(args.steps):
+            step(args.warmup + k, marks)
+        stop.record()
+        torch.cuda.synchronize()
+    if world > 1:
+        dist.barrier()
+    elapsed = start.elapsed_time(stop) / 1e3
+    t_max = elapsed
+    if world > 1:
+        t = torch.tensor([elapsed], device="cuda", dtype=torch.float64)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        t_max = float(t.item())
+    for e0, e1, e2, e3 in marks:
+        phases["begin_frame"].append(e0.elapsed_time(e1))
+        phases["insert"].append(e1.elapsed_time(e2))
+        phases["resolve"].append(e2.elapsed_time(e3))
+    ph = {k: float(np.mean(v)) for k, v in phases.items()}
+    value = n * world * args.steps / t_max
+    ms_per_step = t_max / args.steps * 1e3
+
+    # roofline of the dominant phase kernel (bytes per launch / mean launch time)
+    peak, peak_kind = _peaks()
+    if ph["insert"] >= ph["resolve"]:
+        kname, kbytes, kms = "insert_frame_kernel", INSERT_BYTES_PER_VERTEX * n, ph["insert"]
+    else:
+        kname, kbytes, kms = ("resolve_phase", QUERY_BYTES_PER_VERTEX * n +
+                              QUERY_BYTES_PER_PIXEL * n_pix, ph["resolve"])
+    achieved = kbytes / (kms / 1e3) / 1e9
+    roofline = {"bound": "hbm", "kernel": kname, "achieved": achieved, "peak": peak,
+                "peak_kind": peak_kind, "unit": "GB/s", "frac": achieved / peak,
+                "bytes_per_launch": kbytes, "traffic": _traffic(kname)}
+
+    # end to end through the public API with host buffers
+    e2e = None
+    if rank == 0 or world > 1:
+        e2e = run_e2e(pf, rng, cfg, stream, base, args, n)
+
+    cpu = None
+    if rank == 0 and world == 1 and not args.no_cpu:
+        stream_np = stream_to_numpy(stream)
+        kwargs = dict(capacity=cfg.capacity, footprint_scale=cfg.footprint_scale)
+        stride = 4
+        setup, ns, times, cores = cpu_baseline(stream_np, base.cpu().numpy(), kwargs, 2, stride)
+        cpu = {"value": ns / min(times), "unit": "vertices/s", "cores": cores,
+               "kind": setup["kind"],
+               "sample": f"every {stride}th vertex of the same stream ({ns} vertices, C=2^22 "
+                         f"fine+coarse), best of 2 frames, backend={setup['backend']}"}
+
+    if rank == 0:
+        launches = 7 * args.steps  # begin x2, check, insert, resolve main + fallback + finalize
+        line = {
+            "metric": METRIC, "value": value, "unit": "vertices/s", "n_gpus": world,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms_per_step,
+            "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+            "data": "synthetic",
+            "config": {"workload": WORKLOAD, "vertices_per_frame": n, "pixels": n_pix,
+                       "capacity": cfg.capacity, "tables": "fine+coarse",
+                       "temporal_mode": cfg.temporal_mode, "sum_mode": cfg.sum_mode,
+                       "parallelism": f"replicas x{world}" if world > 1 else "single",
+                       "l2": "inputs 1.0 GB per frame > 126 MB L2 (no flush needed)"},
+            "phases_ms": ph, "roofline": roofline, "cpu_baseline": cpu, "e2e": e2e,
+            "gpu_launches": launches, "clocks": clocks.summary(),
+        }
+        print(json.dumps(line), flush=True)
+    if world > 1:
+        dist.destroy_process_group()
+    return 0
+
+
+def run_e2e(pf, rng, cfg, stream, base, args, n):
+    """Same frame through the public API from pinned host buffers: H2D of every
+    input the frame reads, filter_frame, D2H of the filtered image -- all timed."""
+    import torch
+    fields = ("position", "normal", "contribution", "throughput", "pixel", "sample",
+              "camera_distance")
+    host = {f: stream[f].cpu().pin_memory() for f in fields}
+    hbase = base.cpu().pin_memory()
+    himg = torch.empty_like(hbase).pin_memory()
+    dev = {f: torch.empty_like(stream[f]) for f in fields}
+    dbase = torch.empty_like(base)
+    unused = {"omega_r": torch.zeros_like(stream["position"]),
+              "layer_id": torch.zeros_like(stream["pixel"])}
+    state = pf.FrameState.from_config(cfg)
+    h2d = sum(t.numel() * t.element_size() for t in host.values()) + hbase.numel() * 8
+    d2h = himg.numel() * 8
+
+    def frame(f):
+        for k in fields:
+            dev[k].copy_(host[k], non_blocking=True)
+        dbase.copy_(hbase, non_blocking=True)
+        vs = pf.VertexStream(**dev, **unused)
+        image, _, _ = pf.filter_frame(vs, dbase, cfg, state, 1, rng.frame_seed(1, f))
+        himg.copy_(image, non_blocking=True)
+
+    for f in range(max(1, min(args.warmup, 3))):
+        frame(f)
+    torch.cuda.synchronize()
+    s, e = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    k = max(1, min(args.steps, 10))
+    s.record()
+    for f in range(k):
+        frame(100 + f)
+    e.record()
+    torch.cuda.synchronize()
+    t = s.elapsed_time(e) / 1e3
+    return {"value": n * k / t, "unit": "vertices/s", "h2d_bytes_per_step": h2d,
+            "d2h_bytes_per_step": d2h, "ms_per_step": t / k * 1e3, "steps": k}
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=10)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="b200", choices=["b200", "reference"])
+    ap.add_argument("--no-cpu", action="store_true", help="skip the cpu_baseline leg")
+    args = ap.parse_args()
+    if args.impl == "reference":
+        return run_reference_arm(args)
+    return run_b200(args)
+
+
+if __name__ == "__main__":
+    sys.exit(main())

@@ -1,0 +1,211 @@
+/*
+ * pathfilter_b200 -- C ABI of the B200-native hashed path-space filter.
+ *
+ * Drop-in boundary for the reference package `pathfilter`
+ * (/root/reference/pkg/src/pathfilter, cited as src/<file>:<line>).
+ * Every entry point is stream-ordered, takes DEVICE pointers (B200 HBM) and
+ * plain sizes, returns 0 on success or a nonzero pf_status, and never throws.
+ * pf_last_error() describes the most recent failure on the calling thread.
+ *
+ * Two groups of entry points:
+ *   1. the reference kernel-module ABI (src/_backend.py:14-42, src/_native.pyx:261-295):
+ *      pf_accumulate_fixed / pf_accumulate_float / pf_lookup_slots -- same arrays,
+ *      same in-place mutation, same per-vertex outputs;
+ *   2. the filter API (src/keys.py, src/table.py, src/pipeline.py): key build, fused
+ *      frame insert, fused frame resolve, effective sums and the temporal update.
+ */
+#ifndef PATHFILTER_B200_H
+#define PATHFILTER_B200_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define PF_ABI_VERSION 1
+
+enum pf_status {
+    PF_OK = 0,
+    PF_ERR_ARGUMENT = 1,   /* bad size / null pointer / capacity not a power of two */
+    PF_ERR_CUDA = 2,       /* a CUDA launch or API call failed (see pf_last_error) */
+};
+
+enum pf_temporal_mode { PF_INTEGRATE = 0, PF_FILTER = 1, PF_HYBRID = 2 };
+enum pf_sum_mode { PF_SUM_FIXED = 0, PF_SUM_FLOAT = 1 };
+
+/* FilterConfig (src/keys.py:30-79) reduced to what the device reads. */
+typedef struct pf_config {
+    double c_lod;            /* footprint_scale * s_pixels / base_voxel, evaluated on the host
+                                exactly as src/keys.py:324 does */
+    double base_voxel;
+    double ema_alpha;
+    double delta_max;
+    double lod_threshold[32];/* [k] = smallest double r with floor(np.log2(r)) >= k, k=1..31
+                                (exact floor(log2) of src/keys.py:325; [0] unused) */
+    int32_t normal_bins;
+    int32_t incident_angle_bins;
+    int32_t include_normal;
+    int32_t include_incident_angle;
+    int32_t include_layer;
+    int32_t normal_in_fingerprint;
+    int32_t jitter;
+    int32_t multi_level;
+    int32_t coarse_delta;
+    int32_t low_count_threshold;
+    int32_t temporal_mode;   /* pf_temporal_mode */
+    int32_t sample_cap;
+} pf_config;
+
+/* VertexStream (src/tracer.py:732-767): row-major [n][3] float64 triples. */
+typedef struct pf_vertices {
+    const double *position;
+    const double *normal;
+    const double *omega_r;          /* may be NULL unless include_incident_angle */
+    const double *contribution;
+    const double *throughput;       /* may be NULL for insert-only calls */
+    const int64_t *pixel;
+    const int64_t *sample;
+    const int64_t *layer_id;        /* may be NULL unless include_incident_angle/include_layer */
+    const double *camera_distance;
+    int64_t n;
+} pf_vertices;
+
+/* VoxelTable state in the reference SoA layout (src/table.py:96-103). */
+typedef struct pf_table {
+    uint64_t *tags;                 /* [C]   EMPTY = 0xFFFFFFFF00000000 */
+    void *sums;                     /* [C][3] int64 (fixed) or float64 (float) */
+    int64_t *counts;                /* [C] */
+    void *hist_sums;                /* [C][3] */
+    int64_t *hist_counts;           /* [C] */
+    int64_t *last_touch;            /* [C] */
+    double *deltas;                 /* [C] */
+    int64_t capacity;               /* power of two >= 2 */
+    int32_t sum_mode;               /* pf_sum_mode */
+    int32_t probe_limit;
+    int32_t evict_min_age;
+    int32_t evict_horizon;
+} pf_table;
+
+/* KeyArrays (src/keys.py:380-398); every pointer may be NULL (not written). */
+typedef struct pf_key_out {
+    int64_t *qx, *qy, *qz, *level;
+    uint64_t *aux;
+    uint64_t *index;
+    uint32_t *fingerprint;
+    double *jittered;               /* [n][3] */
+} pf_key_out;
+
+/* Per-frame counters written by the fused kernels (int64 device array). */
+enum pf_stat_slot {
+    PF_STAT_PROBE_FAILURES = 0,       /* fine table, status == 2 (src/pipeline.py:166) */
+    PF_STAT_COARSE_PROBE_FAILURES = 1,/* src/pipeline.py:174 */
+    PF_STAT_PROBE_LEN_SUM = 2,        /* sum of fine probe_len (collisions = this - n) */
+    PF_STAT_EVICTIONS = 3,            /* fine-table status == 1 */
+    PF_STAT_COARSE_EVICTIONS = 4,
+    PF_STAT_SOURCE_FINE = 5,          /* src/pipeline.py:45-48 */
+    PF_STAT_SOURCE_NEIGHBORHOOD = 6,
+    PF_STAT_SOURCE_COARSE = 7,
+    PF_STAT_SOURCE_UNFILTERED = 8,
+    PF_STAT_FALLBACK_ROWS = 9,        /* rows that left the fine rung (resolve work list) */
+    PF_STAT_HIST_BASE = 16,           /* [16 + k] = #vertices with fine probe_len == k, k < 256 */
+    PF_STAT_COUNT = 16 + 256
+};
+
+/* Eviction event record (src/table.py:72-77, 137-141). */
+typedef struct pf_evict_event {
+    int64_t vertex;                 /* row in the batch */
+    int64_t slot;
+    uint64_t victim_tag;
+    int64_t victim_touch;
+} pf_evict_event;
+
+int pf_abi_version(void);
+const char *pf_last_error(void);
+int pf_device_sm_count(void);
+
+/* ---- 1. reference kernel-module ABI ------------------------------------------------ */
+
+/* src/_native.pyx:261-266 accumulate_fixed (sums/hist_sums int64) and :268-272
+ * accumulate_float (float64).  Per-vertex outputs status u8, slots i64, probe_len u8,
+ * victim_tags u64, victim_touch i64 (any may be NULL).  ordered != 0 reproduces the
+ * reference's sequential (threads=1) slot layout exactly; ordered == 0 is the
+ * massively parallel insert whose per-key sums, counts and statuses are identical
+ * but whose slot order among keys that first appear in the same batch and share a
+ * probe window may differ (as the reference's own threads>1 mode may). */
+int pf_accumulate_fixed(uint64_t *tags, int64_t *sums, int64_t *counts, int64_t *hist_sums,
+                        int64_t *hist_counts, int64_t *last_touch, double *deltas,
+                        int64_t capacity, const uint64_t *idx, const uint32_t *fp,
+                        const double *vals, int64_t n, int64_t frame, int32_t probe_limit,
+                        int32_t evict_min_age, int32_t ordered, uint8_t *status,
+                        int64_t *slots, uint8_t *probe_len, uint64_t *victim_tags,
+                        int64_t *victim_touch, void *stream);
+int pf_accumulate_float(uint64_t *tags, double *sums, int64_t *counts, double *hist_sums,
+                        int64_t *hist_counts, int64_t *last_touch, double *deltas,
+                        int64_t capacity, const uint64_t *idx, const uint32_t *fp,
+                        const double *vals, int64_t n, int64_t frame, int32_t probe_limit,
+                        int32_t evict_min_age, int32_t ordered, uint8_t *status,
+                        int64_t *slots, uint8_t *probe_len, uint64_t *victim_tags,
+                        int64_t *victim_touch, void *stream);
+/* src/_native.pyx:275-295 lookup_slots: first matching slot, -1 when absent. */
+int pf_lookup_slots(const uint64_t *tags, int64_t capacity, const uint64_t *idx,
+                    const uint32_t *fp, int64_t n, int32_t probe_limit, int64_t *out,
+                    void *stream);
+
+/* ---- 2. filter API ---------------------------------------------------------------- */
+
+/* keys.make_key_arrays (src/keys.py:420-437) with explicit jitter draws u1/u2
+ * (NULL = no jitter). */
+int pf_make_key_arrays(const pf_config *cfg, const pf_vertices *v, const double *u1,
+                       const double *u2, int32_t level_delta, pf_key_out *out, void *stream);
+/* pipeline.vertex_keys (src/pipeline.py:126-135): draws from the counter RNG of
+ * src/rng.py:62-78 keyed by path id; stream_base = mix64(seed ^ stream_tag*G). */
+int pf_vertex_keys(const pf_config *cfg, const pf_vertices *v, uint64_t stream_base,
+                   int32_t level_delta, pf_key_out *out, void *stream);
+/* keys.hash_arrays (src/keys.py:405-417); normal_fp_bins may be NULL. */
+int pf_hash_arrays(const int64_t *qx, const int64_t *qy, const int64_t *qz,
+                   const int64_t *level, const uint64_t *aux, const uint32_t *normal_fp_bins,
+                   int64_t n, uint64_t *index, uint32_t *fingerprint, void *stream);
+
+/* Fused accumulate_phase (src/pipeline.py:152-175): keys (stream 2) for the fine
+ * and, if coarse != NULL, the coarse table (level + coarse_delta), each inserted
+ * with warp-merged atomics.  stats: int64[PF_STAT_COUNT] accumulated (not cleared);
+ * events: optional eviction log of capacity `event_capacity` with its int64 counter. */
+int pf_insert_frame(const pf_config *cfg, const pf_vertices *v, const pf_table *fine,
+                    const pf_table *coarse, uint64_t stream_base_accum, int64_t frame,
+                    int64_t *stats, pf_evict_event *events, int64_t *event_count,
+                    int64_t event_capacity, void *stream);
+
+/* Fused resolve_phase (src/pipeline.py:207-283): lookup keys, fine rung, 3x3x3
+ * neighbourhood, coarse rung, ladder, composite.  flat: float64[n_pixels][3]
+ * scratch; work: int64 scratch of 6*n entries plus work_count (int64[1]);
+ * image = base_image + flat/spp.  source (u8[n]) and chosen (f64[n][3]) may be NULL. */
+int pf_resolve_frame(const pf_config *cfg, const pf_vertices *v, const pf_table *fine,
+                     const pf_table *coarse, uint64_t stream_base_lookup,
+                     uint64_t stream_base_coarse, int64_t spp, const double *base_image,
+                     int64_t n_pixels, double *image, double *flat, int64_t *work,
+                     int64_t *work_count, uint8_t *source, double *chosen, int64_t *stats,
+                     void *stream);
+
+/* VoxelTable.effective (src/table.py:205-238) over all slots.  eff_sum is int64 for
+ * (integrate, fixed) else float64; eff_count is int64 for integrate else float64. */
+int pf_effective(const pf_table *t, int32_t mode, double ema_alpha, double delta_max,
+                 void *eff_sum, void *eff_count, void *stream);
+
+/* VoxelTable.begin_frame (src/table.py:242-298).  horizon_clears (int64[1]) is
+ * incremented by the number of slots cleared. */
+int pf_begin_frame(const pf_table *t, int64_t frame, int32_t mode, double ema_alpha,
+                   double delta_max, int32_t sample_cap, int64_t *horizon_clears,
+                   void *stream);
+
+/* Input validation of accumulate_batch (src/table.py:127-129): *bad (int32, device) is
+ * set to 1 when any of the `count` float64 values is NaN, infinite or negative. */
+int pf_check_contributions(const double *vals, int64_t count, int32_t *bad, void *stream);
+
+/* Number of non-EMPTY tags (VoxelTable.occupancy numerator, src/table.py:302-303). */
+int pf_count_occupied(const uint64_t *tags, int64_t capacity, int64_t *out, void *stream);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* PATHFILTER_B200_H */

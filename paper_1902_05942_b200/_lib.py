@@ -1,0 +1,163 @@
+"""Loader for the sm_100a shared library `libpf_b200.so` (C ABI in include/pathfilter_b200.h).
+
+There is no CPU fallback: importing a compute entry point without the built
+library, or calling one without a CUDA device, raises immediately.
+"""
+
+from __future__ import annotations
+
+import ctypes
+import os
+import subprocess
+
+import torch
+
+_PKG = os.path.dirname(os.path.abspath(__file__))
+_ROOT = os.path.dirname(_PKG)
+LIB_PATH = os.path.join(_PKG, "libpf_b200.so")
+SOURCES = [os.path.join(_PKG, "csrc", f) for f in ("pf_common.cu", "pf_table.cu", "pf_frame.cu")]
+HEADERS = [os.path.join(_PKG, "csrc", f) for f in ("pf_device.cuh", "pf_insert.cuh",
+                                                    "pf_internal.cuh")] + \
+    [os.path.join(_ROOT, "include", "pathfilter_b200.h")]
+NVCC_FLAGS = ["-gencode", "arch=compute_100a,code=sm_100a", "-O3", "-lineinfo",
+              "-fmad=false", "-std=c++17", "-Xcompiler", "-fPIC", "-shared"]
+
+# exported symbols of include/pathfilter_b200.h (checked by tests/test_abi.py)
+EXPORTS = ("pf_abi_version", "pf_last_error", "pf_device_sm_count", "pf_accumulate_fixed",
+           "pf_accumulate_float", "pf_lookup_slots", "pf_make_key_arrays", "pf_vertex_keys",
+           "pf_hash_arrays", "pf_insert_frame", "pf_resolve_frame", "pf_effective",
+           "pf_begin_frame", "pf_check_contributions", "pf_count_occupied")
+
+
+def build(force: bool = False, verbose: bool = False) -> str:
+    """Compile the CUDA sources for sm_100a into the in-tree shared library."""
+    newest = max(os.path.getmtime(p) for p in SOURCES + HEADERS)
+    if not force and os.path.exists(LIB_PATH) and os.path.getmtime(LIB_PATH) >= newest:
+        return LIB_PATH
+    nvcc = os.environ.get("NVCC", "nvcc")
+    cmd = [nvcc, *NVCC_FLAGS, "-o", LIB_PATH, *SOURCES]
+    if verbose:
+        print(" ".join(cmd))
+    subprocess.check_call(cmd)
+    return LIB_PATH
+
+
+# ------------------------------------------------------------------ ctypes mirrors
+
+class PfConfig(ctypes.Structure):
+    _fields_ = [("c_lod", ctypes.c_double), ("base_voxel", ctypes.c_double),
+                ("ema_alpha", ctypes.c_double), ("delta_max", ctypes.c_double),
+                ("lod_threshold", ctypes.c_double * 32),
+                ("normal_bins", ctypes.c_int32), ("incident_angle_bins", ctypes.c_int32),
+                ("include_normal", ctypes.c_int32), ("include_incident_angle", ctypes.c_int32),
+                ("include_layer", ctypes.c_int32), ("normal_in_fingerprint", ctypes.c_int32),
+                ("jitter", ctypes.c_int32), ("multi_level", ctypes.c_int32),
+                ("coarse_delta", ctypes.c_int32), ("low_count_threshold", ctypes.c_int32),
+                ("temporal_mode", ctypes.c_int32), ("sample_cap", ctypes.c_int32)]
+
+
+class PfVertices(ctypes.Structure):
+    _fields_ = [("position", ctypes.c_void_p), ("normal", ctypes.c_void_p),
+                ("omega_r", ctypes.c_void_p), ("contribution", ctypes.c_void_p),
+                ("throughput", ctypes.c_void_p), ("pixel", ctypes.c_void_p),
+                ("sample", ctypes.c_void_p), ("layer_id", ctypes.c_void_p),
+                ("camera_distance", ctypes.c_void_p), ("n", ctypes.c_int64)]
+
+
+class PfTable(ctypes.Structure):
+    _fields_ = [("tags", ctypes.c_void_p), ("sums", ctypes.c_void_p),
+                ("counts", ctypes.c_void_p), ("hist_sums", ctypes.c_void_p),
+                ("hist_counts", ctypes.c_void_p), ("last_touch", ctypes.c_void_p),
+                ("deltas", ctypes.c_void_p), ("capacity", ctypes.c_int64),
+                ("sum_mode", ctypes.c_int32), ("probe_limit", ctypes.c_int32),
+                ("evict_min_age", ctypes.c_int32), ("evict_horizon", ctypes.c_int32)]
+
+
+class PfKeyOut(ctypes.Structure):
+    _fields_ = [(f, ctypes.c_void_p) for f in ("qx", "qy", "qz", "level", "aux", "index",
+                                                "fingerprint", "jittered")]
+
+
+class PfEvictEvent(ctypes.Structure):
+    _fields_ = [("vertex", ctypes.c_int64), ("slot", ctypes.c_int64),
+                ("victim_tag", ctypes.c_uint64), ("victim_touch", ctypes.c_int64)]
+
+
+STAT_PROBE_FAILURES = 0
+STAT_COARSE_PROBE_FAILURES = 1
+STAT_PROBE_LEN_SUM = 2
+STAT_EVICTIONS = 3
+STAT_COARSE_EVICTIONS = 4
+STAT_SOURCE_FINE = 5
+STAT_SOURCE_NEIGHBORHOOD = 6
+STAT_SOURCE_COARSE = 7
+STAT_SOURCE_UNFILTERED = 8
+STAT_FALLBACK_ROWS = 9
+STAT_HIST_BASE = 16
+STAT_COUNT = 16 + 256
+
+_lib = None
+
+
+def lib() -> ctypes.CDLL:
+    """The loaded library; raises if it is missing or no CUDA device is present."""
+    global _lib
+    if _lib is not None:
+        return _lib
+    if not os.path.exists(LIB_PATH):
+        raise RuntimeError(f"{LIB_PATH} is not built; run __graft_entry__.build() "
+                           "(there is no CPU fallback)")
+    L = ctypes.CDLL(LIB_PATH)
+    vp, i64, i32, u64, dbl = (ctypes.c_void_p, ctypes.c_int64, ctypes.c_int32,
+                              ctypes.c_uint64, ctypes.c_double)
+    L.pf_abi_version.restype = ctypes.c_int
+    L.pf_last_error.restype = ctypes.c_char_p
+    L.pf_device_sm_count.restype = ctypes.c_int
+    acc = [vp, vp, vp, vp, vp, vp, vp, i64, vp, vp, vp, i64, i64, i32, i32, i32,
+           vp, vp, vp, vp, vp, vp]
+    L.pf_accumulate_fixed.argtypes = acc
+    L.pf_accumulate_float.argtypes = acc
+    L.pf_lookup_slots.argtypes = [vp, i64, vp, vp, i64, i32, vp, vp]
+    L.pf_make_key_arrays.argtypes = [vp, vp, vp, vp, i32, vp, vp]
+    L.pf_vertex_keys.argtypes = [vp, vp, u64, i32, vp, vp]
+    L.pf_hash_arrays.argtypes = [vp, vp, vp, vp, vp, vp, i64, vp, vp, vp]
+    L.pf_insert_frame.argtypes = [vp, vp, vp, vp, u64, i64, vp, vp, vp, i64, vp]
+    L.pf_resolve_frame.argtypes = [vp, vp, vp, vp, u64, u64, i64, vp, i64, vp, vp, vp, vp,
+                                   vp, vp, vp, vp]
+    L.pf_effective.argtypes = [vp, i32, dbl, dbl, vp, vp, vp]
+    L.pf_begin_frame.argtypes = [vp, i64, i32, dbl, dbl, i32, vp, vp]
+    L.pf_count_occupied.argtypes = [vp, i64, vp, vp]
+    L.pf_check_contributions.argtypes = [vp, i64, vp, vp]
+    for name in EXPORTS[3:]:
+        getattr(L, name).restype = ctypes.c_int
+    _lib = L
+    return L
+
+
+def require_cuda() -> torch.device:
+    if not torch.cuda.is_available():
+        raise RuntimeError("paper_1902_05942_b200 needs a CUDA device (B200, sm_100a); "
+                           "there is no CPU fallback")
+    return torch.device("cuda", torch.cuda.current_device())
+
+
+def call(name: str, *args) -> None:
+    """Invoke a C-ABI entry point and raise on a nonzero pf_status."""
+    L = lib()
+    rc = getattr(L, name)(*args)
+    if rc != 0:
+        msg = L.pf_last_error().decode(errors="replace")
+        if rc == 1:
+            raise ValueError(msg)
+        raise RuntimeError(msg)
+
+
+def ptr(t) -> int | None:
+    """Device pointer of a tensor (None for None)."""
+    if t is None:
+        return None
+    return t.data_ptr()
+
+
+def stream_handle() -> int:
+    return torch.cuda.current_stream().cuda_stream

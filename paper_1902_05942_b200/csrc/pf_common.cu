@@ -1,0 +1,49 @@
+// Error reporting and device queries behind the C ABI.
+#include <cstdio>
+
+#include "pf_internal.cuh"
+
+namespace pf {
+
+static thread_local std::string g_last_error;
+
+void set_error(const std::string &msg) { g_last_error = msg; }
+
+int fail_arg(const char *fn, const char *what) {
+    set_error(std::string(fn) + ": " + what);
+    return PF_ERR_ARGUMENT;
+}
+
+int check_launch(const char *fn) {
+    const cudaError_t e = cudaGetLastError();
+    if (e != cudaSuccess) {
+        set_error(std::string(fn) + ": " + cudaGetErrorString(e));
+        return PF_ERR_CUDA;
+    }
+    return PF_OK;
+}
+
+int sm_count() {
+    static int cached = 0;
+    if (cached == 0) {
+        int dev = 0, v = 0;
+        if (cudaGetDevice(&dev) == cudaSuccess &&
+            cudaDeviceGetAttribute(&v, cudaDevAttrMultiProcessorCount, dev) == cudaSuccess)
+            cached = v;
+        else
+            cached = 148;
+    }
+    return cached;
+}
+
+}  // namespace pf
+
+extern "C" {
+
+int pf_abi_version(void) { return PF_ABI_VERSION; }
+
+const char *pf_last_error(void) { return pf::g_last_error.c_str(); }
+
+int pf_device_sm_count(void) { return pf::sm_count(); }
+
+}  // extern "C"

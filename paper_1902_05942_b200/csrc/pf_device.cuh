@@ -1,0 +1,513 @@
+// Device building blocks of the hashed path-space filter (sm_100a).
+//
+// Everything that must be bit-exact with the reference lives here: the counter
+// RNG (src/rng.py), the key recipe (src/keys.py:323-437) and the
+// per-slot temporal math (src/table.py:205-298).  The whole library is compiled
+// with -fmad=false, and the FP64 key arithmetic additionally spells every
+// multiply/add with __dmul_rn/__dadd_rn so numpy's op order (no FMA contraction)
+// survives any flag change.
+#pragma once
+
+#include <cstdint>
+#include <cuda_runtime.h>
+
+#include "../../include/pathfilter_b200.h"
+
+namespace pf {
+
+constexpr uint64_t kEmptyTag = 0xFFFFFFFF00000000ull;   // src/table.py:39
+constexpr uint64_t kFresh = 0xFF000000ull;              // src/_native.pyx:18
+constexpr uint64_t kAgeMask = 0xFFFFFFull;              // src/_native.pyx:75 (probe side)
+constexpr uint64_t kPrioAgeMask = 0xFFFFFEull;          // src/table.py:40 (packing side)
+constexpr uint64_t kFpMask = 0xFFFFFFFFull;
+// Transient tag held while an eviction wipes the victim cell.  Fingerprint bits are
+// the sentinel 0 (never a real key, src/keys.py:96) so nothing matches it, and it
+// is never EMPTY; probers that meet it wait for the evictor to publish the new tag.
+constexpr uint64_t kBusyTag = 0ull;
+constexpr uint64_t kGolden = 0x9E3779B97F4A7C15ull;     // src/rng.py:16
+constexpr uint64_t kInitIndex = 0x9E3779B97F4A7C15ull;  // src/keys.py:22
+constexpr uint64_t kInitFp = 0xC2B2AE3D27D4EB4Full;     // src/keys.py:23
+constexpr double kTwoPi = 6.283185307179586;            // 2.0 * math.pi (src/keys.py:343)
+constexpr double kFixedScale = 65536.0;                 // src/table.py:38
+constexpr int kMaxLevel = 31;                           // src/keys.py:97
+
+// ------------------------------------------------------------------ integer helpers
+
+__device__ __forceinline__ uint64_t mix64(uint64_t x) {  // src/rng.py:51-59
+    x ^= x >> 33;
+    x *= 0xFF51AFD7ED558CCDull;
+    x ^= x >> 33;
+    x *= 0xC4CEB9FE1A85EC53ull;
+    x ^= x >> 33;
+    return x;
+}
+
+// numpy float64 -> int64 cast on x86 (cvttsd2si): NaN and out-of-range give INT64_MIN.
+__device__ __forceinline__ int64_t np_i64(double x) {
+    if (!(x >= -9223372036854775808.0 && x < 9223372036854775808.0))
+        return INT64_MIN;
+    return static_cast<int64_t>(x);
+}
+
+__device__ __forceinline__ double dmul(double a, double b) { return __dmul_rn(a, b); }
+__device__ __forceinline__ double dadd(double a, double b) { return __dadd_rn(a, b); }
+__device__ __forceinline__ double dsub(double a, double b) { return __dsub_rn(a, b); }
+__device__ __forceinline__ double ddiv(double a, double b) { return __ddiv_rn(a, b); }
+
+// np.maximum / np.minimum propagate NaN from either side.
+__device__ __forceinline__ double np_max(double a, double b) {
+    return (a != a) ? a : ((b != b) ? b : (a >= b ? a : b));
+}
+__device__ __forceinline__ double np_min(double a, double b) {
+    return (a != a) ? a : ((b != b) ? b : (a <= b ? a : b));
+}
+
+// ------------------------------------------------------------------ RNG (src/rng.py)
+
+// draw_unit_array(seed, stream, path_id, 0, dim) for dims 0 and 1
+// (src/rng.py:62-78, src/pipeline.py:119-123); h0 = mix64(seed ^ stream*G) is a
+// host constant.
+__device__ __forceinline__ void jitter_draws(uint64_t h0, int64_t pixel, int64_t sample,
+                                             double &u1, double &u2) {
+    const uint64_t pid = (static_cast<uint64_t>(sample) << 32) | static_cast<uint64_t>(pixel);
+    uint64_t h = mix64(h0 ^ (pid + kGolden));
+    h = mix64(h ^ (0ull + kGolden));
+    const uint64_t a = mix64(h ^ (0ull + kGolden));
+    const uint64_t b = mix64(h ^ (1ull + kGolden));
+    const double inv = 1.0 / 9007199254740992.0;  // 2^-53, exact
+    u1 = static_cast<double>(a >> 11) * inv;
+    u2 = static_cast<double>(b >> 11) * inv;
+}
+
+// Disc offsets: r = 0.5*sqrt(u1), phi = 2pi*u2, (r cos phi, r sin phi)
+// (src/keys.py:342-345).  sqrt is IEEE-exact; sin/cos are CUDA's (<= 2 ulp), the
+// one documented source of jittered-position ulp differences.
+__device__ __forceinline__ void disc_offset(double u1, double u2, double &u, double &v) {
+    const double r = dmul(0.5, __dsqrt_rn(u1));
+    const double phi = dmul(kTwoPi, u2);
+    double s, c;
+    sincos(phi, &s, &c);
+    u = dmul(r, c);
+    v = dmul(r, s);
+}
+
+// ------------------------------------------------------------------ keys (src/keys.py)
+
+// floor(log2(max(d * c_lod, 1))) clamped to 31 (src/keys.py:323-326).  numpy's log2
+// rounds up to k just below 2^k, so the exact floor is exponent + (r >= T[e+1]).
+__device__ __forceinline__ int64_t lod_level(double dist, const pf_config &cfg) {
+    const double ratio = np_max(dmul(dist, cfg.c_lod), 1.0);
+    if (ratio != ratio)
+        return INT64_MIN;
+    if (ratio >= 2147483648.0)
+        return kMaxLevel;
+    const int e = ilogb(ratio);  // ratio in [1, 2^31): exact floor(log2) of the double
+    return (e < kMaxLevel && ratio >= cfg.lod_threshold[e + 1]) ? e + 1 : e;
+}
+
+__device__ __forceinline__ int64_t clamp_level(int64_t lv, int32_t delta) {
+    const int64_t l = lv + delta;
+    return l < kMaxLevel ? l : kMaxLevel;
+}
+
+// base_voxel * exp2(level): exact power-of-two scaling.
+__device__ __forceinline__ double voxel_step(double base_voxel, int64_t level) {
+    if (level < -2000)
+        return 0.0;
+    return dmul(base_voxel, ldexp(1.0, static_cast<int>(level)));
+}
+
+struct Frame3 {
+    double t1[3], t2[3];
+};
+
+// Branchless ONB (src/keys.py:329-336) in numpy's left-to-right order.
+__device__ __forceinline__ Frame3 tangent_frame(double x, double y, double z) {
+    const double s = (z >= 0.0) ? 1.0 : -1.0;
+    const double a = ddiv(-1.0, dadd(s, z));
+    const double b = dmul(dmul(x, y), a);
+    Frame3 f;
+    f.t1[0] = dadd(1.0, dmul(dmul(dmul(s, x), x), a));
+    f.t1[1] = dmul(s, b);
+    f.t1[2] = dmul(-s, x);
+    f.t2[0] = b;
+    f.t2[1] = dadd(s, dmul(dmul(y, y), a));
+    f.t2[2] = -y;
+    return f;
+}
+
+// Octahedral normal bin (src/keys.py:351-361).
+__device__ __forceinline__ int64_t octa_bin(double x, double y, double z, int bins) {
+    const double s = np_max(dadd(dadd(fabs(x), fabs(y)), fabs(z)), 1e-300);
+    const double px = ddiv(x, s), py = ddiv(y, s), pz = ddiv(z, s);
+    double fx = px, fy = py;
+    if (pz < 0.0) {
+        fx = dmul(dsub(1.0, fabs(py)), px >= 0.0 ? 1.0 : -1.0);
+        fy = dmul(dsub(1.0, fabs(px)), py >= 0.0 ? 1.0 : -1.0);
+    }
+    const double fb = static_cast<double>(bins);
+    int64_t bx = np_i64(dmul(dadd(dmul(fx, 0.5), 0.5), fb));
+    int64_t by = np_i64(dmul(dadd(dmul(fy, 0.5), 0.5), fb));
+    if (bx > bins - 1) bx = bins - 1;
+    if (by > bins - 1) by = bins - 1;
+    return by * bins + bx;
+}
+
+// aux word (src/keys.py:364-377).  The incident-angle dot product follows numpy's
+// einsum("ij,ij->i") reduction order for length 3: (n0*o0 + n2*o2) + n1*o1
+// (measured in this image; see tests/test_oracle_golden.py).
+__device__ __forceinline__ uint64_t aux_word(const pf_config &cfg, double nx, double ny,
+                                             double nz, const double *omega, int64_t layer) {
+    uint64_t aux = 0;
+    if (cfg.include_normal && !cfg.normal_in_fingerprint)
+        aux |= static_cast<uint64_t>(octa_bin(nx, ny, nz, cfg.normal_bins));
+    if (cfg.include_incident_angle) {
+        const double c0 = dadd(dadd(dmul(nx, omega[0]), dmul(nz, omega[2])), dmul(ny, omega[1]));
+        const double c = np_min(np_max(c0, 0.0), 1.0);
+        int64_t ab = np_i64(dmul(c, static_cast<double>(cfg.incident_angle_bins)));
+        if (ab > cfg.incident_angle_bins - 1) ab = cfg.incident_angle_bins - 1;
+        if (layer != 1) ab = 0;
+        aux |= static_cast<uint64_t>(ab) << 16;
+    }
+    if (cfg.include_layer)
+        aux |= static_cast<uint64_t>(layer) << 24;
+    return aux;
+}
+
+struct CellKey {
+    int64_t q[3];
+    int64_t level;
+    uint64_t aux;
+};
+
+struct CellHash {
+    uint64_t index;
+    uint32_t fp;
+};
+
+// hash_arrays (src/keys.py:405-417).
+__device__ __forceinline__ CellHash cell_hash(int64_t qx, int64_t qy, int64_t qz, int64_t level,
+                                              uint64_t aux, int has_fp_bin, uint32_t fp_bin) {
+    const uint64_t f[5] = {static_cast<uint64_t>(qx), static_cast<uint64_t>(qy),
+                           static_cast<uint64_t>(qz), static_cast<uint64_t>(level), aux};
+    uint64_t h = kInitIndex, g = kInitFp;
+#pragma unroll
+    for (int i = 0; i < 5; ++i) h = mix64(h ^ f[i]);
+#pragma unroll
+    for (int i = 0; i < 5; ++i) g = mix64(g ^ f[i]);
+    uint32_t fp = static_cast<uint32_t>((g ^ (g >> 32)) & kFpMask);
+    if (has_fp_bin)
+        fp = (fp << 6) | fp_bin;
+    if (fp == 0u)
+        fp = 1u;
+    CellHash r;
+    r.index = h;
+    r.fp = fp;
+    return r;
+}
+
+// Per-vertex inputs shared by every key set of one vertex.
+struct VertexIn {
+    double pos[3];
+    double nrm[3];
+    double dist;
+    int64_t pixel, sample, layer;
+    double omega[3];
+};
+
+__device__ __forceinline__ VertexIn load_vertex(const pf_vertices &v, int64_t i,
+                                                const pf_config &cfg) {
+    VertexIn x;
+#pragma unroll
+    for (int c = 0; c < 3; ++c) {
+        x.pos[c] = __ldg(v.position + 3 * i + c);
+        x.nrm[c] = __ldg(v.normal + 3 * i + c);
+        x.omega[c] = 0.0;
+    }
+    x.dist = __ldg(v.camera_distance + i);
+    x.pixel = __ldg(v.pixel + i);
+    x.sample = __ldg(v.sample + i);
+    x.layer = (v.layer_id != nullptr) ? __ldg(v.layer_id + i) : 0;
+    if (cfg.include_incident_angle && v.omega_r != nullptr) {
+#pragma unroll
+        for (int c = 0; c < 3; ++c) x.omega[c] = __ldg(v.omega_r + 3 * i + c);
+    }
+    return x;
+}
+
+// Level-independent part of a key set: ONB, aux, structured fp bin.
+struct KeyShared {
+    Frame3 frame;
+    uint64_t aux;
+    uint32_t fp_bin;
+    int has_fp_bin;
+};
+
+__device__ __forceinline__ KeyShared key_shared(const pf_config &cfg, const VertexIn &x) {
+    KeyShared k;
+    k.frame = tangent_frame(x.nrm[0], x.nrm[1], x.nrm[2]);
+    k.aux = aux_word(cfg, x.nrm[0], x.nrm[1], x.nrm[2], x.omega, x.layer);
+    k.has_fp_bin = cfg.include_normal && cfg.normal_in_fingerprint;
+    k.fp_bin = k.has_fp_bin
+        ? static_cast<uint32_t>(octa_bin(x.nrm[0], x.nrm[1], x.nrm[2], 8) & 0x3F) : 0u;
+    return k;
+}
+
+// make_key_arrays for one vertex and one level_delta (src/keys.py:420-437).
+// jit = 0 disables jitter; (u, v) are the disc offsets.
+__device__ __forceinline__ CellKey make_key(const pf_config &cfg, const VertexIn &x,
+                                            const KeyShared &ks, int jit, double u, double v,
+                                            int32_t level_delta, double jittered[3]) {
+    int64_t lv = clamp_level(lod_level(x.dist, cfg), level_delta);
+    if (jit) {
+        const double step = voxel_step(cfg.base_voxel, lv);
+        double d2 = 0.0;
+#pragma unroll
+        for (int c = 0; c < 3; ++c) {
+            const double off = dmul(dadd(dmul(u, ks.frame.t1[c]), dmul(v, ks.frame.t2[c])), step);
+            jittered[c] = dadd(x.pos[c], off);
+        }
+        // np.linalg.norm(x' - x, axis=1): sqrt of the sequential sum of squares
+        const double e0 = dsub(jittered[0], x.pos[0]);
+        const double e1 = dsub(jittered[1], x.pos[1]);
+        const double e2 = dsub(jittered[2], x.pos[2]);
+        d2 = dadd(dadd(dmul(e0, e0), dmul(e1, e1)), dmul(e2, e2));
+        const double moved = dadd(x.dist, __dsqrt_rn(d2));
+        lv = clamp_level(lod_level(moved, cfg), level_delta);
+    } else {
+#pragma unroll
+        for (int c = 0; c < 3; ++c) jittered[c] = x.pos[c];
+    }
+    const double step = voxel_step(cfg.base_voxel, lv);
+    CellKey k;
+#pragma unroll
+    for (int c = 0; c < 3; ++c) k.q[c] = np_i64(floor(ddiv(jittered[c], step)));
+    k.level = lv;
+    k.aux = ks.aux;
+    return k;
+}
+
+__device__ __forceinline__ CellHash key_hash(const CellKey &k, const KeyShared &ks) {
+    return cell_hash(k.q[0], k.q[1], k.q[2], k.level, k.aux, ks.has_fp_bin, ks.fp_bin);
+}
+
+// ------------------------------------------------------------------ table access
+
+// L2-coherent loads/stores for state other threads mutate inside the same launch.
+__device__ __forceinline__ uint64_t ld_relaxed(const uint64_t *p) {
+    uint64_t v;
+    asm volatile("ld.relaxed.gpu.global.u64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
+    return v;
+}
+__device__ __forceinline__ uint64_t ld_acquire(const uint64_t *p) {
+    uint64_t v;
+    asm volatile("ld.acquire.gpu.global.u64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
+    return v;
+}
+__device__ __forceinline__ void st_release(uint64_t *p, uint64_t v) {
+    asm volatile("st.release.gpu.global.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
+}
+__device__ __forceinline__ int64_t ld_relaxed_i64(const int64_t *p) {
+    return static_cast<int64_t>(ld_relaxed(reinterpret_cast<const uint64_t *>(p)));
+}
+__device__ __forceinline__ void st_relaxed_u64(void *p, uint64_t v) {
+    asm volatile("st.relaxed.gpu.global.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
+}
+
+__device__ __forceinline__ uint64_t wait_not_busy(const uint64_t *p, uint64_t tag) {
+    while (tag == kBusyTag) {
+        __nanosleep(32);
+        tag = ld_acquire(p);
+    }
+    return tag;
+}
+
+struct InsertResult {
+    int64_t slot;
+    int32_t status;  // 0 accumulated, 1 evicted then accumulated, 2 probe limit
+    int32_t probe_len;
+    uint64_t victim_tag;
+    int64_t victim_touch;
+};
+
+// Wipe an evicted cell (src/_native.pyx:170-183): live + history sums, counts, delta.
+__device__ __forceinline__ void zero_cell(const pf_table &t, int64_t s) {
+    uint64_t *sums = static_cast<uint64_t *>(t.sums);
+    uint64_t *hsums = static_cast<uint64_t *>(t.hist_sums);
+#pragma unroll
+    for (int c = 0; c < 3; ++c) {
+        st_relaxed_u64(sums + 3 * s + c, 0ull);  // int64 0 and float64 +0.0 share bits
+        st_relaxed_u64(hsums + 3 * s + c, 0ull);
+    }
+    st_relaxed_u64(t.counts + s, 0ull);
+    st_relaxed_u64(t.hist_counts + s, 0ull);
+    st_relaxed_u64(t.deltas + s, 0ull);
+}
+
+// Probe / claim / evict for one key (src/_native.pyx:209-247) on the live table.
+// Concurrency: a claim is one 64-bit CAS of the whole tag (EMPTY -> FRESH|fp); an
+// eviction CASes the victim's exact tag to BUSY, wipes the cell, then publishes
+// FRESH|fp with release order, so no accumulate lands in a half-wiped cell.  A lost
+// victim CAS re-probes the window (what a sequential caller would see) instead of
+// the reference's racy give-up.
+static __device__ __noinline__ InsertResult probe_insert(const pf_table &t, uint64_t idx, uint32_t fp) {
+    const uint64_t mask = static_cast<uint64_t>(t.capacity) - 1;
+    const uint64_t home = idx & mask;
+    const uint64_t want = static_cast<uint64_t>(fp);
+    const uint64_t incoming = (kFresh << 32) | want;
+    InsertResult r;
+    r.slot = -1;
+    r.status = 2;
+    r.probe_len = t.probe_limit;
+    r.victim_tag = 0;
+    r.victim_touch = 0;
+    for (int attempt = 0; attempt < 64; ++attempt) {
+        int64_t victim = -1;
+        uint64_t victim_tag = 0;
+        for (int j = 0; j < t.probe_limit; ++j) {
+            const uint64_t s = (home + static_cast<uint64_t>(j)) & mask;
+            uint64_t tag = wait_not_busy(t.tags + s, ld_relaxed(t.tags + s));
+            if (tag == kEmptyTag) {
+                const uint64_t old = atomicCAS(reinterpret_cast<unsigned long long *>(t.tags + s),
+                                               kEmptyTag, incoming);
+                if (old == kEmptyTag || (old & kFpMask) == want) {
+                    r.slot = static_cast<int64_t>(s);
+                    r.status = 0;
+                    r.probe_len = j + 1;
+                    return r;
+                }
+                continue;  // lost the claim to a different key (src/_native.pyx:221-222)
+            }
+            if ((tag & kFpMask) == want) {
+                r.slot = static_cast<int64_t>(s);
+                r.status = 0;
+                r.probe_len = j + 1;
+                return r;
+            }
+            const uint64_t age = (tag >> 32) & kAgeMask;
+            if (age >= static_cast<uint64_t>(t.evict_min_age) &&
+                ld_relaxed_i64(t.counts + s) == 0) {
+                if (victim < 0 || tag > victim_tag) {
+                    victim = static_cast<int64_t>(s);
+                    victim_tag = tag;
+                }
+            }
+        }
+        if (victim < 0)
+            return r;  // status 2, no mutation
+        uint64_t *vp = t.tags + victim;
+        const uint64_t old = atomicCAS(reinterpret_cast<unsigned long long *>(vp), victim_tag,
+                                       kBusyTag);
+        if (old == victim_tag) {
+            r.victim_touch = ld_relaxed_i64(t.last_touch + victim);
+            zero_cell(t, victim);
+            __threadfence();
+            st_release(vp, incoming);
+            r.slot = victim;
+            r.status = 1;
+            r.probe_len = t.probe_limit;
+            r.victim_tag = victim_tag;
+            return r;
+        }
+        // window changed under us: re-probe
+    }
+    return r;
+}
+
+// lookup_slots for one key (src/_native.pyx:285-294).
+__device__ __forceinline__ int64_t probe_lookup(const uint64_t *tags, uint64_t mask,
+                                                int probe_limit, uint64_t idx, uint32_t fp) {
+    const uint64_t home = idx & mask;
+    for (int j = 0; j < probe_limit; ++j) {
+        const uint64_t s = (home + static_cast<uint64_t>(j)) & mask;
+        const uint64_t tag = __ldg(reinterpret_cast<const unsigned long long *>(tags + s));
+        if (tag == kEmptyTag)
+            return -1;
+        if ((tag & kFpMask) == static_cast<uint64_t>(fp))
+            return static_cast<int64_t>(s);
+    }
+    return -1;
+}
+
+// ------------------------------------------------------------------ temporal math
+
+// VoxelTable.effective for one slot (src/table.py:205-238).  In integrate mode the
+// storage dtype is kept: isum (fixed) or fsum (float) and icnt; filter/hybrid produce
+// float sums and float counts.  Every value equals numpy's elementwise result.
+struct Effective {
+    int64_t isum[3];
+    double fsum[3];
+    int64_t icnt;
+    double fcnt;
+};
+
+__device__ __forceinline__ Effective effective_at(const pf_table &t, int64_t s, int mode,
+                                                  double ema, double delta_max) {
+    Effective e;
+    const bool fixed = t.sum_mode == PF_SUM_FIXED;
+    const int64_t lc_i = __ldg(t.counts + s);
+    const int64_t hc_i = __ldg(t.hist_counts + s);
+    if (mode == PF_INTEGRATE) {
+#pragma unroll
+        for (int c = 0; c < 3; ++c) {
+            if (fixed) {
+                e.isum[c] = __ldg(static_cast<const int64_t *>(t.sums) + 3 * s + c) +
+                            __ldg(static_cast<const int64_t *>(t.hist_sums) + 3 * s + c);
+                e.fsum[c] = 0.0;
+            } else {
+                e.fsum[c] = dadd(__ldg(static_cast<const double *>(t.sums) + 3 * s + c),
+                                 __ldg(static_cast<const double *>(t.hist_sums) + 3 * s + c));
+                e.isum[c] = 0;
+            }
+        }
+        e.icnt = lc_i + hc_i;
+        e.fcnt = static_cast<double>(e.icnt);
+        return e;
+    }
+    const double lc = static_cast<double>(lc_i), hc = static_cast<double>(hc_i);
+    double alpha, cnt;
+    if (mode == PF_FILTER) {
+        alpha = hc > 0.0 ? (lc > 0.0 ? ema : 1.0) : 0.0;
+        cnt = dadd(lc, hc);
+    } else {
+        const double k = np_min(np_max(ddiv(__ldg(t.deltas + s), delta_max), 0.0), 1.0);
+        const double both = np_max(dadd(lc, hc), 1.0);
+        alpha = hc > 0.0 ? (lc > 0.0 ? ddiv(dmul(dsub(1.0, k), hc), both) : 1.0) : 0.0;
+        cnt = dadd(rint(dmul(dsub(1.0, k), hc)), lc);
+    }
+    const double one_minus = dsub(1.0, alpha);
+#pragma unroll
+    for (int c = 0; c < 3; ++c) {
+        double live, hist;
+        if (fixed) {
+            live = static_cast<double>(__ldg(static_cast<const int64_t *>(t.sums) + 3 * s + c)) /
+                   kFixedScale;
+            hist = static_cast<double>(
+                       __ldg(static_cast<const int64_t *>(t.hist_sums) + 3 * s + c)) / kFixedScale;
+        } else {
+            live = __ldg(static_cast<const double *>(t.sums) + 3 * s + c);
+            hist = __ldg(static_cast<const double *>(t.hist_sums) + 3 * s + c);
+        }
+        const double lmean = lc > 0.0 ? ddiv(live, np_max(lc, 1.0)) : 0.0;
+        const double hmean = hc > 0.0 ? ddiv(hist, np_max(hc, 1.0)) : 0.0;
+        const double mean = dadd(dmul(alpha, hmean), dmul(one_minus, lmean));
+        double es = dmul(mean, cnt);
+        if (fixed) es = dmul(es, kFixedScale);
+        e.fsum[c] = es;
+        e.isum[c] = 0;
+    }
+    e.icnt = 0;
+    e.fcnt = cnt;
+    return e;
+}
+
+// True when eff sums are int64 (fixed-point integrate), i.e. numpy kept int64 dtype.
+__device__ __forceinline__ bool eff_is_int(const pf_table &t, int mode) {
+    return mode == PF_INTEGRATE && t.sum_mode == PF_SUM_FIXED;
+}
+
+__device__ __forceinline__ double eff_sum_f64(const Effective &e, bool as_int, int c) {
+    return as_int ? static_cast<double>(e.isum[c]) : e.fsum[c];
+}
+
+}  // namespace pf

@@ -1,0 +1,412 @@
+// Fused per-frame kernels: accumulate_phase (keys + warp-merged insert into the fine
+// and coarse tables in one pass over the vertex buffer) and resolve_phase (lookup
+// keys, fine rung, 3x3x3 neighbourhood + coarse rungs on a compacted work list,
+// composite).  src/pipeline.py:152-283.
+#include "pf_insert.cuh"
+#include "pf_internal.cuh"
+
+namespace pf {
+
+constexpr int kThreads = 256;
+constexpr int kWarps = kThreads / 32;
+
+struct BlockStats {
+    unsigned long long v[10];
+    unsigned hist[256];
+};
+
+__device__ __forceinline__ void stats_init(BlockStats &b) {
+    for (int k = threadIdx.x; k < 10; k += blockDim.x) b.v[k] = 0;
+    for (int k = threadIdx.x; k < 256; k += blockDim.x) b.hist[k] = 0;
+}
+
+// warp-aggregated add of a per-lane predicate into a block counter
+__device__ __forceinline__ void warp_count(BlockStats &b, int slot, bool pred) {
+    const unsigned m = __ballot_sync(kFull, pred);
+    if ((threadIdx.x & 31) == 0 && m) atomicAdd(&b.v[slot], static_cast<unsigned long long>(__popc(m)));
+}
+
+__device__ __forceinline__ void stats_flush(const BlockStats &b, int64_t *stats, bool with_hist) {
+    for (int k = threadIdx.x; k < 10; k += blockDim.x)
+        if (b.v[k]) atomicAdd(reinterpret_cast<unsigned long long *>(stats + k), b.v[k]);
+    if (with_hist)
+        for (int k = threadIdx.x; k < 256; k += blockDim.x)
+            if (b.hist[k])
+                atomicAdd(reinterpret_cast<unsigned long long *>(stats + PF_STAT_HIST_BASE + k),
+                          static_cast<unsigned long long>(b.hist[k]));
+}
+
+__device__ __forceinline__ void log_eviction(pf_evict_event *events, int64_t *count, int64_t cap,
+                                             int64_t vertex, const LaneInsert &r) {
+    if (events == nullptr || count == nullptr) return;
+    const unsigned long long k = atomicAdd(reinterpret_cast<unsigned long long *>(count), 1ull);
+    if (static_cast<int64_t>(k) < cap) {
+        pf_evict_event e;
+        e.vertex = vertex;
+        e.slot = r.slot;
+        e.victim_tag = r.victim_tag;
+        e.victim_touch = r.victim_touch;
+        events[k] = e;
+    }
+}
+
+// ------------------------------------------------------------------ insert
+
+template <bool FIXED>
+__global__ void __launch_bounds__(kThreads)
+insert_frame_kernel(pf_config cfg, pf_vertices v, pf_table fine, pf_table coarse, int has_coarse,
+                    uint64_t h0, int64_t frame, int64_t *stats, pf_evict_event *events,
+                    int64_t *event_count, int64_t event_cap) {
+    __shared__ BlockStats bs;
+    stats_init(bs);
+    __syncthreads();
+    const int64_t i = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+    const bool valid = i < v.n;
+    VertexIn x;
+    double val[3] = {0.0, 0.0, 0.0};
+    double du = 0.0, dv = 0.0;
+    CellHash hf{0ull, 0u}, hc{0ull, 0u};
+    if (valid) {
+        x = load_vertex(v, i, cfg);
+#pragma unroll
+        for (int c = 0; c < 3; ++c) val[c] = __ldg(v.contribution + 3 * i + c);
+        if (cfg.jitter) {
+            double u1, u2;
+            jitter_draws(h0, x.pixel, x.sample, u1, u2);
+            disc_offset(u1, u2, du, dv);
+        }
+        const KeyShared ks = key_shared(cfg, x);
+        double jt[3];
+        const CellKey kf = make_key(cfg, x, ks, cfg.jitter, du, dv, 0, jt);
+        hf = key_hash(kf, ks);
+        if (has_coarse) {
+            const CellKey kc = make_key(cfg, x, ks, cfg.jitter, du, dv, cfg.coarse_delta, jt);
+            hc = key_hash(kc, ks);
+        }
+    }
+    const LaneInsert rf = warp_insert<FIXED>(fine, valid, hf.index, hf.fp, val, frame);
+    warp_count(bs, PF_STAT_PROBE_FAILURES, valid && rf.status == 2);
+    warp_count(bs, PF_STAT_EVICTIONS, valid && rf.leader && rf.status == 1);
+    {
+        // probe-length histogram and sum, merged per distinct length in the warp
+        const int pl = valid ? rf.probe_len : -1;
+        const unsigned same = __match_any_sync(kFull, pl);
+        if (valid && (threadIdx.x & 31) == static_cast<unsigned>(__ffs(same) - 1)) {
+            const unsigned cnt = __popc(same);
+            atomicAdd(&bs.hist[pl & 255], cnt);
+            atomicAdd(&bs.v[PF_STAT_PROBE_LEN_SUM], static_cast<unsigned long long>(cnt) * pl);
+        }
+    }
+    if (valid && rf.leader && rf.status == 1) log_eviction(events, event_count, event_cap, i, rf);
+    if (has_coarse) {
+        const LaneInsert rc = warp_insert<FIXED>(coarse, valid, hc.index, hc.fp, val, frame);
+        warp_count(bs, PF_STAT_COARSE_PROBE_FAILURES, valid && rc.status == 2);
+        warp_count(bs, PF_STAT_COARSE_EVICTIONS, valid && rc.leader && rc.status == 1);
+    }
+    __syncthreads();
+    stats_flush(bs, stats, true);
+}
+
+// ------------------------------------------------------------------ resolve
+
+struct ResolveArgs {
+    pf_config cfg;
+    pf_vertices v;
+    pf_table fine;
+    pf_table coarse;
+    int has_coarse;
+    uint64_t h0_lookup;
+    uint64_t h0_coarse;
+    double *flat;
+    int64_t *work;
+    int64_t *work_count;
+    uint8_t *source;
+    double *chosen;
+    int64_t *stats;
+    double thr;
+};
+
+// _mean_rows (src/pipeline.py:196-200) for one row.
+__device__ __forceinline__ double row_mean(double sum, double cnt, bool fixed) {
+    double d = np_max(cnt, 1e-300);
+    if (fixed) d = dmul(d, kFixedScale);
+    return ddiv(sum, d);
+}
+
+__device__ __forceinline__ void composite(const ResolveArgs &a, int64_t i, int64_t pixel,
+                                          const double chosen[3], int source) {
+#pragma unroll
+    for (int c = 0; c < 3; ++c) {
+        const double tp = __ldg(a.v.throughput + 3 * i + c);
+        atomicAdd(a.flat + 3 * pixel + c, dmul(tp, chosen[c]));
+    }
+    if (a.source) a.source[i] = static_cast<uint8_t>(source);
+    if (a.chosen) {
+#pragma unroll
+        for (int c = 0; c < 3; ++c) a.chosen[3 * i + c] = chosen[c];
+    }
+}
+
+// Rung 1 for every vertex; rows below the threshold go to the work list with their
+// lookup key (row, qx, qy, qz, level, aux).
+__global__ void __launch_bounds__(kThreads) resolve_main_kernel(ResolveArgs a) {
+    __shared__ BlockStats bs;
+    stats_init(bs);
+    __syncthreads();
+    const pf_config &cfg = a.cfg;
+    const int64_t i = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+    const bool valid = i < a.v.n;
+    bool fine_ok = false;
+    CellKey k{};
+    if (valid) {
+        const VertexIn x = load_vertex(a.v, i, cfg);
+        double du = 0.0, dv = 0.0;
+        if (cfg.jitter) {
+            double u1, u2;
+            jitter_draws(a.h0_lookup, x.pixel, x.sample, u1, u2);
+            disc_offset(u1, u2, du, dv);
+        }
+        const KeyShared ks = key_shared(cfg, x);
+        double jt[3];
+        k = make_key(cfg, x, ks, cfg.jitter, du, dv, 0, jt);
+        const CellHash h = key_hash(k, ks);
+        const int64_t s = probe_lookup(a.fine.tags, static_cast<uint64_t>(a.fine.capacity) - 1,
+                                       a.fine.probe_limit, h.index, h.fp);
+        if (s >= 0) {
+            const Effective e = effective_at(a.fine, s, cfg.temporal_mode, cfg.ema_alpha, cfg.delta_max);
+            const double cnt = e.fcnt;
+            if (cnt >= a.thr) {
+                fine_ok = true;
+                const bool as_int = eff_is_int(a.fine, cfg.temporal_mode);
+                const bool fixed = a.fine.sum_mode == PF_SUM_FIXED;
+                double m[3];
+#pragma unroll
+                for (int c = 0; c < 3; ++c) m[c] = row_mean(eff_sum_f64(e, as_int, c), cnt, fixed);
+                composite(a, i, x.pixel, m, 0);
+            }
+        }
+    }
+    const bool need = valid && !fine_ok;
+    const unsigned m = __ballot_sync(kFull, need);
+    if (m) {
+        unsigned long long base = 0;
+        const int lane = threadIdx.x & 31;
+        if (lane == __ffs(m) - 1)
+            base = atomicAdd(reinterpret_cast<unsigned long long *>(a.work_count),
+                             static_cast<unsigned long long>(__popc(m)));
+        base = __shfl_sync(kFull, base, __ffs(m) - 1);
+        if (need) {
+            int64_t *w = a.work + 6 * (static_cast<int64_t>(base) + __popc(m & ((1u << lane) - 1u)));
+            w[0] = i;
+            w[1] = k.q[0];
+            w[2] = k.q[1];
+            w[3] = k.q[2];
+            w[4] = k.level;
+            w[5] = static_cast<int64_t>(k.aux);
+        }
+    }
+    warp_count(bs, PF_STAT_SOURCE_FINE, valid && fine_ok);
+    warp_count(bs, PF_STAT_FALLBACK_ROWS, need);
+    __syncthreads();
+    stats_flush(bs, a.stats, false);
+}
+
+// Rungs 2-5 for one work row per warp: lanes 0..26 probe the 3x3x3 neighbourhood in
+// (dx, dy, dz) nested order; lane 0 sums them in that order (numpy's order for the
+// float64 pools), then runs the coarse rung, the ladder and the composite.
+__global__ void __launch_bounds__(kThreads) resolve_fallback_kernel(ResolveArgs a) {
+    __shared__ BlockStats bs;
+    stats_init(bs);
+    __syncthreads();
+    const pf_config &cfg = a.cfg;
+    const int lane = threadIdx.x & 31;
+    const int64_t n_work = *a.work_count;
+    const int64_t warp0 = static_cast<int64_t>(blockIdx.x) * kWarps + (threadIdx.x >> 5);
+    const int64_t nwarps = static_cast<int64_t>(gridDim.x) * kWarps;
+    const int mode = cfg.temporal_mode;
+    const bool as_int = eff_is_int(a.fine, mode);
+    const bool fixed = a.fine.sum_mode == PF_SUM_FIXED;
+    const uint64_t fmask = static_cast<uint64_t>(a.fine.capacity) - 1;
+    for (int64_t w = warp0; w < n_work; w += nwarps) {
+        const int64_t *rec = a.work + 6 * w;
+        const int64_t row = rec[0];
+        bool found = false;
+        Effective e{};
+        if (lane < 27) {
+            const int dx = lane / 9 - 1, dy = (lane / 3) % 3 - 1, dz = lane % 3 - 1;
+            const CellHash h = cell_hash(rec[1] + dx, rec[2] + dy, rec[3] + dz, rec[4],
+                                         static_cast<uint64_t>(rec[5]), 0, 0u);
+            const int64_t s = probe_lookup(a.fine.tags, fmask, a.fine.probe_limit, h.index, h.fp);
+            if (s >= 0) {
+                found = true;
+                e = effective_at(a.fine, s, mode, cfg.ema_alpha, cfg.delta_max);
+            }
+        }
+        // ordered pool: (src/pipeline.py:185-192)
+        int64_t pis[3] = {0, 0, 0}, pic = 0;
+        double pfs[3] = {0.0, 0.0, 0.0}, pfc = 0.0;
+        const unsigned fm = __ballot_sync(kFull, found);
+        for (int j = 0; j < 27; ++j) {
+            if (!((fm >> j) & 1u)) continue;  // warp-uniform
+#pragma unroll
+            for (int c = 0; c < 3; ++c) {
+                if (as_int) pis[c] += __shfl_sync(kFull, static_cast<long long>(e.isum[c]), j);
+                else pfs[c] = dadd(pfs[c], __shfl_sync(kFull, e.fsum[c], j));
+            }
+            if (mode == PF_INTEGRATE) pic += __shfl_sync(kFull, static_cast<long long>(e.icnt), j);
+            else pfc = dadd(pfc, __shfl_sync(kFull, e.fcnt, j));
+        }
+        if (lane != 0) continue;
+        const double cnt_n = (mode == PF_INTEGRATE) ? static_cast<double>(pic) : pfc;
+        double mean_n[3] = {0.0, 0.0, 0.0};
+        if (cnt_n > 0.0) {
+#pragma unroll
+            for (int c = 0; c < 3; ++c)
+                mean_n[c] = row_mean(as_int ? static_cast<double>(pis[c]) : pfs[c], cnt_n, fixed);
+        }
+        const bool ok_n = cnt_n >= a.thr;
+        double cnt_c = 0.0;
+        double mean_c[3] = {0.0, 0.0, 0.0};
+        const VertexIn x = load_vertex(a.v, row, cfg);
+        if (!ok_n && a.has_coarse) {
+            double du = 0.0, dv = 0.0;
+            if (cfg.jitter) {
+                double u1, u2;
+                jitter_draws(a.h0_coarse, x.pixel, x.sample, u1, u2);
+                disc_offset(u1, u2, du, dv);
+            }
+            const KeyShared ks = key_shared(cfg, x);
+            double jt[3];
+            const CellKey kc = make_key(cfg, x, ks, cfg.jitter, du, dv, cfg.coarse_delta, jt);
+            const CellHash h = key_hash(kc, ks);
+            const int64_t s = probe_lookup(a.coarse.tags, static_cast<uint64_t>(a.coarse.capacity) - 1,
+                                           a.coarse.probe_limit, h.index, h.fp);
+            if (s >= 0) {
+                const Effective ce = effective_at(a.coarse, s, mode, cfg.ema_alpha, cfg.delta_max);
+                cnt_c = ce.fcnt;
+                if (cnt_c > 0.0) {
+                    const bool c_int = eff_is_int(a.coarse, mode);
+#pragma unroll
+                    for (int c = 0; c < 3; ++c)
+                        mean_c[c] = row_mean(eff_sum_f64(ce, c_int, c), cnt_c, fixed);
+                }
+            }
+        }
+        const bool ok_c = !ok_n && cnt_c >= a.thr;
+        const bool any_n = !ok_n && !ok_c && cnt_n >= 1.0;
+        const bool any_c = !ok_n && !ok_c && !any_n && cnt_c >= 1.0;
+        double ch[3];
+        int src;
+        if (ok_n || any_n) {
+            src = 1;
+#pragma unroll
+            for (int c = 0; c < 3; ++c) ch[c] = mean_n[c];
+        } else if (ok_c || any_c) {
+            src = 2;
+#pragma unroll
+            for (int c = 0; c < 3; ++c) ch[c] = mean_c[c];
+        } else {
+            src = 3;
+#pragma unroll
+            for (int c = 0; c < 3; ++c) ch[c] = __ldg(a.v.contribution + 3 * row + c);
+        }
+        composite(a, row, x.pixel, ch, src);
+        atomicAdd(&bs.v[PF_STAT_SOURCE_FINE + src], 1ull);
+    }
+    __syncthreads();
+    stats_flush(bs, a.stats, false);
+}
+
+__global__ void __launch_bounds__(kThreads)
+finalize_image_kernel(const double *__restrict__ base, const double *__restrict__ flat,
+                      double *__restrict__ image, int64_t n, double spp) {
+    const int64_t k = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+    if (k < n) image[k] = dadd(base[k], ddiv(flat[k], spp));
+}
+
+}  // namespace pf
+
+using namespace pf;
+
+extern "C" {
+
+int pf_insert_frame(const pf_config *cfg, const pf_vertices *v, const pf_table *fine,
+                    const pf_table *coarse, uint64_t stream_base_accum, int64_t frame,
+                    int64_t *stats, pf_evict_event *events, int64_t *event_count,
+                    int64_t event_capacity, void *stream) {
+    const char *fn = "pf_insert_frame";
+    if (int rc = validate_vertices(fn, v, cfg)) return rc;
+    if (int rc = validate_table(fn, fine)) return rc;
+    if (coarse) {
+        if (int rc = validate_table(fn, coarse)) return rc;
+        if (coarse->sum_mode != fine->sum_mode) return fail_arg(fn, "fine/coarse sum_mode differ");
+    }
+    if (!stats) return fail_arg(fn, "stats is NULL");
+    if (v->n > 0 && !v->contribution) return fail_arg(fn, "contribution is NULL");
+    if (v->n == 0) return PF_OK;
+    const pf_table c = coarse ? *coarse : *fine;
+    const unsigned g = blocks_for(v->n, kThreads);
+    if (fine->sum_mode == PF_SUM_FIXED)
+        insert_frame_kernel<true><<<g, kThreads, 0, as_stream(stream)>>>(
+            *cfg, *v, *fine, c, coarse != nullptr, stream_base_accum, frame, stats, events,
+            event_count, event_capacity);
+    else
+        insert_frame_kernel<false><<<g, kThreads, 0, as_stream(stream)>>>(
+            *cfg, *v, *fine, c, coarse != nullptr, stream_base_accum, frame, stats, events,
+            event_count, event_capacity);
+    return check_launch(fn);
+}
+
+int pf_resolve_frame(const pf_config *cfg, const pf_vertices *v, const pf_table *fine,
+                     const pf_table *coarse, uint64_t stream_base_lookup,
+                     uint64_t stream_base_coarse, int64_t spp, const double *base_image,
+                     int64_t n_pixels, double *image, double *flat, int64_t *work,
+                     int64_t *work_count, uint8_t *source, double *chosen, int64_t *stats,
+                     void *stream) {
+    const char *fn = "pf_resolve_frame";
+    if (int rc = validate_vertices(fn, v, cfg)) return rc;
+    if (int rc = validate_table(fn, fine)) return rc;
+    if (coarse)
+        if (int rc = validate_table(fn, coarse)) return rc;
+    if (spp < 1) return fail_arg(fn, "spp must be >= 1");
+    if (n_pixels < 0 || !base_image || !image || !flat || !stats)
+        return fail_arg(fn, "image buffers / stats are NULL");
+    if (v->n > 0 && (!v->throughput || !v->contribution || !work || !work_count))
+        return fail_arg(fn, "throughput/contribution/work is NULL");
+    cudaStream_t st = as_stream(stream);
+    if (cudaMemsetAsync(flat, 0, sizeof(double) * 3 * n_pixels, st) != cudaSuccess)
+        return check_launch(fn);
+    if (v->n > 0) {
+        if (cudaMemsetAsync(work_count, 0, sizeof(int64_t), st) != cudaSuccess)
+            return check_launch(fn);
+        ResolveArgs a;
+        a.cfg = *cfg;
+        a.v = *v;
+        a.fine = *fine;
+        a.coarse = coarse ? *coarse : *fine;
+        a.has_coarse = coarse != nullptr;
+        a.h0_lookup = stream_base_lookup;
+        a.h0_coarse = stream_base_coarse;
+        a.flat = flat;
+        a.work = work;
+        a.work_count = work_count;
+        a.source = source;
+        a.chosen = chosen;
+        a.stats = stats;
+        a.thr = static_cast<double>(cfg->low_count_threshold > 1 ? cfg->low_count_threshold : 1);
+        resolve_main_kernel<<<blocks_for(v->n, kThreads), kThreads, 0, st>>>(a);
+        if (int rc = check_launch(fn)) return rc;
+        int64_t fb_blocks = (v->n + kWarps - 1) / kWarps;
+        const int64_t cap = static_cast<int64_t>(sm_count()) * 8;
+        if (fb_blocks > cap) fb_blocks = cap;
+        resolve_fallback_kernel<<<static_cast<unsigned>(fb_blocks), kThreads, 0, st>>>(a);
+        if (int rc = check_launch(fn)) return rc;
+    }
+    const int64_t m = 3 * n_pixels;
+    if (m > 0)
+        finalize_image_kernel<<<blocks_for(m, kThreads), kThreads, 0, st>>>(
+            base_image, flat, image, m, static_cast<double>(spp));
+    return check_launch(fn);
+}
+
+}  // extern "C"

@@ -1,0 +1,106 @@
+// Warp-merged insert: the table write path shared by the batch-accumulate kernel
+// and the fused frame-insert kernel.
+#pragma once
+
+#include "pf_device.cuh"
+
+namespace pf {
+
+constexpr unsigned kFull = 0xFFFFFFFFu;
+
+// 16.16 fixed point, half up (src/_native.pyx:251-253): floor(v*65536 + 0.5).
+__device__ __forceinline__ int64_t quantize_fixed(double v) {
+    return np_i64(floor(dadd(dmul(v, kFixedScale), 0.5)));
+}
+
+struct LaneInsert {
+    int64_t slot;
+    int32_t status;
+    int32_t probe_len;
+    uint64_t victim_tag;
+    int64_t victim_touch;
+    bool leader;      // this lane performed the probe for its key group
+    unsigned peers;   // lanes holding the same (index, fingerprint)
+};
+
+// All 32 lanes must call this together.  Lanes holding the same (index, fp) are
+// merged with __match_any_sync; the lowest lane (= earliest vertex) probes and
+// claims once and adds the group's summed radiance with one atomic per channel,
+// plus popc(peers) to the count.  Followers report what a sequential caller would
+// see after the leader: same slot and probe length, status 1 -> 0.
+template <bool FIXED>
+__device__ __forceinline__ LaneInsert warp_insert(const pf_table &t, bool valid, uint64_t idx,
+                                                  uint32_t fp, const double val[3], int64_t frame) {
+    const unsigned lane = threadIdx.x & 31u;
+    const uint64_t k2 = static_cast<uint64_t>(fp) | (static_cast<uint64_t>(valid) << 32);
+    const unsigned peers = __match_any_sync(kFull, valid ? idx : 0ull) & __match_any_sync(kFull, k2);
+    const int leader = __ffs(peers) - 1;
+    const bool is_leader = valid && static_cast<int>(lane) == leader;
+
+    int64_t qsum[3];
+    double fsum[3];
+#pragma unroll
+    for (int c = 0; c < 3; ++c) {
+        if (FIXED) qsum[c] = valid ? quantize_fixed(val[c]) : 0;
+        else fsum[c] = valid ? val[c] : 0.0;
+    }
+    unsigned followers = __ballot_sync(kFull, valid && static_cast<int>(lane) != leader);
+    while (followers) {  // warp-uniform loop, one iteration per follower lane
+        const int j = __ffs(followers) - 1;
+        followers &= followers - 1;
+        const bool mine = is_leader && ((peers >> j) & 1u);
+#pragma unroll
+        for (int c = 0; c < 3; ++c) {
+            if (FIXED) {
+                const long long x = __shfl_sync(kFull, static_cast<long long>(qsum[c]), j);
+                if (mine) qsum[c] += x;
+            } else {
+                const double x = __shfl_sync(kFull, fsum[c], j);
+                if (mine) fsum[c] = dadd(fsum[c], x);
+            }
+        }
+    }
+
+    InsertResult r;
+    r.slot = -1;
+    r.status = 2;
+    r.probe_len = 0;
+    r.victim_tag = 0;
+    r.victim_touch = 0;
+    if (is_leader) {
+        r = probe_insert(t, idx, fp);
+        if (r.status != 2) {
+            const int64_t s = r.slot;
+#pragma unroll
+            for (int c = 0; c < 3; ++c) {
+                if (FIXED)
+                    atomicAdd(reinterpret_cast<unsigned long long *>(
+                                  static_cast<int64_t *>(t.sums) + 3 * s + c),
+                              static_cast<unsigned long long>(qsum[c]));
+                else
+                    atomicAdd(static_cast<double *>(t.sums) + 3 * s + c, fsum[c]);
+            }
+            atomicAdd(reinterpret_cast<unsigned long long *>(t.counts + s),
+                      static_cast<unsigned long long>(__popc(peers)));
+            st_relaxed_u64(t.last_touch + s, static_cast<uint64_t>(frame));
+        }
+    }
+    LaneInsert out;
+    out.slot = __shfl_sync(kFull, static_cast<long long>(r.slot), leader);
+    out.status = __shfl_sync(kFull, r.status, leader);
+    out.probe_len = __shfl_sync(kFull, r.probe_len, leader);
+    out.victim_tag = is_leader ? r.victim_tag : 0ull;
+    out.victim_touch = is_leader ? r.victim_touch : 0;
+    if (!is_leader && out.status == 1) {
+        // a later vertex of the same key finds the freshly evicted cell
+        out.status = 0;
+        out.probe_len = static_cast<int32_t>(
+            ((static_cast<uint64_t>(out.slot) - (idx & static_cast<uint64_t>(t.capacity - 1))) &
+             static_cast<uint64_t>(t.capacity - 1)) + 1);
+    }
+    out.leader = is_leader;
+    out.peers = peers;
+    return out;
+}
+
+}  // namespace pf

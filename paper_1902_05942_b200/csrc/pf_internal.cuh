@@ -1,0 +1,51 @@
+// Host-side helpers shared by the C-ABI translation units.
+#pragma once
+
+#include <cuda_runtime.h>
+
+#include <cstdint>
+#include <string>
+
+#include "../../include/pathfilter_b200.h"
+
+namespace pf {
+
+void set_error(const std::string &msg);
+int fail_arg(const char *fn, const char *what);
+int check_launch(const char *fn);
+int sm_count();
+
+inline bool is_pow2(int64_t c) { return c >= 2 && (c & (c - 1)) == 0; }
+
+inline int validate_table(const char *fn, const pf_table *t) {
+    if (t == nullptr) return fail_arg(fn, "table is NULL");
+    if (!is_pow2(t->capacity)) return fail_arg(fn, "capacity must be a power of two >= 2");
+    if (t->probe_limit < 1) return fail_arg(fn, "probe_limit must be >= 1");
+    if (!t->tags || !t->sums || !t->counts || !t->hist_sums || !t->hist_counts ||
+        !t->last_touch || !t->deltas)
+        return fail_arg(fn, "table array pointer is NULL");
+    if (t->sum_mode != PF_SUM_FIXED && t->sum_mode != PF_SUM_FLOAT)
+        return fail_arg(fn, "unknown sum_mode");
+    return PF_OK;
+}
+
+inline int validate_vertices(const char *fn, const pf_vertices *v, const pf_config *cfg) {
+    if (v == nullptr || cfg == nullptr) return fail_arg(fn, "vertices/config is NULL");
+    if (v->n < 0) return fail_arg(fn, "negative vertex count");
+    if (v->n == 0) return PF_OK;
+    if (!v->position || !v->normal || !v->camera_distance || !v->pixel || !v->sample)
+        return fail_arg(fn, "vertex array pointer is NULL");
+    if (cfg->include_incident_angle && (!v->omega_r || !v->layer_id))
+        return fail_arg(fn, "include_incident_angle needs omega_r and layer_id");
+    if (cfg->include_layer && !v->layer_id)
+        return fail_arg(fn, "include_layer needs layer_id");
+    return PF_OK;
+}
+
+inline cudaStream_t as_stream(void *s) { return static_cast<cudaStream_t>(s); }
+
+inline unsigned blocks_for(int64_t n, int threads) {
+    return static_cast<unsigned>((n + threads - 1) / threads);
+}
+
+}  // namespace pf

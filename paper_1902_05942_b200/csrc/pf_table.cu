@@ -1,0 +1,518 @@
+// Table kernels behind the reference kernel-module ABI and the VoxelTable API:
+// batch accumulate (parallel warp-merged, or sequential-order), lookup, key build,
+// hashing, effective sums, the temporal update (begin_frame) and occupancy.
+#include "pf_insert.cuh"
+#include "pf_internal.cuh"
+
+namespace pf {
+
+constexpr int kThreads = 256;
+
+// ------------------------------------------------------------------ accumulate
+
+struct BatchOut {
+    uint8_t *status;
+    int64_t *slots;
+    uint8_t *probe_len;
+    uint64_t *victim_tags;
+    int64_t *victim_touch;
+};
+
+// Parallel batch insert (src/_native.pyx:186-258 semantics, warp-merged atomics).
+template <bool FIXED>
+__global__ void __launch_bounds__(kThreads)
+accumulate_kernel(pf_table t, const uint64_t *__restrict__ idx, const uint32_t *__restrict__ fp,
+                  const double *__restrict__ vals, int64_t n, int64_t frame, BatchOut o) {
+    const int64_t i = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+    const bool valid = i < n;
+    double v[3] = {0.0, 0.0, 0.0};
+    uint64_t k = 0;
+    uint32_t f = 0;
+    if (valid) {
+        k = __ldg(reinterpret_cast<const unsigned long long *>(idx) + i);
+        f = __ldg(fp + i);
+#pragma unroll
+        for (int c = 0; c < 3; ++c) v[c] = __ldg(vals + 3 * i + c);
+    }
+    const LaneInsert r = warp_insert<FIXED>(t, valid, k, f, v, frame);
+    if (!valid) return;
+    if (o.status) o.status[i] = static_cast<uint8_t>(r.status);
+    if (o.slots) o.slots[i] = r.status == 2 ? -1 : r.slot;
+    if (o.probe_len) o.probe_len[i] = static_cast<uint8_t>(r.probe_len);
+    if (o.victim_tags) o.victim_tags[i] = r.victim_tag;
+    if (o.victim_touch) o.victim_touch[i] = r.victim_touch;
+}
+
+// Sequential-order batch insert: one warp walks the batch in vertex order, reading
+// each probe window 32 slots at a time.  Reproduces the reference's threads=1 table
+// layout bit for bit (claims, evictions, probe lengths, statuses).
+template <bool FIXED>
+__global__ void __launch_bounds__(32)
+accumulate_ordered_kernel(pf_table t, const uint64_t *__restrict__ idx,
+                          const uint32_t *__restrict__ fp, const double *__restrict__ vals,
+                          int64_t n, int64_t frame, BatchOut o) {
+    const int lane = threadIdx.x;
+    const uint64_t mask = static_cast<uint64_t>(t.capacity) - 1;
+    const int P = t.probe_limit;
+    for (int64_t i = 0; i < n; ++i) {
+        const uint64_t home = idx[i] & mask;
+        const uint64_t want = static_cast<uint64_t>(fp[i]);
+        int stop_j = -1;
+        bool stop_empty = false;
+        int64_t victim = -1;
+        uint64_t victim_tag = 0;
+        for (int base = 0; base < P; base += 32) {
+            const int j = base + lane;
+            const bool in = j < P;
+            const uint64_t s = (home + static_cast<uint64_t>(j)) & mask;
+            const uint64_t tag = in ? ld_relaxed(t.tags + s) : 0ull;
+            const bool is_empty = in && tag == kEmptyTag;
+            const bool stop = in && (is_empty || (tag & kFpMask) == want);
+            const unsigned m = __ballot_sync(kFull, stop);
+            if (m) {
+                const int first = __ffs(m) - 1;
+                stop_j = base + first;
+                stop_empty = __shfl_sync(kFull, is_empty, first);
+                break;
+            }
+            // eviction candidates in this chunk: largest tag, earliest slot on ties
+            bool elig = false;
+            if (in) {
+                const uint64_t age = (tag >> 32) & kAgeMask;
+                elig = age >= static_cast<uint64_t>(t.evict_min_age) &&
+                       ld_relaxed_i64(t.counts + s) == 0;
+            }
+            uint64_t best_tag = tag;
+            int best_j = elig ? j : INT32_MAX;
+#pragma unroll
+            for (int off = 16; off > 0; off >>= 1) {
+                const uint64_t ot = __shfl_xor_sync(kFull, best_tag, off);
+                const int oj = __shfl_xor_sync(kFull, best_j, off);
+                const bool take = oj != INT32_MAX &&
+                                  (best_j == INT32_MAX || ot > best_tag ||
+                                   (ot == best_tag && oj < best_j));
+                if (take) {
+                    best_tag = ot;
+                    best_j = oj;
+                }
+            }
+            if (best_j != INT32_MAX && (victim < 0 || best_tag > victim_tag)) {
+                victim = static_cast<int64_t>((home + static_cast<uint64_t>(best_j)) & mask);
+                victim_tag = best_tag;
+            }
+        }
+        if (lane == 0) {
+            int status = 0;
+            int64_t slot = -1;
+            int plen = P;
+            uint64_t vt = 0;
+            int64_t vtt = 0;
+            if (stop_j >= 0) {
+                slot = static_cast<int64_t>((home + static_cast<uint64_t>(stop_j)) & mask);
+                plen = stop_j + 1;
+                if (stop_empty) st_relaxed_u64(t.tags + slot, (kFresh << 32) | want);
+            } else if (victim >= 0) {
+                status = 1;
+                slot = victim;
+                vt = victim_tag;
+                vtt = ld_relaxed_i64(t.last_touch + victim);
+                zero_cell(t, victim);
+                st_relaxed_u64(t.tags + victim, (kFresh << 32) | want);
+            } else {
+                status = 2;
+            }
+            if (status != 2) {
+#pragma unroll
+                for (int c = 0; c < 3; ++c) {
+                    const double x = vals[3 * i + c];
+                    if (FIXED) {
+                        int64_t *p = static_cast<int64_t *>(t.sums) + 3 * slot + c;
+                        st_relaxed_u64(p, static_cast<uint64_t>(ld_relaxed_i64(p) + quantize_fixed(x)));
+                    } else {
+                        double *p = static_cast<double *>(t.sums) + 3 * slot + c;
+                        const uint64_t bits = ld_relaxed(reinterpret_cast<const uint64_t *>(p));
+                        st_relaxed_u64(p, __double_as_longlong(dadd(__longlong_as_double(bits), x)));
+                    }
+                }
+                st_relaxed_u64(t.counts + slot, static_cast<uint64_t>(ld_relaxed_i64(t.counts + slot) + 1));
+                st_relaxed_u64(t.last_touch + slot, static_cast<uint64_t>(frame));
+            }
+            if (o.status) o.status[i] = static_cast<uint8_t>(status);
+            if (o.slots) o.slots[i] = slot;
+            if (o.probe_len) o.probe_len[i] = static_cast<uint8_t>(plen);
+            if (o.victim_tags) o.victim_tags[i] = vt;
+            if (o.victim_touch) o.victim_touch[i] = vtt;
+            __threadfence_block();
+        }
+        __syncwarp();
+    }
+}
+
+// ------------------------------------------------------------------ lookup
+
+__global__ void __launch_bounds__(kThreads)
+lookup_kernel(const uint64_t *__restrict__ tags, uint64_t mask, int probe_limit,
+              const uint64_t *__restrict__ idx, const uint32_t *__restrict__ fp, int64_t n,
+              int64_t *__restrict__ out) {
+    const int64_t i = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+    if (i >= n) return;
+    out[i] = probe_lookup(tags, mask, probe_limit,
+                          __ldg(reinterpret_cast<const unsigned long long *>(idx) + i), __ldg(fp + i));
+}
+
+// ------------------------------------------------------------------ keys
+
+__device__ __forceinline__ void store_key(const pf_key_out &o, int64_t i, const CellKey &k,
+                                          const CellHash &h, const double jt[3]) {
+    if (o.qx) o.qx[i] = k.q[0];
+    if (o.qy) o.qy[i] = k.q[1];
+    if (o.qz) o.qz[i] = k.q[2];
+    if (o.level) o.level[i] = k.level;
+    if (o.aux) o.aux[i] = k.aux;
+    if (o.index) o.index[i] = h.index;
+    if (o.fingerprint) o.fingerprint[i] = h.fp;
+    if (o.jittered) {
+#pragma unroll
+        for (int c = 0; c < 3; ++c) o.jittered[3 * i + c] = jt[c];
+    }
+}
+
+// mode 0: explicit draws (u1/u2 may be NULL -> no jitter); mode 1: counter RNG.
+__global__ void __launch_bounds__(kThreads)
+keys_kernel(pf_config cfg, pf_vertices v, const double *__restrict__ u1,
+            const double *__restrict__ u2, int use_rng, uint64_t h0, int32_t level_delta,
+            pf_key_out o) {
+    const int64_t i = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+    if (i >= v.n) return;
+    const VertexIn x = load_vertex(v, i, cfg);
+    const KeyShared ks = key_shared(cfg, x);
+    int jit = 0;
+    double du = 0.0, dv = 0.0;
+    if (cfg.jitter) {
+        double a, b;
+        if (use_rng) {
+            jitter_draws(h0, x.pixel, x.sample, a, b);
+            jit = 1;
+        } else if (u1 != nullptr && u2 != nullptr) {
+            a = __ldg(u1 + i);
+            b = __ldg(u2 + i);
+            jit = 1;
+        }
+        if (jit) disc_offset(a, b, du, dv);
+    }
+    double jt[3];
+    const CellKey k = make_key(cfg, x, ks, jit, du, dv, level_delta, jt);
+    store_key(o, i, k, key_hash(k, ks), jt);
+}
+
+__global__ void __launch_bounds__(kThreads)
+hash_kernel(const int64_t *__restrict__ qx, const int64_t *__restrict__ qy,
+            const int64_t *__restrict__ qz, const int64_t *__restrict__ level,
+            const uint64_t *__restrict__ aux, const uint32_t *__restrict__ fp_bins, int64_t n,
+            uint64_t *__restrict__ index, uint32_t *__restrict__ fp) {
+    const int64_t i = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+    if (i >= n) return;
+    const CellHash h = cell_hash(qx[i], qy[i], qz[i], level[i], aux[i], fp_bins != nullptr,
+                                 fp_bins ? fp_bins[i] : 0u);
+    index[i] = h.index;
+    fp[i] = h.fp;
+}
+
+// ------------------------------------------------------------------ effective / begin_frame
+
+__global__ void __launch_bounds__(kThreads)
+effective_kernel(pf_table t, int mode, double ema, double delta_max, void *eff_sum,
+                 void *eff_count) {
+    const int64_t s = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+    if (s >= t.capacity) return;
+    const Effective e = effective_at(t, s, mode, ema, delta_max);
+    const bool as_int = eff_is_int(t, mode);
+#pragma unroll
+    for (int c = 0; c < 3; ++c) {
+        if (as_int) static_cast<int64_t *>(eff_sum)[3 * s + c] = e.isum[c];
+        else static_cast<double *>(eff_sum)[3 * s + c] = e.fsum[c];
+    }
+    if (mode == PF_INTEGRATE) static_cast<int64_t *>(eff_count)[s] = e.icnt;
+    else static_cast<double *>(eff_count)[s] = e.fcnt;
+}
+
+// begin_frame for one slot (src/table.py:242-298).  Empty slots hold all-zero state
+// (invariant of every reference code path), so only occupied slots are touched.
+template <bool FIXED>
+__global__ void __launch_bounds__(kThreads)
+begin_frame_kernel(pf_table t, int64_t frame, int mode, double ema, double delta_max,
+                   int32_t sample_cap, int64_t *horizon_clears) {
+    __shared__ int block_clears;
+    if (threadIdx.x == 0) block_clears = 0;
+    __syncthreads();
+    const int64_t s = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+    bool cleared = false;
+    if (s < t.capacity) {
+        const uint64_t tag = t.tags[s];
+        if (tag != kEmptyTag) {
+            int64_t *sums_i = static_cast<int64_t *>(t.sums) + 3 * s;
+            int64_t *hist_i = static_cast<int64_t *>(t.hist_sums) + 3 * s;
+            double *sums_f = static_cast<double *>(t.sums) + 3 * s;
+            double *hist_f = static_cast<double *>(t.hist_sums) + 3 * s;
+            const int64_t age = frame - t.last_touch[s];
+            cleared = age > t.evict_horizon;
+            if (!cleared) {
+                if (mode == PF_INTEGRATE) {
+#pragma unroll
+                    for (int c = 0; c < 3; ++c) {
+                        if (FIXED) hist_i[c] += sums_i[c];
+                        else hist_f[c] = dadd(hist_f[c], sums_f[c]);
+                    }
+                    t.hist_counts[s] += t.counts[s];
+                } else {
+                    const Effective e = effective_at(t, s, mode, ema, delta_max);
+                    int64_t cnt = np_i64(rint(e.fcnt));
+                    if (mode == PF_FILTER && cnt > 1) cnt = 1;
+                    if (cnt > 0) {
+                        const double denom = np_max(e.fcnt, 1e-300);
+#pragma unroll
+                        for (int c = 0; c < 3; ++c) {
+                            const double nh = dmul(ddiv(e.fsum[c], denom), static_cast<double>(cnt));
+                            if (FIXED) hist_i[c] = np_i64(floor(dadd(nh, 0.5)));
+                            else hist_f[c] = nh;
+                        }
+                        t.hist_counts[s] = cnt;
+                    } else {
+#pragma unroll
+                        for (int c = 0; c < 3; ++c) {
+                            if (FIXED) hist_i[c] = 0;
+                            else hist_f[c] = 0.0;
+                        }
+                        t.hist_counts[s] = 0;
+                    }
+                }
+                if (sample_cap && (mode == PF_INTEGRATE || mode == PF_HYBRID) &&
+                    t.hist_counts[s] > sample_cap) {
+                    const double scale = ddiv(static_cast<double>(sample_cap),
+                                              static_cast<double>(t.hist_counts[s]));
+#pragma unroll
+                    for (int c = 0; c < 3; ++c) {
+                        if (FIXED)
+                            hist_i[c] = np_i64(floor(dadd(dmul(static_cast<double>(hist_i[c]), scale), 0.5)));
+                        else
+                            hist_f[c] = dmul(hist_f[c], scale);
+                    }
+                    t.hist_counts[s] = sample_cap;
+                }
+                // re-prioritise (src/table.py:53-57, 289-290)
+                const int64_t hc = t.hist_counts[s];
+                const uint64_t c8 = static_cast<uint64_t>(hc < 255 ? hc : 255);
+                const uint64_t a24 = static_cast<uint64_t>(age < static_cast<int64_t>(kPrioAgeMask)
+                                                               ? age : static_cast<int64_t>(kPrioAgeMask));
+                const uint64_t prio = ((255ull - c8) << 24) | a24;
+                t.tags[s] = (prio << 32) | (tag & kFpMask);
+            }
+#pragma unroll
+            for (int c = 0; c < 3; ++c) sums_i[c] = 0;  // live generation reset (bits of 0.0)
+            t.counts[s] = 0;
+            t.deltas[s] = 0.0;
+            if (cleared) {
+                t.tags[s] = kEmptyTag;
+#pragma unroll
+                for (int c = 0; c < 3; ++c) hist_i[c] = 0;
+                t.hist_counts[s] = 0;
+                t.last_touch[s] = 0;
+            }
+        }
+    }
+    const unsigned m = __ballot_sync(kFull, cleared);
+    if ((threadIdx.x & 31) == 0 && m) atomicAdd(&block_clears, __popc(m));
+    __syncthreads();
+    if (threadIdx.x == 0 && block_clears && horizon_clears)
+        atomicAdd(reinterpret_cast<unsigned long long *>(horizon_clears),
+                  static_cast<unsigned long long>(block_clears));
+}
+
+__global__ void __launch_bounds__(kThreads)
+count_occupied_kernel(const uint64_t *__restrict__ tags, int64_t capacity, int64_t *out) {
+    __shared__ int block_count;
+    if (threadIdx.x == 0) block_count = 0;
+    __syncthreads();
+    int local = 0;
+    for (int64_t s = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x; s < capacity;
+         s += static_cast<int64_t>(gridDim.x) * blockDim.x)
+        local += __ldg(reinterpret_cast<const unsigned long long *>(tags) + s) != kEmptyTag;
+#pragma unroll
+    for (int off = 16; off > 0; off >>= 1) local += __shfl_xor_sync(kFull, local, off);
+    if ((threadIdx.x & 31) == 0 && local) atomicAdd(&block_count, local);
+    __syncthreads();
+    if (threadIdx.x == 0 && block_count)
+        atomicAdd(reinterpret_cast<unsigned long long *>(out),
+                  static_cast<unsigned long long>(block_count));
+}
+
+__global__ void __launch_bounds__(kThreads)
+check_contributions_kernel(const double *__restrict__ vals, int64_t count, int32_t *bad) {
+    bool any = false;
+    for (int64_t k = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x; k < count;
+         k += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+        const double x = __ldg(vals + k);
+        any |= !(x >= 0.0 && x <= 1.7976931348623157e308);  // NaN, +-inf or negative
+    }
+    if (__any_sync(kFull, any) && (threadIdx.x & 31) == 0) atomicExch(bad, 1);
+}
+
+// ------------------------------------------------------------------ host wrappers
+
+static int accumulate_impl(const char *fn, bool fixed, uint64_t *tags, void *sums, int64_t *counts,
+                           void *hist_sums, int64_t *hist_counts, int64_t *last_touch,
+                           double *deltas, int64_t capacity, const uint64_t *idx,
+                           const uint32_t *fp, const double *vals, int64_t n, int64_t frame,
+                           int32_t probe_limit, int32_t evict_min_age, int32_t ordered,
+                           BatchOut o, void *stream) {
+    pf_table t{tags, sums, counts, hist_sums, hist_counts, last_touch, deltas, capacity,
+               fixed ? PF_SUM_FIXED : PF_SUM_FLOAT, probe_limit, evict_min_age, 0};
+    if (int rc = validate_table(fn, &t)) return rc;
+    if (n < 0) return fail_arg(fn, "negative batch size");
+    if (n == 0) return PF_OK;
+    if (!idx || !fp || !vals) return fail_arg(fn, "idx/fp/vals is NULL");
+    cudaStream_t st = as_stream(stream);
+    if (ordered) {
+        if (fixed) accumulate_ordered_kernel<true><<<1, 32, 0, st>>>(t, idx, fp, vals, n, frame, o);
+        else accumulate_ordered_kernel<false><<<1, 32, 0, st>>>(t, idx, fp, vals, n, frame, o);
+    } else {
+        const unsigned g = blocks_for(n, kThreads);
+        if (fixed) accumulate_kernel<true><<<g, kThreads, 0, st>>>(t, idx, fp, vals, n, frame, o);
+        else accumulate_kernel<false><<<g, kThreads, 0, st>>>(t, idx, fp, vals, n, frame, o);
+    }
+    return check_launch(fn);
+}
+
+}  // namespace pf
+
+using namespace pf;
+
+extern "C" {
+
+int pf_accumulate_fixed(uint64_t *tags, int64_t *sums, int64_t *counts, int64_t *hist_sums,
+                        int64_t *hist_counts, int64_t *last_touch, double *deltas,
+                        int64_t capacity, const uint64_t *idx, const uint32_t *fp,
+                        const double *vals, int64_t n, int64_t frame, int32_t probe_limit,
+                        int32_t evict_min_age, int32_t ordered, uint8_t *status,
+                        int64_t *slots, uint8_t *probe_len, uint64_t *victim_tags,
+                        int64_t *victim_touch, void *stream) {
+    return accumulate_impl("pf_accumulate_fixed", true, tags, sums, counts, hist_sums, hist_counts,
+                           last_touch, deltas, capacity, idx, fp, vals, n, frame, probe_limit,
+                           evict_min_age, ordered,
+                           BatchOut{status, slots, probe_len, victim_tags, victim_touch}, stream);
+}
+
+int pf_accumulate_float(uint64_t *tags, double *sums, int64_t *counts, double *hist_sums,
+                        int64_t *hist_counts, int64_t *last_touch, double *deltas,
+                        int64_t capacity, const uint64_t *idx, const uint32_t *fp,
+                        const double *vals, int64_t n, int64_t frame, int32_t probe_limit,
+                        int32_t evict_min_age, int32_t ordered, uint8_t *status,
+                        int64_t *slots, uint8_t *probe_len, uint64_t *victim_tags,
+                        int64_t *victim_touch, void *stream) {
+    return accumulate_impl("pf_accumulate_float", false, tags, sums, counts, hist_sums,
+                           hist_counts, last_touch, deltas, capacity, idx, fp, vals, n, frame,
+                           probe_limit, evict_min_age, ordered,
+                           BatchOut{status, slots, probe_len, victim_tags, victim_touch}, stream);
+}
+
+int pf_lookup_slots(const uint64_t *tags, int64_t capacity, const uint64_t *idx,
+                    const uint32_t *fp, int64_t n, int32_t probe_limit, int64_t *out,
+                    void *stream) {
+    const char *fn = "pf_lookup_slots";
+    if (!is_pow2(capacity)) return fail_arg(fn, "capacity must be a power of two >= 2");
+    if (probe_limit < 1) return fail_arg(fn, "probe_limit must be >= 1");
+    if (n < 0) return fail_arg(fn, "negative batch size");
+    if (n == 0) return PF_OK;
+    if (!tags || !idx || !fp || !out) return fail_arg(fn, "NULL pointer");
+    lookup_kernel<<<blocks_for(n, kThreads), kThreads, 0, as_stream(stream)>>>(
+        tags, static_cast<uint64_t>(capacity) - 1, probe_limit, idx, fp, n, out);
+    return check_launch(fn);
+}
+
+int pf_make_key_arrays(const pf_config *cfg, const pf_vertices *v, const double *u1,
+                       const double *u2, int32_t level_delta, pf_key_out *out, void *stream) {
+    const char *fn = "pf_make_key_arrays";
+    if (int rc = validate_vertices(fn, v, cfg)) return rc;
+    if (out == nullptr) return fail_arg(fn, "out is NULL");
+    if (v->n == 0) return PF_OK;
+    keys_kernel<<<blocks_for(v->n, kThreads), kThreads, 0, as_stream(stream)>>>(
+        *cfg, *v, u1, u2, 0, 0ull, level_delta, *out);
+    return check_launch(fn);
+}
+
+int pf_vertex_keys(const pf_config *cfg, const pf_vertices *v, uint64_t stream_base,
+                   int32_t level_delta, pf_key_out *out, void *stream) {
+    const char *fn = "pf_vertex_keys";
+    if (int rc = validate_vertices(fn, v, cfg)) return rc;
+    if (out == nullptr) return fail_arg(fn, "out is NULL");
+    if (v->n == 0) return PF_OK;
+    keys_kernel<<<blocks_for(v->n, kThreads), kThreads, 0, as_stream(stream)>>>(
+        *cfg, *v, nullptr, nullptr, 1, stream_base, level_delta, *out);
+    return check_launch(fn);
+}
+
+int pf_hash_arrays(const int64_t *qx, const int64_t *qy, const int64_t *qz, const int64_t *level,
+                   const uint64_t *aux, const uint32_t *normal_fp_bins, int64_t n,
+                   uint64_t *index, uint32_t *fingerprint, void *stream) {
+    const char *fn = "pf_hash_arrays";
+    if (n < 0) return fail_arg(fn, "negative size");
+    if (n == 0) return PF_OK;
+    if (!qx || !qy || !qz || !level || !aux || !index || !fingerprint)
+        return fail_arg(fn, "NULL pointer");
+    hash_kernel<<<blocks_for(n, kThreads), kThreads, 0, as_stream(stream)>>>(
+        qx, qy, qz, level, aux, normal_fp_bins, n, index, fingerprint);
+    return check_launch(fn);
+}
+
+int pf_effective(const pf_table *t, int32_t mode, double ema_alpha, double delta_max,
+                 void *eff_sum, void *eff_count, void *stream) {
+    const char *fn = "pf_effective";
+    if (int rc = validate_table(fn, t)) return rc;
+    if (mode < PF_INTEGRATE || mode > PF_HYBRID) return fail_arg(fn, "unknown temporal mode");
+    if (!eff_sum || !eff_count) return fail_arg(fn, "NULL output");
+    effective_kernel<<<blocks_for(t->capacity, kThreads), kThreads, 0, as_stream(stream)>>>(
+        *t, mode, ema_alpha, delta_max, eff_sum, eff_count);
+    return check_launch(fn);
+}
+
+int pf_begin_frame(const pf_table *t, int64_t frame, int32_t mode, double ema_alpha,
+                   double delta_max, int32_t sample_cap, int64_t *horizon_clears, void *stream) {
+    const char *fn = "pf_begin_frame";
+    if (int rc = validate_table(fn, t)) return rc;
+    if (mode < PF_INTEGRATE || mode > PF_HYBRID) return fail_arg(fn, "unknown temporal mode");
+    const unsigned g = blocks_for(t->capacity, kThreads);
+    if (t->sum_mode == PF_SUM_FIXED)
+        begin_frame_kernel<true><<<g, kThreads, 0, as_stream(stream)>>>(
+            *t, frame, mode, ema_alpha, delta_max, sample_cap, horizon_clears);
+    else
+        begin_frame_kernel<false><<<g, kThreads, 0, as_stream(stream)>>>(
+            *t, frame, mode, ema_alpha, delta_max, sample_cap, horizon_clears);
+    return check_launch(fn);
+}
+
+int pf_check_contributions(const double *vals, int64_t count, int32_t *bad, void *stream) {
+    const char *fn = "pf_check_contributions";
+    if (count < 0 || !bad) return fail_arg(fn, "bad arguments");
+    if (count == 0) return PF_OK;
+    if (!vals) return fail_arg(fn, "vals is NULL");
+    int64_t blocks = (count + kThreads - 1) / kThreads;
+    const int64_t cap = static_cast<int64_t>(sm_count()) * 8;
+    if (blocks > cap) blocks = cap;
+    check_contributions_kernel<<<static_cast<unsigned>(blocks), kThreads, 0, as_stream(stream)>>>(
+        vals, count, bad);
+    return check_launch(fn);
+}
+
+int pf_count_occupied(const uint64_t *tags, int64_t capacity, int64_t *out, void *stream) {
+    const char *fn = "pf_count_occupied";
+    if (!is_pow2(capacity)) return fail_arg(fn, "capacity must be a power of two >= 2");
+    if (!tags || !out) return fail_arg(fn, "NULL pointer");
+    int64_t blocks = (capacity + kThreads - 1) / kThreads;
+    const int64_t cap_blocks = static_cast<int64_t>(sm_count()) * 8;
+    if (blocks > cap_blocks) blocks = cap_blocks;
+    count_occupied_kernel<<<static_cast<unsigned>(blocks), kThreads, 0, as_stream(stream)>>>(
+        tags, capacity, out);
+    return check_launch(fn);
+}
+
+}  // extern "C"

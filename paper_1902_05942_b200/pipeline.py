@@ -1,0 +1,359 @@
+"""Per-frame filter orchestration on the device (src/pipeline.py, tracer excluded).
+
+accumulate_phase launches ONE fused kernel per frame (keys for the fine and coarse
+tables + warp-merged inserts); resolve_phase launches the fine-rung kernel, the
+fallback kernel over the compacted low-count rows and the image finalisation.
+Nothing synchronises with the host until a statistic or host array is read.
+
+Ladder (src/pipeline.py:1-15): fine voxel >= threshold -> 3x3x3 neighbourhood ->
+coarse voxel -> any neighbourhood / coarse samples -> unfiltered contribution.
+"""
+
+from __future__ import annotations
+
+import ctypes
+from dataclasses import dataclass, field
+
+import numpy as np
+import torch
+
+from . import _lib, rng
+from .keys import FilterConfig, KeyArrays, _empty_keys, _key_out, as_f64, as_i64, device, \
+    vertices_c
+from .table import EvictionEvent, VoxelTable, _AGE_MASK
+
+SOURCE_FINE = 0
+SOURCE_NEIGHBORHOOD = 1
+SOURCE_COARSE = 2
+SOURCE_UNFILTERED = 3
+
+_FIELDS = ("position", "normal", "omega_r", "contribution", "throughput", "pixel", "sample",
+           "layer_id", "camera_distance")
+
+
+@dataclass
+class VertexStream:
+    """Struct-of-arrays vertex record (src/tracer.py:732-767) as CUDA tensors."""
+
+    position: torch.Tensor
+    normal: torch.Tensor
+    omega_r: torch.Tensor
+    contribution: torch.Tensor
+    throughput: torch.Tensor
+    pixel: torch.Tensor
+    sample: torch.Tensor
+    layer_id: torch.Tensor
+    camera_distance: torch.Tensor
+
+    def __len__(self) -> int:
+        return int(self.pixel.shape[0])
+
+    @property
+    def path_id(self) -> torch.Tensor:
+        return (self.sample << 32) | self.pixel
+
+    @classmethod
+    def from_any(cls, vs) -> "VertexStream":
+        """Upload a reference VertexStream (numpy fields) or pass a device one through."""
+        if isinstance(vs, cls):
+            return vs
+        vec = {"position", "normal", "omega_r", "contribution", "throughput"}
+        return cls(**{f: (as_f64(getattr(vs, f), 3) if f in vec else
+                          as_f64(getattr(vs, f)).reshape(-1) if f == "camera_distance" else
+                          as_i64(getattr(vs, f)).reshape(-1)) for f in _FIELDS})
+
+    def select(self, rows) -> "VertexStream":
+        r = as_i64(rows).reshape(-1)
+        return VertexStream(*(getattr(self, f)[r] for f in _FIELDS))
+
+    def c_struct(self):
+        return vertices_c(self.position, self.normal, self.omega_r, self.layer_id,
+                          self.camera_distance, pixel=self.pixel, sample=self.sample,
+                          contribution=self.contribution, throughput=self.throughput)
+
+
+@dataclass
+class ResolveReport:
+    source: torch.Tensor
+    image: torch.Tensor
+    means: torch.Tensor | None = None
+
+    @property
+    def counts(self) -> dict[str, int]:
+        c = torch.bincount(self.source.to(torch.int64), minlength=4).cpu().numpy()
+        return {"fine_voxel": int(c[0]), "neighborhood": int(c[1]),
+                "coarse_voxel": int(c[2]), "unfiltered": int(c[3])}
+
+
+class FrameStats:
+    """Frame statistics (src/pipeline.py:51-85) backed by a device counter array;
+    values synchronise on first read."""
+
+    _SCALARS = ("frame", "n_vertices", "probe_failures", "coarse_probe_failures", "collisions",
+                "evictions", "horizon_clears", "occupancy_fine", "occupancy_coarse",
+                "time_trace", "time_accumulate", "time_resolve", "time_total")
+
+    def __init__(self, frame: int = 0, n_vertices: int = 0, counters: torch.Tensor | None = None):
+        self.frame = frame
+        self.n_vertices = n_vertices
+        self.counters = counters
+        self._host = None
+        self.evictions = 0
+        self.horizon_clears = 0
+        self.occupancy_fine = 0.0
+        self.occupancy_coarse = 0.0
+        self.source_counts: dict[str, int] = {}
+        self.time_trace = 0.0
+        self.time_accumulate = 0.0
+        self.time_resolve = 0.0
+        self.time_total = 0.0
+
+    def _c(self) -> np.ndarray:
+        if self._host is None:
+            self._host = (self.counters.cpu().numpy() if self.counters is not None
+                          else np.zeros(_lib.STAT_COUNT, np.int64))
+        return self._host
+
+    @property
+    def probe_failures(self) -> int:
+        return int(self._c()[_lib.STAT_PROBE_FAILURES])
+
+    @property
+    def coarse_probe_failures(self) -> int:
+        return int(self._c()[_lib.STAT_COARSE_PROBE_FAILURES])
+
+    @property
+    def collisions(self) -> int:
+        return int(self._c()[_lib.STAT_PROBE_LEN_SUM]) - self.n_vertices if self.n_vertices else 0
+
+    @property
+    def probe_histogram(self) -> dict[int, int]:
+        h = self._c()[_lib.STAT_HIST_BASE:_lib.STAT_HIST_BASE + 256]
+        return {int(k): int(v) for k, v in enumerate(h) if v and k}
+
+    def lines(self) -> list[str]:
+        out = [f"frame={self.frame}", f"vertices={self.n_vertices}",
+               f"probe_failures={self.probe_failures}",
+               f"coarse_probe_failures={self.coarse_probe_failures}",
+               f"collisions={self.collisions}", f"evictions={self.evictions}",
+               f"horizon_clears={self.horizon_clears}",
+               f"occupancy_fine={self.occupancy_fine:.6f}",
+               f"occupancy_coarse={self.occupancy_coarse:.6f}"]
+        for k in sorted(self.probe_histogram):
+            out.append(f"probe_hist_{k}={self.probe_histogram[k]}")
+        for k, v in self.source_counts.items():
+            out.append(f"source_{k}={v}")
+        out += [f"time_trace={self.time_trace:.6f}", f"time_accumulate={self.time_accumulate:.6f}",
+                f"time_resolve={self.time_resolve:.6f}", f"time_total={self.time_total:.6f}"]
+        return out
+
+
+@dataclass
+class FrameState:
+    """Persistent fine/coarse tables (src/pipeline.py:88-105)."""
+
+    fine: VoxelTable
+    coarse: VoxelTable | None
+    frame: int = 0
+    prev_fine_keys: KeyArrays | None = None
+    prev_coarse_keys: KeyArrays | None = None
+    prev_seed: int = 0
+    prev_spp: int = 0
+    scratch: dict = field(default_factory=dict)
+
+    @classmethod
+    def from_config(cls, cfg: FilterConfig, backend: str | None = None,
+                    ordered: bool = False) -> "FrameState":
+        fine = VoxelTable.from_config(cfg, backend, ordered)
+        coarse = VoxelTable.from_config(cfg, backend, ordered) if cfg.multi_level else None
+        return cls(fine, coarse)
+
+    def buffer(self, name: str, shape, dtype) -> torch.Tensor:
+        """Reusable device scratch (caching allocator friendly, no per-frame memsets)."""
+        n = int(np.prod(shape))
+        b = self.scratch.get(name)
+        if b is None or b.numel() < n or b.dtype != dtype:
+            b = torch.empty(max(n, 1), dtype=dtype, device=device())
+            self.scratch[name] = b
+        return b[:n].view(*shape) if n else b[:0]
+
+
+class LazyKeyArrays:
+    """KeyArrays that are only materialised (one key-kernel launch) when read.
+
+    accumulate_phase returns these: the fused insert kernel never writes per-vertex
+    keys to HBM, yet the reference API (src/pipeline.py:175) hands keys back."""
+
+    def __init__(self, vs: VertexStream, cfg: FilterConfig, seed: int, stream_tag: int,
+                 level_delta: int):
+        self._args = (vs, cfg, seed, stream_tag, level_delta)
+        self._keys: KeyArrays | None = None
+
+    def materialize(self) -> KeyArrays:
+        if self._keys is None:
+            self._keys = vertex_keys(*self._args)
+        return self._keys
+
+    def __len__(self):
+        return len(self._args[0])
+
+    def __getattr__(self, name):
+        if name.startswith("_"):
+            raise AttributeError(name)
+        return getattr(self.materialize(), name)
+
+
+def vertex_keys(vertices, cfg: FilterConfig, seed: int,
+                stream_tag: int = rng.STREAM_JITTER_ACCUM, level_delta: int = 0) -> KeyArrays:
+    """Key arrays of a vertex stream with the given jitter stream (src/pipeline.py:126-135)."""
+    vs = VertexStream.from_any(vertices)
+    n = len(vs)
+    out = _empty_keys(n)
+    if n == 0:
+        return out
+    v, keep = vs.c_struct()
+    ko = _key_out(out)
+    _lib.call("pf_vertex_keys", ctypes.byref(cfg.to_c()), ctypes.byref(v),
+              rng.stream_base(seed, stream_tag), int(level_delta), ctypes.byref(ko),
+              _lib.stream_handle())
+    del keep
+    return out
+
+
+def _check_contributions(vs: VertexStream, state: "FrameState"):
+    """accumulate_batch's input check (src/table.py:127-129) as one device pass."""
+    check_contributions(vs.contribution, state.buffer("bad_flag", (1,), torch.int32))
+
+
+def check_contributions(vals: torch.Tensor, flag: torch.Tensor):
+    flag.zero_()
+    _lib.call("pf_check_contributions", vals.data_ptr(), int(vals.numel()), flag.data_ptr(),
+              _lib.stream_handle())
+    if int(flag.item()):
+        raise ValueError("contributions must be finite and non-negative")
+
+
+def accumulate_phase(vertices, cfg: FilterConfig, state: FrameState, frame: int, seed: int,
+                     threads: int = 1, validate: bool = True):
+    """Insert all vertices into the fine and coarse tables (src/pipeline.py:152-175).
+
+    Returns (fine keys, coarse keys, stats); keys are lazy (computed on first read)."""
+    vs = VertexStream.from_any(vertices)
+    n = len(vs)
+    counters = state.buffer("stats_acc", (_lib.STAT_COUNT,), torch.int64)
+    counters.zero_()
+    stats = FrameStats(frame=frame, n_vertices=n, counters=counters)
+    fine_keys = LazyKeyArrays(vs, cfg, seed, rng.STREAM_JITTER_ACCUM, 0)
+    coarse_keys = None
+    if n == 0:
+        return fine_keys, coarse_keys, stats
+    if validate:
+        _check_contributions(vs, state)
+    if state.coarse is not None:
+        coarse_keys = LazyKeyArrays(vs, cfg, seed, rng.STREAM_JITTER_ACCUM, cfg.coarse_delta)
+    if state.fine.ordered:
+        return _accumulate_ordered(vs, cfg, state, frame, seed, stats, fine_keys, coarse_keys)
+    events = state.buffer("events", (n, 4), torch.int64)
+    ev_count = state.buffer("event_count", (1,), torch.int64)
+    ev_count.zero_()
+    v, keep = vs.c_struct()
+    ft = state.fine.c_table()
+    ct = state.coarse.c_table() if state.coarse is not None else None
+    _lib.call("pf_insert_frame", ctypes.byref(cfg.to_c()), ctypes.byref(v), ctypes.byref(ft),
+              ctypes.byref(ct) if ct is not None else None,
+              rng.stream_base(seed, rng.STREAM_JITTER_ACCUM), int(frame), counters.data_ptr(),
+              events.data_ptr(), ev_count.data_ptr(), n, _lib.stream_handle())
+    del keep
+    ev_snapshot = (events, ev_count.clone())
+
+    def drain(snap=ev_snapshot, frame=frame):
+        ev, cnt = snap
+        k = int(cnt.item())
+        if k == 0:
+            return []
+        rows = ev[:k].cpu().numpy()
+        rows = rows[np.argsort(rows[:, 0], kind="stable")]
+        out = []
+        for _, slot, vtag, vtouch in rows:
+            age = (int(np.int64(vtag).view(np.uint64)) >> 32) & _AGE_MASK
+            out.append(EvictionEvent(frame, int(slot), age, int(vtouch)))
+        return out
+
+    state.fine._add_pending_events(drain)
+    # the event buffer is reused next frame: detach this frame's copy
+    state.scratch.pop("events", None)
+    return fine_keys, coarse_keys, stats
+
+
+def _accumulate_ordered(vs, cfg, state, frame, seed, stats, fine_keys, coarse_keys):
+    """Sequential-order variant (tables created with ordered=True): materialise keys,
+    then the in-order batch insert, reproducing the reference's threads=1 layout."""
+    c = stats.counters
+    fk = fine_keys.materialize()
+    st, _, pl = state.fine.accumulate_batch(fk.index, fk.fingerprint, vs.contribution, frame)
+    c[_lib.STAT_PROBE_FAILURES] = (st == 2).sum()
+    c[_lib.STAT_EVICTIONS] = (st == 1).sum()
+    pl64 = pl.to(torch.int64)
+    c[_lib.STAT_PROBE_LEN_SUM] = pl64.sum()
+    c[_lib.STAT_HIST_BASE:_lib.STAT_HIST_BASE + 256] += torch.bincount(pl64, minlength=256)[:256]
+    if state.coarse is not None:
+        ck = coarse_keys.materialize()
+        cst, _, _ = state.coarse.accumulate_batch(ck.index, ck.fingerprint, vs.contribution, frame)
+        c[_lib.STAT_COARSE_PROBE_FAILURES] = (cst == 2).sum()
+        c[_lib.STAT_COARSE_EVICTIONS] = (cst == 1).sum()
+    return fine_keys, coarse_keys, stats
+
+
+def resolve_phase(vertices, cfg: FilterConfig, state: FrameState, frame: int, seed: int,
+                  spp: int, base_image, fine_keys=None, want_means: bool = True):
+    """Per-vertex filtered means composited onto the base image (src/pipeline.py:207-283).
+
+    Returns (image, ResolveReport) as device tensors.  With jitter disabled the
+    lookup keys equal the accumulate keys, which the kernel recomputes in registers
+    instead of reading `fine_keys` back from HBM."""
+    vs = VertexStream.from_any(vertices)
+    base = as_f64(base_image)
+    h, w = int(base.shape[0]), int(base.shape[1])
+    n = len(vs)
+    dev = base.device
+    source = torch.empty(n, dtype=torch.uint8, device=dev)
+    chosen = torch.empty((n, 3), dtype=torch.float64, device=dev) if want_means else None
+    image = torch.empty_like(base)
+    flat = state.buffer("flat", (h * w, 3), torch.float64)
+    work = state.buffer("work", (max(n, 1), 6), torch.int64)
+    work_count = state.buffer("work_count", (1,), torch.int64)
+    counters = state.buffer("stats_res", (_lib.STAT_COUNT,), torch.int64)
+    counters.zero_()
+    v, keep = vs.c_struct()
+    ft = state.fine.c_table()
+    ct = state.coarse.c_table() if state.coarse is not None else None
+    coarse_tag = rng.STREAM_JITTER_LOOKUP if cfg.jitter else rng.STREAM_JITTER_ACCUM
+    _lib.call("pf_resolve_frame", ctypes.byref(cfg.to_c()), ctypes.byref(v), ctypes.byref(ft),
+              ctypes.byref(ct) if ct is not None else None,
+              rng.stream_base(seed, rng.STREAM_JITTER_LOOKUP), rng.stream_base(seed, coarse_tag),
+              int(spp), base.data_ptr(), h * w, image.data_ptr(), flat.data_ptr(),
+              work.data_ptr(), work_count.data_ptr(), source.data_ptr(), _lib.ptr(chosen),
+              counters.data_ptr(), _lib.stream_handle())
+    del keep
+    report = ResolveReport(source, image, chosen)
+    report.counters = counters
+    return image, report
+
+
+def filter_frame(vertices, base_image, cfg: FilterConfig, state: FrameState, spp: int,
+                 seed: int, validate: bool = True):
+    """One frame of the filter without the tracer: begin_frame on both tables,
+    accumulate, resolve (src/pipeline.py:321-363 minus trace/hybrid replay)."""
+    frame = state.frame
+    state.fine.begin_frame(frame, cfg)
+    if state.coarse is not None:
+        state.coarse.begin_frame(frame, cfg)
+    fine_keys, coarse_keys, stats = accumulate_phase(vertices, cfg, state, frame, seed,
+                                                     validate=validate)
+    image, report = resolve_phase(vertices, cfg, state, frame, seed, spp, base_image, fine_keys)
+    state.prev_fine_keys = fine_keys
+    state.prev_coarse_keys = coarse_keys
+    state.prev_seed = seed
+    state.prev_spp = spp
+    state.frame = frame + 1
+    return image, report, stats

@@ -1,0 +1,303 @@
+"""Generate the golden fixtures in tests/golden/ by running the REFERENCE itself.
+
+Run in the build container (where the reference imports), never on the GPU box:
+
+    PF_REFERENCE=baseline/_ref python tests/golden/make_golden.py
+
+PF_REFERENCE points at a directory containing the reference package `pathfilter`
+(the contract's `pip install --target baseline/_ref` of /root/reference/pkg, or a
+`setup.py build_ext --inplace` copy's src/).  Every array here is produced by the
+reference's own code path (render_frame / accumulate_phase / resolve_phase /
+VoxelTable / make_key_arrays); nothing is computed by this repo.
+"""
+
+from __future__ import annotations
+
+import json
+import os
+import platform
+import sys
+
+import numpy as np
+
+HERE = os.path.dirname(os.path.abspath(__file__))
+REF = os.environ.get("PF_REFERENCE", os.path.join(HERE, "..", "..", "baseline", "_ref"))
+sys.path.insert(0, os.path.abspath(REF))
+
+import pathfilter as pf  # noqa: E402
+from pathfilter import rng as prng  # noqa: E402
+from pathfilter.keys import FilterConfig, hash_arrays, make_key_arrays  # noqa: E402
+from pathfilter.pipeline import FrameState, _jitter_draws, accumulate_phase, render_frame, \
+    resolve_phase  # noqa: E402
+from pathfilter.scene import parse_scene  # noqa: E402
+from pathfilter.tracer import TraceOptions, VertexStream, trace  # noqa: E402
+
+assert pf.BACKEND == "native", "build the reference's Cython extension first"
+
+STREAM_FIELDS = ("position", "normal", "omega_r", "contribution", "throughput", "pixel",
+                 "sample", "layer_id", "camera_distance")
+TABLE_FIELDS = ("tags", "sums", "counts", "hist_sums", "hist_counts", "last_touch", "deltas")
+
+CLOSED_BOX = """camera 2.75 2.75 0.6  2.75 2.75 5.5  0 1 0  1.2 {w} {h}
+material white 0.73 0.73 0.73
+material red 0.65 0.05 0.05
+material green 0.12 0.45 0.15
+material lamp 0 0 0
+quad 0 0 0  0 0 5.5  5.5 0 5.5  5.5 0 0  white
+quad 0 5.5 0  5.5 5.5 0  5.5 5.5 5.5  0 5.5 5.5  white
+quad 0 0 5.5  0 5.5 5.5  5.5 5.5 5.5  5.5 0 5.5  white
+quad 0 0 0  0 5.5 0  0 5.5 5.5  0 0 5.5  red
+quad 5.5 0 0  5.5 0 5.5  5.5 5.5 5.5  5.5 5.5 0  green
+quad 0 0 0  5.5 0 0  5.5 5.5 0  0 5.5 0  white
+quad 1.925 5.49 1.925  3.575 5.49 1.925  3.575 5.49 3.575  1.925 5.49 3.575  lamp emit 17 13 6
+"""
+
+
+def cfg_dict(cfg: FilterConfig) -> str:
+    return json.dumps({k: getattr(cfg, k) for k in cfg.__dataclass_fields__})
+
+
+def put_stream(out: dict, prefix: str, vs: VertexStream):
+    for f in STREAM_FIELDS:
+        out[f"{prefix}{f}"] = np.ascontiguousarray(getattr(vs, f))
+
+
+def put_table(out: dict, prefix: str, t):
+    for f in TABLE_FIELDS:
+        out[f"{prefix}{f}"] = getattr(t, f).copy()
+    out[f"{prefix}horizon_clears"] = np.int64(t.horizon_clears)
+    ev = t.eviction_events
+    out[f"{prefix}events"] = np.array([[e.frame, e.slot, e.victim_age, e.victim_last_touch]
+                                       for e in ev], np.int64).reshape(-1, 4)
+
+
+def put_keys(out: dict, prefix: str, k):
+    for f in ("qx", "qy", "qz", "level", "aux", "index", "fingerprint", "jittered"):
+        out[f"{prefix}{f}"] = np.ascontiguousarray(getattr(k, f))
+
+
+def next_pow2(n: int) -> int:
+    return 1 << (int(n) - 1).bit_length()
+
+
+def save(name: str, out: dict):
+    out["meta"] = np.array(json.dumps({
+        "generator": "tests/golden/make_golden.py", "reference": "pathfilter " + pf.__version__,
+        "backend": pf.BACKEND, "numpy": np.__version__, "python": platform.python_version(),
+        "libc": " ".join(platform.libc_ver())}))
+    path = os.path.join(HERE, name)
+    np.savez_compressed(path, **out)
+    print(f"{name}: {os.path.getsize(path) / 1e6:.2f} MB")
+
+
+def random_stream(n, seed, n_keys=None, spread=100.0):
+    """The reference conftest.random_stream recipe (pkg/tests/conftest.py:28-46),
+    plus random layers and exit directions so aux options are exercised."""
+    r = np.random.default_rng(seed)
+    n_keys = n_keys or max(4, n // 8)
+    pts = r.uniform(-spread, spread, (n_keys, 3))
+    pick = r.integers(0, n_keys, n)
+    normals = r.normal(size=(n, 3))
+    normals /= np.linalg.norm(normals, axis=1, keepdims=True)
+    om = r.normal(size=(n, 3))
+    om /= np.linalg.norm(om, axis=1, keepdims=True)
+    return VertexStream(position=pts[pick], normal=normals, omega_r=om,
+                        contribution=r.uniform(0.0, 4.0, (n, 3)), throughput=np.ones((n, 3)),
+                        pixel=r.integers(0, 4096, n), sample=r.integers(0, 3, n),
+                        layer_id=r.integers(0, 3, n), camera_distance=r.uniform(1.0, 50.0, n))
+
+
+def gen_rng_hash():
+    out = {}
+    ids = np.concatenate([np.arange(64, dtype=np.uint64),
+                          np.random.default_rng(3).integers(0, 2**63, 192).astype(np.uint64)
+                          * np.uint64(2) + np.uint64(1)])
+    seeds = [0, 1, 999, 2**63 + 12345, 2**64 - 1]
+    for si, seed in enumerate(seeds):
+        for stream in (1, 2, 3):
+            for dim in (0, 1):
+                out[f"draw_u64_{si}_{stream}_{dim}"] = prng.draw_u64_array(seed, stream, ids, 0, dim)
+                out[f"draw_unit_{si}_{stream}_{dim}"] = prng.draw_unit_array(seed, stream, ids, 0, dim)
+    out["draw_ids"] = ids
+    out["draw_seeds"] = np.array(seeds, dtype=np.uint64)
+    r = np.random.default_rng(11)
+    n = 4096
+    q = r.integers(-2**40, 2**40, (n, 3))
+    q[:8] = [[0, 0, 0], [1, 0, 0], [-1, 2, -3], [6, -3, 1], [123456, -654321, 42], [0, 0, 0],
+             [5, 5, 5], [-1099511627776, 1099511627776, -7]]
+    lvl = r.integers(0, 32, n)
+    lvl[:8] = [0, 0, 0, 0, 7, 31, 3, 12]
+    aux = r.integers(0, 2**32, n).astype(np.uint64)
+    aux[:8] = [0, 0, 0, 0, 0, 0, 16909060, 63]
+    idx, fp = hash_arrays(q[:, 0], q[:, 1], q[:, 2], lvl, aux)
+    bins = r.integers(0, 64, n).astype(np.uint32)
+    idx2, fp2 = hash_arrays(q[:, 0], q[:, 1], q[:, 2], lvl, aux, bins)
+    out.update(hq=q, hlevel=lvl, haux=aux, hindex=idx, hfp=fp, hbins=bins, hindex_b=idx2,
+               hfp_b=fp2)
+    save("rng_hash.npz", out)
+
+
+def gen_keys_random():
+    out = {}
+    vs = random_stream(3000, seed=7)
+    put_stream(out, "v_", vs)
+    variants = {
+        "default": FilterConfig(base_voxel=0.02, footprint_scale=0.003),
+        "aux": FilterConfig(base_voxel=0.02, footprint_scale=0.003, include_incident_angle=True,
+                            include_layer=True, normal_bins=6),
+        "nfp": FilterConfig(base_voxel=0.05, footprint_scale=0.001, normal_in_fingerprint=True),
+        "nojit": FilterConfig(base_voxel=0.02, footprint_scale=0.003, jitter=False,
+                              include_normal=False),
+    }
+    seed = 4242
+    for name, cfg in variants.items():
+        out[f"{name}_cfg"] = np.array(cfg_dict(cfg))
+        for tag, stream, delta in (("fine", 2, 0), ("coarse", 2, 2), ("lookup", 3, 0)):
+            u1 = u2 = None
+            if cfg.jitter:
+                u1, u2 = _jitter_draws(stream, vs, seed)
+                out[f"{name}_{tag}_u1"] = u1
+                out[f"{name}_{tag}_u2"] = u2
+            k = make_key_arrays(vs.position, vs.normal, vs.omega_r, vs.layer_id,
+                                vs.camera_distance, cfg, u1, u2, delta)
+            put_keys(out, f"{name}_{tag}_", k)
+    out["seed"] = np.uint64(seed)
+    save("keys_random.npz", out)
+
+
+def frame_outputs(out, prefix, state, fine_keys, coarse_keys, image, report, stats):
+    put_table(out, f"{prefix}fine_", state.fine)
+    if state.coarse is not None:
+        put_table(out, f"{prefix}coarse_", state.coarse)
+    put_keys(out, f"{prefix}fk_", fine_keys)
+    if coarse_keys is not None:
+        put_keys(out, f"{prefix}ck_", coarse_keys)
+    out[f"{prefix}image"] = image
+    out[f"{prefix}source"] = report.source
+    out[f"{prefix}chosen"] = report.means
+    out[f"{prefix}stats"] = np.array("\n".join(l for l in stats.lines() if not l.startswith("time_")))
+
+
+def gen_frame_cornell():
+    out = {}
+    scene = pf.cornell_box(128, 128)
+    for mode in ("fixed", "float"):
+        cfg = FilterConfig(capacity=next_pow2(2 * 128 * 128), sum_mode=mode)
+        cfg_f = cfg.for_camera(scene.camera.fov, scene.camera.height)
+        state = FrameState.from_config(cfg_f)
+        res = render_frame(scene, cfg, state, spp=1, seed=1, threads=1)
+        if mode == "fixed":
+            put_stream(out, "v_", res.trace_result.vertices)
+            out["base"] = res.trace_result.base_image
+        out[f"{mode}_cfg"] = np.array(cfg_dict(cfg_f))
+        frame_outputs(out, f"{mode}_", state, res.fine_keys, res.coarse_keys, res.filtered,
+                      res.report, res.stats)
+    out["seed"] = np.uint64(1)
+    out["spp"] = np.int64(1)
+    save("frame_cornell128.npz", out)
+
+
+def box_stream(w, h, seed=1):
+    scene = parse_scene(CLOSED_BOX.format(w=w, h=h))
+    parts, base = [], None
+    for k in range(1, 5):
+        tr = trace(scene, spp=1, seed=seed, options=TraceOptions(select_k=k, rr_start=9), threads=1)
+        vs = tr.vertices
+        vs.sample = vs.sample + (k - 1)
+        parts.append(vs)
+        if k == 1:
+            base = tr.base_image
+    return scene, VertexStream.concat(parts), base
+
+
+def gen_frame_box4():
+    out = {}
+    w, h = 80, 45
+    scene, vs, base = box_stream(w, h)
+    put_stream(out, "v_", vs)
+    out["base"] = base
+    seed = 1
+    for mode in ("fixed", "float"):
+        cfg = FilterConfig(capacity=next_pow2(2 * w * h), sum_mode=mode).for_camera(
+            scene.camera.fov, scene.camera.height)
+        state = FrameState.from_config(cfg)
+        state.fine.begin_frame(0, cfg)
+        state.coarse.begin_frame(0, cfg)
+        fk, ck, stats = accumulate_phase(vs, cfg, state, 0, seed)
+        image, report = resolve_phase(vs, cfg, state, 0, seed, 1, base, fk)
+        stats.source_counts = report.counts
+        out[f"{mode}_cfg"] = np.array(cfg_dict(cfg))
+        frame_outputs(out, f"{mode}_", state, fk, ck, image, report, stats)
+    out["seed"] = np.uint64(seed)
+    out["spp"] = np.int64(1)
+    save("frame_box4.npz", out)
+
+
+def gen_temporal():
+    """Corridor pan with a 128-slot table: claims, evictions and horizon clears."""
+    out = {}
+    frames = 10
+    scene = pf.scene.corridor(24, 24, frames=frames)
+    for mode in ("integrate", "filter"):
+        cfg = FilterConfig(capacity=128, probe_limit=4, temporal_mode=mode, evict_horizon=3,
+                           evict_min_age=1, sample_cap=24)
+        cfg_f = cfg.for_camera(scene.camera.fov, scene.camera.height)
+        state = FrameState.from_config(cfg_f)
+        out[f"{mode}_cfg"] = np.array(cfg_dict(cfg_f))
+        for f in range(frames):
+            res = render_frame(scene, cfg, state, spp=1, seed=5, threads=1)
+            p = f"{mode}_f{f}_"
+            if mode == "integrate":
+                put_stream(out, f"f{f}_v_", res.trace_result.vertices)
+                out[f"f{f}_base"] = res.trace_result.base_image
+                out[f"f{f}_seed"] = np.uint64(state.prev_seed)
+            put_table(out, f"{p}fine_", state.fine)
+            put_table(out, f"{p}coarse_", state.coarse)
+            out[f"{p}image"] = res.filtered
+            out[f"{p}source"] = res.report.source
+            out[f"{p}chosen"] = res.report.means
+    out["frames"] = np.int64(frames)
+    save("temporal_corridor.npz", out)
+
+
+def gen_hybrid():
+    """effective()/begin_frame() in hybrid and filter modes with nonzero deltas."""
+    from pathfilter.table import VoxelTable
+    out = {}
+    vs = random_stream(2000, seed=9, n_keys=300, spread=2.0)
+    for sm in ("fixed", "float"):
+        cfg = FilterConfig(capacity=1024, probe_limit=8, temporal_mode="hybrid", sample_cap=5,
+                           sum_mode=sm, base_voxel=0.05, footprint_scale=0.002)
+        keys = make_key_arrays(vs.position, vs.normal, vs.omega_r, vs.layer_id,
+                               vs.camera_distance, cfg)
+        t = VoxelTable.from_config(cfg)
+        r = np.random.default_rng(1)
+        for f in range(4):
+            t.begin_frame(f, cfg)
+            part = slice(f * 400, f * 400 + 900)
+            t.accumulate_batch(keys.index[part], keys.fingerprint[part], vs.contribution[part], f)
+            occ = np.nonzero(t.tags != np.uint64(0xFFFFFFFF00000000))[0]
+            t.set_deltas(occ, r.uniform(0.0, 0.8, len(occ)))
+            put_table(out, f"{sm}_f{f}_pre_", t)
+            for mode in ("integrate", "filter", "hybrid"):
+                es, ec = t.effective(mode, 0.7, 0.5)
+                out[f"{sm}_f{f}_eff_{mode}_sum"] = es
+                out[f"{sm}_f{f}_eff_{mode}_cnt"] = ec
+        for mode in ("integrate", "filter", "hybrid"):
+            t2 = VoxelTable.from_config(cfg)
+            for k in TABLE_FIELDS:
+                getattr(t2, k)[...] = out[f"{sm}_f3_pre_{k}"]
+            c2 = FilterConfig(**{**{k: getattr(cfg, k) for k in cfg.__dataclass_fields__},
+                                 "temporal_mode": mode, "ema_alpha": 0.7})
+            t2.begin_frame(5, c2)
+            put_table(out, f"{sm}_post_{mode}_", t2)
+        out[f"{sm}_cfg"] = np.array(cfg_dict(cfg))
+    save("hybrid_table.npz", out)
+
+
+if __name__ == "__main__":
+    which = sys.argv[1:] or ["rng", "keys", "cornell", "box4", "temporal", "hybrid"]
+    fns = {"rng": gen_rng_hash, "keys": gen_keys_random, "cornell": gen_frame_cornell,
+           "box4": gen_frame_box4, "temporal": gen_temporal, "hybrid": gen_hybrid}
+    for w in which:
+        fns[w]()

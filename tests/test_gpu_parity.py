@@ -1,0 +1,491 @@
+"""GPU parity: the sm_100a kernels (through the C ABI) against the reference's golden
+fixtures and the CPU oracle.  Bar: bit-exact keys, statuses, per-key table
+contents, sources and fixed-point means; float-mode sums within 1e-12 relative
+(order of float atomics); jittered positions within a few ulp (CUDA sin/cos)."""
+
+import numpy as np
+import pytest
+import torch
+
+from conftest import TABLE_FIELDS, golden_cfg, golden_stream, golden_table, load_golden
+
+pytestmark = pytest.mark.gpu
+
+EMPTY = np.uint64(0xFFFFFFFF00000000)
+KEY_FIELDS = ("qx", "qy", "qz", "level", "aux", "index", "fingerprint")
+
+
+def _np(t):
+    return t.cpu().numpy() if isinstance(t, torch.Tensor) else np.asarray(t)
+
+
+def canon(st: dict, fixed: bool = True):
+    """Order-free view of a table: sorted rows of every occupied slot."""
+    occ = np.nonzero(st["tags"] != EMPTY)[0]
+    rows = []
+    for s in occ:
+        rows.append((int(st["tags"][s]), int(st["counts"][s]), int(st["hist_counts"][s]),
+                     int(st["last_touch"][s]), tuple(st["sums"][s].tolist()),
+                     tuple(st["hist_sums"][s].tolist())))
+    return sorted(rows)
+
+
+def assert_tables_equal(got: dict, want: dict, ordered: bool, float_rtol=0.0):
+    if ordered:
+        for f in TABLE_FIELDS:
+            if float_rtol and f in ("sums", "hist_sums") and got[f].dtype == np.float64:
+                np.testing.assert_allclose(got[f], want[f], rtol=float_rtol, atol=0)
+            else:
+                assert np.array_equal(got[f], want[f]), f
+        return
+    a, b = canon(got), canon(want)
+    assert len(a) == len(b)
+    for ra, rb in zip(a, b):
+        assert ra[:4] == rb[:4]
+        if float_rtol:
+            np.testing.assert_allclose(ra[4] + ra[5], rb[4] + rb[5], rtol=float_rtol, atol=0)
+        else:
+            assert ra[4:] == rb[4:]
+
+
+def cfg_of(pf, d, key, **over):
+    c = golden_cfg(d, key)
+    c.update(over)
+    return pf.FilterConfig(**c)
+
+
+# ------------------------------------------------------------------ hashing / keys
+
+def test_reference_hash_vectors(gpu):
+    from test_oracle_golden import REFERENCE_GOLDEN_VECTORS
+    for (qx, qy, qz, lv, aux), index, fp in REFERENCE_GOLDEN_VECTORS:
+        h = gpu.hashes(gpu.CellKey(qx, qy, qz, lv, aux))
+        assert (h.index, h.fingerprint) == (index, fp)
+    assert gpu.hashes(gpu.CellKey(4, 4, 4, 1, 0), normal_fp_bin=5).fingerprint & 0x3F == 5
+
+
+def test_hash_arrays_golden(gpu):
+    from paper_1902_05942_b200.keys import u32_numpy, u64_numpy
+    d = load_golden("rng_hash.npz")
+    q = d["hq"]
+    i, f = gpu.hash_arrays(q[:, 0], q[:, 1], q[:, 2], d["hlevel"], d["haux"])
+    assert np.array_equal(u64_numpy(i), d["hindex"]) and np.array_equal(u32_numpy(f), d["hfp"])
+    i, f = gpu.hash_arrays(q[:, 0], q[:, 1], q[:, 2], d["hlevel"], d["haux"], d["hbins"])
+    assert np.array_equal(u64_numpy(i), d["hindex_b"]) and np.array_equal(u32_numpy(f), d["hfp_b"])
+
+
+def test_never_sentinel_in_bulk(gpu):
+    from paper_1902_05942_b200.keys import u32_numpy
+    r = np.random.default_rng(23)
+    n = 1_000_000
+    _, fp = gpu.hash_arrays(r.integers(-2**40, 2**40, n), r.integers(-2**40, 2**40, n),
+                            r.integers(-2**40, 2**40, n), r.integers(0, 32, n),
+                            r.integers(0, 2**32, n).astype(np.uint64))
+    assert not np.any(u32_numpy(fp) == 0)
+
+
+def _ulps(a, b):
+    ai = a.view(np.int64)
+    bi = b.view(np.int64)
+    return np.abs(ai - bi)
+
+
+@pytest.mark.parametrize("variant", ["default", "aux", "nfp", "nojit"])
+def test_make_key_arrays_golden(gpu, variant):
+    d = load_golden("keys_random.npz")
+    vs = golden_stream(d)
+    cfg = cfg_of(gpu, d, f"{variant}_cfg")
+    for tag, delta in (("fine", 0), ("coarse", 2), ("lookup", 0)):
+        u1 = d[f"{variant}_{tag}_u1"] if cfg.jitter else None
+        u2 = d[f"{variant}_{tag}_u2"] if cfg.jitter else None
+        k = gpu.make_key_arrays(vs.position, vs.normal, vs.omega_r, vs.layer_id,
+                                vs.camera_distance, cfg, u1, u2, delta).numpy()
+        for f in KEY_FIELDS:
+            assert np.array_equal(k[f], d[f"{variant}_{tag}_{f}"]), (tag, f)
+        ulp = _ulps(k["jittered"], d[f"{variant}_{tag}_jittered"])
+        assert ulp.max() <= 4, ulp.max()
+        assert (ulp > 0).mean() < 0.05
+
+
+@pytest.mark.parametrize("variant", ["default", "aux", "nfp", "nojit"])
+def test_vertex_keys_device_rng(gpu, variant):
+    """Keys from the on-device counter RNG equal the reference's keys from its numpy draws."""
+    d = load_golden("keys_random.npz")
+    vs = golden_stream(d)
+    cfg = cfg_of(gpu, d, f"{variant}_cfg")
+    seed = int(d["seed"])
+    for tag, stream, delta in (("fine", 2, 0), ("coarse", 2, 2), ("lookup", 3, 0)):
+        k = gpu.vertex_keys(vs, cfg, seed, stream, delta).numpy()
+        for f in KEY_FIELDS:
+            assert np.array_equal(k[f], d[f"{variant}_{tag}_{f}"]), (tag, f)
+
+
+# ------------------------------------------------------------------ table semantics
+# Ported from pkg/tests/test_table.py; run in both insert modes.
+
+def h(i, f):
+    return (np.array([i], np.uint64), np.array([f], np.uint32))
+
+
+def rgb(*v):
+    return np.array([v], np.float64)
+
+
+@pytest.fixture(params=[False, True], ids=["parallel", "ordered"])
+def ordered(request):
+    return request.param
+
+
+def test_single_insert(gpu, ordered):
+    t = gpu.VoxelTable(64, ordered=ordered)
+    status, slots, _ = t.accumulate_batch(*h(5, 77), rgb(1.0, 2.0, 3.0), 0)
+    assert int(status[0]) == 0
+    s = int(slots[0])
+    assert int(t.counts[s]) == 1
+    assert np.array_equal(_np(t.sums[s]), gpu.quantize_fixed(np.array([1.0, 2.0, 3.0])))
+    mean, count = t.lookup(gpu.CellHashes(5, 77))
+    assert count == 1 and np.array_equal(mean, np.array([1.0, 2.0, 3.0]))
+
+
+def test_thousand_identical(gpu, ordered):
+    t = gpu.VoxelTable(64, ordered=ordered)
+    t.accumulate_batch(np.full(1000, 5, np.uint64), np.full(1000, 77, np.uint32),
+                       np.ones((1000, 3)), 0)
+    mean, count = t.lookup(gpu.CellHashes(5, 77))
+    assert count == 1000 and np.array_equal(mean, np.ones(3))
+    assert np.array_equal(t.total_sums(), np.full(3, 1000 * 65536))
+
+
+def test_index_collision_resolved_by_probing(gpu, ordered):
+    t = gpu.VoxelTable(64, ordered=ordered)
+    _, s1, _ = t.accumulate_batch(*h(9, 100), rgb(1, 1, 1), 0)
+    _, s2, p2 = t.accumulate_batch(*h(9, 200), rgb(2, 2, 2), 0)
+    assert int(s2[0]) == (int(s1[0]) + 1) % 64 and int(p2[0]) == 2
+    assert t.lookup(gpu.CellHashes(9, 100))[0][0] == 1.0
+    assert t.lookup(gpu.CellHashes(9, 200))[0][0] == 2.0
+
+
+def test_rejects_bad_contributions(gpu):
+    t = gpu.VoxelTable(64)
+    with pytest.raises(ValueError):
+        t.accumulate_batch(*h(1, 2), rgb(-1.0, 0, 0), 0)
+    with pytest.raises(ValueError):
+        t.accumulate_batch(*h(1, 2), rgb(np.nan, 0, 0), 0)
+
+
+def test_probe_limit_exceeded_leaves_table_unchanged(gpu, ordered):
+    t = gpu.VoxelTable(64, probe_limit=4, ordered=ordered)
+    for f in range(1, 5):
+        t.accumulate_batch(*h(3, f), rgb(1, 1, 1), 0)
+    before = t.state()
+    status, slots, probe_len = t.accumulate_batch(*h(3, 99), rgb(5, 5, 5), 0)
+    assert (int(status[0]), int(slots[0]), int(probe_len[0])) == (2, -1, 4)
+    after = t.state()
+    for f in ("tags", "sums", "counts"):
+        assert np.array_equal(before[f], after[f])
+
+
+def test_conservation_fixed_point_exact(gpu):
+    for seed in range(10):
+        r = np.random.default_rng(seed)
+        n = 5000
+        t = gpu.VoxelTable(1024, probe_limit=8)
+        idx = r.integers(0, 2**63, n).astype(np.uint64)
+        idx[n // 2:] = idx[: n // 2]
+        fp = r.integers(1, 2**32, n).astype(np.uint32)
+        fp[n // 2:] = fp[: n // 2]
+        vals = r.uniform(0, 10, (n, 3))
+        status, _, _ = t.accumulate_batch(idx, fp, vals, 0)
+        ok = _np(status) != 2
+        assert t.total_counts() == int(ok.sum())
+        assert np.array_equal(t.total_sums(), gpu.quantize_fixed(vals[ok]).sum(axis=0))
+
+
+def test_float_mode_tolerance(gpu):
+    r = np.random.default_rng(42)
+    n = 4000
+    t = gpu.VoxelTable(2048, sum_mode="float")
+    idx = r.integers(0, 2**63, n).astype(np.uint64)
+    fp = r.integers(1, 2**32, n).astype(np.uint32)
+    vals = r.uniform(0, 10, (n, 3))
+    status, _, _ = t.accumulate_batch(idx, fp, vals, 0)
+    ok = _np(status) != 2
+    np.testing.assert_allclose(t.total_sums(), vals[ok].sum(axis=0), rtol=1e-12)
+
+
+def test_lookup_absent_and_generation_shift(gpu):
+    t = gpu.VoxelTable(64)
+    assert t.lookup(gpu.CellHashes(123, 456)) is None
+    t.accumulate_batch(*h(5, 9), rgb(1, 1, 1), 0)
+    t.begin_frame(1, gpu.FilterConfig(capacity=64))
+    assert t.lookup(gpu.CellHashes(5, 9)) is None
+
+
+def test_stale_cell_cleared_and_slot_reused(gpu):
+    cfg = gpu.FilterConfig(capacity=64, evict_horizon=8)
+    t = gpu.VoxelTable.from_config(cfg)
+    _, slots, _ = t.accumulate_batch(*h(10, 1), rgb(1, 1, 1), 0)
+    stale = int(slots[0])
+    for f in range(1, 10):
+        t.begin_frame(f, cfg)
+    assert t.state()["tags"][stale] == EMPTY
+    assert t.horizon_clears == 1
+    _, slots2, _ = t.accumulate_batch(*h(10, 2), rgb(2, 2, 2), 9)
+    assert int(slots2[0]) == stale
+
+
+def test_eviction_prefers_stale_sparse_cells(gpu, ordered):
+    cfg = gpu.FilterConfig(capacity=64, probe_limit=4, evict_horizon=100, evict_min_age=3)
+    t = gpu.VoxelTable.from_config(cfg, ordered=ordered)
+    for j, c in enumerate([5, 1, 5, 5]):
+        for _ in range(c):
+            t.accumulate_batch(*h(20, 100 + j), rgb(1, 1, 1), 0)
+    for f in range(1, 5):
+        t.begin_frame(f, cfg)
+    status, slots, _ = t.accumulate_batch(*h(20, 999), rgb(3, 3, 3), 4)
+    assert int(status[0]) == 1
+    assert int(slots[0]) == 20 % 64 + 1
+    assert len(t.eviction_events) == 1
+    assert t.lookup(gpu.CellHashes(20, 999))[1] == 1
+
+
+def test_no_eviction_of_recent_cells(gpu, ordered):
+    cfg = gpu.FilterConfig(capacity=64, probe_limit=3, evict_horizon=100, evict_min_age=3)
+    t = gpu.VoxelTable.from_config(cfg, ordered=ordered)
+    for j in range(3):
+        t.accumulate_batch(*h(8, 300 + j), rgb(1, 1, 1), 0)
+    t.begin_frame(1, cfg)
+    for j in range(3):
+        t.accumulate_batch(*h(8, 300 + j), rgb(1, 1, 1), 1)
+    t.begin_frame(2, cfg)
+    status, _, _ = t.accumulate_batch(*h(8, 999), rgb(1, 1, 1), 2)
+    assert int(status[0]) == 2 and len(t.eviction_events) == 0
+
+
+def test_integrate_fold_matches_one_shot(gpu):
+    cfg = gpu.FilterConfig(capacity=64, temporal_mode="integrate")
+    split = gpu.VoxelTable.from_config(cfg)
+    for f in range(4):
+        split.begin_frame(f, cfg)
+        split.accumulate_batch(*h(3, 9), rgb(0.5, 1.0, 1.5), f)
+    whole = gpu.VoxelTable.from_config(cfg)
+    whole.begin_frame(0, cfg)
+    for _ in range(4):
+        whole.accumulate_batch(*h(3, 9), rgb(0.5, 1.0, 1.5), 0)
+    es, ec = split.effective("integrate")
+    ws, wc = whole.effective("integrate")
+    assert torch.equal(es, ws) and torch.equal(ec, wc)
+
+
+def test_sample_cap_limits_history(gpu):
+    cfg = gpu.FilterConfig(capacity=64, temporal_mode="integrate", sample_cap=10)
+    t = gpu.VoxelTable.from_config(cfg)
+    for f in range(5):
+        t.begin_frame(f, cfg)
+        t.accumulate_batch(np.full(4, 3, np.uint64), np.full(4, 9, np.uint32), np.ones((4, 3)), f)
+    t.begin_frame(5, cfg)
+    st = t.state()
+    assert st["hist_counts"].max() == 10
+    slot = int(np.nonzero(st["hist_counts"])[0][0])
+    np.testing.assert_allclose(gpu.fixed_to_float(st["hist_sums"][slot]), 10.0, rtol=1e-4)
+
+
+def test_shadow_audit_no_false_merges(gpu):
+    t = gpu.VoxelTable(1 << 14)
+    t.shadow = {}
+    r = np.random.default_rng(1)
+    for _ in range(300):
+        key = gpu.CellKey(int(r.integers(-50, 50)), int(r.integers(-50, 50)),
+                          int(r.integers(-50, 50)), int(r.integers(0, 4)), 0)
+        t.accumulate(gpu.hashes(key), np.abs(r.uniform(0, 1, 3)), 0, key=key)
+    assert t.audit_no_false_merge() == 0
+
+
+def test_csv_and_binary_dump_layout(gpu, tmp_path):
+    import struct
+    t = gpu.VoxelTable(64)
+    t.accumulate_batch(*h(5, 9), rgb(1.5, 0.25, 0.125), 3)
+    csv = tmp_path / "t.csv"
+    t.export_csv(csv)
+    lines = csv.read_text().strip().splitlines()
+    assert lines[0] == "slot,fingerprint,count,sum_r,sum_g,sum_b"
+    _, fp, count, r, _, _ = lines[1].split(",")
+    assert (int(fp), int(count), float(r)) == (9, 1, 1.5)
+    binf = tmp_path / "t.bin"
+    t.dump(binf)
+    raw = binf.read_bytes()
+    assert raw[:5] == b"PFVT\x01"
+    assert struct.unpack_from("<QBQ", raw, 5)[:2] == (64, 0)
+    tags = np.frombuffer(raw, np.uint64, 64, offset=5 + 17)
+    assert (tags != EMPTY).sum() == 1
+    assert len(raw) == 22 + 64 * 8 * 10
+
+
+# ------------------------------------------------------------------ temporal math
+
+@pytest.mark.parametrize("sm", ["fixed", "float"])
+def test_effective_and_begin_frame_golden(gpu, sm):
+    d = load_golden("hybrid_table.npz")
+    cfg = cfg_of(gpu, d, f"{sm}_cfg")
+    for f in range(4):
+        t = gpu.VoxelTable.from_config(cfg)
+        t.load_state(golden_table(d, f"{sm}_f{f}_pre_"))
+        for mode in ("integrate", "filter", "hybrid"):
+            es, ec = t.effective(mode, 0.7, 0.5)
+            assert np.array_equal(_np(es), d[f"{sm}_f{f}_eff_{mode}_sum"]), mode
+            assert np.array_equal(_np(ec), d[f"{sm}_f{f}_eff_{mode}_cnt"]), mode
+    for mode in ("integrate", "filter", "hybrid"):
+        t = gpu.VoxelTable.from_config(cfg)
+        t.load_state(golden_table(d, f"{sm}_f3_pre_"))
+        c = cfg_of(gpu, d, f"{sm}_cfg", temporal_mode=mode, ema_alpha=0.7)
+        t.begin_frame(5, c)
+        assert_tables_equal(t.state(), golden_table(d, f"{sm}_post_{mode}_"), ordered=True)
+
+
+# ------------------------------------------------------------------ whole frames
+
+@pytest.mark.parametrize("ordered", [False, True], ids=["parallel", "ordered"])
+@pytest.mark.parametrize("mode", ["fixed", "float"])
+@pytest.mark.parametrize("fixture", ["frame_cornell128.npz", "frame_box4.npz"])
+def test_frame_golden(gpu, fixture, mode, ordered):
+    d = load_golden(fixture)
+    vs = golden_stream(d)
+    cfg = cfg_of(gpu, d, f"{mode}_cfg")
+    state = gpu.FrameState.from_config(cfg, ordered=ordered)
+    image, report, stats = gpu.filter_frame(vs, d["base"], cfg, state, int(d["spp"]),
+                                            int(d["seed"]))
+    rtol = 1e-12 if mode == "float" else 0.0
+    assert_tables_equal(state.fine.state(), golden_table(d, f"{mode}_fine_"), ordered, rtol)
+    assert_tables_equal(state.coarse.state(), golden_table(d, f"{mode}_coarse_"), ordered, rtol)
+    assert np.array_equal(_np(report.source), d[f"{mode}_source"])
+    multi = fixture == "frame_box4.npz"
+    if mode == "fixed" and (ordered or True):
+        assert np.array_equal(_np(report.means), d[f"{mode}_chosen"])
+    else:
+        np.testing.assert_allclose(_np(report.means), d[f"{mode}_chosen"], rtol=1e-12, atol=0)
+    if mode == "fixed" and not multi:
+        assert np.array_equal(_np(image), d[f"{mode}_image"])
+    else:
+        np.testing.assert_allclose(_np(image), d[f"{mode}_image"], rtol=1e-12, atol=1e-300)
+    want = dict(l.split("=", 1) for l in str(d[f"{mode}_stats"]).splitlines())
+    assert stats.probe_failures == int(want["probe_failures"])
+    assert stats.coarse_probe_failures == int(want["coarse_probe_failures"])
+    if ordered:
+        assert stats.collisions == int(want["collisions"])
+        hist = {int(k.split("_")[-1]): int(v) for k, v in want.items() if k.startswith("probe_hist_")}
+        assert stats.probe_histogram == hist
+    # fine keys handed back by accumulate_phase (lazy) equal the reference's
+    fk = state.prev_fine_keys.materialize().numpy()
+    for f in KEY_FIELDS:
+        assert np.array_equal(fk[f], d[f"{mode}_fk_{f}"]), f
+
+
+@pytest.mark.parametrize("mode", ["integrate", "filter"])
+def test_temporal_corridor_golden(gpu, mode):
+    """10-frame pan over a 128-slot table: claims, evictions, horizon clears, folds."""
+    d = load_golden("temporal_corridor.npz")
+    cfg = cfg_of(gpu, d, f"{mode}_cfg")
+    state = gpu.FrameState.from_config(cfg, ordered=True)
+    for f in range(int(d["frames"])):
+        vs = golden_stream(d, f"f{f}_v_")
+        image, report, _ = gpu.filter_frame(vs, d[f"f{f}_base"], cfg, state, 1,
+                                            int(d[f"f{f}_seed"]))
+        p = f"{mode}_f{f}_"
+        assert_tables_equal(state.fine.state(), golden_table(d, f"{p}fine_"), True)
+        assert_tables_equal(state.coarse.state(), golden_table(d, f"{p}coarse_"), True)
+        assert state.fine.horizon_clears == int(d[f"{p}fine_horizon_clears"])
+        ev = [[e.frame, e.slot, e.victim_age, e.victim_last_touch]
+              for e in state.fine.eviction_events]
+        assert np.array_equal(np.array(ev, np.int64).reshape(-1, 4), d[f"{p}fine_events"])
+        assert np.array_equal(_np(report.source), d[f"{p}source"])
+        assert np.array_equal(_np(report.means), d[f"{p}chosen"])
+        assert np.array_equal(_np(image), d[f"{p}image"])
+
+
+# ------------------------------------------------------------------ drop-in kernel module
+
+@pytest.mark.parametrize("fixed", [True, False])
+def test_kernel_module_dropin_matches_oracle(gpu, oracle, fixed):
+    """numpy arrays through kernels.accumulate_* mutate in place exactly like the
+    reference's sequential native kernel (oracle/pf_table_ref.c)."""
+    from paper_1902_05942_b200 import kernels
+    r = np.random.default_rng(5)
+    cap, n = 256, 3000
+    idx = r.integers(0, 2**63, 400).astype(np.uint64)[r.integers(0, 400, n)]
+    fp = (idx >> np.uint64(20)).astype(np.uint32) | np.uint32(1)
+    vals = r.uniform(0, 3, (n, 3))
+    mode = "fixed" if fixed else "float"
+    a = oracle.Table(cap, 6, mode, 8, 1)
+    b = oracle.Table(cap, 6, mode, 8, 1)
+    for frame in range(3):
+        a.begin_frame(frame)
+        b.begin_frame(frame)
+        part = slice(frame * 900, frame * 900 + 1200)
+        want = a.accumulate(idx[part], fp[part], vals[part], frame)
+        fn = kernels.accumulate_fixed if fixed else kernels.accumulate_float
+        got = fn(b.tags, b.sums, b.counts, b.hist_sums, b.hist_counts, b.last_touch, b.deltas,
+                 idx[part], fp[part], np.ascontiguousarray(vals[part]), frame, 6, 1)
+        for x, y in zip(got, want):
+            assert np.array_equal(x, y)
+        for f in TABLE_FIELDS:
+            assert np.array_equal(getattr(a, f), getattr(b, f)), f
+        assert np.array_equal(kernels.lookup_slots(b.tags, idx[part], fp[part], 6),
+                              a.lookup(idx[part], fp[part]))
+
+
+# ------------------------------------------------------------------ larger inputs vs oracle
+
+def _synthetic(gpu, w, hgt, bounces, seed=3):
+    from paper_1902_05942_b200.streams import camera_footprint, closed_box_stream, \
+        stream_to_numpy
+    s, base = closed_box_stream(w, hgt, bounces, seed)
+    return s, base, stream_to_numpy(s), base.cpu().numpy(), camera_footprint(hgt)
+
+
+@pytest.mark.parametrize("sum_mode", ["fixed", "float"])
+def test_synthetic_box_vs_oracle(gpu, oracle, sum_mode):
+    w, hgt = 320, 180
+    s, base, hs, hbase, fs = _synthetic(gpu, w, hgt, 4)
+    n = len(hs.pixel)
+    cap = 1 << (2 * w * hgt - 1).bit_length()
+    cfg = gpu.FilterConfig(capacity=cap, footprint_scale=fs, sum_mode=sum_mode)
+    state = gpu.FrameState.from_config(cfg)
+    vs = gpu.VertexStream(**s)
+    image, report, stats = gpu.filter_frame(vs, base, cfg, state, 1, 77)
+    ocfg = oracle.Config(capacity=cap, footprint_scale=fs, sum_mode=sum_mode)
+    ost = oracle.State.from_config(ocfg)
+    oimg, osrc, ochosen, ostats = oracle.filter_frame(hs, ocfg, ost, 0, 77, 1, hbase)
+    rtol = 1e-12 if sum_mode == "float" else 0.0
+    assert_tables_equal(state.fine.state(), {f: getattr(ost.fine, f) for f in TABLE_FIELDS},
+                        False, rtol)
+    assert_tables_equal(state.coarse.state(), {f: getattr(ost.coarse, f) for f in TABLE_FIELDS},
+                        False, rtol)
+    assert np.array_equal(_np(report.source), osrc)
+    if sum_mode == "fixed":
+        assert np.array_equal(_np(report.means), ochosen)
+    else:
+        np.testing.assert_allclose(_np(report.means), ochosen, rtol=1e-12)
+    np.testing.assert_allclose(_np(image), oimg, rtol=1e-12, atol=1e-300)
+    assert stats.probe_failures == ostats["probe_failures"] == 0
+    assert n == 4 * w * hgt
+
+
+def test_full_size_conservation(gpu):
+    """1080p, 4 bounces (the benchmark workload): size-independent properties."""
+    from paper_1902_05942_b200.streams import camera_footprint, closed_box_stream
+    w, hgt = 1920, 1080
+    s, base = closed_box_stream(w, hgt, 4, 1)
+    n = int(s["pixel"].shape[0])
+    cfg = gpu.FilterConfig(capacity=1 << 22, footprint_scale=camera_footprint(hgt))
+    state = gpu.FrameState.from_config(cfg)
+    vs = gpu.VertexStream(**s)
+    image, report, stats = gpu.filter_frame(vs, base, cfg, state, 1, 1)
+    q = torch.floor(vs.contribution * 65536.0 + 0.5).to(torch.int64).sum(0)
+    for t in (state.fine, state.coarse):
+        assert t.total_counts() == n
+        assert torch.equal(t.sums.sum(0), q)
+    src = torch.bincount(report.source.to(torch.int64), minlength=4)
+    assert int(src.sum()) == n and int(src[3]) == 0
+    assert bool(torch.isfinite(image).all())
+    assert stats.probe_failures == 0
+    assert sum(stats.probe_histogram.values()) == n
