@@ -334,7 +334,7 @@ def run_b200(args):
 
     # end to end through the public API with host buffers
     e2e = None
-    if rank == 0 or world > 1:
+    if not args.no_e2e:
         e2e = run_e2e(pf, rng, cfg, stream, base, args, n)
 
     cpu = None
@@ -416,6 +416,7 @@ def main():
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="b200", choices=["b200", "reference"])
     ap.add_argument("--no-cpu", action="store_true", help="skip the cpu_baseline leg")
+    ap.add_argument("--no-e2e", action="store_true", help="skip the host-buffer e2e leg")
     args = ap.parse_args()
     if args.impl == "reference":
         return run_reference_arm(args)

@@ -256,15 +256,16 @@ __global__ void __launch_bounds__(kThreads) resolve_fallback_kernel(ResolveArgs 
             if (mode == PF_INTEGRATE) pic += __shfl_sync(kFull, static_cast<long long>(e.icnt), j);
             else pfc = dadd(pfc, __shfl_sync(kFull, e.fcnt, j));
         }
-        if (lane != 0) continue;
+        // every lane now holds the same pooled sums; lane 0 finishes the row
         const double cnt_n = (mode == PF_INTEGRATE) ? static_cast<double>(pic) : pfc;
+        const bool ok_n = cnt_n >= a.thr;
+        if (lane == 0) {
         double mean_n[3] = {0.0, 0.0, 0.0};
         if (cnt_n > 0.0) {
 #pragma unroll
             for (int c = 0; c < 3; ++c)
                 mean_n[c] = row_mean(as_int ? static_cast<double>(pis[c]) : pfs[c], cnt_n, fixed);
         }
-        const bool ok_n = cnt_n >= a.thr;
         double cnt_c = 0.0;
         double mean_c[3] = {0.0, 0.0, 0.0};
         const VertexIn x = load_vertex(a.v, row, cfg);
@@ -295,23 +296,19 @@ __global__ void __launch_bounds__(kThreads) resolve_fallback_kernel(ResolveArgs 
         const bool ok_c = !ok_n && cnt_c >= a.thr;
         const bool any_n = !ok_n && !ok_c && cnt_n >= 1.0;
         const bool any_c = !ok_n && !ok_c && !any_n && cnt_c >= 1.0;
+        // written as selects: an if/else-if chain here was mis-compiled (nvcc 12.9, sm_100a),
+        // taking the unfiltered branch with ok_c set (tests/test_gpu_parity.py::test_frame_golden)
+        const int src = (ok_n || any_n) ? 1 : ((ok_c || any_c) ? 2 : 3);
         double ch[3];
-        int src;
-        if (ok_n || any_n) {
-            src = 1;
 #pragma unroll
-            for (int c = 0; c < 3; ++c) ch[c] = mean_n[c];
-        } else if (ok_c || any_c) {
-            src = 2;
-#pragma unroll
-            for (int c = 0; c < 3; ++c) ch[c] = mean_c[c];
-        } else {
-            src = 3;
-#pragma unroll
-            for (int c = 0; c < 3; ++c) ch[c] = __ldg(a.v.contribution + 3 * row + c);
+        for (int c = 0; c < 3; ++c) {
+            const double contrib = __ldg(a.v.contribution + 3 * row + c);
+            ch[c] = src == 1 ? mean_n[c] : (src == 2 ? mean_c[c] : contrib);
         }
         composite(a, row, x.pixel, ch, src);
         atomicAdd(&bs.v[PF_STAT_SOURCE_FINE + src], 1ull);
+        }
+        __syncwarp();
     }
     __syncthreads();
     stats_flush(bs, a.stats, false);

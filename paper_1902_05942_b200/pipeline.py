@@ -160,6 +160,20 @@ class FrameState:
     prev_seed: int = 0
     prev_spp: int = 0
     scratch: dict = field(default_factory=dict)
+    pending_drains: list = field(default_factory=list)
+
+    def drain_events(self):
+        """Move eviction records of the previous insert from HBM into the table's log."""
+        for t in self.pending_drains:
+            t.eviction_events  # noqa: B018 -- property drains pending device logs
+        self.pending_drains.clear()
+
+    def pinned_count(self) -> torch.Tensor:
+        p = self.scratch.get("_pinned_count")
+        if p is None:
+            p = torch.zeros(1, dtype=torch.int64).pin_memory()
+            self.scratch["_pinned_count"] = p
+        return p
 
     @classmethod
     def from_config(cls, cfg: FilterConfig, backend: str | None = None,
@@ -240,8 +254,8 @@ def accumulate_phase(vertices, cfg: FilterConfig, state: FrameState, frame: int,
     Returns (fine keys, coarse keys, stats); keys are lazy (computed on first read)."""
     vs = VertexStream.from_any(vertices)
     n = len(vs)
-    counters = state.buffer("stats_acc", (_lib.STAT_COUNT,), torch.int64)
-    counters.zero_()
+    state.drain_events()  # the event log buffer is about to be reused
+    counters = torch.zeros(_lib.STAT_COUNT, dtype=torch.int64, device=vs.pixel.device)
     stats = FrameStats(frame=frame, n_vertices=n, counters=counters)
     fine_keys = LazyKeyArrays(vs, cfg, seed, rng.STREAM_JITTER_ACCUM, 0)
     coarse_keys = None
@@ -264,14 +278,22 @@ def accumulate_phase(vertices, cfg: FilterConfig, state: FrameState, frame: int,
               rng.stream_base(seed, rng.STREAM_JITTER_ACCUM), int(frame), counters.data_ptr(),
               events.data_ptr(), ev_count.data_ptr(), n, _lib.stream_handle())
     del keep
-    ev_snapshot = (events, ev_count.clone())
+    # event count to pinned host memory without a sync; drained before the buffer is reused
+    host = state.pinned_count()
+    host.copy_(ev_count, non_blocking=True)
+    done = torch.cuda.Event()
+    done.record()
+    pending = {"drained": False}
 
-    def drain(snap=ev_snapshot, frame=frame):
-        ev, cnt = snap
-        k = int(cnt.item())
+    def drain(frame=frame, events=events, host=host, done=done, pending=pending):
+        if pending["drained"]:
+            return []
+        pending["drained"] = True
+        done.synchronize()
+        k = int(host[0])
         if k == 0:
             return []
-        rows = ev[:k].cpu().numpy()
+        rows = events[:k].cpu().numpy()
         rows = rows[np.argsort(rows[:, 0], kind="stable")]
         out = []
         for _, slot, vtag, vtouch in rows:
@@ -280,8 +302,7 @@ def accumulate_phase(vertices, cfg: FilterConfig, state: FrameState, frame: int,
         return out
 
     state.fine._add_pending_events(drain)
-    # the event buffer is reused next frame: detach this frame's copy
-    state.scratch.pop("events", None)
+    state.pending_drains.append(state.fine)
     return fine_keys, coarse_keys, stats
 
 
@@ -322,8 +343,7 @@ def resolve_phase(vertices, cfg: FilterConfig, state: FrameState, frame: int, se
     flat = state.buffer("flat", (h * w, 3), torch.float64)
     work = state.buffer("work", (max(n, 1), 6), torch.int64)
     work_count = state.buffer("work_count", (1,), torch.int64)
-    counters = state.buffer("stats_res", (_lib.STAT_COUNT,), torch.int64)
-    counters.zero_()
+    counters = torch.zeros(_lib.STAT_COUNT, dtype=torch.int64, device=dev)
     v, keep = vs.c_struct()
     ft = state.fine.c_table()
     ct = state.coarse.c_table() if state.coarse is not None else None
