@@ -64,7 +64,7 @@ class ClockSampler:
             self._proc = subprocess.Popen(
                 ["nvidia-smi", "-i", str(self.index),
                  "--query-gpu=clocks.sm,clocks.max.sm,clocks_event_reasons.active",
-                 "--format=csv,noheader,nounits", "-lms", "100"],
+                 "--format=csv,noheader,nounits", "-lms", "20"],
                 stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
             self._thread = threading.Thread(target=self._read, daemon=True)
             self._thread.start()
@@ -77,9 +77,22 @@ class ClockSampler:
             parts = [p.strip() for p in line.split(",")]
             if len(parts) >= 3:
                 try:
-                    self.samples.append((float(parts[0]), float(parts[1]), int(parts[2], 16)))
+                    self.samples.append((float(parts[0]), float(parts[1]), int(parts[2], 16),
+                                         time.time()))
                 except ValueError:
                     pass
+
+    def wait_first(self, timeout=5.0):
+        t0 = time.time()
+        while self._proc is not None and not self.samples and time.time() - t0 < timeout:
+            time.sleep(0.02)
+
+    def window(self, t0, t1):
+        """Keep the samples taken inside [t0, t1] (plus the nearest one if none)."""
+        inside = [s for s in self.samples if t0 <= s[3] <= t1]
+        if not inside and self.samples:
+            inside = [min(self.samples, key=lambda s: abs(s[3] - (t0 + t1) / 2))]
+        self.samples = inside
 
     def __exit__(self, *exc):
         if self._proc is not None:
@@ -290,6 +303,9 @@ def run_b200(args):
         state.frame = frame + 1
         timing.append((e0, e1, e2, e3))
 
+    clocks = ClockSampler(local)
+    clocks.__enter__()
+    clocks.wait_first()
     for f in range(args.warmup):
         step(f)
     torch.cuda.synchronize()
@@ -298,12 +314,16 @@ def run_b200(args):
     torch.cuda.synchronize()
     marks = []
     start, stop = ev(), ev()
-    with ClockSampler(local) as clocks:
-        start.record()
-        for k in range(args.steps):
-            step(args.warmup + k, marks)
-        stop.record()
-        torch.cuda.synchronize()
+    t_wall0 = time.time()
+    start.record()
+    for k in range(args.steps):
+        step(args.warmup + k, marks)
+    stop.record()
+    torch.cuda.synchronize()
+    t_wall1 = time.time()
+    time.sleep(0.05)
+    clocks.__exit__(None, None, None)
+    clocks.window(t_wall0 - 0.05, t_wall1 + 0.05)
     if world > 1:
         dist.barrier()
     elapsed = start.elapsed_time(stop) / 1e3

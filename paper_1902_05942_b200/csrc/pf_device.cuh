@@ -350,7 +350,7 @@ __device__ __forceinline__ void zero_cell(const pf_table &t, int64_t s) {
 // FRESH|fp with release order, so no accumulate lands in a half-wiped cell.  A lost
 // victim CAS re-probes the window (what a sequential caller would see) instead of
 // the reference's racy give-up.
-static __device__ __noinline__ InsertResult probe_insert(const pf_table &t, uint64_t idx, uint32_t fp) {
+__device__ __forceinline__ InsertResult probe_insert(const pf_table &t, uint64_t idx, uint32_t fp) {
     const uint64_t mask = static_cast<uint64_t>(t.capacity) - 1;
     const uint64_t home = idx & mask;
     const uint64_t want = static_cast<uint64_t>(fp);

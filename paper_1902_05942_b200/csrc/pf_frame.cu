@@ -60,7 +60,10 @@ insert_frame_kernel(pf_config cfg, pf_vertices v, pf_table fine, pf_table coarse
     __shared__ BlockStats bs;
     stats_init(bs);
     __syncthreads();
-    const int64_t i = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+    // persistent: each block walks 256-vertex tiles; block counters flush once at exit
+    const int64_t tiles = (v.n + kThreads - 1) / kThreads;
+    for (int64_t tile = blockIdx.x; tile < tiles; tile += gridDim.x) {
+    const int64_t i = tile * kThreads + threadIdx.x;
     const bool valid = i < v.n;
     VertexIn x;
     double val[3] = {0.0, 0.0, 0.0};
@@ -103,8 +106,18 @@ insert_frame_kernel(pf_config cfg, pf_vertices v, pf_table fine, pf_table coarse
         warp_count(bs, PF_STAT_COARSE_PROBE_FAILURES, valid && rc.status == 2);
         warp_count(bs, PF_STAT_COARSE_EVICTIONS, valid && rc.leader && rc.status == 1);
     }
+    }
     __syncthreads();
     stats_flush(bs, stats, true);
+}
+
+// Resident blocks per SM for a kernel (cached per function), for persistent grids.
+template <typename K>
+static int resident_blocks(K kernel, int threads) {
+    int b = 0;
+    if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&b, kernel, threads, 0) != cudaSuccess || b < 1)
+        b = 1;
+    return b;
 }
 
 // ------------------------------------------------------------------ resolve
@@ -342,7 +355,12 @@ int pf_insert_frame(const pf_config *cfg, const pf_vertices *v, const pf_table *
     if (v->n > 0 && !v->contribution) return fail_arg(fn, "contribution is NULL");
     if (v->n == 0) return PF_OK;
     const pf_table c = coarse ? *coarse : *fine;
-    const unsigned g = blocks_for(v->n, kThreads);
+    static const int per_sm_fixed = resident_blocks(insert_frame_kernel<true>, kThreads);
+    static const int per_sm_float = resident_blocks(insert_frame_kernel<false>, kThreads);
+    const int64_t tiles = (v->n + kThreads - 1) / kThreads;
+    int64_t cap = static_cast<int64_t>(sm_count()) *
+                  (fine->sum_mode == PF_SUM_FIXED ? per_sm_fixed : per_sm_float);
+    const unsigned g = static_cast<unsigned>(tiles < cap ? tiles : cap);
     if (fine->sum_mode == PF_SUM_FIXED)
         insert_frame_kernel<true><<<g, kThreads, 0, as_stream(stream)>>>(
             *cfg, *v, *fine, c, coarse != nullptr, stream_base_accum, frame, stats, events,

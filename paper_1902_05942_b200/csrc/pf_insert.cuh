@@ -44,21 +44,27 @@ __device__ __forceinline__ LaneInsert warp_insert(const pf_table &t, bool valid,
         if (FIXED) qsum[c] = valid ? quantize_fixed(val[c]) : 0;
         else fsum[c] = valid ? val[c] : 0.0;
     }
-    unsigned followers = __ballot_sync(kFull, valid && static_cast<int>(lane) != leader);
-    while (followers) {  // warp-uniform loop, one iteration per follower lane
-        const int j = __ffs(followers) - 1;
-        followers &= followers - 1;
-        const bool mine = is_leader && ((peers >> j) & 1u);
+    // Group sums by pointer jumping over each group's member list: every lane links to
+    // the next higher lane of its group and adds its successor's partial sum, doubling
+    // the stride each round, so the leader holds the group total after
+    // ceil(log2(group size)) rounds (0 rounds when all 32 keys differ).  The
+    // summation tree depends only on lane positions, so float totals are repeatable.
+    const unsigned above = valid && lane < 31 ? (peers & (0xFFFFFFFFu << (lane + 1))) : 0u;
+    int nxt = above ? __ffs(above) - 1 : -1;
+    while (__any_sync(kFull, nxt >= 0)) {
+        const int src = nxt >= 0 ? nxt : static_cast<int>(lane);
+        const int nn = __shfl_sync(kFull, nxt, src);
 #pragma unroll
         for (int c = 0; c < 3; ++c) {
             if (FIXED) {
-                const long long x = __shfl_sync(kFull, static_cast<long long>(qsum[c]), j);
-                if (mine) qsum[c] += x;
+                const long long x = __shfl_sync(kFull, static_cast<long long>(qsum[c]), src);
+                if (nxt >= 0) qsum[c] += x;
             } else {
-                const double x = __shfl_sync(kFull, fsum[c], j);
-                if (mine) fsum[c] = dadd(fsum[c], x);
+                const double x = __shfl_sync(kFull, fsum[c], src);
+                if (nxt >= 0) fsum[c] = dadd(fsum[c], x);
             }
         }
+        if (nxt >= 0) nxt = nn;
     }
 
     InsertResult r;

