@@ -202,6 +202,12 @@ int pf_begin_frame(const pf_table *t, int64_t frame, int32_t mode, double ema_al
  * set to 1 when any of the `count` float64 values is NaN, infinite or negative. */
 int pf_check_contributions(const double *vals, int64_t count, int32_t *bad, void *stream);
 
+/* Diagnostic: counts (into mismatches[0..1], int64 device) the inputs for which the
+ * kernels' reciprocal-based division differs from IEEE division -- [0] random
+ * operands, [1] quantiser divisors base_voxel*2^level.  Both must stay 0. */
+int pf_selftest_division(uint64_t seed, int64_t n, double base_voxel, int64_t *mismatches,
+                         void *stream);
+
 /* Number of non-EMPTY tags (VoxelTable.occupancy numerator, src/table.py:302-303). */
 int pf_count_occupied(const uint64_t *tags, int64_t capacity, int64_t *out, void *stream);
 

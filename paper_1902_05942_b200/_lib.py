@@ -26,7 +26,8 @@ NVCC_FLAGS = ["-gencode", "arch=compute_100a,code=sm_100a", "-O3", "-lineinfo",
 EXPORTS = ("pf_abi_version", "pf_last_error", "pf_device_sm_count", "pf_accumulate_fixed",
            "pf_accumulate_float", "pf_lookup_slots", "pf_make_key_arrays", "pf_vertex_keys",
            "pf_hash_arrays", "pf_insert_frame", "pf_resolve_frame", "pf_effective",
-           "pf_begin_frame", "pf_check_contributions", "pf_count_occupied")
+           "pf_begin_frame", "pf_check_contributions", "pf_selftest_division",
+           "pf_count_occupied")
 
 
 def build(force: bool = False, verbose: bool = False) -> str:
@@ -128,6 +129,7 @@ def lib() -> ctypes.CDLL:
     L.pf_begin_frame.argtypes = [vp, i64, i32, dbl, dbl, i32, vp, vp]
     L.pf_count_occupied.argtypes = [vp, i64, vp, vp]
     L.pf_check_contributions.argtypes = [vp, i64, vp, vp]
+    L.pf_selftest_division.argtypes = [u64, i64, dbl, vp, vp]
     for name in EXPORTS[3:]:
         getattr(L, name).restype = ctypes.c_int
     _lib = L

@@ -54,6 +54,20 @@ __device__ __forceinline__ double dadd(double a, double b) { return __dadd_rn(a,
 __device__ __forceinline__ double dsub(double a, double b) { return __dsub_rn(a, b); }
 __device__ __forceinline__ double ddiv(double a, double b) { return __ddiv_rn(a, b); }
 
+// Correctly rounded x / y from r = RN(1/y) (Markstein's theorem): q0 = RN(x*r) is a
+// faithful quotient, rem = x - q0*y is exact under FMA, and RN(q0 + rem*r) = RN(x/y).
+// Three FP64 ops instead of a full division when the reciprocal is shared; zero,
+// huge and tiny numerators (outside the theorem's no-underflow range) take __ddiv_rn.
+// Verified bitwise against __ddiv_rn by pf_selftest_division (tests/test_gpu_parity.py).
+__device__ __forceinline__ double div_rcp(double x, double y, double r) {
+    const double ax = fabs(x);
+    if (!(ax > 0x1p-900 && ax < 0x1p+900))
+        return __ddiv_rn(x, y);
+    const double q0 = __dmul_rn(x, r);
+    const double rem = __fma_rn(-q0, y, x);
+    return __fma_rn(rem, r, q0);
+}
+
 // np.maximum / np.minimum propagate NaN from either side.
 __device__ __forceinline__ double np_max(double a, double b) {
     return (a != a) ? a : ((b != b) ? b : (a >= b ? a : b));
@@ -110,11 +124,16 @@ __device__ __forceinline__ int64_t clamp_level(int64_t lv, int32_t delta) {
     return l < kMaxLevel ? l : kMaxLevel;
 }
 
+// 2^e as a double for |e| <= 1022, built from its exponent bits.
+__device__ __forceinline__ double pow2i(int64_t e) {
+    if (e < -1022 || e > 1023)
+        return ldexp(1.0, static_cast<int>(e < -2000 ? -2000 : (e > 2000 ? 2000 : e)));
+    return __longlong_as_double((e + 1023) << 52);
+}
+
 // base_voxel * exp2(level): exact power-of-two scaling.
 __device__ __forceinline__ double voxel_step(double base_voxel, int64_t level) {
-    if (level < -2000)
-        return 0.0;
-    return dmul(base_voxel, ldexp(1.0, static_cast<int>(level)));
+    return dmul(base_voxel, pow2i(level));
 }
 
 struct Frame3 {
@@ -124,7 +143,7 @@ struct Frame3 {
 // Branchless ONB (src/keys.py:329-336) in numpy's left-to-right order.
 __device__ __forceinline__ Frame3 tangent_frame(double x, double y, double z) {
     const double s = (z >= 0.0) ? 1.0 : -1.0;
-    const double a = ddiv(-1.0, dadd(s, z));
+    const double a = -__drcp_rn(dadd(s, z));  // -1.0 / (s + z): negation is exact
     const double b = dmul(dmul(x, y), a);
     Frame3 f;
     f.t1[0] = dadd(1.0, dmul(dmul(dmul(s, x), x), a));
@@ -139,7 +158,8 @@ __device__ __forceinline__ Frame3 tangent_frame(double x, double y, double z) {
 // Octahedral normal bin (src/keys.py:351-361).
 __device__ __forceinline__ int64_t octa_bin(double x, double y, double z, int bins) {
     const double s = np_max(dadd(dadd(fabs(x), fabs(y)), fabs(z)), 1e-300);
-    const double px = ddiv(x, s), py = ddiv(y, s), pz = ddiv(z, s);
+    const double rs = __drcp_rn(s);
+    const double px = div_rcp(x, s, rs), py = div_rcp(y, s, rs), pz = div_rcp(z, s, rs);
     double fx = px, fy = py;
     if (pz < 0.0) {
         fx = dmul(dsub(1.0, fabs(py)), px >= 0.0 ? 1.0 : -1.0);
@@ -241,10 +261,12 @@ struct KeyShared {
     uint64_t aux;
     uint32_t fp_bin;
     int has_fp_bin;
+    double rbv;  // RN(1 / base_voxel): RN(1/step) = rbv * 2^-level exactly
 };
 
 __device__ __forceinline__ KeyShared key_shared(const pf_config &cfg, const VertexIn &x) {
     KeyShared k;
+    k.rbv = __drcp_rn(cfg.base_voxel);
     k.frame = tangent_frame(x.nrm[0], x.nrm[1], x.nrm[2]);
     k.aux = aux_word(cfg, x.nrm[0], x.nrm[1], x.nrm[2], x.omega, x.layer);
     k.has_fp_bin = cfg.include_normal && cfg.normal_in_fingerprint;
@@ -279,9 +301,11 @@ __device__ __forceinline__ CellKey make_key(const pf_config &cfg, const VertexIn
         for (int c = 0; c < 3; ++c) jittered[c] = x.pos[c];
     }
     const double step = voxel_step(cfg.base_voxel, lv);
+    const double rstep = dmul(ks.rbv, pow2i(-lv));
     CellKey k;
+    // IEEE x / step (not a reciprocal multiply: base_voxel is inexact), via Markstein
 #pragma unroll
-    for (int c = 0; c < 3; ++c) k.q[c] = np_i64(floor(ddiv(jittered[c], step)));
+    for (int c = 0; c < 3; ++c) k.q[c] = np_i64(floor(div_rcp(jittered[c], step, rstep)));
     k.level = lv;
     k.aux = ks.aux;
     return k;

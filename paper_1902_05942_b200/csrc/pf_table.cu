@@ -384,6 +384,36 @@ check_contributions_kernel(const double *__restrict__ vals, int64_t count, int32
     if (__any_sync(kFull, any) && (threadIdx.x & 31) == 0) atomicExch(bad, 1);
 }
 
+// Self-test of div_rcp against IEEE division: random numerators and divisors over a
+// wide exponent range, plus the quantiser's divisors base_voxel * 2^level with the
+// reciprocal scaled by 2^-level (mismatches[0] and [1]).
+__global__ void __launch_bounds__(kThreads)
+selftest_division_kernel(uint64_t seed, int64_t n, double base_voxel, unsigned long long *bad) {
+    unsigned long long b0 = 0, b1 = 0;
+    const double rbv = __drcp_rn(base_voxel);
+    for (int64_t i = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x; i < n;
+         i += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+        const uint64_t h1 = mix64(seed ^ (2 * static_cast<uint64_t>(i) + 1));
+        const uint64_t h2 = mix64(h1 ^ 0x9E3779B97F4A7C15ull);
+        const int ex = static_cast<int>((h1 >> 52) % 241) - 120;
+        const int ey = static_cast<int>((h2 >> 52) % 241) - 120;
+        const double mx = 1.0 + static_cast<double>(h1 & 0xFFFFFFFFFFFFFull) * 0x1p-52;
+        const double my = 1.0 + static_cast<double>(h2 & 0xFFFFFFFFFFFFFull) * 0x1p-52;
+        const double x = ((h1 >> 51) & 1 ? -mx : mx) * pow2i(ex);
+        const double y = ((h2 >> 51) & 1 ? -my : my) * pow2i(ey);
+        if (__double_as_longlong(div_rcp(x, y, __drcp_rn(y))) != __double_as_longlong(__ddiv_rn(x, y)))
+            ++b0;
+        const int64_t lv = static_cast<int64_t>(h2 % 32);
+        const double step = voxel_step(base_voxel, lv);
+        const double xs = (static_cast<double>(static_cast<int64_t>(h1 >> 20)) - 8.0e12) * 0x1p-30;
+        const double q = div_rcp(xs, step, dmul(rbv, pow2i(-lv)));
+        if (__double_as_longlong(q) != __double_as_longlong(__ddiv_rn(xs, step)))
+            ++b1;
+    }
+    if (b0) atomicAdd(bad, b0);
+    if (b1) atomicAdd(bad + 1, b1);
+}
+
 // ------------------------------------------------------------------ host wrappers
 
 static int accumulate_impl(const char *fn, bool fixed, uint64_t *tags, void *sums, int64_t *counts,
@@ -516,6 +546,16 @@ int pf_begin_frame(const pf_table *t, int64_t frame, int32_t mode, double ema_al
     else
         begin_frame_kernel<false><<<g, kThreads, 0, as_stream(stream)>>>(
             *t, frame, mode, ema_alpha, delta_max, sample_cap, horizon_clears);
+    return check_launch(fn);
+}
+
+int pf_selftest_division(uint64_t seed, int64_t n, double base_voxel, int64_t *mismatches,
+                         void *stream) {
+    const char *fn = "pf_selftest_division";
+    if (n < 0 || !mismatches) return fail_arg(fn, "bad arguments");
+    selftest_division_kernel<<<static_cast<unsigned>(sm_count()) * 8, kThreads, 0,
+                               as_stream(stream)>>>(
+        seed, n, base_voxel, reinterpret_cast<unsigned long long *>(mismatches));
     return check_launch(fn);
 }
 

@@ -84,6 +84,17 @@ def test_never_sentinel_in_bulk(gpu):
     assert not np.any(u32_numpy(fp) == 0)
 
 
+@pytest.mark.parametrize("base_voxel", [0.01, 0.02, 0.05, 0.013, 1.0 / 3.0])
+def test_reciprocal_division_is_ieee(gpu, base_voxel):
+    """The kernels divide through a shared reciprocal (Markstein); it must equal IEEE
+    division bit for bit on 2^26 random operands and quantiser divisors."""
+    from paper_1902_05942_b200 import _lib
+    bad = torch.zeros(2, dtype=torch.int64, device="cuda")
+    _lib.call("pf_selftest_division", 12345, 1 << 26, base_voxel, bad.data_ptr(),
+              _lib.stream_handle())
+    assert bad.tolist() == [0, 0]
+
+
 def _ulps(a, b):
     ai = a.view(np.int64)
     bi = b.view(np.int64)
