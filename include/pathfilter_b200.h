@@ -55,6 +55,8 @@ typedef struct pf_config {
     int32_t low_count_threshold;
     int32_t temporal_mode;   /* pf_temporal_mode */
     int32_t sample_cap;
+    uint64_t lod_ulps[2];    /* filled by the library from lod_threshold (callers leave 0):
+                                4-bit count of doubles between T[k] and 2^k, k = 0..31 */
 } pf_config;
 
 /* VertexStream (src/tracer.py:732-767): row-major [n][3] float64 triples. */

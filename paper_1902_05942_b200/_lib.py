@@ -14,7 +14,7 @@ import torch
 
 _PKG = os.path.dirname(os.path.abspath(__file__))
 _ROOT = os.path.dirname(_PKG)
-LIB_PATH = os.path.join(_PKG, "libpf_b200.so")
+LIB_PATH = os.environ.get("PF_LIB") or os.path.join(_PKG, "libpf_b200.so")
 SOURCES = [os.path.join(_PKG, "csrc", f) for f in ("pf_common.cu", "pf_table.cu", "pf_frame.cu")]
 HEADERS = [os.path.join(_PKG, "csrc", f) for f in ("pf_device.cuh", "pf_insert.cuh",
                                                     "pf_internal.cuh")] + \
@@ -54,7 +54,8 @@ class PfConfig(ctypes.Structure):
                 ("include_layer", ctypes.c_int32), ("normal_in_fingerprint", ctypes.c_int32),
                 ("jitter", ctypes.c_int32), ("multi_level", ctypes.c_int32),
                 ("coarse_delta", ctypes.c_int32), ("low_count_threshold", ctypes.c_int32),
-                ("temporal_mode", ctypes.c_int32), ("sample_cap", ctypes.c_int32)]
+                ("temporal_mode", ctypes.c_int32), ("sample_cap", ctypes.c_int32),
+                ("lod_ulps", ctypes.c_uint64 * 2)]
 
 
 class PfVertices(ctypes.Structure):

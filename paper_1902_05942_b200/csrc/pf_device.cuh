@@ -61,6 +61,8 @@ __device__ __forceinline__ double ddiv(double a, double b) { return __ddiv_rn(a,
 // Verified bitwise against __ddiv_rn by pf_selftest_division (tests/test_gpu_parity.py).
 __device__ __forceinline__ double div_rcp(double x, double y, double r) {
     const double ax = fabs(x);
+    if (ax == 0.0)
+        return __dmul_rn(x, r);  // signed zero: sign(x) * sign(y), like IEEE division
     if (!(ax > 0x1p-900 && ax < 0x1p+900))
         return __ddiv_rn(x, y);
     const double q0 = __dmul_rn(x, r);
@@ -109,14 +111,22 @@ __device__ __forceinline__ void disc_offset(double u1, double u2, double &u, dou
 
 // floor(log2(max(d * c_lod, 1))) clamped to 31 (src/keys.py:323-326).  numpy's log2
 // rounds up to k just below 2^k, so the exact floor is exponent + (r >= T[e+1]).
+// T[k] = 2^k - m_k ulps with m_k < 16 packed as 4-bit fields in cfg.lod_ulps, so
+// ratio >= T[e+1] <=> mantissa >= 2^52 - m_{e+1}: pure integer work on the bits
+// (no dynamic indexing into the kernel-parameter array, which would spill it).
 __device__ __forceinline__ int64_t lod_level(double dist, const pf_config &cfg) {
     const double ratio = np_max(dmul(dist, cfg.c_lod), 1.0);
     if (ratio != ratio)
         return INT64_MIN;
     if (ratio >= 2147483648.0)
         return kMaxLevel;
-    const int e = ilogb(ratio);  // ratio in [1, 2^31): exact floor(log2) of the double
-    return (e < kMaxLevel && ratio >= cfg.lod_threshold[e + 1]) ? e + 1 : e;
+    const uint64_t bits = static_cast<uint64_t>(__double_as_longlong(ratio));
+    const int e = static_cast<int>(bits >> 52) - 1023;  // ratio in [1, 2^31): exact floor(log2)
+    const int k = e + 1;
+    const uint64_t word = k >= 16 ? cfg.lod_ulps[1] : cfg.lod_ulps[0];
+    const uint64_t m = (word >> ((k & 15) * 4)) & 15u;
+    const uint64_t mant = bits & 0xFFFFFFFFFFFFFull;
+    return mant >= (0x10000000000000ull - m) ? k : e;
 }
 
 __device__ __forceinline__ int64_t clamp_level(int64_t lv, int32_t delta) {
@@ -336,6 +346,15 @@ __device__ __forceinline__ int64_t ld_relaxed_i64(const int64_t *p) {
 }
 __device__ __forceinline__ void st_relaxed_u64(void *p, uint64_t v) {
     asm volatile("st.relaxed.gpu.global.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
+}
+
+// Fire-and-forget L2 reductions (RED, no return value): nvcc otherwise emits ATOMG
+// with a result round trip for 64-bit atomicAdd even when the result is unused.
+__device__ __forceinline__ void red_add_u64(void *p, uint64_t v) {
+    asm volatile("red.relaxed.gpu.global.add.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
+}
+__device__ __forceinline__ void red_add_f64(double *p, double v) {
+    asm volatile("red.relaxed.gpu.global.add.f64 [%0], %1;" ::"l"(p), "d"(v) : "memory");
 }
 
 __device__ __forceinline__ uint64_t wait_not_busy(const uint64_t *p, uint64_t tag) {

@@ -10,8 +10,10 @@ namespace pf {
 constexpr int kThreads = 256;
 constexpr int kWarps = kThreads / 32;
 
+// Per-CTA counters in 32-bit shared words (native ATOMS; a CTA never sees 2^32
+// events), flushed once as 64-bit global adds.
 struct BlockStats {
-    unsigned long long v[10];
+    unsigned v[10];
     unsigned hist[256];
 };
 
@@ -23,12 +25,14 @@ __device__ __forceinline__ void stats_init(BlockStats &b) {
 // warp-aggregated add of a per-lane predicate into a block counter
 __device__ __forceinline__ void warp_count(BlockStats &b, int slot, bool pred) {
     const unsigned m = __ballot_sync(kFull, pred);
-    if ((threadIdx.x & 31) == 0 && m) atomicAdd(&b.v[slot], static_cast<unsigned long long>(__popc(m)));
+    if ((threadIdx.x & 31) == 0 && m) atomicAdd(&b.v[slot], static_cast<unsigned>(__popc(m)));
 }
 
 __device__ __forceinline__ void stats_flush(const BlockStats &b, int64_t *stats, bool with_hist) {
     for (int k = threadIdx.x; k < 10; k += blockDim.x)
-        if (b.v[k]) atomicAdd(reinterpret_cast<unsigned long long *>(stats + k), b.v[k]);
+        if (b.v[k])
+            atomicAdd(reinterpret_cast<unsigned long long *>(stats + k),
+                      static_cast<unsigned long long>(b.v[k]));
     if (with_hist)
         for (int k = threadIdx.x; k < 256; k += blockDim.x)
             if (b.hist[k])
@@ -63,14 +67,15 @@ insert_frame_kernel(pf_config cfg, pf_vertices v, pf_table fine, pf_table coarse
     // persistent: each block walks 256-vertex tiles; block counters flush once at exit
     const int64_t tiles = (v.n + kThreads - 1) / kThreads;
     for (int64_t tile = blockIdx.x; tile < tiles; tile += gridDim.x) {
-    const int64_t i = tile * kThreads + threadIdx.x;
-    const bool valid = i < v.n;
-    VertexIn x;
-    double val[3] = {0.0, 0.0, 0.0};
+    const int64_t i0 = tile * kThreads + threadIdx.x;
+    const bool valid = i0 < v.n;
+    // tail lanes recompute the last vertex (no divergent key code); warp_insert ignores them
+    const int64_t i = valid ? i0 : v.n - 1;
+    double val[3];
     double du = 0.0, dv = 0.0;
     CellHash hf{0ull, 0u}, hc{0ull, 0u};
-    if (valid) {
-        x = load_vertex(v, i, cfg);
+    {
+        const VertexIn x = load_vertex(v, i, cfg);
 #pragma unroll
         for (int c = 0; c < 3; ++c) val[c] = __ldg(v.contribution + 3 * i + c);
         if (cfg.jitter) {
@@ -97,7 +102,7 @@ insert_frame_kernel(pf_config cfg, pf_vertices v, pf_table fine, pf_table coarse
         if (valid && (threadIdx.x & 31) == static_cast<unsigned>(__ffs(same) - 1)) {
             const unsigned cnt = __popc(same);
             atomicAdd(&bs.hist[pl & 255], cnt);
-            atomicAdd(&bs.v[PF_STAT_PROBE_LEN_SUM], static_cast<unsigned long long>(cnt) * pl);
+            atomicAdd(&bs.v[PF_STAT_PROBE_LEN_SUM], cnt * static_cast<unsigned>(pl));
         }
     }
     if (valid && rf.leader && rf.status == 1) log_eviction(events, event_count, event_cap, i, rf);
@@ -151,7 +156,7 @@ __device__ __forceinline__ void composite(const ResolveArgs &a, int64_t i, int64
 #pragma unroll
     for (int c = 0; c < 3; ++c) {
         const double tp = __ldg(a.v.throughput + 3 * i + c);
-        atomicAdd(a.flat + 3 * pixel + c, dmul(tp, chosen[c]));
+        red_add_f64(a.flat + 3 * pixel + c, dmul(tp, chosen[c]));
     }
     if (a.source) a.source[i] = static_cast<uint8_t>(source);
     if (a.chosen) {
@@ -167,11 +172,12 @@ __global__ void __launch_bounds__(kThreads) resolve_main_kernel(ResolveArgs a) {
     stats_init(bs);
     __syncthreads();
     const pf_config &cfg = a.cfg;
-    const int64_t i = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
-    const bool valid = i < a.v.n;
+    const int64_t i0 = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+    const bool valid = i0 < a.v.n;
+    const int64_t i = valid ? i0 : a.v.n - 1;  // tail lanes shadow the last vertex
     bool fine_ok = false;
     CellKey k{};
-    if (valid) {
+    {
         const VertexIn x = load_vertex(a.v, i, cfg);
         double du = 0.0, dv = 0.0;
         if (cfg.jitter) {
@@ -188,7 +194,7 @@ __global__ void __launch_bounds__(kThreads) resolve_main_kernel(ResolveArgs a) {
         if (s >= 0) {
             const Effective e = effective_at(a.fine, s, cfg.temporal_mode, cfg.ema_alpha, cfg.delta_max);
             const double cnt = e.fcnt;
-            if (cnt >= a.thr) {
+            if (valid && cnt >= a.thr) {
                 fine_ok = true;
                 const bool as_int = eff_is_int(a.fine, cfg.temporal_mode);
                 const bool fixed = a.fine.sum_mode == PF_SUM_FIXED;
@@ -319,7 +325,7 @@ __global__ void __launch_bounds__(kThreads) resolve_fallback_kernel(ResolveArgs 
             ch[c] = src == 1 ? mean_n[c] : (src == 2 ? mean_c[c] : contrib);
         }
         composite(a, row, x.pixel, ch, src);
-        atomicAdd(&bs.v[PF_STAT_SOURCE_FINE + src], 1ull);
+        atomicAdd(&bs.v[PF_STAT_SOURCE_FINE + src], 1u);
         }
         __syncwarp();
     }
@@ -346,6 +352,8 @@ int pf_insert_frame(const pf_config *cfg, const pf_vertices *v, const pf_table *
                     int64_t event_capacity, void *stream) {
     const char *fn = "pf_insert_frame";
     if (int rc = validate_vertices(fn, v, cfg)) return rc;
+    pf_config kc;
+    if (int rc = prepare_config(fn, cfg, &kc)) return rc;
     if (int rc = validate_table(fn, fine)) return rc;
     if (coarse) {
         if (int rc = validate_table(fn, coarse)) return rc;
@@ -363,11 +371,11 @@ int pf_insert_frame(const pf_config *cfg, const pf_vertices *v, const pf_table *
     const unsigned g = static_cast<unsigned>(tiles < cap ? tiles : cap);
     if (fine->sum_mode == PF_SUM_FIXED)
         insert_frame_kernel<true><<<g, kThreads, 0, as_stream(stream)>>>(
-            *cfg, *v, *fine, c, coarse != nullptr, stream_base_accum, frame, stats, events,
+            kc, *v, *fine, c, coarse != nullptr, stream_base_accum, frame, stats, events,
             event_count, event_capacity);
     else
         insert_frame_kernel<false><<<g, kThreads, 0, as_stream(stream)>>>(
-            *cfg, *v, *fine, c, coarse != nullptr, stream_base_accum, frame, stats, events,
+            kc, *v, *fine, c, coarse != nullptr, stream_base_accum, frame, stats, events,
             event_count, event_capacity);
     return check_launch(fn);
 }
@@ -380,6 +388,8 @@ int pf_resolve_frame(const pf_config *cfg, const pf_vertices *v, const pf_table 
                      void *stream) {
     const char *fn = "pf_resolve_frame";
     if (int rc = validate_vertices(fn, v, cfg)) return rc;
+    pf_config kc;
+    if (int rc = prepare_config(fn, cfg, &kc)) return rc;
     if (int rc = validate_table(fn, fine)) return rc;
     if (coarse)
         if (int rc = validate_table(fn, coarse)) return rc;
@@ -395,7 +405,7 @@ int pf_resolve_frame(const pf_config *cfg, const pf_vertices *v, const pf_table 
         if (cudaMemsetAsync(work_count, 0, sizeof(int64_t), st) != cudaSuccess)
             return check_launch(fn);
         ResolveArgs a;
-        a.cfg = *cfg;
+        a.cfg = kc;
         a.v = *v;
         a.fine = *fine;
         a.coarse = coarse ? *coarse : *fine;

@@ -80,14 +80,12 @@ __device__ __forceinline__ LaneInsert warp_insert(const pf_table &t, bool valid,
 #pragma unroll
             for (int c = 0; c < 3; ++c) {
                 if (FIXED)
-                    atomicAdd(reinterpret_cast<unsigned long long *>(
-                                  static_cast<int64_t *>(t.sums) + 3 * s + c),
-                              static_cast<unsigned long long>(qsum[c]));
+                    red_add_u64(static_cast<int64_t *>(t.sums) + 3 * s + c,
+                                static_cast<uint64_t>(qsum[c]));
                 else
-                    atomicAdd(static_cast<double *>(t.sums) + 3 * s + c, fsum[c]);
+                    red_add_f64(static_cast<double *>(t.sums) + 3 * s + c, fsum[c]);
             }
-            atomicAdd(reinterpret_cast<unsigned long long *>(t.counts + s),
-                      static_cast<unsigned long long>(__popc(peers)));
+            red_add_u64(t.counts + s, static_cast<uint64_t>(__popc(peers)));
             st_relaxed_u64(t.last_touch + s, static_cast<uint64_t>(frame));
         }
     }

@@ -4,6 +4,7 @@
 #include <cuda_runtime.h>
 
 #include <cstdint>
+#include <cstring>
 #include <string>
 
 #include "../../include/pathfilter_b200.h"
@@ -43,6 +44,24 @@ inline int validate_vertices(const char *fn, const pf_vertices *v, const pf_conf
 }
 
 inline cudaStream_t as_stream(void *s) { return static_cast<cudaStream_t>(s); }
+
+// Copy of the caller's config with the derived fields the kernels read: lod_ulps[]
+// packs m_k = (bits(2^k) - bits(T[k])) for k = 1..31 in 4-bit fields.  Thresholds
+// must lie in [2^k - 15 ulp, 2^k] (numpy's log2 rounds up at most a few ulps).
+inline int prepare_config(const char *fn, const pf_config *in, pf_config *out) {
+    *out = *in;
+    out->lod_ulps[0] = out->lod_ulps[1] = 0;
+    for (int k = 1; k < 32; ++k) {
+        const double p = static_cast<double>(1ull << k);
+        int64_t bp, bt;
+        std::memcpy(&bp, &p, 8);
+        std::memcpy(&bt, &in->lod_threshold[k], 8);
+        const int64_t m = bp - bt;
+        if (m < 0 || m > 15) return fail_arg(fn, "lod_threshold[k] must be within 15 ulps below 2^k");
+        out->lod_ulps[k >> 4] |= static_cast<uint64_t>(m) << ((k & 15) * 4);
+    }
+    return PF_OK;
+}
 
 inline unsigned blocks_for(int64_t n, int threads) {
     return static_cast<unsigned>((n + threads - 1) / threads);

@@ -248,29 +248,62 @@ template <bool FIXED>
 __global__ void __launch_bounds__(kThreads)
 begin_frame_kernel(pf_table t, int64_t frame, int mode, double ema, double delta_max,
                    int32_t sample_cap, int64_t *horizon_clears) {
-    // grid-stride over pairs of slots: one 16-byte tag load per thread per step
-    const int64_t pairs = t.capacity / 2;
-    for (int64_t p = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x; ;
-         p += static_cast<int64_t>(gridDim.x) * blockDim.x) {
-        const bool live = p < pairs;
-        ulonglong2 tg = make_ulonglong2(kEmptyTag, kEmptyTag);
-        if (live) tg = reinterpret_cast<const ulonglong2 *>(t.tags)[p];
-        int cleared = 0;
-        if (tg.x != kEmptyTag)
-            cleared += fold_slot<FIXED>(t, 2 * p, tg.x, frame, mode, ema, delta_max, sample_cap);
-        if (tg.y != kEmptyTag)
-            cleared += fold_slot<FIXED>(t, 2 * p + 1, tg.y, frame, mode, ema, delta_max, sample_cap);
-        const unsigned any = __ballot_sync(kFull, cleared != 0);
-        if (any) {
-            int c = cleared;
+    // Each step a CTA streams kChunk tags with 16-byte loads, compacts the occupied
+    // slots (a few percent) into a shared queue, then folds the queue with all its
+    // threads -- the dependent per-slot loads run fully parallel instead of one
+    // latency chain per sweeping thread.
+    constexpr int kPairsPerThread = 4;
+    constexpr int kChunk = kThreads * 2 * kPairsPerThread;
+    __shared__ int64_t q_slot[kChunk];
+    __shared__ uint64_t q_tag[kChunk];
+    __shared__ int q_n;
+    __shared__ int block_clears;
+    if (threadIdx.x == 0) block_clears = 0;
+    const int lane = threadIdx.x & 31;
+    const ulonglong2 *tags2 = reinterpret_cast<const ulonglong2 *>(t.tags);
+    int cleared = 0;
+    for (int64_t base = static_cast<int64_t>(blockIdx.x) * kChunk; base < t.capacity;
+         base += static_cast<int64_t>(gridDim.x) * kChunk) {
+        if (threadIdx.x == 0) q_n = 0;
+        __syncthreads();
+        ulonglong2 tg[kPairsPerThread];
 #pragma unroll
-            for (int off = 16; off > 0; off >>= 1) c += __shfl_xor_sync(kFull, c, off);
-            if ((threadIdx.x & 31) == 0 && horizon_clears)
-                atomicAdd(reinterpret_cast<unsigned long long *>(horizon_clears),
-                          static_cast<unsigned long long>(c));
+        for (int j = 0; j < kPairsPerThread; ++j) {
+            const int64_t p = base / 2 + j * kThreads + threadIdx.x;
+            tg[j] = 2 * p < t.capacity ? tags2[p] : make_ulonglong2(kEmptyTag, kEmptyTag);
         }
-        if (!__any_sync(kFull, p + static_cast<int64_t>(gridDim.x) * blockDim.x < pairs)) break;
+#pragma unroll
+        for (int j = 0; j < kPairsPerThread; ++j) {
+            const int64_t p = base / 2 + j * kThreads + threadIdx.x;
+#pragma unroll
+            for (int h = 0; h < 2; ++h) {
+                const uint64_t tag = h ? tg[j].y : tg[j].x;
+                const bool occ = tag != kEmptyTag;
+                const unsigned m = __ballot_sync(kFull, occ);
+                if (m) {
+                    int q0 = 0;
+                    if (lane == __ffs(m) - 1) q0 = atomicAdd(&q_n, __popc(m));
+                    q0 = __shfl_sync(kFull, q0, __ffs(m) - 1);
+                    if (occ) {
+                        const int q = q0 + __popc(m & ((1u << lane) - 1u));
+                        q_slot[q] = 2 * p + h;
+                        q_tag[q] = tag;
+                    }
+                }
+            }
+        }
+        __syncthreads();
+        const int n_q = q_n;
+        for (int q = threadIdx.x; q < n_q; q += kThreads)
+            cleared += fold_slot<FIXED>(t, q_slot[q], q_tag[q], frame, mode, ema, delta_max,
+                                        sample_cap);
+        __syncthreads();
     }
+    if (cleared) atomicAdd(&block_clears, cleared);
+    __syncthreads();
+    if (threadIdx.x == 0 && block_clears && horizon_clears)
+        atomicAdd(reinterpret_cast<unsigned long long *>(horizon_clears),
+                  static_cast<unsigned long long>(block_clears));
 }
 
 // begin_frame for one occupied slot (src/table.py:242-298); returns 1 when the slot
@@ -491,9 +524,11 @@ int pf_make_key_arrays(const pf_config *cfg, const pf_vertices *v, const double 
     const char *fn = "pf_make_key_arrays";
     if (int rc = validate_vertices(fn, v, cfg)) return rc;
     if (out == nullptr) return fail_arg(fn, "out is NULL");
+    pf_config kc;
+    if (int rc = prepare_config(fn, cfg, &kc)) return rc;
     if (v->n == 0) return PF_OK;
     keys_kernel<<<blocks_for(v->n, kThreads), kThreads, 0, as_stream(stream)>>>(
-        *cfg, *v, u1, u2, 0, 0ull, level_delta, *out);
+        kc, *v, u1, u2, 0, 0ull, level_delta, *out);
     return check_launch(fn);
 }
 
@@ -502,9 +537,11 @@ int pf_vertex_keys(const pf_config *cfg, const pf_vertices *v, uint64_t stream_b
     const char *fn = "pf_vertex_keys";
     if (int rc = validate_vertices(fn, v, cfg)) return rc;
     if (out == nullptr) return fail_arg(fn, "out is NULL");
+    pf_config kc;
+    if (int rc = prepare_config(fn, cfg, &kc)) return rc;
     if (v->n == 0) return PF_OK;
     keys_kernel<<<blocks_for(v->n, kThreads), kThreads, 0, as_stream(stream)>>>(
-        *cfg, *v, nullptr, nullptr, 1, stream_base, level_delta, *out);
+        kc, *v, nullptr, nullptr, 1, stream_base, level_delta, *out);
     return check_launch(fn);
 }
 
@@ -537,7 +574,7 @@ int pf_begin_frame(const pf_table *t, int64_t frame, int32_t mode, double ema_al
     const char *fn = "pf_begin_frame";
     if (int rc = validate_table(fn, t)) return rc;
     if (mode < PF_INTEGRATE || mode > PF_HYBRID) return fail_arg(fn, "unknown temporal mode");
-    int64_t blocks = (t->capacity / 2 + kThreads - 1) / kThreads;
+    int64_t blocks = (t->capacity + 8 * kThreads - 1) / (8 * kThreads);  // kChunk slots each
     const int64_t cap = static_cast<int64_t>(sm_count()) * 8;
     const unsigned g = static_cast<unsigned>(blocks < cap ? blocks : cap);
     if (t->sum_mode == PF_SUM_FIXED)
