@@ -172,22 +172,31 @@ int pf_hash_arrays(const int64_t *qx, const int64_t *qy, const int64_t *qz,
 /* Fused accumulate_phase (src/pipeline.py:152-175): keys (stream 2) for the fine
  * and, if coarse != NULL, the coarse table (level + coarse_delta), each inserted
  * with warp-merged atomics.  stats: int64[PF_STAT_COUNT] accumulated (not cleared);
- * events: optional eviction log of capacity `event_capacity` with its int64 counter. */
+ * events: optional eviction log of capacity `event_capacity` with its int64 counter.
+ * abort_flag (device int32, may be NULL): when nonzero at launch the kernel leaves
+ * the tables untouched (set by pf_check_contributions for invalid input).
+ * lookup_index/lookup_fp (may be NULL): also emit the resolve phase's fine lookup
+ * key (stream_base_lookup, level_delta 0) for every vertex, so pf_resolve_frame
+ * does not rebuild it from the vertex buffer. */
 int pf_insert_frame(const pf_config *cfg, const pf_vertices *v, const pf_table *fine,
                     const pf_table *coarse, uint64_t stream_base_accum, int64_t frame,
                     int64_t *stats, pf_evict_event *events, int64_t *event_count,
-                    int64_t event_capacity, void *stream);
+                    int64_t event_capacity, const int32_t *abort_flag,
+                    uint64_t stream_base_lookup, uint64_t *lookup_index, uint32_t *lookup_fp,
+                    void *stream);
 
 /* Fused resolve_phase (src/pipeline.py:207-283): lookup keys, fine rung, 3x3x3
  * neighbourhood, coarse rung, ladder, composite.  flat: float64[n_pixels][3]
- * scratch; work: int64 scratch of 6*n entries plus work_count (int64[1]);
- * image = base_image + flat/spp.  source (u8[n]) and chosen (f64[n][3]) may be NULL. */
+ * scratch; work: int64 scratch of n entries plus work_count (int64[1]);
+ * image = base_image + flat/spp.  source (u8[n]) and chosen (f64[n][3]) may be NULL.
+ * lookup_index/lookup_fp: the keys pf_insert_frame emitted for the same vertices and
+ * stream_base_lookup, or NULL to build them here. */
 int pf_resolve_frame(const pf_config *cfg, const pf_vertices *v, const pf_table *fine,
                      const pf_table *coarse, uint64_t stream_base_lookup,
                      uint64_t stream_base_coarse, int64_t spp, const double *base_image,
                      int64_t n_pixels, double *image, double *flat, int64_t *work,
                      int64_t *work_count, uint8_t *source, double *chosen, int64_t *stats,
-                     void *stream);
+                     const uint64_t *lookup_index, const uint32_t *lookup_fp, void *stream);
 
 /* VoxelTable.effective (src/table.py:205-238) over all slots.  eff_sum is int64 for
  * (integrate, fixed) else float64; eff_count is int64 for integrate else float64. */

@@ -123,9 +123,10 @@ def lib() -> ctypes.CDLL:
     L.pf_make_key_arrays.argtypes = [vp, vp, vp, vp, i32, vp, vp]
     L.pf_vertex_keys.argtypes = [vp, vp, u64, i32, vp, vp]
     L.pf_hash_arrays.argtypes = [vp, vp, vp, vp, vp, vp, i64, vp, vp, vp]
-    L.pf_insert_frame.argtypes = [vp, vp, vp, vp, u64, i64, vp, vp, vp, i64, vp]
+    L.pf_insert_frame.argtypes = [vp, vp, vp, vp, u64, i64, vp, vp, vp, i64, vp, u64, vp, vp,
+                                  vp]
     L.pf_resolve_frame.argtypes = [vp, vp, vp, vp, u64, u64, i64, vp, i64, vp, vp, vp, vp,
-                                   vp, vp, vp, vp]
+                                   vp, vp, vp, vp, vp, vp]
     L.pf_effective.argtypes = [vp, i32, dbl, dbl, vp, vp, vp]
     L.pf_begin_frame.argtypes = [vp, i64, i32, dbl, dbl, i32, vp, vp]
     L.pf_count_occupied.argtypes = [vp, i64, vp, vp]

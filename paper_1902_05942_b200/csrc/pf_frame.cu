@@ -60,8 +60,10 @@ template <bool FIXED>
 __global__ void __launch_bounds__(kThreads)
 insert_frame_kernel(pf_config cfg, pf_vertices v, pf_table fine, pf_table coarse, int has_coarse,
                     uint64_t h0, int64_t frame, int64_t *stats, pf_evict_event *events,
-                    int64_t *event_count, int64_t event_cap) {
+                    int64_t *event_count, int64_t event_cap, const int32_t *abort_flag,
+                    uint64_t h0_lookup, uint64_t *lk_index, uint32_t *lk_fp) {
     __shared__ BlockStats bs;
+    if (abort_flag != nullptr && *abort_flag != 0) return;  // invalid input: no mutation
     stats_init(bs);
     __syncthreads();
     // persistent: each block walks 256-vertex tiles; block counters flush once at exit
@@ -90,6 +92,20 @@ insert_frame_kernel(pf_config cfg, pf_vertices v, pf_table fine, pf_table coarse
         if (has_coarse) {
             const CellKey kc = make_key(cfg, x, ks, cfg.jitter, du, dv, cfg.coarse_delta, jt);
             hc = key_hash(kc, ks);
+        }
+        if (lk_index != nullptr) {
+            // the resolve phase's lookup key: independent jitter stream, same ONB / aux
+            double lu = 0.0, lv = 0.0;
+            if (cfg.jitter) {
+                double u1, u2;
+                jitter_draws(h0_lookup, x.pixel, x.sample, u1, u2);
+                disc_offset(u1, u2, lu, lv);
+            }
+            const CellHash hl = key_hash(make_key(cfg, x, ks, cfg.jitter, lu, lv, 0, jt), ks);
+            if (valid) {
+                lk_index[i] = hl.index;
+                lk_fp[i] = hl.fp;
+            }
         }
     }
     const LaneInsert rf = warp_insert<FIXED>(fine, valid, hf.index, hf.fp, val, frame);
@@ -142,7 +158,33 @@ struct ResolveArgs {
     double *chosen;
     int64_t *stats;
     double thr;
+    const uint64_t *lk_index;  // precomputed lookup keys (or NULL)
+    const uint32_t *lk_fp;
 };
+
+struct KeyAndHash {
+    CellKey first;
+    CellHash second;
+};
+
+// The fine lookup key of one vertex: jitter stream 3 when jitter is on
+// (src/pipeline.py:222-225), level_delta 0.
+__device__ __forceinline__ KeyAndHash lookup_key(const ResolveArgs &a, int64_t row) {
+    const pf_config &cfg = a.cfg;
+    const VertexIn x = load_vertex(a.v, row, cfg);
+    double du = 0.0, dv = 0.0;
+    if (cfg.jitter) {
+        double u1, u2;
+        jitter_draws(a.h0_lookup, x.pixel, x.sample, u1, u2);
+        disc_offset(u1, u2, du, dv);
+    }
+    const KeyShared ks = key_shared(cfg, x);
+    double jt[3];
+    KeyAndHash r;
+    r.first = make_key(cfg, x, ks, cfg.jitter, du, dv, 0, jt);
+    r.second = key_hash(r.first, ks);
+    return r;
+}
 
 // _mean_rows (src/pipeline.py:196-200) for one row.
 __device__ __forceinline__ double row_mean(double sum, double cnt, bool fixed) {
@@ -176,19 +218,14 @@ __global__ void __launch_bounds__(kThreads) resolve_main_kernel(ResolveArgs a) {
     const bool valid = i0 < a.v.n;
     const int64_t i = valid ? i0 : a.v.n - 1;  // tail lanes shadow the last vertex
     bool fine_ok = false;
-    CellKey k{};
     {
-        const VertexIn x = load_vertex(a.v, i, cfg);
-        double du = 0.0, dv = 0.0;
-        if (cfg.jitter) {
-            double u1, u2;
-            jitter_draws(a.h0_lookup, x.pixel, x.sample, u1, u2);
-            disc_offset(u1, u2, du, dv);
+        CellHash h;
+        if (a.lk_index != nullptr) {  // keys emitted by the insert pass
+            h.index = __ldg(reinterpret_cast<const unsigned long long *>(a.lk_index) + i);
+            h.fp = __ldg(a.lk_fp + i);
+        } else {
+            h = lookup_key(a, i).second;
         }
-        const KeyShared ks = key_shared(cfg, x);
-        double jt[3];
-        k = make_key(cfg, x, ks, cfg.jitter, du, dv, 0, jt);
-        const CellHash h = key_hash(k, ks);
         const int64_t s = probe_lookup(a.fine.tags, static_cast<uint64_t>(a.fine.capacity) - 1,
                                        a.fine.probe_limit, h.index, h.fp);
         if (s >= 0) {
@@ -201,10 +238,11 @@ __global__ void __launch_bounds__(kThreads) resolve_main_kernel(ResolveArgs a) {
                 double m[3];
 #pragma unroll
                 for (int c = 0; c < 3; ++c) m[c] = row_mean(eff_sum_f64(e, as_int, c), cnt, fixed);
-                composite(a, i, x.pixel, m, 0);
+                composite(a, i, __ldg(a.v.pixel + i), m, 0);
             }
         }
     }
+    // rows below the threshold: append the row id to the work list (warp-aggregated)
     const bool need = valid && !fine_ok;
     const unsigned m = __ballot_sync(kFull, need);
     if (m) {
@@ -214,15 +252,7 @@ __global__ void __launch_bounds__(kThreads) resolve_main_kernel(ResolveArgs a) {
             base = atomicAdd(reinterpret_cast<unsigned long long *>(a.work_count),
                              static_cast<unsigned long long>(__popc(m)));
         base = __shfl_sync(kFull, base, __ffs(m) - 1);
-        if (need) {
-            int64_t *w = a.work + 6 * (static_cast<int64_t>(base) + __popc(m & ((1u << lane) - 1u)));
-            w[0] = i;
-            w[1] = k.q[0];
-            w[2] = k.q[1];
-            w[3] = k.q[2];
-            w[4] = k.level;
-            w[5] = static_cast<int64_t>(k.aux);
-        }
+        if (need) a.work[static_cast<int64_t>(base) + __popc(m & ((1u << lane) - 1u))] = i;
     }
     warp_count(bs, PF_STAT_SOURCE_FINE, valid && fine_ok);
     warp_count(bs, PF_STAT_FALLBACK_ROWS, need);
@@ -247,14 +277,27 @@ __global__ void __launch_bounds__(kThreads) resolve_fallback_kernel(ResolveArgs 
     const bool fixed = a.fine.sum_mode == PF_SUM_FIXED;
     const uint64_t fmask = static_cast<uint64_t>(a.fine.capacity) - 1;
     for (int64_t w = warp0; w < n_work; w += nwarps) {
-        const int64_t *rec = a.work + 6 * w;
-        const int64_t row = rec[0];
+        const int64_t row = a.work[w];
+        // the row's lookup key (rebuilt by lane 0, broadcast to the 27 probing lanes)
+        int64_t kq[3] = {0, 0, 0}, klev = 0, kaux = 0;
+        if (lane == 0) {
+            const CellKey k = lookup_key(a, row).first;
+            kq[0] = k.q[0];
+            kq[1] = k.q[1];
+            kq[2] = k.q[2];
+            klev = k.level;
+            kaux = static_cast<int64_t>(k.aux);
+        }
+#pragma unroll
+        for (int c = 0; c < 3; ++c) kq[c] = __shfl_sync(kFull, static_cast<long long>(kq[c]), 0);
+        klev = __shfl_sync(kFull, static_cast<long long>(klev), 0);
+        kaux = __shfl_sync(kFull, static_cast<long long>(kaux), 0);
         bool found = false;
         Effective e{};
         if (lane < 27) {
             const int dx = lane / 9 - 1, dy = (lane / 3) % 3 - 1, dz = lane % 3 - 1;
-            const CellHash h = cell_hash(rec[1] + dx, rec[2] + dy, rec[3] + dz, rec[4],
-                                         static_cast<uint64_t>(rec[5]), 0, 0u);
+            const CellHash h = cell_hash(kq[0] + dx, kq[1] + dy, kq[2] + dz, klev,
+                                         static_cast<uint64_t>(kaux), 0, 0u);
             const int64_t s = probe_lookup(a.fine.tags, fmask, a.fine.probe_limit, h.index, h.fp);
             if (s >= 0) {
                 found = true;
@@ -349,8 +392,12 @@ extern "C" {
 int pf_insert_frame(const pf_config *cfg, const pf_vertices *v, const pf_table *fine,
                     const pf_table *coarse, uint64_t stream_base_accum, int64_t frame,
                     int64_t *stats, pf_evict_event *events, int64_t *event_count,
-                    int64_t event_capacity, void *stream) {
+                    int64_t event_capacity, const int32_t *abort_flag,
+                    uint64_t stream_base_lookup, uint64_t *lookup_index, uint32_t *lookup_fp,
+                    void *stream) {
     const char *fn = "pf_insert_frame";
+    if ((lookup_index == nullptr) != (lookup_fp == nullptr))
+        return fail_arg(fn, "lookup_index and lookup_fp go together");
     if (int rc = validate_vertices(fn, v, cfg)) return rc;
     pf_config kc;
     if (int rc = prepare_config(fn, cfg, &kc)) return rc;
@@ -372,11 +419,11 @@ int pf_insert_frame(const pf_config *cfg, const pf_vertices *v, const pf_table *
     if (fine->sum_mode == PF_SUM_FIXED)
         insert_frame_kernel<true><<<g, kThreads, 0, as_stream(stream)>>>(
             kc, *v, *fine, c, coarse != nullptr, stream_base_accum, frame, stats, events,
-            event_count, event_capacity);
+            event_count, event_capacity, abort_flag, stream_base_lookup, lookup_index, lookup_fp);
     else
         insert_frame_kernel<false><<<g, kThreads, 0, as_stream(stream)>>>(
             kc, *v, *fine, c, coarse != nullptr, stream_base_accum, frame, stats, events,
-            event_count, event_capacity);
+            event_count, event_capacity, abort_flag, stream_base_lookup, lookup_index, lookup_fp);
     return check_launch(fn);
 }
 
@@ -385,8 +432,10 @@ int pf_resolve_frame(const pf_config *cfg, const pf_vertices *v, const pf_table 
                      uint64_t stream_base_coarse, int64_t spp, const double *base_image,
                      int64_t n_pixels, double *image, double *flat, int64_t *work,
                      int64_t *work_count, uint8_t *source, double *chosen, int64_t *stats,
-                     void *stream) {
+                     const uint64_t *lookup_index, const uint32_t *lookup_fp, void *stream) {
     const char *fn = "pf_resolve_frame";
+    if ((lookup_index == nullptr) != (lookup_fp == nullptr))
+        return fail_arg(fn, "lookup_index and lookup_fp go together");
     if (int rc = validate_vertices(fn, v, cfg)) return rc;
     pf_config kc;
     if (int rc = prepare_config(fn, cfg, &kc)) return rc;
@@ -419,6 +468,8 @@ int pf_resolve_frame(const pf_config *cfg, const pf_vertices *v, const pf_table 
         a.chosen = chosen;
         a.stats = stats;
         a.thr = static_cast<double>(cfg->low_count_threshold > 1 ? cfg->low_count_threshold : 1);
+        a.lk_index = lookup_index;
+        a.lk_fp = lookup_fp;
         resolve_main_kernel<<<blocks_for(v->n, kThreads), kThreads, 0, st>>>(a);
         if (int rc = check_launch(fn)) return rc;
         int64_t fb_blocks = (v->n + kWarps - 1) / kWarps;

@@ -91,7 +91,17 @@ class FilterConfig:
         return self.base_voxel * float(2 ** level)
 
     def to_c(self) -> _lib.PfConfig:
-        """The pf_config the kernels read; c_lod evaluated as src/keys.py:324 does."""
+        """The pf_config the kernels read; c_lod evaluated as src/keys.py:324 does.
+        Cached per field values (it is rebuilt only when a knob changes)."""
+        key = tuple(getattr(self, f) for f in self.__dataclass_fields__)
+        cached = self.__dict__.get("_c_cache")
+        if cached is not None and cached[0] == key:
+            return cached[1]
+        c = self._build_c()
+        self.__dict__["_c_cache"] = (key, c)
+        return c
+
+    def _build_c(self) -> _lib.PfConfig:
         c = _lib.PfConfig()
         c.c_lod = self.footprint_scale * self.s_pixels / self.base_voxel
         c.base_voxel = float(self.base_voxel)

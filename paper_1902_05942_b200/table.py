@@ -113,6 +113,15 @@ class VoxelTable:
     # -- C view ---------------------------------------------------------------
 
     def c_table(self) -> _lib.PfTable:
+        key = (self.tags.data_ptr(), self.probe_limit, self.evict_min_age, self.evict_horizon)
+        cached = self.__dict__.get("_c_cache")
+        if cached is not None and cached[0] == key:
+            return cached[1]
+        t = self._build_c()
+        self.__dict__["_c_cache"] = (key, t)
+        return t
+
+    def _build_c(self) -> _lib.PfTable:
         t = _lib.PfTable()
         t.tags = self.tags.data_ptr()
         t.sums = self.sums.data_ptr()
