@@ -190,13 +190,17 @@ int pf_insert_frame(const pf_config *cfg, const pf_vertices *v, const pf_table *
  * scratch; work: int64 scratch of n entries plus work_count (int64[1]);
  * image = base_image + flat/spp.  source (u8[n]) and chosen (f64[n][3]) may be NULL.
  * lookup_index/lookup_fp: the keys pf_insert_frame emitted for the same vertices and
- * stream_base_lookup, or NULL to build them here. */
+ * stream_base_lookup, or NULL to build them here.
+ * eff_records (may be NULL): scratch of 4 * fine->capacity uint64; when given, the
+ * fine table's effective (sum, count) is computed once per occupied slot into one
+ * 32-byte record that every lookup then reads. */
 int pf_resolve_frame(const pf_config *cfg, const pf_vertices *v, const pf_table *fine,
                      const pf_table *coarse, uint64_t stream_base_lookup,
                      uint64_t stream_base_coarse, int64_t spp, const double *base_image,
                      int64_t n_pixels, double *image, double *flat, int64_t *work,
                      int64_t *work_count, uint8_t *source, double *chosen, int64_t *stats,
-                     const uint64_t *lookup_index, const uint32_t *lookup_fp, void *stream);
+                     const uint64_t *lookup_index, const uint32_t *lookup_fp,
+                     uint64_t *eff_records, void *stream);
 
 /* VoxelTable.effective (src/table.py:205-238) over all slots.  eff_sum is int64 for
  * (integrate, fixed) else float64; eff_count is int64 for integrate else float64. */

@@ -17,7 +17,7 @@ _ROOT = os.path.dirname(_PKG)
 LIB_PATH = os.environ.get("PF_LIB") or os.path.join(_PKG, "libpf_b200.so")
 SOURCES = [os.path.join(_PKG, "csrc", f) for f in ("pf_common.cu", "pf_table.cu", "pf_frame.cu")]
 HEADERS = [os.path.join(_PKG, "csrc", f) for f in ("pf_device.cuh", "pf_insert.cuh",
-                                                    "pf_internal.cuh")] + \
+                                                    "pf_internal.cuh", "pf_sweep.cuh")] + \
     [os.path.join(_ROOT, "include", "pathfilter_b200.h")]
 NVCC_FLAGS = ["-gencode", "arch=compute_100a,code=sm_100a", "-O3", "-lineinfo",
               "-fmad=false", "-std=c++17", "-Xcompiler", "-fPIC", "-shared"]
@@ -126,7 +126,7 @@ def lib() -> ctypes.CDLL:
     L.pf_insert_frame.argtypes = [vp, vp, vp, vp, u64, i64, vp, vp, vp, i64, vp, u64, vp, vp,
                                   vp]
     L.pf_resolve_frame.argtypes = [vp, vp, vp, vp, u64, u64, i64, vp, i64, vp, vp, vp, vp,
-                                   vp, vp, vp, vp, vp, vp]
+                                   vp, vp, vp, vp, vp, vp, vp]
     L.pf_effective.argtypes = [vp, i32, dbl, dbl, vp, vp, vp]
     L.pf_begin_frame.argtypes = [vp, i64, i32, dbl, dbl, i32, vp, vp]
     L.pf_count_occupied.argtypes = [vp, i64, vp, vp]

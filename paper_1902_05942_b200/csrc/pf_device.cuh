@@ -59,12 +59,16 @@ __device__ __forceinline__ double ddiv(double a, double b) { return __ddiv_rn(a,
 // Three FP64 ops instead of a full division when the reciprocal is shared; zero,
 // huge and tiny numerators (outside the theorem's no-underflow range) take __ddiv_rn.
 // Verified bitwise against __ddiv_rn by pf_selftest_division (tests/test_gpu_parity.py).
+// Out of line: the full IEEE division is a cold path, kept out of the hot loops'
+// instruction footprint.
+static __device__ __noinline__ double ddiv_cold(double x, double y) { return __ddiv_rn(x, y); }
+
 __device__ __forceinline__ double div_rcp(double x, double y, double r) {
     const double ax = fabs(x);
     if (ax == 0.0)
         return __dmul_rn(x, r);  // signed zero: sign(x) * sign(y), like IEEE division
     if (!(ax > 0x1p-900 && ax < 0x1p+900))
-        return __ddiv_rn(x, y);
+        return ddiv_cold(x, y);
     const double q0 = __dmul_rn(x, r);
     const double rem = __fma_rn(-q0, y, x);
     return __fma_rn(rem, r, q0);
@@ -245,24 +249,74 @@ struct VertexIn {
     double omega[3];
 };
 
+// ------------------------------------------------------------------ L2 residency
+//
+// The vertex stream is read exactly once per pass; the voxel tables and the
+// composite buffer are re-touched all frame.  Stream loads therefore carry an L2
+// evict_first policy and table/composite updates an evict_last one, so a 1 GB
+// vertex buffer does not flush the ~40 MB of live table lines out of the 126 MB L2.
+__device__ __forceinline__ uint64_t l2_evict_first() {
+    uint64_t p;
+    asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(p));
+    return p;
+}
+__device__ __forceinline__ uint64_t l2_evict_last() {
+    uint64_t p;
+    asm volatile("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;" : "=l"(p));
+    return p;
+}
+__device__ __forceinline__ double ld_stream(const double *p, uint64_t pol) {
+    double d;
+    asm volatile("ld.global.nc.L1::no_allocate.L2::cache_hint.f64 %0, [%1], %2;"
+                 : "=d"(d) : "l"(p), "l"(pol));
+    return d;
+}
+__device__ __forceinline__ int64_t ld_stream(const int64_t *p, uint64_t pol) {
+    int64_t d;
+    asm volatile("ld.global.nc.L1::no_allocate.L2::cache_hint.s64 %0, [%1], %2;"
+                 : "=l"(d) : "l"(p), "l"(pol));
+    return d;
+}
+__device__ __forceinline__ uint64_t ld_stream(const uint64_t *p, uint64_t pol) {
+    uint64_t d;
+    asm volatile("ld.global.nc.L1::no_allocate.L2::cache_hint.u64 %0, [%1], %2;"
+                 : "=l"(d) : "l"(p), "l"(pol));
+    return d;
+}
+__device__ __forceinline__ uint32_t ld_stream(const uint32_t *p, uint64_t pol) {
+    uint32_t d;
+    asm volatile("ld.global.nc.L1::no_allocate.L2::cache_hint.u32 %0, [%1], %2;"
+                 : "=r"(d) : "l"(p), "l"(pol));
+    return d;
+}
+
+__device__ __forceinline__ void prefetch_l2(const void *p) {
+    asm volatile("prefetch.global.L2 [%0];" ::"l"(p));
+}
+
 __device__ __forceinline__ VertexIn load_vertex(const pf_vertices &v, int64_t i,
-                                                const pf_config &cfg) {
+                                                const pf_config &cfg, uint64_t pol) {
     VertexIn x;
 #pragma unroll
     for (int c = 0; c < 3; ++c) {
-        x.pos[c] = __ldg(v.position + 3 * i + c);
-        x.nrm[c] = __ldg(v.normal + 3 * i + c);
+        x.pos[c] = ld_stream(v.position + 3 * i + c, pol);
+        x.nrm[c] = ld_stream(v.normal + 3 * i + c, pol);
         x.omega[c] = 0.0;
     }
-    x.dist = __ldg(v.camera_distance + i);
-    x.pixel = __ldg(v.pixel + i);
-    x.sample = __ldg(v.sample + i);
-    x.layer = (v.layer_id != nullptr) ? __ldg(v.layer_id + i) : 0;
+    x.dist = ld_stream(v.camera_distance + i, pol);
+    x.pixel = ld_stream(v.pixel + i, pol);
+    x.sample = ld_stream(v.sample + i, pol);
+    x.layer = (v.layer_id != nullptr) ? ld_stream(v.layer_id + i, pol) : 0;
     if (cfg.include_incident_angle && v.omega_r != nullptr) {
 #pragma unroll
-        for (int c = 0; c < 3; ++c) x.omega[c] = __ldg(v.omega_r + 3 * i + c);
+        for (int c = 0; c < 3; ++c) x.omega[c] = ld_stream(v.omega_r + 3 * i + c, pol);
     }
     return x;
+}
+
+__device__ __forceinline__ VertexIn load_vertex(const pf_vertices &v, int64_t i,
+                                                const pf_config &cfg) {
+    return load_vertex(v, i, cfg, l2_evict_first());
 }
 
 // Level-independent part of a key set: ONB, aux, structured fp bin.
@@ -350,11 +404,16 @@ __device__ __forceinline__ void st_relaxed_u64(void *p, uint64_t v) {
 
 // Fire-and-forget L2 reductions (RED, no return value): nvcc otherwise emits ATOMG
 // with a result round trip for 64-bit atomicAdd even when the result is unused.
-__device__ __forceinline__ void red_add_u64(void *p, uint64_t v) {
-    asm volatile("red.relaxed.gpu.global.add.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
+// `pol` is an L2 cache policy (l2_evict_last() keeps table / composite lines resident).
+__device__ __forceinline__ void red_add_u64(void *p, uint64_t v, uint64_t pol) {
+    asm volatile("red.relaxed.gpu.global.add.L2::cache_hint.u64 [%0], %1, %2;" ::"l"(p), "l"(v),
+                 "l"(pol)
+                 : "memory");
 }
-__device__ __forceinline__ void red_add_f64(double *p, double v) {
-    asm volatile("red.relaxed.gpu.global.add.f64 [%0], %1;" ::"l"(p), "d"(v) : "memory");
+__device__ __forceinline__ void red_add_f64(double *p, double v, uint64_t pol) {
+    asm volatile("red.relaxed.gpu.global.add.L2::cache_hint.f64 [%0], %1, %2;" ::"l"(p), "d"(v),
+                 "l"(pol)
+                 : "memory");
 }
 
 __device__ __forceinline__ uint64_t wait_not_busy(const uint64_t *p, uint64_t tag) {
@@ -387,13 +446,33 @@ __device__ __forceinline__ void zero_cell(const pf_table &t, int64_t s) {
     st_relaxed_u64(t.deltas + s, 0ull);
 }
 
+// Eviction (cold path, out of line): CAS the victim's exact tag to BUSY, wipe the
+// cell, publish the new tag.  Returns the victim's last_touch, or INT64_MIN when the
+// victim changed before the CAS.
+static __device__ __noinline__ int64_t evict_cell(const pf_table &t, int64_t victim,
+                                                  uint64_t victim_tag, uint64_t incoming) {
+    uint64_t *vp = t.tags + victim;
+    const uint64_t old = atomicCAS(reinterpret_cast<unsigned long long *>(vp), victim_tag,
+                                   kBusyTag);
+    if (old != victim_tag)
+        return INT64_MIN;
+    const int64_t touch = ld_relaxed_i64(t.last_touch + victim);
+    zero_cell(t, victim);
+    __threadfence();
+    st_release(vp, incoming);
+    return touch;
+}
+
 // Probe / claim / evict for one key (src/_native.pyx:209-247) on the live table.
 // Concurrency: a claim is one 64-bit CAS of the whole tag (EMPTY -> FRESH|fp); an
 // eviction CASes the victim's exact tag to BUSY, wipes the cell, then publishes
 // FRESH|fp with release order, so no accumulate lands in a half-wiped cell.  A lost
 // victim CAS re-probes the window (what a sequential caller would see) instead of
 // the reference's racy give-up.
-__device__ __forceinline__ InsertResult probe_insert(const pf_table &t, uint64_t idx, uint32_t fp) {
+// `home_tag` is the caller's early (prefetched) load of tags[home]; it only seeds the
+// first probe of the first attempt and is re-read after any contention.
+__device__ __forceinline__ InsertResult probe_insert(const pf_table &t, uint64_t idx, uint32_t fp,
+                                                     uint64_t home_tag) {
     const uint64_t mask = static_cast<uint64_t>(t.capacity) - 1;
     const uint64_t home = idx & mask;
     const uint64_t want = static_cast<uint64_t>(fp);
@@ -409,7 +488,8 @@ __device__ __forceinline__ InsertResult probe_insert(const pf_table &t, uint64_t
         uint64_t victim_tag = 0;
         for (int j = 0; j < t.probe_limit; ++j) {
             const uint64_t s = (home + static_cast<uint64_t>(j)) & mask;
-            uint64_t tag = wait_not_busy(t.tags + s, ld_relaxed(t.tags + s));
+            uint64_t tag = (attempt == 0 && j == 0) ? home_tag : ld_relaxed(t.tags + s);
+            tag = wait_not_busy(t.tags + s, tag);
             if (tag == kEmptyTag) {
                 const uint64_t old = atomicCAS(reinterpret_cast<unsigned long long *>(t.tags + s),
                                                kEmptyTag, incoming);
@@ -438,14 +518,9 @@ __device__ __forceinline__ InsertResult probe_insert(const pf_table &t, uint64_t
         }
         if (victim < 0)
             return r;  // status 2, no mutation
-        uint64_t *vp = t.tags + victim;
-        const uint64_t old = atomicCAS(reinterpret_cast<unsigned long long *>(vp), victim_tag,
-                                       kBusyTag);
-        if (old == victim_tag) {
-            r.victim_touch = ld_relaxed_i64(t.last_touch + victim);
-            zero_cell(t, victim);
-            __threadfence();
-            st_release(vp, incoming);
+        const int64_t touch = evict_cell(t, victim, victim_tag, incoming);
+        if (touch != INT64_MIN) {
+            r.victim_touch = touch;
             r.slot = victim;
             r.status = 1;
             r.probe_len = t.probe_limit;
@@ -484,22 +559,44 @@ struct Effective {
     double fcnt;
 };
 
-__device__ __forceinline__ Effective effective_at(const pf_table &t, int64_t s, int mode,
+// One slot's stored state, raw 64-bit words (int64 or float64 sums by sum_mode).
+struct CellState {
+    uint64_t sums[3], hist[3];
+    int64_t counts, hist_counts, last_touch;
+    double delta;
+};
+
+// All loads of a slot issued together (one memory latency).  `ro` selects the
+// read-only path for kernels that never write the table.
+__device__ __forceinline__ CellState load_cell(const pf_table &t, int64_t s, bool ro) {
+    CellState c;
+    const unsigned long long *sums = static_cast<const unsigned long long *>(t.sums) + 3 * s;
+    const unsigned long long *hist = static_cast<const unsigned long long *>(t.hist_sums) + 3 * s;
+#pragma unroll
+    for (int k = 0; k < 3; ++k) {
+        c.sums[k] = ro ? __ldg(sums + k) : sums[k];
+        c.hist[k] = ro ? __ldg(hist + k) : hist[k];
+    }
+    c.counts = ro ? __ldg(t.counts + s) : t.counts[s];
+    c.hist_counts = ro ? __ldg(t.hist_counts + s) : t.hist_counts[s];
+    c.last_touch = ro ? __ldg(t.last_touch + s) : t.last_touch[s];
+    c.delta = ro ? __ldg(t.deltas + s) : t.deltas[s];
+    return c;
+}
+
+__device__ __forceinline__ Effective effective_of(const CellState &cs, bool fixed, int mode,
                                                   double ema, double delta_max) {
     Effective e;
-    const bool fixed = t.sum_mode == PF_SUM_FIXED;
-    const int64_t lc_i = __ldg(t.counts + s);
-    const int64_t hc_i = __ldg(t.hist_counts + s);
+    const int64_t lc_i = cs.counts;
+    const int64_t hc_i = cs.hist_counts;
     if (mode == PF_INTEGRATE) {
 #pragma unroll
         for (int c = 0; c < 3; ++c) {
             if (fixed) {
-                e.isum[c] = __ldg(static_cast<const int64_t *>(t.sums) + 3 * s + c) +
-                            __ldg(static_cast<const int64_t *>(t.hist_sums) + 3 * s + c);
+                e.isum[c] = static_cast<int64_t>(cs.sums[c]) + static_cast<int64_t>(cs.hist[c]);
                 e.fsum[c] = 0.0;
             } else {
-                e.fsum[c] = dadd(__ldg(static_cast<const double *>(t.sums) + 3 * s + c),
-                                 __ldg(static_cast<const double *>(t.hist_sums) + 3 * s + c));
+                e.fsum[c] = dadd(__longlong_as_double(cs.sums[c]), __longlong_as_double(cs.hist[c]));
                 e.isum[c] = 0;
             }
         }
@@ -513,7 +610,7 @@ __device__ __forceinline__ Effective effective_at(const pf_table &t, int64_t s, 
         alpha = hc > 0.0 ? (lc > 0.0 ? ema : 1.0) : 0.0;
         cnt = dadd(lc, hc);
     } else {
-        const double k = np_min(np_max(ddiv(__ldg(t.deltas + s), delta_max), 0.0), 1.0);
+        const double k = np_min(np_max(ddiv(cs.delta, delta_max), 0.0), 1.0);
         const double both = np_max(dadd(lc, hc), 1.0);
         alpha = hc > 0.0 ? (lc > 0.0 ? ddiv(dmul(dsub(1.0, k), hc), both) : 1.0) : 0.0;
         cnt = dadd(rint(dmul(dsub(1.0, k), hc)), lc);
@@ -523,13 +620,11 @@ __device__ __forceinline__ Effective effective_at(const pf_table &t, int64_t s, 
     for (int c = 0; c < 3; ++c) {
         double live, hist;
         if (fixed) {
-            live = static_cast<double>(__ldg(static_cast<const int64_t *>(t.sums) + 3 * s + c)) /
-                   kFixedScale;
-            hist = static_cast<double>(
-                       __ldg(static_cast<const int64_t *>(t.hist_sums) + 3 * s + c)) / kFixedScale;
+            live = static_cast<double>(static_cast<int64_t>(cs.sums[c])) / kFixedScale;
+            hist = static_cast<double>(static_cast<int64_t>(cs.hist[c])) / kFixedScale;
         } else {
-            live = __ldg(static_cast<const double *>(t.sums) + 3 * s + c);
-            hist = __ldg(static_cast<const double *>(t.hist_sums) + 3 * s + c);
+            live = __longlong_as_double(cs.sums[c]);
+            hist = __longlong_as_double(cs.hist[c]);
         }
         const double lmean = lc > 0.0 ? ddiv(live, np_max(lc, 1.0)) : 0.0;
         const double hmean = hc > 0.0 ? ddiv(hist, np_max(hc, 1.0)) : 0.0;
@@ -542,6 +637,12 @@ __device__ __forceinline__ Effective effective_at(const pf_table &t, int64_t s, 
     e.icnt = 0;
     e.fcnt = cnt;
     return e;
+}
+
+// VoxelTable.effective of one slot of a table the kernel does not write.
+__device__ __forceinline__ Effective effective_at(const pf_table &t, int64_t s, int mode,
+                                                  double ema, double delta_max) {
+    return effective_of(load_cell(t, s, true), t.sum_mode == PF_SUM_FIXED, mode, ema, delta_max);
 }
 
 // True when eff sums are int64 (fixed-point integrate), i.e. numpy kept int64 dtype.

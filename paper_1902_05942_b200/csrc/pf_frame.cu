@@ -3,11 +3,16 @@
 // keys, fine rung, 3x3x3 neighbourhood + coarse rungs on a compacted work list,
 // composite).  src/pipeline.py:152-283.
 #include "pf_insert.cuh"
+#include "pf_sweep.cuh"
 #include "pf_internal.cuh"
 
 namespace pf {
 
 constexpr int kThreads = 256;
+#ifndef PF_RESOLVE_KV
+#define PF_RESOLVE_KV 4
+#endif
+constexpr int kResolveKV = PF_RESOLVE_KV;  // vertices per thread in resolve_main
 constexpr int kWarps = kThreads / 32;
 
 // Per-CTA counters in 32-bit shared words (native ATOMS; a CTA never sees 2^32
@@ -56,8 +61,12 @@ __device__ __forceinline__ void log_eviction(pf_evict_event *events, int64_t *co
 
 // ------------------------------------------------------------------ insert
 
+#ifndef PF_INSERT_MIN_BLOCKS
+#define PF_INSERT_MIN_BLOCKS 3  // 3 x 256 threads per SM: <= 85 registers
+#endif
+
 template <bool FIXED>
-__global__ void __launch_bounds__(kThreads)
+__global__ void __launch_bounds__(kThreads, PF_INSERT_MIN_BLOCKS)
 insert_frame_kernel(pf_config cfg, pf_vertices v, pf_table fine, pf_table coarse, int has_coarse,
                     uint64_t h0, int64_t frame, int64_t *stats, pf_evict_event *events,
                     int64_t *event_count, int64_t event_cap, const int32_t *abort_flag,
@@ -74,58 +83,87 @@ insert_frame_kernel(pf_config cfg, pf_vertices v, pf_table fine, pf_table coarse
     // tail lanes recompute the last vertex (no divergent key code); warp_insert ignores them
     const int64_t i = valid ? i0 : v.n - 1;
     double val[3];
-    double du = 0.0, dv = 0.0;
     CellHash hf{0ull, 0u}, hc{0ull, 0u};
+    uint64_t ht_f = 0, ht_c = 0;
     {
-        const VertexIn x = load_vertex(v, i, cfg);
+        // warm L2 with the next tile of this CTA (one line per thread per array)
+        {
+            const int64_t nxt = (tile + gridDim.x) * kThreads;
+            const int64_t lines3 = 3 * kThreads * 8 / 128, lines1 = kThreads * 8 / 128;
+            const int k = threadIdx.x;
+            if (nxt < v.n) {
+                if (k < lines3) {
+                    prefetch_l2(reinterpret_cast<const char *>(v.position + 3 * nxt) + 128 * k);
+                    prefetch_l2(reinterpret_cast<const char *>(v.normal + 3 * nxt) + 128 * k);
+                    prefetch_l2(reinterpret_cast<const char *>(v.contribution + 3 * nxt) + 128 * k);
+                } else if (k < lines3 + lines1) {
+                    const int64_t o = 128 * (k - lines3);
+                    prefetch_l2(reinterpret_cast<const char *>(v.camera_distance + nxt) + o);
+                    prefetch_l2(reinterpret_cast<const char *>(v.pixel + nxt) + o);
+                    prefetch_l2(reinterpret_cast<const char *>(v.sample + nxt) + o);
+                }
+            }
+        }
+        const uint64_t stream = l2_evict_first();
+        const VertexIn x = load_vertex(v, i, cfg, stream);
 #pragma unroll
-        for (int c = 0; c < 3; ++c) val[c] = __ldg(v.contribution + 3 * i + c);
-        if (cfg.jitter) {
-            double u1, u2;
-            jitter_draws(h0, x.pixel, x.sample, u1, u2);
-            disc_offset(u1, u2, du, dv);
-        }
+        for (int c = 0; c < 3; ++c) val[c] = ld_stream(v.contribution + 3 * i + c, stream);
         const KeyShared ks = key_shared(cfg, x);
-        double jt[3];
-        const CellKey kf = make_key(cfg, x, ks, cfg.jitter, du, dv, 0, jt);
-        hf = key_hash(kf, ks);
-        if (has_coarse) {
-            const CellKey kc = make_key(cfg, x, ks, cfg.jitter, du, dv, cfg.coarse_delta, jt);
-            hc = key_hash(kc, ks);
-        }
-        if (lk_index != nullptr) {
-            // the resolve phase's lookup key: independent jitter stream, same ONB / aux
-            double lu = 0.0, lv = 0.0;
-            if (cfg.jitter) {
+        // Key sets in one rolled loop (one copy of the key code keeps the kernel's
+        // instruction footprint inside the SM's instruction caches):
+        //   0 fine (jitter stream 2), 1 coarse (stream 2, level + coarse_delta),
+        //   2 the resolve phase's fine lookup key (stream 3)
+        const int nsets = lk_index != nullptr ? 3 : (has_coarse ? 2 : 1);
+        double du = 0.0, dv = 0.0;
+#pragma unroll 1
+        for (int set = 0; set < nsets; ++set) {
+            if (set == 1 && !has_coarse) continue;
+            if (set != 1 && cfg.jitter) {  // set 1 reuses set 0's disc offsets
                 double u1, u2;
-                jitter_draws(h0_lookup, x.pixel, x.sample, u1, u2);
-                disc_offset(u1, u2, lu, lv);
+                jitter_draws(set == 0 ? h0 : h0_lookup, x.pixel, x.sample, u1, u2);
+                disc_offset(u1, u2, du, dv);
             }
-            const CellHash hl = key_hash(make_key(cfg, x, ks, cfg.jitter, lu, lv, 0, jt), ks);
-            if (valid) {
-                lk_index[i] = hl.index;
-                lk_fp[i] = hl.fp;
+            double jt[3];
+            const CellHash h = key_hash(
+                make_key(cfg, x, ks, cfg.jitter, du, dv, set == 1 ? cfg.coarse_delta : 0, jt), ks);
+            // home-slot tag loads go out as soon as a hash exists; the next key set's
+            // arithmetic hides their L2 latency before warp_insert consumes them
+            if (set == 0) {
+                hf = h;
+                ht_f = ld_relaxed(fine.tags + (h.index & static_cast<uint64_t>(fine.capacity - 1)));
+            } else if (set == 1) {
+                hc = h;
+                ht_c = ld_relaxed(coarse.tags +
+                                  (h.index & static_cast<uint64_t>(coarse.capacity - 1)));
+            } else if (valid) {
+                lk_index[i] = h.index;
+                lk_fp[i] = h.fp;
             }
         }
     }
-    const LaneInsert rf = warp_insert<FIXED>(fine, valid, hf.index, hf.fp, val, frame);
-    warp_count(bs, PF_STAT_PROBE_FAILURES, valid && rf.status == 2);
-    warp_count(bs, PF_STAT_EVICTIONS, valid && rf.leader && rf.status == 1);
-    {
-        // probe-length histogram and sum, merged per distinct length in the warp
-        const int pl = valid ? rf.probe_len : -1;
-        const unsigned same = __match_any_sync(kFull, pl);
-        if (valid && (threadIdx.x & 31) == static_cast<unsigned>(__ffs(same) - 1)) {
-            const unsigned cnt = __popc(same);
-            atomicAdd(&bs.hist[pl & 255], cnt);
-            atomicAdd(&bs.v[PF_STAT_PROBE_LEN_SUM], cnt * static_cast<unsigned>(pl));
+    const int ntables = has_coarse ? 2 : 1;
+#pragma unroll 1
+    for (int tb = 0; tb < ntables; ++tb) {
+        const pf_table t = tb == 0 ? fine : coarse;
+        const CellHash h = tb == 0 ? hf : hc;
+        const LaneInsert r = warp_insert<FIXED>(t, valid, h.index, h.fp, val, frame,
+                                                tb == 0 ? ht_f : ht_c);
+        warp_count(bs, tb == 0 ? PF_STAT_PROBE_FAILURES : PF_STAT_COARSE_PROBE_FAILURES,
+                   valid && r.status == 2);
+        warp_count(bs, tb == 0 ? PF_STAT_EVICTIONS : PF_STAT_COARSE_EVICTIONS,
+                   valid && r.leader && r.status == 1);
+        if (tb == 0) {
+            // probe-length histogram and sum, merged per distinct length in the warp
+            const int pl = valid ? r.probe_len : -1;
+            const unsigned same = __match_any_sync(kFull, pl);
+            if (valid && (threadIdx.x & 31) == static_cast<unsigned>(__ffs(same) - 1)) {
+                const unsigned cnt = __popc(same);
+                atomicAdd(&bs.hist[pl & 255], cnt);
+                atomicAdd(&bs.v[PF_STAT_PROBE_LEN_SUM], cnt * static_cast<unsigned>(pl));
+            }
+            if (valid && r.leader && r.status == 1)
+                log_eviction(events, event_count, event_cap, i, r);
         }
-    }
-    if (valid && rf.leader && rf.status == 1) log_eviction(events, event_count, event_cap, i, rf);
-    if (has_coarse) {
-        const LaneInsert rc = warp_insert<FIXED>(coarse, valid, hc.index, hc.fp, val, frame);
-        warp_count(bs, PF_STAT_COARSE_PROBE_FAILURES, valid && rc.status == 2);
-        warp_count(bs, PF_STAT_COARSE_EVICTIONS, valid && rc.leader && rc.status == 1);
     }
     }
     __syncthreads();
@@ -160,7 +198,56 @@ struct ResolveArgs {
     double thr;
     const uint64_t *lk_index;  // precomputed lookup keys (or NULL)
     const uint32_t *lk_fp;
+    const ulonglong4 *rec;     // per-slot effective records of the fine table (or NULL)
 };
+
+// Per-slot effective record: three sum words (int64 or float64 bits, as
+// VoxelTable.effective's dtype) and the count as a float64 -- one 32-byte sector.
+__device__ __forceinline__ ulonglong4 pack_effective(const Effective &e, bool as_int) {
+    ulonglong4 r;
+    r.x = as_int ? static_cast<unsigned long long>(e.isum[0]) : __double_as_longlong(e.fsum[0]);
+    r.y = as_int ? static_cast<unsigned long long>(e.isum[1]) : __double_as_longlong(e.fsum[1]);
+    r.z = as_int ? static_cast<unsigned long long>(e.isum[2]) : __double_as_longlong(e.fsum[2]);
+    r.w = __double_as_longlong(e.fcnt);
+    return r;
+}
+
+__device__ __forceinline__ Effective unpack_effective(const ulonglong4 &r, bool as_int) {
+    Effective e;
+    const unsigned long long w[3] = {r.x, r.y, r.z};
+#pragma unroll
+    for (int c = 0; c < 3; ++c) {
+        e.isum[c] = as_int ? static_cast<int64_t>(w[c]) : 0;
+        e.fsum[c] = as_int ? 0.0 : __longlong_as_double(w[c]);
+    }
+    e.fcnt = __longlong_as_double(r.w);
+    e.icnt = static_cast<int64_t>(e.fcnt);  // exact: counts < 2^53
+    return e;
+}
+
+// The fine table's effective value of slot s: its record when the effective pass ran.
+__device__ __forceinline__ Effective fine_effective(const ResolveArgs &a, int64_t s) {
+    const int mode = a.cfg.temporal_mode;
+    if (a.rec != nullptr) {
+        const ulonglong2 *p = reinterpret_cast<const ulonglong2 *>(a.rec + s);
+        const ulonglong2 lo = __ldg(p), hi = __ldg(p + 1);
+        return unpack_effective(make_ulonglong4(lo.x, lo.y, hi.x, hi.y), eff_is_int(a.fine, mode));
+    }
+    return effective_at(a.fine, s, mode, a.cfg.ema_alpha, a.cfg.delta_max);
+}
+
+// VoxelTable.effective of every occupied fine slot, once per resolve: lookups then
+// read one sector instead of the five SoA sectors of a slot's state.
+__global__ void __launch_bounds__(kThreads)
+effective_records_kernel(pf_table t, int mode, double ema, double delta_max, ulonglong4 *rec) {
+    __shared__ SweepSmem<kThreads> q;
+    const bool fixed = t.sum_mode == PF_SUM_FIXED;
+    const bool as_int = eff_is_int(t, mode);
+    for_each_occupied<kThreads>(t.tags, t.capacity, q, [&](int64_t s, uint64_t) {
+        rec[s] = pack_effective(effective_of(load_cell(t, s, true), fixed, mode, ema, delta_max),
+                                as_int);
+    });
+}
 
 struct KeyAndHash {
     CellKey first;
@@ -195,10 +282,11 @@ __device__ __forceinline__ double row_mean(double sum, double cnt, bool fixed) {
 
 __device__ __forceinline__ void composite(const ResolveArgs &a, int64_t i, int64_t pixel,
                                           const double chosen[3], int source) {
+    const uint64_t stream = l2_evict_first(), keep = l2_evict_last();
 #pragma unroll
     for (int c = 0; c < 3; ++c) {
-        const double tp = __ldg(a.v.throughput + 3 * i + c);
-        red_add_f64(a.flat + 3 * pixel + c, dmul(tp, chosen[c]));
+        const double tp = ld_stream(a.v.throughput + 3 * i + c, stream);
+        red_add_f64(a.flat + 3 * pixel + c, dmul(tp, chosen[c]), keep);
     }
     if (a.source) a.source[i] = static_cast<uint8_t>(source);
     if (a.chosen) {
@@ -207,55 +295,94 @@ __device__ __forceinline__ void composite(const ResolveArgs &a, int64_t i, int64
     }
 }
 
-// Rung 1 for every vertex; rows below the threshold go to the work list with their
-// lookup key (row, qx, qy, qz, level, aux).
+// Rung 1 for every vertex; rows below the threshold go to the work list (row ids).
+// KV vertices per thread, each step issued for all KV rows before the next (key ->
+// home tag -> cell state -> composite), so a thread keeps KV independent L2/HBM
+// round trips in flight: the kernel is bound by memory latency, not arithmetic.
+template <int KV, bool HAVE_KEYS>
 __global__ void __launch_bounds__(kThreads) resolve_main_kernel(ResolveArgs a) {
     __shared__ BlockStats bs;
     stats_init(bs);
     __syncthreads();
     const pf_config &cfg = a.cfg;
-    const int64_t i0 = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
-    const bool valid = i0 < a.v.n;
-    const int64_t i = valid ? i0 : a.v.n - 1;  // tail lanes shadow the last vertex
-    bool fine_ok = false;
-    {
-        CellHash h;
-        if (a.lk_index != nullptr) {  // keys emitted by the insert pass
-            h.index = __ldg(reinterpret_cast<const unsigned long long *>(a.lk_index) + i);
-            h.fp = __ldg(a.lk_fp + i);
+    const uint64_t stream = l2_evict_first(), keep = l2_evict_last();
+    const uint64_t fmask = static_cast<uint64_t>(a.fine.capacity) - 1;
+    const int64_t base = static_cast<int64_t>(blockIdx.x) * blockDim.x * KV + threadIdx.x;
+    int64_t row[KV];
+    bool valid[KV];
+    CellHash h[KV];
+    uint64_t tag[KV];
+#pragma unroll
+    for (int k = 0; k < KV; ++k) {
+        const int64_t i0 = base + static_cast<int64_t>(k) * blockDim.x;
+        valid[k] = i0 < a.v.n;
+        row[k] = valid[k] ? i0 : a.v.n - 1;  // tail lanes shadow the last vertex
+        if (HAVE_KEYS) {  // keys emitted by the insert pass
+            h[k].index = ld_stream(a.lk_index + row[k], stream);
+            h[k].fp = ld_stream(a.lk_fp + row[k], stream);
         } else {
-            h = lookup_key(a, i).second;
+            h[k] = lookup_key(a, row[k]).second;
         }
-        const int64_t s = probe_lookup(a.fine.tags, static_cast<uint64_t>(a.fine.capacity) - 1,
-                                       a.fine.probe_limit, h.index, h.fp);
-        if (s >= 0) {
-            const Effective e = effective_at(a.fine, s, cfg.temporal_mode, cfg.ema_alpha, cfg.delta_max);
+    }
+#pragma unroll
+    for (int k = 0; k < KV; ++k) tag[k] = __ldg(reinterpret_cast<const unsigned long long *>(
+                                      a.fine.tags) + (h[k].index & fmask));
+    int64_t slot[KV];
+#pragma unroll
+    for (int k = 0; k < KV; ++k) {
+        // first probe from the prefetched home tag; longer chains are rare
+        if (tag[k] == kEmptyTag) slot[k] = -1;
+        else if ((tag[k] & kFpMask) == h[k].fp) slot[k] = static_cast<int64_t>(h[k].index & fmask);
+        else slot[k] = probe_lookup(a.fine.tags, fmask, a.fine.probe_limit, h[k].index, h[k].fp);
+    }
+    Effective ef[KV];
+    int64_t pixel[KV];
+    double tp[KV][3];
+#pragma unroll
+    for (int k = 0; k < KV; ++k) {
+        if (slot[k] >= 0) ef[k] = fine_effective(a, slot[k]);
+        pixel[k] = ld_stream(a.v.pixel + row[k], stream);
+#pragma unroll
+        for (int c = 0; c < 3; ++c) tp[k][c] = ld_stream(a.v.throughput + 3 * row[k] + c, stream);
+    }
+    const bool as_int = eff_is_int(a.fine, cfg.temporal_mode);
+    const bool fixed = a.fine.sum_mode == PF_SUM_FIXED;
+#pragma unroll
+    for (int k = 0; k < KV; ++k) {
+        bool fine_ok = false;
+        if (slot[k] >= 0) {
+            const Effective &e = ef[k];
             const double cnt = e.fcnt;
-            if (valid && cnt >= a.thr) {
+            if (valid[k] && cnt >= a.thr) {
                 fine_ok = true;
-                const bool as_int = eff_is_int(a.fine, cfg.temporal_mode);
-                const bool fixed = a.fine.sum_mode == PF_SUM_FIXED;
                 double m[3];
 #pragma unroll
-                for (int c = 0; c < 3; ++c) m[c] = row_mean(eff_sum_f64(e, as_int, c), cnt, fixed);
-                composite(a, i, __ldg(a.v.pixel + i), m, 0);
+                for (int c = 0; c < 3; ++c) {
+                    m[c] = row_mean(eff_sum_f64(e, as_int, c), cnt, fixed);
+                    red_add_f64(a.flat + 3 * pixel[k] + c, dmul(tp[k][c], m[c]), keep);
+                }
+                if (a.source) a.source[row[k]] = 0;
+                if (a.chosen) {
+#pragma unroll
+                    for (int c = 0; c < 3; ++c) a.chosen[3 * row[k] + c] = m[c];
+                }
             }
         }
+        // rows below the threshold: append the row id to the work list (warp-aggregated)
+        const bool need = valid[k] && !fine_ok;
+        const unsigned m = __ballot_sync(kFull, need);
+        if (m) {
+            unsigned long long wb = 0;
+            const int lane = threadIdx.x & 31;
+            if (lane == __ffs(m) - 1)
+                wb = atomicAdd(reinterpret_cast<unsigned long long *>(a.work_count),
+                               static_cast<unsigned long long>(__popc(m)));
+            wb = __shfl_sync(kFull, wb, __ffs(m) - 1);
+            if (need) a.work[static_cast<int64_t>(wb) + __popc(m & ((1u << lane) - 1u))] = row[k];
+        }
+        warp_count(bs, PF_STAT_SOURCE_FINE, valid[k] && fine_ok);
+        warp_count(bs, PF_STAT_FALLBACK_ROWS, need);
     }
-    // rows below the threshold: append the row id to the work list (warp-aggregated)
-    const bool need = valid && !fine_ok;
-    const unsigned m = __ballot_sync(kFull, need);
-    if (m) {
-        unsigned long long base = 0;
-        const int lane = threadIdx.x & 31;
-        if (lane == __ffs(m) - 1)
-            base = atomicAdd(reinterpret_cast<unsigned long long *>(a.work_count),
-                             static_cast<unsigned long long>(__popc(m)));
-        base = __shfl_sync(kFull, base, __ffs(m) - 1);
-        if (need) a.work[static_cast<int64_t>(base) + __popc(m & ((1u << lane) - 1u))] = i;
-    }
-    warp_count(bs, PF_STAT_SOURCE_FINE, valid && fine_ok);
-    warp_count(bs, PF_STAT_FALLBACK_ROWS, need);
     __syncthreads();
     stats_flush(bs, a.stats, false);
 }
@@ -301,7 +428,7 @@ __global__ void __launch_bounds__(kThreads) resolve_fallback_kernel(ResolveArgs 
             const int64_t s = probe_lookup(a.fine.tags, fmask, a.fine.probe_limit, h.index, h.fp);
             if (s >= 0) {
                 found = true;
-                e = effective_at(a.fine, s, mode, cfg.ema_alpha, cfg.delta_max);
+                e = fine_effective(a, s);
             }
         }
         // ordered pool: (src/pipeline.py:185-192)
@@ -432,7 +559,8 @@ int pf_resolve_frame(const pf_config *cfg, const pf_vertices *v, const pf_table 
                      uint64_t stream_base_coarse, int64_t spp, const double *base_image,
                      int64_t n_pixels, double *image, double *flat, int64_t *work,
                      int64_t *work_count, uint8_t *source, double *chosen, int64_t *stats,
-                     const uint64_t *lookup_index, const uint32_t *lookup_fp, void *stream) {
+                     const uint64_t *lookup_index, const uint32_t *lookup_fp,
+                     uint64_t *eff_records, void *stream) {
     const char *fn = "pf_resolve_frame";
     if ((lookup_index == nullptr) != (lookup_fp == nullptr))
         return fail_arg(fn, "lookup_index and lookup_fp go together");
@@ -470,7 +598,19 @@ int pf_resolve_frame(const pf_config *cfg, const pf_vertices *v, const pf_table 
         a.thr = static_cast<double>(cfg->low_count_threshold > 1 ? cfg->low_count_threshold : 1);
         a.lk_index = lookup_index;
         a.lk_fp = lookup_fp;
-        resolve_main_kernel<<<blocks_for(v->n, kThreads), kThreads, 0, st>>>(a);
+        a.rec = reinterpret_cast<const ulonglong4 *>(eff_records);
+        if (eff_records != nullptr) {
+            effective_records_kernel<<<sweep_blocks<kThreads>(fine->capacity, sm_count()), kThreads,
+                                       0, st>>>(*fine, kc.temporal_mode, kc.ema_alpha,
+                                                kc.delta_max,
+                                                reinterpret_cast<ulonglong4 *>(eff_records));
+            if (int rc = check_launch(fn)) return rc;
+        }
+        if (lookup_index != nullptr)
+            resolve_main_kernel<kResolveKV, true>
+                <<<blocks_for(v->n, kThreads * kResolveKV), kThreads, 0, st>>>(a);
+        else
+            resolve_main_kernel<1, false><<<blocks_for(v->n, kThreads), kThreads, 0, st>>>(a);
         if (int rc = check_launch(fn)) return rc;
         int64_t fb_blocks = (v->n + kWarps - 1) / kWarps;
         const int64_t cap = static_cast<int64_t>(sm_count()) * 8;

@@ -30,7 +30,8 @@ struct LaneInsert {
 // see after the leader: same slot and probe length, status 1 -> 0.
 template <bool FIXED>
 __device__ __forceinline__ LaneInsert warp_insert(const pf_table &t, bool valid, uint64_t idx,
-                                                  uint32_t fp, const double val[3], int64_t frame) {
+                                                  uint32_t fp, const double val[3], int64_t frame,
+                                                  uint64_t home_tag) {
     const unsigned lane = threadIdx.x & 31u;
     const uint64_t k2 = static_cast<uint64_t>(fp) | (static_cast<uint64_t>(valid) << 32);
     const unsigned peers = __match_any_sync(kFull, valid ? idx : 0ull) & __match_any_sync(kFull, k2);
@@ -74,18 +75,19 @@ __device__ __forceinline__ LaneInsert warp_insert(const pf_table &t, bool valid,
     r.victim_tag = 0;
     r.victim_touch = 0;
     if (is_leader) {
-        r = probe_insert(t, idx, fp);
+        r = probe_insert(t, idx, fp, home_tag);
         if (r.status != 2) {
             const int64_t s = r.slot;
+            const uint64_t keep = l2_evict_last();
 #pragma unroll
             for (int c = 0; c < 3; ++c) {
                 if (FIXED)
                     red_add_u64(static_cast<int64_t *>(t.sums) + 3 * s + c,
-                                static_cast<uint64_t>(qsum[c]));
+                                static_cast<uint64_t>(qsum[c]), keep);
                 else
-                    red_add_f64(static_cast<double *>(t.sums) + 3 * s + c, fsum[c]);
+                    red_add_f64(static_cast<double *>(t.sums) + 3 * s + c, fsum[c], keep);
             }
-            red_add_u64(t.counts + s, static_cast<uint64_t>(__popc(peers)));
+            red_add_u64(t.counts + s, static_cast<uint64_t>(__popc(peers)), keep);
             st_relaxed_u64(t.last_touch + s, static_cast<uint64_t>(frame));
         }
     }

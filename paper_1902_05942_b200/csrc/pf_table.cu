@@ -2,6 +2,7 @@
 // batch accumulate (parallel warp-merged, or sequential-order), lookup, key build,
 // hashing, effective sums, the temporal update (begin_frame) and occupancy.
 #include "pf_insert.cuh"
+#include "pf_sweep.cuh"
 #include "pf_internal.cuh"
 
 namespace pf {
@@ -34,7 +35,9 @@ accumulate_kernel(pf_table t, const uint64_t *__restrict__ idx, const uint32_t *
 #pragma unroll
         for (int c = 0; c < 3; ++c) v[c] = __ldg(vals + 3 * i + c);
     }
-    const LaneInsert r = warp_insert<FIXED>(t, valid, k, f, v, frame);
+    const uint64_t home_tag =
+        valid ? ld_relaxed(t.tags + (k & static_cast<uint64_t>(t.capacity - 1))) : 0ull;
+    const LaneInsert r = warp_insert<FIXED>(t, valid, k, f, v, frame, home_tag);
     if (!valid) return;
     if (o.status) o.status[i] = static_cast<uint8_t>(r.status);
     if (o.slots) o.slots[i] = r.status == 2 ? -1 : r.slot;
@@ -248,57 +251,13 @@ template <bool FIXED>
 __global__ void __launch_bounds__(kThreads)
 begin_frame_kernel(pf_table t, int64_t frame, int mode, double ema, double delta_max,
                    int32_t sample_cap, int64_t *horizon_clears) {
-    // Each step a CTA streams kChunk tags with 16-byte loads, compacts the occupied
-    // slots (a few percent) into a shared queue, then folds the queue with all its
-    // threads -- the dependent per-slot loads run fully parallel instead of one
-    // latency chain per sweeping thread.
-    constexpr int kPairsPerThread = 4;
-    constexpr int kChunk = kThreads * 2 * kPairsPerThread;
-    __shared__ int64_t q_slot[kChunk];
-    __shared__ uint64_t q_tag[kChunk];
-    __shared__ int q_n;
+    __shared__ SweepSmem<kThreads> q;
     __shared__ int block_clears;
     if (threadIdx.x == 0) block_clears = 0;
-    const int lane = threadIdx.x & 31;
-    const ulonglong2 *tags2 = reinterpret_cast<const ulonglong2 *>(t.tags);
     int cleared = 0;
-    for (int64_t base = static_cast<int64_t>(blockIdx.x) * kChunk; base < t.capacity;
-         base += static_cast<int64_t>(gridDim.x) * kChunk) {
-        if (threadIdx.x == 0) q_n = 0;
-        __syncthreads();
-        ulonglong2 tg[kPairsPerThread];
-#pragma unroll
-        for (int j = 0; j < kPairsPerThread; ++j) {
-            const int64_t p = base / 2 + j * kThreads + threadIdx.x;
-            tg[j] = 2 * p < t.capacity ? tags2[p] : make_ulonglong2(kEmptyTag, kEmptyTag);
-        }
-#pragma unroll
-        for (int j = 0; j < kPairsPerThread; ++j) {
-            const int64_t p = base / 2 + j * kThreads + threadIdx.x;
-#pragma unroll
-            for (int h = 0; h < 2; ++h) {
-                const uint64_t tag = h ? tg[j].y : tg[j].x;
-                const bool occ = tag != kEmptyTag;
-                const unsigned m = __ballot_sync(kFull, occ);
-                if (m) {
-                    int q0 = 0;
-                    if (lane == __ffs(m) - 1) q0 = atomicAdd(&q_n, __popc(m));
-                    q0 = __shfl_sync(kFull, q0, __ffs(m) - 1);
-                    if (occ) {
-                        const int q = q0 + __popc(m & ((1u << lane) - 1u));
-                        q_slot[q] = 2 * p + h;
-                        q_tag[q] = tag;
-                    }
-                }
-            }
-        }
-        __syncthreads();
-        const int n_q = q_n;
-        for (int q = threadIdx.x; q < n_q; q += kThreads)
-            cleared += fold_slot<FIXED>(t, q_slot[q], q_tag[q], frame, mode, ema, delta_max,
-                                        sample_cap);
-        __syncthreads();
-    }
+    for_each_occupied<kThreads>(t.tags, t.capacity, q, [&](int64_t s, uint64_t tag) {
+        cleared += fold_slot<FIXED>(t, s, tag, frame, mode, ema, delta_max, sample_cap);
+    });
     if (cleared) atomicAdd(&block_clears, cleared);
     __syncthreads();
     if (threadIdx.x == 0 && block_clears && horizon_clears)
@@ -312,79 +271,77 @@ template <bool FIXED>
 __device__ __forceinline__ int fold_slot(const pf_table &t, int64_t s, uint64_t tag, int64_t frame,
                                          int mode, double ema, double delta_max,
                                          int32_t sample_cap) {
-    bool cleared = false;
-    {
-        {
-            int64_t *sums_i = static_cast<int64_t *>(t.sums) + 3 * s;
-            int64_t *hist_i = static_cast<int64_t *>(t.hist_sums) + 3 * s;
-            double *sums_f = static_cast<double *>(t.sums) + 3 * s;
-            double *hist_f = static_cast<double *>(t.hist_sums) + 3 * s;
-            const int64_t age = frame - t.last_touch[s];
-            cleared = age > t.evict_horizon;
-            if (!cleared) {
-                if (mode == PF_INTEGRATE) {
+    // every field loaded at once, folded in registers, stored once
+    const CellState cs = load_cell(t, s, false);
+    uint64_t hist[3];
+    int64_t hc = cs.hist_counts;
 #pragma unroll
-                    for (int c = 0; c < 3; ++c) {
-                        if (FIXED) hist_i[c] += sums_i[c];
-                        else hist_f[c] = dadd(hist_f[c], sums_f[c]);
-                    }
-                    t.hist_counts[s] += t.counts[s];
-                } else {
-                    const Effective e = effective_at(t, s, mode, ema, delta_max);
-                    int64_t cnt = np_i64(rint(e.fcnt));
-                    if (mode == PF_FILTER && cnt > 1) cnt = 1;
-                    if (cnt > 0) {
-                        const double denom = np_max(e.fcnt, 1e-300);
+    for (int c = 0; c < 3; ++c) hist[c] = cs.hist[c];
+    const int64_t age = frame - cs.last_touch;
+    const bool cleared = age > t.evict_horizon;
+    uint64_t new_tag = kEmptyTag;
+    if (!cleared) {
+        if (mode == PF_INTEGRATE) {
 #pragma unroll
-                        for (int c = 0; c < 3; ++c) {
-                            const double nh = dmul(ddiv(e.fsum[c], denom), static_cast<double>(cnt));
-                            if (FIXED) hist_i[c] = np_i64(floor(dadd(nh, 0.5)));
-                            else hist_f[c] = nh;
-                        }
-                        t.hist_counts[s] = cnt;
-                    } else {
-#pragma unroll
-                        for (int c = 0; c < 3; ++c) {
-                            if (FIXED) hist_i[c] = 0;
-                            else hist_f[c] = 0.0;
-                        }
-                        t.hist_counts[s] = 0;
-                    }
-                }
-                if (sample_cap && (mode == PF_INTEGRATE || mode == PF_HYBRID) &&
-                    t.hist_counts[s] > sample_cap) {
-                    const double scale = ddiv(static_cast<double>(sample_cap),
-                                              static_cast<double>(t.hist_counts[s]));
-#pragma unroll
-                    for (int c = 0; c < 3; ++c) {
-                        if (FIXED)
-                            hist_i[c] = np_i64(floor(dadd(dmul(static_cast<double>(hist_i[c]), scale), 0.5)));
-                        else
-                            hist_f[c] = dmul(hist_f[c], scale);
-                    }
-                    t.hist_counts[s] = sample_cap;
-                }
-                // re-prioritise (src/table.py:53-57, 289-290)
-                const int64_t hc = t.hist_counts[s];
-                const uint64_t c8 = static_cast<uint64_t>(hc < 255 ? hc : 255);
-                const uint64_t a24 = static_cast<uint64_t>(age < static_cast<int64_t>(kPrioAgeMask)
-                                                               ? age : static_cast<int64_t>(kPrioAgeMask));
-                const uint64_t prio = ((255ull - c8) << 24) | a24;
-                t.tags[s] = (prio << 32) | (tag & kFpMask);
+            for (int c = 0; c < 3; ++c) {
+                if (FIXED) hist[c] = cs.hist[c] + cs.sums[c];
+                else hist[c] = __double_as_longlong(dadd(__longlong_as_double(cs.hist[c]),
+                                                          __longlong_as_double(cs.sums[c])));
             }
+            hc = cs.hist_counts + cs.counts;
+        } else {
+            const Effective e = effective_of(cs, FIXED, mode, ema, delta_max);
+            int64_t cnt = np_i64(rint(e.fcnt));
+            if (mode == PF_FILTER && cnt > 1) cnt = 1;
+            if (cnt > 0) {
+                const double denom = np_max(e.fcnt, 1e-300);
 #pragma unroll
-            for (int c = 0; c < 3; ++c) sums_i[c] = 0;  // live generation reset (bits of 0.0)
-            t.counts[s] = 0;
-            t.deltas[s] = 0.0;
-            if (cleared) {
-                t.tags[s] = kEmptyTag;
+                for (int c = 0; c < 3; ++c) {
+                    const double nh = dmul(ddiv(e.fsum[c], denom), static_cast<double>(cnt));
+                    hist[c] = FIXED ? static_cast<uint64_t>(np_i64(floor(dadd(nh, 0.5))))
+                                    : static_cast<uint64_t>(__double_as_longlong(nh));
+                }
+                hc = cnt;
+            } else {
 #pragma unroll
-                for (int c = 0; c < 3; ++c) hist_i[c] = 0;
-                t.hist_counts[s] = 0;
-                t.last_touch[s] = 0;
+                for (int c = 0; c < 3; ++c) hist[c] = 0;  // int64 0 / +0.0
+                hc = 0;
             }
         }
+        if (sample_cap && (mode == PF_INTEGRATE || mode == PF_HYBRID) && hc > sample_cap) {
+            const double scale = ddiv(static_cast<double>(sample_cap), static_cast<double>(hc));
+#pragma unroll
+            for (int c = 0; c < 3; ++c) {
+                if (FIXED)
+                    hist[c] = static_cast<uint64_t>(np_i64(floor(dadd(
+                        dmul(static_cast<double>(static_cast<int64_t>(hist[c])), scale), 0.5))));
+                else
+                    hist[c] = __double_as_longlong(dmul(__longlong_as_double(hist[c]), scale));
+            }
+            hc = sample_cap;
+        }
+        // re-prioritise (src/table.py:53-57, 289-290)
+        const uint64_t c8 = static_cast<uint64_t>(hc < 255 ? hc : 255);
+        const uint64_t a24 = static_cast<uint64_t>(
+            age < static_cast<int64_t>(kPrioAgeMask) ? age : static_cast<int64_t>(kPrioAgeMask));
+        const uint64_t prio = ((255ull - c8) << 24) | a24;
+        new_tag = (prio << 32) | (tag & kFpMask);
+    } else {
+        hist[0] = hist[1] = hist[2] = 0;
+        hc = 0;
+        t.last_touch[s] = 0;
     }
+    unsigned long long *sums = static_cast<unsigned long long *>(t.sums) + 3 * s;
+    unsigned long long *hsum = static_cast<unsigned long long *>(t.hist_sums) + 3 * s;
+#pragma unroll
+    for (int c = 0; c < 3; ++c) {
+        sums[c] = 0;  // live generation reset (bits of 0.0)
+        hsum[c] = hist[c];
+    }
+    t.counts[s] = 0;
+    t.hist_counts[s] = hc;
+    t.deltas[s] = 0.0;
+    t.tags[s] = new_tag;
     return cleared ? 1 : 0;
 }
 
@@ -574,9 +531,7 @@ int pf_begin_frame(const pf_table *t, int64_t frame, int32_t mode, double ema_al
     const char *fn = "pf_begin_frame";
     if (int rc = validate_table(fn, t)) return rc;
     if (mode < PF_INTEGRATE || mode > PF_HYBRID) return fail_arg(fn, "unknown temporal mode");
-    int64_t blocks = (t->capacity + 8 * kThreads - 1) / (8 * kThreads);  // kChunk slots each
-    const int64_t cap = static_cast<int64_t>(sm_count()) * 8;
-    const unsigned g = static_cast<unsigned>(blocks < cap ? blocks : cap);
+    const unsigned g = sweep_blocks<kThreads>(t->capacity, sm_count());
     if (t->sum_mode == PF_SUM_FIXED)
         begin_frame_kernel<true><<<g, kThreads, 0, as_stream(stream)>>>(
             *t, frame, mode, ema_alpha, delta_max, sample_cap, horizon_clears);

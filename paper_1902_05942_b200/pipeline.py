@@ -381,7 +381,9 @@ def resolve_phase(vertices, cfg: FilterConfig, state: FrameState, frame: int, se
               int(spp), base.data_ptr(), h * w, image.data_ptr(), flat.data_ptr(),
               work.data_ptr(), work_count.data_ptr(), source.data_ptr(), _lib.ptr(chosen),
               counters.data_ptr(), lk[3].data_ptr() if lk_ok else None,
-              lk[4].data_ptr() if lk_ok else None, _lib.stream_handle())
+              lk[4].data_ptr() if lk_ok else None,
+              state.buffer("eff_records", (state.fine.capacity, 4), torch.int64).data_ptr(),
+              _lib.stream_handle())
     del keep
     report = ResolveReport(source, image, chosen)
     report.counters = counters

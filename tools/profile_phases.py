@@ -27,21 +27,30 @@ def run(name, frames=6, **over):
     acc = {"begin": 0.0, "insert": 0.0, "resolve": 0.0}
     for f in range(frames):
         seed = rng.frame_seed(1, f)
-        e = [ev() for _ in range(4)]
+        e = [ev() for _ in range(6)]
+        # each phase is enqueued behind a GPU sleep so the events bracket GPU time only
+        torch.cuda.synchronize()
+        torch.cuda._sleep(2_000_000)
         e[0].record()
         st.fine.begin_frame(f, cfg)
         if st.coarse is not None:
             st.coarse.begin_frame(f, cfg)
         e[1].record()
-        fk, _, stats = pf.accumulate_phase(vs, cfg, st, f, seed)
+        torch.cuda.synchronize()
+        torch.cuda._sleep(2_000_000)
+        e[4].record()
+        fk, _, stats = pf.accumulate_phase(vs, cfg, st, f, seed, validate=False)
         e[2].record()
+        torch.cuda.synchronize()
+        torch.cuda._sleep(2_000_000)
+        e[5].record()
         _, rep = pf.resolve_phase(vs, cfg, st, f, seed, 1, base, fk, want_means=False)
         e[3].record()
         torch.cuda.synchronize()
         if f >= 2:
             acc["begin"] += e[0].elapsed_time(e[1])
-            acc["insert"] += e[1].elapsed_time(e[2])
-            acc["resolve"] += e[2].elapsed_time(e[3])
+            acc["insert"] += e[4].elapsed_time(e[2])
+            acc["resolve"] += e[5].elapsed_time(e[3])
     k = frames - 2
     occ = st.fine.occupied_count()
     cocc = st.coarse.occupied_count() if st.coarse is not None else 0
