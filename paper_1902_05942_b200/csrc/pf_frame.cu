@@ -10,7 +10,7 @@ namespace pf {
 
 constexpr int kThreads = 256;
 #ifndef PF_RESOLVE_KV
-#define PF_RESOLVE_KV 4
+#define PF_RESOLVE_KV 2
 #endif
 constexpr int kResolveKV = PF_RESOLVE_KV;  // vertices per thread in resolve_main
 constexpr int kWarps = kThreads / 32;
