@@ -202,6 +202,36 @@ int pf_resolve_frame(const pf_config *cfg, const pf_vertices *v, const pf_table 
                      const uint64_t *lookup_index, const uint32_t *lookup_fp,
                      uint64_t *eff_records, void *stream);
 
+/* Device scratch and outputs of pf_filter_frame (all device pointers). */
+typedef struct pf_frame_buffers {
+    int64_t *acc_stats;             /* int64[PF_STAT_COUNT]: accumulate counters (zeroed) */
+    int64_t *res_stats;             /* int64[PF_STAT_COUNT]: resolve counters (zeroed) */
+    pf_evict_event *events;         /* eviction log (may be NULL) ... */
+    int64_t *event_count;           /* ... and its counter (zeroed) */
+    int64_t event_capacity;
+    int32_t *bad_flag;              /* input check flag, or NULL to skip validation */
+    int64_t *horizon_clears_fine;   /* int64[1] counters incremented by begin_frame */
+    int64_t *horizon_clears_coarse;
+    uint64_t *lookup_index;         /* n: lookup keys handed from insert to resolve */
+    uint32_t *lookup_fp;
+    uint64_t *eff_records;          /* 4 * fine->capacity */
+    double *flat;                   /* [n_pixels][3] */
+    int64_t *work;                  /* n */
+    int64_t *work_count;            /* 1 */
+    void *phase_events[4];          /* optional cudaEvent_t recorded at frame start, just
+                                       before the insert kernel, after it, at frame end */
+} pf_frame_buffers;
+
+/* One whole frame of the filter -- src/pipeline.py:321-363 (render_frame) minus the
+ * tracer -- in one call and one stream: begin_frame on both tables, the input check,
+ * the flag-guarded fused insert, and the resolve.  The host reads bad_flag afterwards
+ * (nonzero: the tables were left untouched and the inputs must be rejected). */
+int pf_filter_frame(const pf_config *cfg, const pf_vertices *v, const pf_table *fine,
+                    const pf_table *coarse, int64_t frame, uint64_t stream_base_accum,
+                    uint64_t stream_base_lookup, uint64_t stream_base_coarse, int64_t spp,
+                    const double *base_image, int64_t n_pixels, double *image, uint8_t *source,
+                    double *chosen, const pf_frame_buffers *buffers, void *stream);
+
 /* VoxelTable.effective (src/table.py:205-238) over all slots.  eff_sum is int64 for
  * (integrate, fixed) else float64; eff_count is int64 for integrate else float64. */
 int pf_effective(const pf_table *t, int32_t mode, double ema_alpha, double delta_max,

@@ -25,7 +25,8 @@ NVCC_FLAGS = ["-gencode", "arch=compute_100a,code=sm_100a", "-O3", "-lineinfo",
 # exported symbols of include/pathfilter_b200.h (checked by tests/test_abi.py)
 EXPORTS = ("pf_abi_version", "pf_last_error", "pf_device_sm_count", "pf_accumulate_fixed",
            "pf_accumulate_float", "pf_lookup_slots", "pf_make_key_arrays", "pf_vertex_keys",
-           "pf_hash_arrays", "pf_insert_frame", "pf_resolve_frame", "pf_effective",
+           "pf_hash_arrays", "pf_insert_frame", "pf_resolve_frame", "pf_filter_frame",
+           "pf_effective",
            "pf_begin_frame", "pf_check_contributions", "pf_selftest_division",
            "pf_count_occupied")
 
@@ -80,6 +81,17 @@ class PfKeyOut(ctypes.Structure):
                                                 "fingerprint", "jittered")]
 
 
+class PfFrameBuffers(ctypes.Structure):
+    _fields_ = [("acc_stats", ctypes.c_void_p), ("res_stats", ctypes.c_void_p),
+                ("events", ctypes.c_void_p), ("event_count", ctypes.c_void_p),
+                ("event_capacity", ctypes.c_int64), ("bad_flag", ctypes.c_void_p),
+                ("horizon_clears_fine", ctypes.c_void_p),
+                ("horizon_clears_coarse", ctypes.c_void_p), ("lookup_index", ctypes.c_void_p),
+                ("lookup_fp", ctypes.c_void_p), ("eff_records", ctypes.c_void_p),
+                ("flat", ctypes.c_void_p), ("work", ctypes.c_void_p),
+                ("work_count", ctypes.c_void_p), ("phase_events", ctypes.c_void_p * 4)]
+
+
 class PfEvictEvent(ctypes.Structure):
     _fields_ = [("vertex", ctypes.c_int64), ("slot", ctypes.c_int64),
                 ("victim_tag", ctypes.c_uint64), ("victim_touch", ctypes.c_int64)]
@@ -127,6 +139,8 @@ def lib() -> ctypes.CDLL:
                                   vp]
     L.pf_resolve_frame.argtypes = [vp, vp, vp, vp, u64, u64, i64, vp, i64, vp, vp, vp, vp,
                                    vp, vp, vp, vp, vp, vp, vp]
+    L.pf_filter_frame.argtypes = [vp, vp, vp, vp, i64, u64, u64, u64, i64, vp, i64, vp, vp, vp,
+                                  vp, vp]
     L.pf_effective.argtypes = [vp, i32, dbl, dbl, vp, vp, vp]
     L.pf_begin_frame.argtypes = [vp, i64, i32, dbl, dbl, i32, vp, vp]
     L.pf_count_occupied.argtypes = [vp, i64, vp, vp]

@@ -139,10 +139,14 @@ __device__ __forceinline__ int64_t clamp_level(int64_t lv, int32_t delta) {
 }
 
 // 2^e as a double for |e| <= 1022, built from its exponent bits.
+// exp2(e) for integer e, as numpy computes it: normal powers from the exponent field,
+// subnormals below 2^-1022, 0 below 2^-1074 and +inf above 2^1023 -- bit ops, no branch.
 __device__ __forceinline__ double pow2i(int64_t e) {
-    if (e < -1022 || e > 1023)
-        return ldexp(1.0, static_cast<int>(e < -2000 ? -2000 : (e > 2000 ? 2000 : e)));
-    return __longlong_as_double((e + 1023) << 52);
+    const int64_t en = e < -1022 ? -1022 : (e > 1024 ? 1024 : e);
+    const uint64_t normal = static_cast<uint64_t>(en + 1023) << 52;  // e = 1024 -> inf bits
+    const int64_t sh = e + 1074;                                      // subnormal bit index
+    const uint64_t sub = (sh >= 0 && sh < 52) ? (1ull << sh) : 0ull;
+    return __longlong_as_double(e >= -1022 ? normal : sub);
 }
 
 // base_voxel * exp2(level): exact power-of-two scaling.

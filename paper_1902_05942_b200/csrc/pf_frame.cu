@@ -141,10 +141,11 @@ insert_frame_kernel(pf_config cfg, pf_vertices v, pf_table fine, pf_table coarse
             }
         }
     }
-    const int ntables = has_coarse ? 2 : 1;
-#pragma unroll 1
-    for (int tb = 0; tb < ntables; ++tb) {
-        const pf_table t = tb == 0 ? fine : coarse;
+    // unrolled: each copy of warp_insert addresses its table's parameters directly
+#pragma unroll
+    for (int tb = 0; tb < 2; ++tb) {
+        if (tb == 1 && !has_coarse) break;
+        const pf_table &t = tb == 0 ? fine : coarse;
         const CellHash h = tb == 0 ? hf : hc;
         const LaneInsert r = warp_insert<FIXED>(t, valid, h.index, h.fp, val, frame,
                                                 tb == 0 ? ht_f : ht_c);
@@ -623,6 +624,55 @@ int pf_resolve_frame(const pf_config *cfg, const pf_vertices *v, const pf_table 
         finalize_image_kernel<<<blocks_for(m, kThreads), kThreads, 0, st>>>(
             base_image, flat, image, m, static_cast<double>(spp));
     return check_launch(fn);
+}
+
+int pf_filter_frame(const pf_config *cfg, const pf_vertices *v, const pf_table *fine,
+                    const pf_table *coarse, int64_t frame, uint64_t stream_base_accum,
+                    uint64_t stream_base_lookup, uint64_t stream_base_coarse, int64_t spp,
+                    const double *base_image, int64_t n_pixels, double *image, uint8_t *source,
+                    double *chosen, const pf_frame_buffers *b, void *stream) {
+    const char *fn = "pf_filter_frame";
+    if (b == nullptr || cfg == nullptr) return fail_arg(fn, "config/buffers are NULL");
+    if (!b->acc_stats || !b->res_stats) return fail_arg(fn, "stats buffers are NULL");
+    cudaStream_t st = as_stream(stream);
+    auto mark = [&](int k) {
+        if (b->phase_events[k]) cudaEventRecord(static_cast<cudaEvent_t>(b->phase_events[k]), st);
+    };
+    mark(0);
+    // generation fold on both tables (src/pipeline.py:331-333)
+    if (int rc = pf_begin_frame(fine, frame, cfg->temporal_mode, cfg->ema_alpha, cfg->delta_max,
+                                cfg->sample_cap, b->horizon_clears_fine, stream))
+        return rc;
+    if (coarse)
+        if (int rc = pf_begin_frame(coarse, frame, cfg->temporal_mode, cfg->ema_alpha,
+                                    cfg->delta_max, cfg->sample_cap, b->horizon_clears_coarse,
+                                    stream))
+            return rc;
+    if (cudaMemsetAsync(b->acc_stats, 0, sizeof(int64_t) * PF_STAT_COUNT, st) != cudaSuccess ||
+        cudaMemsetAsync(b->res_stats, 0, sizeof(int64_t) * PF_STAT_COUNT, st) != cudaSuccess ||
+        (b->event_count &&
+         cudaMemsetAsync(b->event_count, 0, sizeof(int64_t), st) != cudaSuccess))
+        return check_launch(fn);
+    if (b->bad_flag) {
+        if (cudaMemsetAsync(b->bad_flag, 0, sizeof(int32_t), st) != cudaSuccess)
+            return check_launch(fn);
+        if (v->n > 0)
+            if (int rc = pf_check_contributions(v->contribution, 3 * v->n, b->bad_flag, stream))
+                return rc;
+    }
+    // accumulate_phase (fused, flag-guarded) + the resolve phase's lookup keys
+    mark(1);
+    if (int rc = pf_insert_frame(cfg, v, fine, coarse, stream_base_accum, frame, b->acc_stats,
+                                 b->events, b->event_count, b->event_capacity, b->bad_flag,
+                                 stream_base_lookup, b->lookup_index, b->lookup_fp, stream))
+        return rc;
+    mark(2);
+    const int rc = pf_resolve_frame(cfg, v, fine, coarse, stream_base_lookup, stream_base_coarse,
+                                    spp, base_image, n_pixels, image, b->flat, b->work,
+                                    b->work_count, source, chosen, b->res_stats, b->lookup_index,
+                                    b->lookup_fp, b->eff_records, stream);
+    mark(3);
+    return rc;
 }
 
 }  // extern "C"

@@ -167,20 +167,39 @@ class FrameState:
     prev_seed: int = 0
     prev_spp: int = 0
     scratch: dict = field(default_factory=dict)
-    pending_drains: list = field(default_factory=list)
     lookup_keys: tuple | None = None
+    pending_validation: list = field(default_factory=list)
 
-    def drain_events(self):
-        """Move eviction records of the previous insert from HBM into the table's log."""
-        for t in self.pending_drains:
-            t.eviction_events  # noqa: B018 -- property drains pending device logs
-        self.pending_drains.clear()
+    def poll_validation(self, wait: bool = False, parity: int | None = None):
+        """Raise for a frame whose device input check failed (its kernels were guarded:
+        the tables are untouched).  Non-blocking for landed flags; waits for all flags
+        when wait=True and for the flag of `parity` (its pinned slot is about to be
+        reused)."""
+        keep = []
+        bad = None
+        for host, done, frame, par in self.pending_validation:
+            if wait or par == parity or done.query():
+                done.synchronize()
+                if int(host[0]) and bad is None:
+                    bad = frame
+            else:
+                keep.append((host, done, frame, par))
+        self.pending_validation = keep
+        if bad is not None:
+            raise ValueError(f"frame {bad}: contributions must be finite and non-negative "
+                             "(the frame was rejected; tables unchanged)")
 
-    def pinned_count(self) -> torch.Tensor:
-        p = self.scratch.get("_pinned_count")
+    def drain_events(self, parity: int):
+        """Move the eviction records still held in the event buffer of this parity
+        (written two frames ago) into the table's log before the buffer is reused."""
+        self.fine._drain_tag(parity)
+
+    def pinned_count(self, parity: int) -> torch.Tensor:
+        key = f"_pinned_count{parity}"
+        p = self.scratch.get(key)
         if p is None:
             p = torch.zeros(1, dtype=torch.int64).pin_memory()
-            self.scratch["_pinned_count"] = p
+            self.scratch[key] = p
         return p
 
     @classmethod
@@ -264,7 +283,8 @@ def accumulate_phase(vertices, cfg: FilterConfig, state: FrameState, frame: int,
     Returns (fine keys, coarse keys, stats); keys are lazy (computed on first read)."""
     vs = VertexStream.from_any(vertices)
     n = len(vs)
-    state.drain_events()  # the event log buffer is about to be reused
+    parity = int(frame) & 1
+    state.drain_events(parity)  # this parity's event log buffer is about to be reused
     counters = torch.zeros(_lib.STAT_COUNT, dtype=torch.int64, device=vs.pixel.device)
     stats = FrameStats(frame=frame, n_vertices=n, counters=counters)
     fine_keys = LazyKeyArrays(vs, cfg, seed, rng.STREAM_JITTER_ACCUM, 0)
@@ -285,8 +305,8 @@ def accumulate_phase(vertices, cfg: FilterConfig, state: FrameState, frame: int,
     lk_index = state.buffer("lk_index", (n,), torch.int64)
     lk_fp = state.buffer("lk_fp", (n,), torch.int32)
     lookup_seed = rng.stream_base(seed, rng.STREAM_JITTER_LOOKUP)
-    events = state.buffer("events", (n, 4), torch.int64)
-    ev_count = state.buffer("event_count", (1,), torch.int64)
+    events = state.buffer(f"events{parity}", (n, 4), torch.int64)
+    ev_count = state.buffer(f"event_count{parity}", (1,), torch.int64)
     ev_count.zero_()
     v, keep = vs.c_struct()
     ft = state.fine.c_table()
@@ -299,13 +319,21 @@ def accumulate_phase(vertices, cfg: FilterConfig, state: FrameState, frame: int,
     del keep
     # resolve_phase reuses these lookup keys when called for the same stream / seed / knobs
     state.lookup_keys = (vs, lookup_seed, cfg.to_c(), lk_index, lk_fp)
-    # event count to pinned host memory without a sync; drained before the buffer is reused
-    host = state.pinned_count()
+    _register_event_drain(state, frame, events, ev_count, parity)
+    if flag is not None:
+        raise_if_bad(flag)  # the guarded kernel left the tables untouched
+    return fine_keys, coarse_keys, stats
+
+
+def _register_event_drain(state: FrameState, frame: int, events: torch.Tensor,
+                          ev_count: torch.Tensor, parity: int):
+    """Queue the eviction log of this frame: its count goes to pinned host memory
+    without a sync; the rows are read before the device buffer (one of two, by frame
+    parity) is reused two frames later."""
+    host = state.pinned_count(parity)
     host.copy_(ev_count, non_blocking=True)
     done = torch.cuda.Event()
     done.record()
-    if flag is not None:
-        raise_if_bad(flag)  # the guarded kernel left the tables untouched
     pending = {"drained": False}
 
     def drain(frame=frame, events=events, host=host, done=done, pending=pending):
@@ -324,9 +352,7 @@ def accumulate_phase(vertices, cfg: FilterConfig, state: FrameState, frame: int,
             out.append(EvictionEvent(frame, int(slot), age, int(vtouch)))
         return out
 
-    state.fine._add_pending_events(drain)
-    state.pending_drains.append(state.fine)
-    return fine_keys, coarse_keys, stats
+    state.fine._add_pending_events(drain, parity)
 
 
 def _accumulate_ordered(vs, cfg, state, frame, seed, stats, fine_keys, coarse_keys):
@@ -390,18 +416,101 @@ def resolve_phase(vertices, cfg: FilterConfig, state: FrameState, frame: int, se
     return image, report
 
 
+def _fused_frame(vs: VertexStream, base_image, cfg: FilterConfig, state: FrameState, frame: int,
+                 spp: int, seed: int, validate: bool, want_means: bool, phase_events=None):
+    n = len(vs)
+    base = as_f64(base_image)
+    h, w = int(base.shape[0]), int(base.shape[1])
+    dev = base.device
+    parity = int(frame) & 1
+    state.drain_events(parity)
+    state.poll_validation(parity=parity)  # surface a rejected earlier frame
+    acc = torch.empty(_lib.STAT_COUNT, dtype=torch.int64, device=dev)
+    res = torch.empty(_lib.STAT_COUNT, dtype=torch.int64, device=dev)
+    source = torch.empty(n, dtype=torch.uint8, device=dev)
+    chosen = torch.empty((n, 3), dtype=torch.float64, device=dev) if want_means else None
+    image = torch.empty_like(base)
+    events = state.buffer(f"events{parity}", (max(n, 1), 4), torch.int64)
+    ev_count = state.buffer(f"event_count{parity}", (1,), torch.int64)
+    flag = state.buffer("bad_flag", (1,), torch.int32) if validate else None
+    lk_index = state.buffer("lk_index", (max(n, 1),), torch.int64)
+    lk_fp = state.buffer("lk_fp", (max(n, 1),), torch.int32)
+    b = _lib.PfFrameBuffers()
+    b.acc_stats, b.res_stats = acc.data_ptr(), res.data_ptr()
+    b.events, b.event_count, b.event_capacity = events.data_ptr(), ev_count.data_ptr(), n
+    b.bad_flag = _lib.ptr(flag)
+    b.horizon_clears_fine = state.fine._clears.data_ptr()
+    b.horizon_clears_coarse = state.coarse._clears.data_ptr() if state.coarse is not None else None
+    b.lookup_index, b.lookup_fp = lk_index.data_ptr(), lk_fp.data_ptr()
+    b.eff_records = state.buffer("eff_records", (state.fine.capacity, 4), torch.int64).data_ptr()
+    b.flat = state.buffer("flat", (h * w, 3), torch.float64).data_ptr()
+    b.work = state.buffer("work", (max(n, 1),), torch.int64).data_ptr()
+    b.work_count = state.buffer("work_count", (1,), torch.int64).data_ptr()
+    if phase_events is not None:  # torch.cuda.Events recorded inside the C call
+        for k, e in enumerate(phase_events):
+            b.phase_events[k] = e.cuda_event
+    v, keep = vs.c_struct()
+    ft = state.fine.c_table()
+    ct = state.coarse.c_table() if state.coarse is not None else None
+    cc = cfg.to_c()
+    lookup_seed = rng.stream_base(seed, rng.STREAM_JITTER_LOOKUP)
+    coarse_tag = rng.STREAM_JITTER_LOOKUP if cfg.jitter else rng.STREAM_JITTER_ACCUM
+    _lib.call("pf_filter_frame", ctypes.byref(cc), ctypes.byref(v), ctypes.byref(ft),
+              ctypes.byref(ct) if ct is not None else None, int(frame),
+              rng.stream_base(seed, rng.STREAM_JITTER_ACCUM), lookup_seed,
+              rng.stream_base(seed, coarse_tag), int(spp), base.data_ptr(), h * w,
+              image.data_ptr(), source.data_ptr(), _lib.ptr(chosen), ctypes.byref(b),
+              _lib.stream_handle())
+    del keep
+    state.fine.frame = frame
+    if state.coarse is not None:
+        state.coarse.frame = frame
+    state.lookup_keys = (vs, lookup_seed, cc, lk_index[:n], lk_fp[:n])
+    if n:
+        _register_event_drain(state, frame, events, ev_count, parity)
+    stats = FrameStats(frame=frame, n_vertices=n, counters=acc)
+    report = ResolveReport(source, image, chosen)
+    report.counters = res
+    fine_keys = LazyKeyArrays(vs, cfg, seed, rng.STREAM_JITTER_ACCUM, 0)
+    coarse_keys = (LazyKeyArrays(vs, cfg, seed, rng.STREAM_JITTER_ACCUM, cfg.coarse_delta)
+                   if state.coarse is not None else None)
+    if flag is not None and n:
+        if validate == "sync":
+            raise_if_bad(flag)
+        else:  # deferred: queue the flag read, raise when it has landed
+            key = f"_pinned_flag{parity}"
+            if key not in state.scratch:
+                state.scratch[key] = torch.empty(1, dtype=torch.int32).pin_memory()
+            host = state.scratch[key]
+            host.copy_(flag, non_blocking=True)
+            done = torch.cuda.Event()
+            done.record()
+            state.pending_validation.append((host, done, frame, parity))
+    return image, report, stats, fine_keys, coarse_keys
+
+
 def filter_frame(vertices, base_image, cfg: FilterConfig, state: FrameState, spp: int,
-                 seed: int, validate: bool = True):
+                 seed: int, validate: bool = True, want_means: bool = True, phase_events=None):
     """One frame of the filter without the tracer: begin_frame on both tables,
-    accumulate, resolve (src/pipeline.py:321-363 minus trace/hybrid replay)."""
+    accumulate, resolve (src/pipeline.py:321-363 minus trace/hybrid replay).
+
+    Parallel-insert tables run the whole frame as ONE C-ABI call (pf_filter_frame):
+    every kernel is queued back to back on the current stream; the only host sync is
+    the input-check flag read at the end (validate=True), after which a ValueError
+    means the guarded kernels left the tables untouched."""
     frame = state.frame
     vs = VertexStream.from_any(vertices)  # upload once for both phases
-    state.fine.begin_frame(frame, cfg)
-    if state.coarse is not None:
-        state.coarse.begin_frame(frame, cfg)
-    fine_keys, coarse_keys, stats = accumulate_phase(vs, cfg, state, frame, seed,
-                                                     validate=validate)
-    image, report = resolve_phase(vs, cfg, state, frame, seed, spp, base_image, fine_keys)
+    if state.fine.ordered:
+        state.fine.begin_frame(frame, cfg)
+        if state.coarse is not None:
+            state.coarse.begin_frame(frame, cfg)
+        fine_keys, coarse_keys, stats = accumulate_phase(vs, cfg, state, frame, seed,
+                                                         validate=validate)
+        image, report = resolve_phase(vs, cfg, state, frame, seed, spp, base_image, fine_keys,
+                                      want_means=want_means)
+    else:
+        image, report, stats, fine_keys, coarse_keys = _fused_frame(
+            vs, base_image, cfg, state, frame, spp, seed, validate, want_means, phase_events)
     state.prev_fine_keys = fine_keys
     state.prev_coarse_keys = coarse_keys
     state.prev_seed = seed

@@ -186,24 +186,34 @@ class VoxelTable:
     @property
     def eviction_events(self) -> list[EvictionEvent]:
         """Eviction log (src/table.py:137-141); synchronises pending device results."""
-        for frame, status, slots, vtags, vtouch in self._pending_events:
-            if callable(status):
-                self._events.extend(status())
-                continue
-            st = status.cpu().numpy()
-            ev = np.nonzero(st == 1)[0]
-            if len(ev):
-                sl = slots.cpu().numpy()
-                vt = u64_numpy(vtags)
-                vtt = vtouch.cpu().numpy()
-                for i in ev:
-                    age = (int(vt[i]) >> 32) & _AGE_MASK
-                    self._events.append(EvictionEvent(frame, int(sl[i]), age, int(vtt[i])))
-        self._pending_events.clear()
+        while self._pending_events:
+            self._drain_front()
         return self._events
 
-    def _add_pending_events(self, producer):
-        self._pending_events.append((None, producer, None, None, None))
+    def _drain_front(self):
+        frame, status, slots, vtags, vtouch = self._pending_events.pop(0)
+        if callable(status):  # a fused-frame log (producer closure, see pipeline.py)
+            self._events.extend(status())
+            return
+        st = status.cpu().numpy()
+        ev = np.nonzero(st == 1)[0]
+        if len(ev):
+            sl = slots.cpu().numpy()
+            vt = u64_numpy(vtags)
+            vtt = vtouch.cpu().numpy()
+            for i in ev:
+                age = (int(vt[i]) >> 32) & _AGE_MASK
+                self._events.append(EvictionEvent(frame, int(sl[i]), age, int(vtt[i])))
+
+    def _add_pending_events(self, producer, tag=None):
+        self._pending_events.append((tag, producer, None, None, None))
+
+    def _drain_tag(self, tag):
+        """Drain, in order, every pending log up to and including the last one with `tag`
+        (its device buffer is about to be reused); later logs stay pending."""
+        idx = [k for k, p in enumerate(self._pending_events) if callable(p[1]) and p[0] == tag]
+        for _ in range(idx[-1] + 1 if idx else 0):
+            self._drain_front()
 
     # -- queries --------------------------------------------------------------
 

@@ -501,3 +501,27 @@ def test_full_size_conservation(gpu):
     assert bool(torch.isfinite(image).all())
     assert stats.probe_failures == 0
     assert sum(stats.probe_histogram.values()) == n
+
+
+def test_filter_frame_rejects_invalid_contributions(gpu):
+    """A NaN / negative contribution rejects the frame on the device: begin_frame has
+    folded the tables (as render_frame does before accumulate raises), nothing was
+    inserted, and ValueError surfaces -- immediately with validate='sync', at the next
+    poll with the default deferred check."""
+    d = load_golden("frame_cornell128.npz")
+    vs = golden_stream(d)
+    cfg = cfg_of(gpu, d, "fixed_cfg")
+    for mode in ("sync", True):
+        state = gpu.FrameState.from_config(cfg)
+        gpu.filter_frame(vs, d["base"], cfg, state, 1, 1)
+        bad = gpu.VertexStream.from_any(vs)
+        bad.contribution[7, 1] = float("nan")
+        if mode == "sync":
+            with pytest.raises(ValueError):
+                gpu.filter_frame(bad, d["base"], cfg, state, 1, 2, validate="sync")
+        else:
+            gpu.filter_frame(bad, d["base"], cfg, state, 1, 2)
+            with pytest.raises(ValueError):
+                state.poll_validation(wait=True)
+        st = state.fine.state()
+        assert st["counts"].sum() == 0 and st["hist_counts"].sum() == len(vs)
