@@ -23,6 +23,22 @@ int check_launch(const char *fn) {
     return PF_OK;
 }
 
+SideStream &side_stream() {
+    static SideStream per_device[64];
+    int dev = 0;
+    if (cudaGetDevice(&dev) != cudaSuccess || dev < 0 || dev >= 64) {
+        static SideStream none;
+        return none;
+    }
+    SideStream &s = per_device[dev];
+    if (!s.ok && s.stream == nullptr) {
+        s.ok = cudaStreamCreateWithFlags(&s.stream, cudaStreamNonBlocking) == cudaSuccess &&
+               cudaEventCreateWithFlags(&s.fork, cudaEventDisableTiming) == cudaSuccess &&
+               cudaEventCreateWithFlags(&s.join, cudaEventDisableTiming) == cudaSuccess;
+    }
+    return s;
+}
+
 int sm_count() {
     static int cached = 0;
     if (cached == 0) {

@@ -11,6 +11,15 @@
 
 namespace pf {
 
+// A non-blocking helper stream (plus fork/join events) for work that can overlap the
+// caller's stream inside one C-ABI call; one per device, created on first use.
+struct SideStream {
+    cudaStream_t stream = nullptr;
+    cudaEvent_t fork = nullptr, join = nullptr;
+    bool ok = false;
+};
+SideStream &side_stream();
+
 void set_error(const std::string &msg);
 int fail_arg(const char *fn, const char *what);
 int check_launch(const char *fn);
