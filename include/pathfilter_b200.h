@@ -110,6 +110,9 @@ enum pf_stat_slot {
     PF_STAT_SOURCE_COARSE = 7,
     PF_STAT_SOURCE_UNFILTERED = 8,
     PF_STAT_FALLBACK_ROWS = 9,        /* rows that left the fine rung (resolve work list) */
+    PF_STAT_BAD_PIXELS = 10,          /* rows whose pixel lies outside the image (skipped) */
+    PF_STAT_SHARD_RECORDS = 11,       /* sharded insert: records applied by this owner */
+    PF_STAT_SHARD_REQUESTS = 12,      /* sharded resolve: lookups answered by this owner */
     PF_STAT_HIST_BASE = 16,           /* [16 + k] = #vertices with fine probe_len == k, k < 256 */
     PF_STAT_COUNT = 16 + 256
 };
@@ -231,6 +234,96 @@ int pf_filter_frame(const pf_config *cfg, const pf_vertices *v, const pf_table *
                     uint64_t stream_base_lookup, uint64_t stream_base_coarse, int64_t spp,
                     const double *base_image, int64_t n_pixels, double *image, uint8_t *source,
                     double *chosen, const pf_frame_buffers *buffers, void *stream);
+
+/* image = base + flat / spp over n_pixels RGB pixels (the last line of
+ * src/pipeline.py:282-283). */
+int pf_finalize_image(const double *base_image, const double *flat, double *image,
+                      int64_t n_pixels, int64_t spp, void *stream);
+
+/* ---- 3. key-sharded multi-GPU frame --------------------------------
+ * G ranks (one per GPU, G a power of two <= 64) hold the global fine and coarse
+ * tables of capacity C = 2^log2_capacity as G contiguous slices of S = C/G home
+ * slots: owner(home) = home >> (log2 C - log2 G), so home slots and probe order are
+ * the single-GPU table's.  The owner keeps its slice in a local pf_table of capacity
+ * 2S (C when G == 1) indexed by home - rank*S: a probe chain that would leave the
+ * slice continues in the slice's private tail instead of the next owner's slots.
+ *
+ * One frame, per rank (the exchanges are the caller's all-to-alls, e.g. NCCL):
+ *   pf_begin_frame (both local tables) ; pf_shard_keys ; pf_shard_emit
+ *   -> all-to-all records (int64[5]) and requests (uint64)
+ *   pf_shard_apply(records) ; pf_shard_answer(requests) -> all-to-all answers back
+ *   pf_shard_resolve(answers) ; pf_shard_reset ; pf_shard_fallback_keys ; pf_shard_emit
+ *   -> all-to-all requests ; pf_shard_answer -> all-to-all answers back
+ *   pf_shard_ladder(answers) ; pf_finalize_image ; pf_shard_reset
+ * Every rank pre-aggregates its vertices per distinct key before sending (fixed-point
+ * sums are exactly associative) and deduplicates its lookups, so the exchanges carry
+ * one record per distinct key per rank, not one per vertex.
+ *
+ * Aggregation table key: kind << 61 | home << 32 | fingerprint (home < 2^29), EMPTY
+ * = ~0.  kinds: 0 fine record, 1 coarse record, 2 fine lookup, 3 neighbourhood lookup
+ * (fine table), 4 coarse lookup.  Wire formats: record = int64[5] {key, sum[3],
+ * weight} with sums in the table's sum_mode; request = uint64 key; answer =
+ * uint64[4] {sum[3] (int64 or float64 bits, as VoxelTable.effective), count as
+ * float64 bits, or all ones when the cell is absent}. */
+typedef struct pf_shard {
+    int32_t rank;
+    int32_t world;                  /* power of two, <= 64 */
+    int32_t log2_capacity;          /* global C of both tables, C >= world, <= 2^29 */
+    int32_t sum_mode;               /* pf_sum_mode of both tables */
+    int64_t pixel_base;             /* first pixel id of this rank's image band */
+    uint64_t *agg_keys;             /* [agg_capacity], EMPTY = ~0 */
+    int64_t *agg_sums;              /* [agg_capacity][3] */
+    int64_t *agg_counts;            /* [agg_capacity] weight (records) / send position (lookups) */
+    int64_t agg_capacity;           /* power of two >= 64; at most agg_capacity/2 keys a round */
+    int32_t *distinct;              /* [agg_capacity/2] claimed slots in claim order (-1 hole) */
+    int64_t *n_distinct;            /* [1] slot reservations of the current round */
+    int32_t *overflow;              /* [1] set when a round needed more than agg_capacity/2 keys */
+    int64_t *owner_counts;          /* [2][world] keys per owner: records, requests */
+    int64_t *owner_cursor;          /* [2][world] emit cursors */
+    int32_t *vertex_slot;           /* [n] aggregation slot of each vertex's fine lookup */
+    int32_t *work_slot;             /* [n][28] slots of each work row's 27 neighbour + coarse lookups */
+} pf_shard;
+
+/* Round 1 keys: every vertex's fine and coarse keys (jitter stream 2) are
+ * pre-aggregated as records, its fine lookup key (stream 3) deduplicated as a request.
+ * abort_flag as in pf_insert_frame. */
+int pf_shard_keys(const pf_config *cfg, const pf_vertices *v, const pf_shard *sh,
+                  int32_t has_coarse, uint64_t stream_base_accum, uint64_t stream_base_lookup,
+                  const int32_t *abort_flag, void *stream);
+/* Write the round's records (kinds 0-1) and requests (kinds 2-4) grouped by owner:
+ * owner o's records start at row sum(owner_counts[0][:o]) of send_records, its
+ * requests at sum(owner_counts[1][:o]) of send_requests.  Each request's position is
+ * remembered for the answers.  No-op when overflow is set. */
+int pf_shard_emit(const pf_shard *sh, int64_t *send_records, uint64_t *send_requests,
+                  void *stream);
+/* Owner side: insert received records into the local slices (warp-merged, weighted),
+ * stats as pf_insert_frame (probe failures / histogram weighted by vertex count). */
+int pf_shard_apply(const pf_shard *sh, const pf_table *fine, const pf_table *coarse,
+                   const int64_t *records, int64_t n_records, int64_t frame, int64_t *stats,
+                   void *stream);
+/* Owner side: answer received requests with the effective (sum, count) of the cell. */
+int pf_shard_answer(const pf_shard *sh, const pf_config *cfg, const pf_table *fine,
+                    const pf_table *coarse, const uint64_t *requests, int64_t n_requests,
+                    uint64_t *answers, int64_t *stats, void *stream);
+/* Fine rung from the answers to this rank's round-1 requests; rows below the
+ * threshold go to the work list.  flat holds this rank's pixels [pixel_base,
+ * pixel_base + n_pixels). */
+int pf_shard_resolve(const pf_shard *sh, const pf_config *cfg, const pf_vertices *v,
+                     const uint64_t *answers, double *flat, int64_t n_pixels, int64_t *work,
+                     int64_t *work_count, uint8_t *source, double *chosen, int64_t *stats,
+                     void *stream);
+/* Round 2 keys: the 27 neighbourhood cells and the coarse cell of every work row. */
+int pf_shard_fallback_keys(const pf_config *cfg, const pf_vertices *v, const pf_shard *sh,
+                           int32_t has_coarse, uint64_t stream_base_lookup,
+                           uint64_t stream_base_coarse, const int64_t *work,
+                           const int64_t *work_count, void *stream);
+/* Rungs 2-5 and the composite of every work row from the round-2 answers. */
+int pf_shard_ladder(const pf_shard *sh, const pf_config *cfg, const pf_vertices *v,
+                    int32_t has_coarse, const uint64_t *answers, const int64_t *work,
+                    const int64_t *work_count, double *flat, int64_t n_pixels, uint8_t *source,
+                    double *chosen, int64_t *stats, void *stream);
+/* Empty the aggregation table (only the slots this round claimed) and its counters. */
+int pf_shard_reset(const pf_shard *sh, void *stream);
 
 /* VoxelTable.effective (src/table.py:205-238) over all slots.  eff_sum is int64 for
  * (integrate, fixed) else float64; eff_count is int64 for integrate else float64. */

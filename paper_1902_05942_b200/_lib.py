@@ -15,9 +15,11 @@ import torch
 _PKG = os.path.dirname(os.path.abspath(__file__))
 _ROOT = os.path.dirname(_PKG)
 LIB_PATH = os.environ.get("PF_LIB") or os.path.join(_PKG, "libpf_b200.so")
-SOURCES = [os.path.join(_PKG, "csrc", f) for f in ("pf_common.cu", "pf_table.cu", "pf_frame.cu")]
+SOURCES = [os.path.join(_PKG, "csrc", f) for f in ("pf_common.cu", "pf_table.cu", "pf_frame.cu",
+                                                    "pf_shard.cu")]
 HEADERS = [os.path.join(_PKG, "csrc", f) for f in ("pf_device.cuh", "pf_insert.cuh",
-                                                    "pf_internal.cuh", "pf_sweep.cuh")] + \
+                                                    "pf_internal.cuh", "pf_sweep.cuh",
+                                                    "pf_resolve.cuh")] + \
     [os.path.join(_ROOT, "include", "pathfilter_b200.h")]
 NVCC_FLAGS = ["-gencode", "arch=compute_100a,code=sm_100a", "-O3", "-lineinfo",
               "-fmad=false", "-std=c++17", "-Xcompiler", "-fPIC", "-shared"]
@@ -28,7 +30,9 @@ EXPORTS = ("pf_abi_version", "pf_last_error", "pf_device_sm_count", "pf_accumula
            "pf_hash_arrays", "pf_insert_frame", "pf_resolve_frame", "pf_filter_frame",
            "pf_effective",
            "pf_begin_frame", "pf_check_contributions", "pf_selftest_division",
-           "pf_count_occupied")
+           "pf_count_occupied", "pf_finalize_image", "pf_shard_keys", "pf_shard_emit",
+           "pf_shard_apply", "pf_shard_answer", "pf_shard_resolve", "pf_shard_fallback_keys",
+           "pf_shard_ladder", "pf_shard_reset")
 
 
 def build(force: bool = False, verbose: bool = False) -> str:
@@ -92,6 +96,17 @@ class PfFrameBuffers(ctypes.Structure):
                 ("work_count", ctypes.c_void_p), ("phase_events", ctypes.c_void_p * 4)]
 
 
+class PfShard(ctypes.Structure):
+    _fields_ = [("rank", ctypes.c_int32), ("world", ctypes.c_int32),
+                ("log2_capacity", ctypes.c_int32), ("sum_mode", ctypes.c_int32),
+                ("pixel_base", ctypes.c_int64), ("agg_keys", ctypes.c_void_p),
+                ("agg_sums", ctypes.c_void_p), ("agg_counts", ctypes.c_void_p),
+                ("agg_capacity", ctypes.c_int64), ("distinct", ctypes.c_void_p),
+                ("n_distinct", ctypes.c_void_p), ("overflow", ctypes.c_void_p),
+                ("owner_counts", ctypes.c_void_p), ("owner_cursor", ctypes.c_void_p),
+                ("vertex_slot", ctypes.c_void_p), ("work_slot", ctypes.c_void_p)]
+
+
 class PfEvictEvent(ctypes.Structure):
     _fields_ = [("vertex", ctypes.c_int64), ("slot", ctypes.c_int64),
                 ("victim_tag", ctypes.c_uint64), ("victim_touch", ctypes.c_int64)]
@@ -107,6 +122,9 @@ STAT_SOURCE_NEIGHBORHOOD = 6
 STAT_SOURCE_COARSE = 7
 STAT_SOURCE_UNFILTERED = 8
 STAT_FALLBACK_ROWS = 9
+STAT_BAD_PIXELS = 10
+STAT_SHARD_RECORDS = 11
+STAT_SHARD_REQUESTS = 12
 STAT_HIST_BASE = 16
 STAT_COUNT = 16 + 256
 
@@ -146,6 +164,15 @@ def lib() -> ctypes.CDLL:
     L.pf_count_occupied.argtypes = [vp, i64, vp, vp]
     L.pf_check_contributions.argtypes = [vp, i64, vp, vp]
     L.pf_selftest_division.argtypes = [u64, i64, dbl, vp, vp]
+    L.pf_finalize_image.argtypes = [vp, vp, vp, i64, i64, vp]
+    L.pf_shard_keys.argtypes = [vp, vp, vp, i32, u64, u64, vp, vp]
+    L.pf_shard_emit.argtypes = [vp, vp, vp, vp]
+    L.pf_shard_apply.argtypes = [vp, vp, vp, vp, i64, i64, vp, vp]
+    L.pf_shard_answer.argtypes = [vp, vp, vp, vp, vp, i64, vp, vp, vp]
+    L.pf_shard_resolve.argtypes = [vp, vp, vp, vp, vp, i64, vp, vp, vp, vp, vp, vp]
+    L.pf_shard_fallback_keys.argtypes = [vp, vp, vp, i32, u64, u64, vp, vp, vp]
+    L.pf_shard_ladder.argtypes = [vp, vp, vp, i32, vp, vp, vp, vp, i64, vp, vp, vp, vp]
+    L.pf_shard_reset.argtypes = [vp, vp]
     for name in EXPORTS[3:]:
         getattr(L, name).restype = ctypes.c_int
     _lib = L

@@ -2,7 +2,7 @@
 // and coarse tables in one pass over the vertex buffer) and resolve_phase (lookup
 // keys, fine rung, 3x3x3 neighbourhood + coarse rungs on a compacted work list,
 // composite).  src/pipeline.py:152-283.
-#include "pf_insert.cuh"
+#include "pf_resolve.cuh"
 #include "pf_sweep.cuh"
 #include "pf_internal.cuh"
 
@@ -14,36 +14,6 @@ constexpr int kThreads = 256;
 #endif
 constexpr int kResolveKV = PF_RESOLVE_KV;  // vertices per thread in resolve_main
 constexpr int kWarps = kThreads / 32;
-
-// Per-CTA counters in 32-bit shared words (native ATOMS; a CTA never sees 2^32
-// events), flushed once as 64-bit global adds.
-struct BlockStats {
-    unsigned v[10];
-    unsigned hist[256];
-};
-
-__device__ __forceinline__ void stats_init(BlockStats &b) {
-    for (int k = threadIdx.x; k < 10; k += blockDim.x) b.v[k] = 0;
-    for (int k = threadIdx.x; k < 256; k += blockDim.x) b.hist[k] = 0;
-}
-
-// warp-aggregated add of a per-lane predicate into a block counter
-__device__ __forceinline__ void warp_count(BlockStats &b, int slot, bool pred) {
-    const unsigned m = __ballot_sync(kFull, pred);
-    if ((threadIdx.x & 31) == 0 && m) atomicAdd(&b.v[slot], static_cast<unsigned>(__popc(m)));
-}
-
-__device__ __forceinline__ void stats_flush(const BlockStats &b, int64_t *stats, bool with_hist) {
-    for (int k = threadIdx.x; k < 10; k += blockDim.x)
-        if (b.v[k])
-            atomicAdd(reinterpret_cast<unsigned long long *>(stats + k),
-                      static_cast<unsigned long long>(b.v[k]));
-    if (with_hist)
-        for (int k = threadIdx.x; k < 256; k += blockDim.x)
-            if (b.hist[k])
-                atomicAdd(reinterpret_cast<unsigned long long *>(stats + PF_STAT_HIST_BASE + k),
-                          static_cast<unsigned long long>(b.hist[k]));
-}
 
 __device__ __forceinline__ void log_eviction(pf_evict_event *events, int64_t *count, int64_t cap,
                                              int64_t vertex, const LaneInsert &r) {
@@ -200,40 +170,13 @@ struct ResolveArgs {
     const uint64_t *lk_index;  // precomputed lookup keys (or NULL)
     const uint32_t *lk_fp;
     const ulonglong4 *rec;     // per-slot effective records of the fine table (or NULL)
+    int64_t n_pixels;          // flat holds pixels [0, n_pixels)
 };
-
-// Per-slot effective record: three sum words (int64 or float64 bits, as
-// VoxelTable.effective's dtype) and the count as a float64 -- one 32-byte sector.
-__device__ __forceinline__ ulonglong4 pack_effective(const Effective &e, bool as_int) {
-    ulonglong4 r;
-    r.x = as_int ? static_cast<unsigned long long>(e.isum[0]) : __double_as_longlong(e.fsum[0]);
-    r.y = as_int ? static_cast<unsigned long long>(e.isum[1]) : __double_as_longlong(e.fsum[1]);
-    r.z = as_int ? static_cast<unsigned long long>(e.isum[2]) : __double_as_longlong(e.fsum[2]);
-    r.w = __double_as_longlong(e.fcnt);
-    return r;
-}
-
-__device__ __forceinline__ Effective unpack_effective(const ulonglong4 &r, bool as_int) {
-    Effective e;
-    const unsigned long long w[3] = {r.x, r.y, r.z};
-#pragma unroll
-    for (int c = 0; c < 3; ++c) {
-        e.isum[c] = as_int ? static_cast<int64_t>(w[c]) : 0;
-        e.fsum[c] = as_int ? 0.0 : __longlong_as_double(w[c]);
-    }
-    e.fcnt = __longlong_as_double(r.w);
-    e.icnt = static_cast<int64_t>(e.fcnt);  // exact: counts < 2^53
-    return e;
-}
 
 // The fine table's effective value of slot s: its record when the effective pass ran.
 __device__ __forceinline__ Effective fine_effective(const ResolveArgs &a, int64_t s) {
     const int mode = a.cfg.temporal_mode;
-    if (a.rec != nullptr) {
-        const ulonglong2 *p = reinterpret_cast<const ulonglong2 *>(a.rec + s);
-        const ulonglong2 lo = __ldg(p), hi = __ldg(p + 1);
-        return unpack_effective(make_ulonglong4(lo.x, lo.y, hi.x, hi.y), eff_is_int(a.fine, mode));
-    }
+    if (a.rec != nullptr) return unpack_effective(load_record(a.rec, s), eff_is_int(a.fine, mode));
     return effective_at(a.fine, s, mode, a.cfg.ema_alpha, a.cfg.delta_max);
 }
 
@@ -250,44 +193,21 @@ effective_records_kernel(pf_table t, int mode, double ema, double delta_max, ulo
     });
 }
 
-struct KeyAndHash {
-    CellKey first;
-    CellHash second;
-};
-
 // The fine lookup key of one vertex: jitter stream 3 when jitter is on
 // (src/pipeline.py:222-225), level_delta 0.
 __device__ __forceinline__ KeyAndHash lookup_key(const ResolveArgs &a, int64_t row) {
-    const pf_config &cfg = a.cfg;
-    const VertexIn x = load_vertex(a.v, row, cfg);
-    double du = 0.0, dv = 0.0;
-    if (cfg.jitter) {
-        double u1, u2;
-        jitter_draws(a.h0_lookup, x.pixel, x.sample, u1, u2);
-        disc_offset(u1, u2, du, dv);
-    }
-    const KeyShared ks = key_shared(cfg, x);
-    double jt[3];
-    KeyAndHash r;
-    r.first = make_key(cfg, x, ks, cfg.jitter, du, dv, 0, jt);
-    r.second = key_hash(r.first, ks);
-    return r;
-}
-
-// _mean_rows (src/pipeline.py:196-200) for one row.
-__device__ __forceinline__ double row_mean(double sum, double cnt, bool fixed) {
-    double d = np_max(cnt, 1e-300);
-    if (fixed) d = dmul(d, kFixedScale);
-    return ddiv(sum, d);
+    return vertex_key(a.cfg, a.v, a.h0_lookup, row, 0);
 }
 
 __device__ __forceinline__ void composite(const ResolveArgs &a, int64_t i, int64_t pixel,
                                           const double chosen[3], int source) {
     const uint64_t stream = l2_evict_first(), keep = l2_evict_last();
+    if (pixel >= 0 && pixel < a.n_pixels) {
 #pragma unroll
-    for (int c = 0; c < 3; ++c) {
-        const double tp = ld_stream(a.v.throughput + 3 * i + c, stream);
-        red_add_f64(a.flat + 3 * pixel + c, dmul(tp, chosen[c]), keep);
+        for (int c = 0; c < 3; ++c) {
+            const double tp = ld_stream(a.v.throughput + 3 * i + c, stream);
+            red_add_f64(a.flat + 3 * pixel + c, dmul(tp, chosen[c]), keep);
+        }
     }
     if (a.source) a.source[i] = static_cast<uint8_t>(source);
     if (a.chosen) {
@@ -357,10 +277,11 @@ __global__ void __launch_bounds__(kThreads) resolve_main_kernel(ResolveArgs a) {
             if (valid[k] && cnt >= a.thr) {
                 fine_ok = true;
                 double m[3];
+                const bool in_image = pixel[k] >= 0 && pixel[k] < a.n_pixels;
 #pragma unroll
                 for (int c = 0; c < 3; ++c) {
                     m[c] = row_mean(eff_sum_f64(e, as_int, c), cnt, fixed);
-                    red_add_f64(a.flat + 3 * pixel[k] + c, dmul(tp[k][c], m[c]), keep);
+                    if (in_image) red_add_f64(a.flat + 3 * pixel[k] + c, dmul(tp[k][c], m[c]), keep);
                 }
                 if (a.source) a.source[row[k]] = 0;
                 if (a.chosen) {
@@ -382,6 +303,7 @@ __global__ void __launch_bounds__(kThreads) resolve_main_kernel(ResolveArgs a) {
             if (need) a.work[static_cast<int64_t>(wb) + __popc(m & ((1u << lane) - 1u))] = row[k];
         }
         warp_count(bs, PF_STAT_SOURCE_FINE, valid[k] && fine_ok);
+        warp_count(bs, PF_STAT_BAD_PIXELS, valid[k] && fine_ok && !(pixel[k] >= 0 && pixel[k] < a.n_pixels));
         warp_count(bs, PF_STAT_FALLBACK_ROWS, need);
     }
     __syncthreads();
@@ -423,8 +345,8 @@ __global__ void __launch_bounds__(kThreads) resolve_fallback_kernel(ResolveArgs 
         bool found = false;
         Effective e{};
         if (lane < 27) {
-            const int dx = lane / 9 - 1, dy = (lane / 3) % 3 - 1, dz = lane % 3 - 1;
-            const CellHash h = cell_hash(kq[0] + dx, kq[1] + dy, kq[2] + dz, klev,
+            const CellHash h = cell_hash(kq[0] + neighbour_dx(lane), kq[1] + neighbour_dy(lane),
+                                         kq[2] + neighbour_dz(lane), klev,
                                          static_cast<uint64_t>(kaux), 0, 0u);
             const int64_t s = probe_lookup(a.fine.tags, fmask, a.fine.probe_limit, h.index, h.fp);
             if (s >= 0) {
@@ -432,70 +354,29 @@ __global__ void __launch_bounds__(kThreads) resolve_fallback_kernel(ResolveArgs 
                 e = fine_effective(a, s);
             }
         }
-        // ordered pool: (src/pipeline.py:185-192)
-        int64_t pis[3] = {0, 0, 0}, pic = 0;
-        double pfs[3] = {0.0, 0.0, 0.0}, pfc = 0.0;
-        const unsigned fm = __ballot_sync(kFull, found);
-        for (int j = 0; j < 27; ++j) {
-            if (!((fm >> j) & 1u)) continue;  // warp-uniform
-#pragma unroll
-            for (int c = 0; c < 3; ++c) {
-                if (as_int) pis[c] += __shfl_sync(kFull, static_cast<long long>(e.isum[c]), j);
-                else pfs[c] = dadd(pfs[c], __shfl_sync(kFull, e.fsum[c], j));
-            }
-            if (mode == PF_INTEGRATE) pic += __shfl_sync(kFull, static_cast<long long>(e.icnt), j);
-            else pfc = dadd(pfc, __shfl_sync(kFull, e.fcnt, j));
-        }
+        const Pool pool = pool_neighbours(found, e, as_int, mode);
         // every lane now holds the same pooled sums; lane 0 finishes the row
-        const double cnt_n = (mode == PF_INTEGRATE) ? static_cast<double>(pic) : pfc;
-        const bool ok_n = cnt_n >= a.thr;
+        const bool ok_n = ((mode == PF_INTEGRATE) ? static_cast<double>(pool.icnt) : pool.fcnt) >= a.thr;
         if (lane == 0) {
-        double mean_n[3] = {0.0, 0.0, 0.0};
-        if (cnt_n > 0.0) {
-#pragma unroll
-            for (int c = 0; c < 3; ++c)
-                mean_n[c] = row_mean(as_int ? static_cast<double>(pis[c]) : pfs[c], cnt_n, fixed);
-        }
-        double cnt_c = 0.0;
-        double mean_c[3] = {0.0, 0.0, 0.0};
         const VertexIn x = load_vertex(a.v, row, cfg);
+        bool coarse_found = false;
+        Effective ce{};
         if (!ok_n && a.has_coarse) {
-            double du = 0.0, dv = 0.0;
-            if (cfg.jitter) {
-                double u1, u2;
-                jitter_draws(a.h0_coarse, x.pixel, x.sample, u1, u2);
-                disc_offset(u1, u2, du, dv);
-            }
-            const KeyShared ks = key_shared(cfg, x);
-            double jt[3];
-            const CellKey kc = make_key(cfg, x, ks, cfg.jitter, du, dv, cfg.coarse_delta, jt);
-            const CellHash h = key_hash(kc, ks);
+            const CellHash h = vertex_key(cfg, a.v, a.h0_coarse, row, cfg.coarse_delta).second;
             const int64_t s = probe_lookup(a.coarse.tags, static_cast<uint64_t>(a.coarse.capacity) - 1,
                                            a.coarse.probe_limit, h.index, h.fp);
             if (s >= 0) {
-                const Effective ce = effective_at(a.coarse, s, mode, cfg.ema_alpha, cfg.delta_max);
-                cnt_c = ce.fcnt;
-                if (cnt_c > 0.0) {
-                    const bool c_int = eff_is_int(a.coarse, mode);
-#pragma unroll
-                    for (int c = 0; c < 3; ++c)
-                        mean_c[c] = row_mean(eff_sum_f64(ce, c_int, c), cnt_c, fixed);
-                }
+                coarse_found = true;
+                ce = effective_at(a.coarse, s, mode, cfg.ema_alpha, cfg.delta_max);
             }
         }
-        const bool ok_c = !ok_n && cnt_c >= a.thr;
-        const bool any_n = !ok_n && !ok_c && cnt_n >= 1.0;
-        const bool any_c = !ok_n && !ok_c && !any_n && cnt_c >= 1.0;
-        // written as selects: an if/else-if chain here was mis-compiled (nvcc 12.9, sm_100a),
-        // taking the unfiltered branch with ok_c set (tests/test_gpu_parity.py::test_frame_golden)
-        const int src = (ok_n || any_n) ? 1 : ((ok_c || any_c) ? 2 : 3);
-        double ch[3];
+        double contrib[3], ch[3];
 #pragma unroll
-        for (int c = 0; c < 3; ++c) {
-            const double contrib = __ldg(a.v.contribution + 3 * row + c);
-            ch[c] = src == 1 ? mean_n[c] : (src == 2 ? mean_c[c] : contrib);
-        }
+        for (int c = 0; c < 3; ++c) contrib[c] = __ldg(a.v.contribution + 3 * row + c);
+        const int src = ladder_choose(pool, as_int, mode, fixed, a.thr, coarse_found, ce,
+                                      eff_is_int(a.coarse, mode), contrib, ch);
         composite(a, row, x.pixel, ch, src);
+        if (!(x.pixel >= 0 && x.pixel < a.n_pixels)) atomicAdd(&bs.v[PF_STAT_BAD_PIXELS], 1u);
         atomicAdd(&bs.v[PF_STAT_SOURCE_FINE + src], 1u);
         }
         __syncwarp();
@@ -600,6 +481,7 @@ int pf_resolve_frame(const pf_config *cfg, const pf_vertices *v, const pf_table 
         a.lk_index = lookup_index;
         a.lk_fp = lookup_fp;
         a.rec = reinterpret_cast<const ulonglong4 *>(eff_records);
+        a.n_pixels = n_pixels;
         if (eff_records != nullptr) {
             effective_records_kernel<<<sweep_blocks<kThreads>(fine->capacity, sm_count()), kThreads,
                                        0, st>>>(*fine, kc.temporal_mode, kc.ema_alpha,
@@ -623,6 +505,18 @@ int pf_resolve_frame(const pf_config *cfg, const pf_vertices *v, const pf_table 
     if (m > 0)
         finalize_image_kernel<<<blocks_for(m, kThreads), kThreads, 0, st>>>(
             base_image, flat, image, m, static_cast<double>(spp));
+    return check_launch(fn);
+}
+
+int pf_finalize_image(const double *base_image, const double *flat, double *image,
+                      int64_t n_pixels, int64_t spp, void *stream) {
+    const char *fn = "pf_finalize_image";
+    if (n_pixels < 0 || spp < 1) return fail_arg(fn, "n_pixels must be >= 0 and spp >= 1");
+    const int64_t m = 3 * n_pixels;
+    if (m == 0) return PF_OK;
+    if (!base_image || !flat || !image) return fail_arg(fn, "image buffers are NULL");
+    finalize_image_kernel<<<blocks_for(m, kThreads), kThreads, 0, as_stream(stream)>>>(
+        base_image, flat, image, m, static_cast<double>(spp));
     return check_launch(fn);
 }
 

@@ -26,25 +26,23 @@ struct LaneInsert {
 // All 32 lanes must call this together.  Lanes holding the same (index, fp) are
 // merged with __match_any_sync; the lowest lane (= earliest vertex) probes and
 // claims once and adds the group's summed radiance with one atomic per channel,
-// plus popc(peers) to the count.  Followers report what a sequential caller would
-// see after the leader: same slot and probe length, status 1 -> 0.
-template <bool FIXED>
-__device__ __forceinline__ LaneInsert warp_insert(const pf_table &t, bool valid, uint64_t idx,
-                                                  uint32_t fp, const double val[3], int64_t frame,
-                                                  uint64_t home_tag) {
+// plus the group's weight to the count (popc(peers) for one vertex per lane, the
+// summed per-lane weights when WEIGHTED -- pre-aggregated shard records).  Lane
+// sums arrive already quantised (FIXED) or as float64.  Followers report what a
+// sequential caller would see after the leader: same slot and probe length,
+// status 1 -> 0.
+template <bool FIXED, bool WEIGHTED>
+__device__ __forceinline__ LaneInsert warp_insert_sums(const pf_table &t, bool valid, uint64_t idx,
+                                                       uint32_t fp, int64_t qsum[3],
+                                                       double fsum[3], uint64_t weight,
+                                                       int64_t frame, uint64_t home_tag) {
     const unsigned lane = threadIdx.x & 31u;
     const uint64_t k2 = static_cast<uint64_t>(fp) | (static_cast<uint64_t>(valid) << 32);
     const unsigned peers = __match_any_sync(kFull, valid ? idx : 0ull) & __match_any_sync(kFull, k2);
     const int leader = __ffs(peers) - 1;
     const bool is_leader = valid && static_cast<int>(lane) == leader;
+    if (WEIGHTED && !valid) weight = 0;
 
-    int64_t qsum[3];
-    double fsum[3];
-#pragma unroll
-    for (int c = 0; c < 3; ++c) {
-        if (FIXED) qsum[c] = valid ? quantize_fixed(val[c]) : 0;
-        else fsum[c] = valid ? val[c] : 0.0;
-    }
     // Group sums by pointer jumping over each group's member list: every lane links to
     // the next higher lane of its group and adds its successor's partial sum, doubling
     // the stride each round, so the leader holds the group total after
@@ -64,6 +62,10 @@ __device__ __forceinline__ LaneInsert warp_insert(const pf_table &t, bool valid,
                 const double x = __shfl_sync(kFull, fsum[c], src);
                 if (nxt >= 0) fsum[c] = dadd(fsum[c], x);
             }
+        }
+        if (WEIGHTED) {
+            const unsigned long long x = __shfl_sync(kFull, static_cast<unsigned long long>(weight), src);
+            if (nxt >= 0) weight += x;
         }
         if (nxt >= 0) nxt = nn;
     }
@@ -87,7 +89,7 @@ __device__ __forceinline__ LaneInsert warp_insert(const pf_table &t, bool valid,
                 else
                     red_add_f64(static_cast<double *>(t.sums) + 3 * s + c, fsum[c], keep);
             }
-            red_add_u64(t.counts + s, static_cast<uint64_t>(__popc(peers)), keep);
+            red_add_u64(t.counts + s, WEIGHTED ? weight : static_cast<uint64_t>(__popc(peers)), keep);
             st_relaxed_u64(t.last_touch + s, static_cast<uint64_t>(frame));
         }
     }
@@ -107,6 +109,21 @@ __device__ __forceinline__ LaneInsert warp_insert(const pf_table &t, bool valid,
     out.leader = is_leader;
     out.peers = peers;
     return out;
+}
+
+// One vertex per lane: quantise the lane's radiance and insert it (weight 1).
+template <bool FIXED>
+__device__ __forceinline__ LaneInsert warp_insert(const pf_table &t, bool valid, uint64_t idx,
+                                                  uint32_t fp, const double val[3], int64_t frame,
+                                                  uint64_t home_tag) {
+    int64_t qsum[3];
+    double fsum[3];
+#pragma unroll
+    for (int c = 0; c < 3; ++c) {
+        if (FIXED) qsum[c] = valid ? quantize_fixed(val[c]) : 0;
+        else fsum[c] = valid ? val[c] : 0.0;
+    }
+    return warp_insert_sums<FIXED, false>(t, valid, idx, fp, qsum, fsum, 1, frame, home_tag);
 }
 
 }  // namespace pf

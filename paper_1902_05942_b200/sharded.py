@@ -1,0 +1,400 @@
+"""Key-sharded multi-GPU filter frame.
+
+One process per GPU.  The global fine and coarse tables (capacity C each, the
+single-GPU layout) are split into G contiguous slices of home slots; rank r owns
+homes [r*S, (r+1)*S), S = C/G, and keeps them in a local table of capacity 2S
+(C when G == 1) so probe chains stay on the owner (include/pathfilter_b200.h, section 3).
+
+A frame is a generator that yields its collectives and receives their results:
+
+    round 1   keys of every local vertex; pre-aggregated records (fine, coarse) and
+              deduplicated fine lookups, bucketed by owner            (pf_shard_keys/emit)
+              -> all-to-all of counts (+ overflow / bad-input flags), records, requests
+              owner applies the records, answers the lookups        (pf_shard_apply/answer)
+              -> all-to-all of answers; fine rung + work list       (pf_shard_resolve)
+    round 2   27 neighbourhood + coarse lookups of the work rows     (pf_shard_fallback_keys)
+              -> counts, requests; owner answers; answers back; ladder (pf_shard_ladder)
+    image     composite local to the rank's pixels ("band"), or summed over ranks with
+              a reduce-scatter of the flat buffer ("reduce": ranks trace different
+              samples of the same pixels), then base + flat / spp    (pf_finalize_image)
+
+`run_dist` drives a frame with torch.distributed (NCCL on B200; gloo copies through
+host memory); `run_loopback` drives G virtual ranks in one process (tests).
+
+Results equal the single-GPU frame over the ranks' concatenated vertex streams: each
+key's records reach exactly one owner, 16.16 fixed-point sums are exactly associative,
+and every rung consumes the same effective (sum, count) values in the reference's
+order.  Only the slot a key occupies can differ (chains never cross slices), which
+matters only when a chain reaches probe_limit.
+"""
+
+from __future__ import annotations
+
+import ctypes
+from dataclasses import dataclass
+
+import numpy as np
+import torch
+
+from . import _lib, rng
+from .keys import FilterConfig, as_f64, device
+from .pipeline import FrameStats, ResolveReport, VertexStream
+from .table import VoxelTable
+
+WORK_KEYS = 28
+_AGG_EMPTY = -1  # ~0 as int64
+
+
+@dataclass
+class Exchange:
+    """One all-to-all: rows [sum(send_rows[:p]), +send_rows[p]) of `tensor` go to rank p;
+    the result holds recv_rows[p] rows from each rank p, in rank order."""
+
+    tensor: torch.Tensor
+    send_rows: list
+    recv_rows: list
+
+
+@dataclass
+class ReduceScatter:
+    """Sum `tensor` (rows divisible by world) over ranks; rank r receives block r."""
+
+    tensor: torch.Tensor
+
+
+def _next_pow2(x: int) -> int:
+    return 1 << max(int(x) - 1, 1).bit_length()
+
+
+class ShardedState:
+    """This rank's slices of the fine/coarse tables plus the aggregation scratch."""
+
+    def __init__(self, cfg: FilterConfig, rank: int, world: int, agg_capacity: int = 1 << 20):
+        _lib.require_cuda()
+        C = int(cfg.capacity)
+        if world < 1 or world & (world - 1) or world > 64:
+            raise ValueError("world must be a power of two <= 64")
+        if C < world or C & (C - 1):
+            raise ValueError("capacity must be a power of two >= world")
+        if not 0 <= rank < world:
+            raise ValueError("rank out of range")
+        self.cfg_capacity = C
+        self.rank, self.world = int(rank), int(world)
+        self.slice = C // world
+        local = C if world == 1 else 2 * self.slice
+        self.fine = VoxelTable(local, cfg.probe_limit, cfg.sum_mode, cfg.evict_horizon,
+                               cfg.evict_min_age)
+        self.coarse = (VoxelTable(local, cfg.probe_limit, cfg.sum_mode, cfg.evict_horizon,
+                                  cfg.evict_min_age) if cfg.multi_level else None)
+        self.sum_mode = cfg.sum_mode
+        self.frame = 0
+        dev = device()
+        self._dev = dev
+        self.n_distinct = torch.zeros(1, dtype=torch.int64, device=dev)
+        self.overflow = torch.zeros(1, dtype=torch.int32, device=dev)
+        self.owner_counts = torch.zeros((2, world), dtype=torch.int64, device=dev)
+        self.owner_cursor = torch.zeros((2, world), dtype=torch.int64, device=dev)
+        self.bad_flag = torch.zeros(1, dtype=torch.int32, device=dev)
+        self._alloc_agg(_next_pow2(max(int(agg_capacity), 64)))
+        self.vertex_slot = torch.empty(0, dtype=torch.int32, device=dev)
+        self.work_slot = torch.empty(0, dtype=torch.int32, device=dev)
+        self.scratch: dict = {}
+        self.regrows = 0
+
+    # -- buffers ------------------------------------------------------------------
+
+    def _alloc_agg(self, cap: int):
+        dev = self._dev
+        self.agg_capacity = cap
+        self.agg_keys = torch.full((cap,), _AGG_EMPTY, dtype=torch.int64, device=dev)
+        self.agg_sums = torch.zeros((cap, 3), dtype=torch.int64, device=dev)
+        self.agg_counts = torch.zeros(cap, dtype=torch.int64, device=dev)
+        self.distinct = torch.empty(cap // 2, dtype=torch.int32, device=dev)
+        self.send_records = torch.empty((cap // 2, 5), dtype=torch.int64, device=dev)
+        self.send_requests = torch.empty(cap // 2, dtype=torch.int64, device=dev)
+
+    def grow_agg(self, need: int):
+        """Re-allocate the aggregation table for `need` distinct keys (empty)."""
+        self._alloc_agg(_next_pow2(2 * int(need) + 2))
+        self.n_distinct.zero_()
+        self.overflow.zero_()
+        self.owner_counts.zero_()
+        self.regrows += 1
+
+    def buffer(self, name: str, shape, dtype) -> torch.Tensor:
+        n = int(np.prod(shape))
+        b = self.scratch.get(name)
+        if b is None or b.numel() < n or b.dtype != dtype:
+            b = torch.empty(max(n, 1), dtype=dtype, device=self._dev)
+            self.scratch[name] = b
+        return b[:n].view(*shape)
+
+    def ensure_rows(self, n: int):
+        if self.vertex_slot.numel() < n:
+            self.vertex_slot = torch.empty(n, dtype=torch.int32, device=self._dev)
+            self.work_slot = torch.empty((n, WORK_KEYS), dtype=torch.int32, device=self._dev)
+
+    def c_shard(self, pixel_base: int) -> _lib.PfShard:
+        s = _lib.PfShard()
+        s.rank, s.world = self.rank, self.world
+        s.log2_capacity = self.cfg_capacity.bit_length() - 1
+        s.sum_mode = 0 if self.sum_mode == "fixed" else 1
+        s.pixel_base = int(pixel_base)
+        s.agg_keys, s.agg_sums = self.agg_keys.data_ptr(), self.agg_sums.data_ptr()
+        s.agg_counts, s.agg_capacity = self.agg_counts.data_ptr(), self.agg_capacity
+        s.distinct, s.n_distinct = self.distinct.data_ptr(), self.n_distinct.data_ptr()
+        s.overflow = self.overflow.data_ptr()
+        s.owner_counts, s.owner_cursor = self.owner_counts.data_ptr(), self.owner_cursor.data_ptr()
+        s.vertex_slot = self.vertex_slot.data_ptr()
+        s.work_slot = self.work_slot.data_ptr()
+        return s
+
+
+def _stats_message(st: ShardedState, records: bool) -> torch.Tensor:
+    """[world, 4] int64 per destination: records, requests, overflow, bad input."""
+    oc = st.owner_counts
+    cols = [oc[0] if records else torch.zeros_like(oc[0]), oc[1],
+            st.overflow.to(torch.int64).expand(st.world),
+            st.bad_flag.to(torch.int64).expand(st.world)]
+    return torch.stack(cols, dim=1).contiguous()
+
+
+def filter_frame_sharded(vertices, base_image, cfg: FilterConfig, st: ShardedState, spp: int,
+                         seed: int, pixel_base: int = 0, composite: str = "band",
+                         validate: bool = True, want_means: bool = True):
+    """One frame on this rank (generator: yields Exchange / ReduceScatter).
+
+    composite="band": the rank's vertices all land in its pixel band
+    [pixel_base, pixel_base + H*W) and `base_image` is that band (H x W x 3).
+    composite="reduce": every rank's vertices address the whole image of H x W
+    pixels (pixel_base 0) -- e.g. each rank traced other samples -- and the result is
+    this rank's block of rows of the final image (H divisible by world).
+
+    Returns (image, ResolveReport, FrameStats) via StopIteration.value."""
+    if composite not in ("band", "reduce"):
+        raise ValueError("composite must be 'band' or 'reduce'")
+    frame = st.frame
+    vs = VertexStream.from_any(vertices)
+    n = len(vs)
+    base = as_f64(base_image)
+    H, W = int(base.shape[0]), int(base.shape[1])
+    G = st.world
+    if composite == "reduce" and (H % G or pixel_base):
+        raise ValueError("reduce composite needs H divisible by world and pixel_base 0")
+    n_pix = H * W
+    dev = base.device
+    st.ensure_rows(max(n, 1))
+    cc = cfg.to_c()
+    v, keep = vs.c_struct()
+    ft = st.fine.c_table()
+    ct = st.coarse.c_table() if st.coarse is not None else None
+    has_coarse = int(st.coarse is not None)
+    stream = _lib.stream_handle()
+    acc = torch.zeros(_lib.STAT_COUNT, dtype=torch.int64, device=dev)
+    res = torch.zeros(_lib.STAT_COUNT, dtype=torch.int64, device=dev)
+    accum_seed = rng.stream_base(seed, rng.STREAM_JITTER_ACCUM)
+    lookup_seed = rng.stream_base(seed, rng.STREAM_JITTER_LOOKUP)
+    coarse_seed = rng.stream_base(seed, rng.STREAM_JITTER_LOOKUP if cfg.jitter
+                                  else rng.STREAM_JITTER_ACCUM)
+
+    # temporal update on the local slices (src/pipeline.py:331-333)
+    st.fine.begin_frame(frame, cfg)
+    if st.coarse is not None:
+        st.coarse.begin_frame(frame, cfg)
+
+    # ---- round 1: records + fine lookups
+    st.bad_flag.zero_()
+    if validate and n:
+        _lib.call("pf_check_contributions", vs.contribution.data_ptr(), 3 * n,
+                  st.bad_flag.data_ptr(), stream)
+    while True:
+        sh = st.c_shard(pixel_base)
+        _lib.call("pf_shard_keys", ctypes.byref(cc), ctypes.byref(v), ctypes.byref(sh), has_coarse,
+                  accum_seed, lookup_seed, st.bad_flag.data_ptr(), stream)
+        _lib.call("pf_shard_emit", ctypes.byref(sh), st.send_records.data_ptr(),
+                  st.send_requests.data_ptr(), stream)
+        msg = _stats_message(st, True)
+        recv = yield Exchange(msg, [1] * G, [1] * G)
+        mine, theirs = msg.cpu().numpy(), recv.cpu().numpy()
+        if theirs[:, 3].any():
+            _lib.call("pf_shard_reset", ctypes.byref(sh), stream)
+            raise ValueError("contributions must be finite and non-negative "
+                             "(frame rejected on every rank; tables unchanged)")
+        if not theirs[:, 2].any():
+            break
+        if mine[0, 2]:  # this rank overflowed: grow and redo its round-1 keys
+            st.grow_agg(int(st.n_distinct.item()))
+        else:  # a peer overflowed: keep this rank's round, repeat the count exchange
+            st.overflow.zero_()
+            while True:
+                recv = yield Exchange(msg, [1] * G, [1] * G)
+                if not recv.cpu().numpy()[:, 2].any():
+                    break
+            theirs = recv.cpu().numpy()
+            break
+    send_rec, send_req = mine[:, 0].tolist(), mine[:, 1].tolist()
+    recv_rec, recv_req = theirs[:, 0].tolist(), theirs[:, 1].tolist()
+    records = yield Exchange(st.send_records[:sum(send_rec)], send_rec, recv_rec)
+    requests = yield Exchange(st.send_requests[:sum(send_req)], send_req, recv_req)
+    _lib.call("pf_shard_apply", ctypes.byref(sh), ctypes.byref(ft),
+              ctypes.byref(ct) if ct is not None else None, records.data_ptr(),
+              int(records.shape[0]), int(frame), acc.data_ptr(), stream)
+    answers = st.buffer("answers1", (max(int(requests.shape[0]), 1), 4), torch.int64)
+    _lib.call("pf_shard_answer", ctypes.byref(sh), ctypes.byref(cc), ctypes.byref(ft),
+              ctypes.byref(ct) if ct is not None else None, requests.data_ptr(),
+              int(requests.shape[0]), answers.data_ptr(), res.data_ptr(), stream)
+    mine_ans = yield Exchange(answers[:int(requests.shape[0])], recv_req, send_req)
+
+    # fine rung
+    source = torch.empty(n, dtype=torch.uint8, device=dev)
+    chosen = torch.empty((n, 3), dtype=torch.float64, device=dev) if want_means else None
+    flat = st.buffer("flat", (n_pix, 3), torch.float64)
+    flat.zero_()
+    work = st.buffer("work", (max(n, 1),), torch.int64)
+    work_count = st.buffer("work_count", (1,), torch.int64)
+    work_count.zero_()
+    if mine_ans.shape[0] == 0:
+        mine_ans = st.buffer("answers_none", (1, 4), torch.int64)
+    _lib.call("pf_shard_resolve", ctypes.byref(sh), ctypes.byref(cc), ctypes.byref(v),
+              mine_ans.data_ptr(), flat.data_ptr(), n_pix, work.data_ptr(),
+              work_count.data_ptr(), source.data_ptr(), _lib.ptr(chosen), res.data_ptr(), stream)
+    _lib.call("pf_shard_reset", ctypes.byref(sh), stream)
+
+    # ---- round 2: neighbourhood + coarse lookups of the work rows
+    while True:
+        sh = st.c_shard(pixel_base)
+        _lib.call("pf_shard_fallback_keys", ctypes.byref(cc), ctypes.byref(v), ctypes.byref(sh),
+                  has_coarse, lookup_seed, coarse_seed, work.data_ptr(), work_count.data_ptr(),
+                  stream)
+        _lib.call("pf_shard_emit", ctypes.byref(sh), st.send_records.data_ptr(),
+                  st.send_requests.data_ptr(), stream)
+        msg = _stats_message(st, False)
+        recv = yield Exchange(msg, [1] * G, [1] * G)
+        mine, theirs = msg.cpu().numpy(), recv.cpu().numpy()
+        if not theirs[:, 2].any():
+            break
+        if mine[0, 2]:
+            st.grow_agg(int(st.n_distinct.item()))
+        else:
+            st.overflow.zero_()
+            while True:
+                recv = yield Exchange(msg, [1] * G, [1] * G)
+                if not recv.cpu().numpy()[:, 2].any():
+                    break
+            theirs = recv.cpu().numpy()
+            break
+    send_req, recv_req = mine[:, 1].tolist(), theirs[:, 1].tolist()
+    requests = yield Exchange(st.send_requests[:sum(send_req)], send_req, recv_req)
+    answers = st.buffer("answers2", (max(int(requests.shape[0]), 1), 4), torch.int64)
+    _lib.call("pf_shard_answer", ctypes.byref(sh), ctypes.byref(cc), ctypes.byref(ft),
+              ctypes.byref(ct) if ct is not None else None, requests.data_ptr(),
+              int(requests.shape[0]), answers.data_ptr(), res.data_ptr(), stream)
+    mine_ans = yield Exchange(answers[:int(requests.shape[0])], recv_req, send_req)
+    if mine_ans.shape[0] == 0:
+        mine_ans = st.buffer("answers_none", (1, 4), torch.int64)
+    _lib.call("pf_shard_ladder", ctypes.byref(sh), ctypes.byref(cc), ctypes.byref(v), has_coarse,
+              mine_ans.data_ptr(), work.data_ptr(), work_count.data_ptr(), flat.data_ptr(),
+              n_pix, source.data_ptr(), _lib.ptr(chosen), res.data_ptr(), stream)
+    _lib.call("pf_shard_reset", ctypes.byref(sh), stream)
+    del keep
+
+    # ---- image
+    if composite == "reduce":
+        band_flat = yield ReduceScatter(flat)
+        rows = H // G
+        base_band = base[st.rank * rows:(st.rank + 1) * rows]
+    else:
+        band_flat, base_band = flat, base
+    image = torch.empty_like(base_band)
+    _lib.call("pf_finalize_image", base_band.data_ptr(), band_flat.data_ptr(), image.data_ptr(),
+              int(base_band.shape[0] * base_band.shape[1]), int(spp), stream)
+    st.fine.frame = frame
+    if st.coarse is not None:
+        st.coarse.frame = frame
+    st.frame = frame + 1
+    report = ResolveReport(source, image, chosen)
+    report.counters = res
+    return image, report, FrameStats(frame=frame, n_vertices=n, counters=acc)
+
+
+# ------------------------------------------------------------------ drivers
+
+def _a2a_dist(ex: Exchange, group=None) -> torch.Tensor:
+    import torch.distributed as dist
+    t = ex.tensor.contiguous()
+    out_shape = (int(sum(ex.recv_rows)),) + tuple(t.shape[1:])
+    via_host = t.is_cuda and dist.get_backend(group) == "gloo"
+    src = t.cpu() if via_host else t
+    out = torch.empty(out_shape, dtype=t.dtype, device=src.device)
+    dist.all_to_all_single(out, src, [int(x) for x in ex.recv_rows],
+                           [int(x) for x in ex.send_rows], group=group)
+    return out.to(t.device) if via_host else out
+
+
+def _reduce_scatter_dist(rs: ReduceScatter, group=None) -> torch.Tensor:
+    import torch.distributed as dist
+    t = rs.tensor.contiguous()
+    g = dist.get_world_size(group)
+    rows = t.shape[0] // g
+    via_host = t.is_cuda and dist.get_backend(group) == "gloo"
+    src = t.cpu() if via_host else t
+    if via_host:  # gloo has no reduce_scatter: all-reduce and keep this rank's block
+        dist.all_reduce(src, group=group)
+        r = dist.get_rank(group)
+        return src[r * rows:(r + 1) * rows].to(t.device)
+    out = torch.empty((rows,) + tuple(t.shape[1:]), dtype=t.dtype, device=t.device)
+    dist.reduce_scatter_tensor(out, src, group=group)
+    return out
+
+
+def run_dist(gen, group=None):
+    """Drive one rank's frame generator with torch.distributed collectives."""
+    try:
+        op = next(gen)
+        while True:
+            if isinstance(op, Exchange):
+                op = gen.send(_a2a_dist(op, group))
+            elif isinstance(op, ReduceScatter):
+                op = gen.send(_reduce_scatter_dist(op, group))
+            else:
+                raise TypeError(f"unknown collective {op!r}")
+    except StopIteration as e:
+        return e.value
+
+
+def run_loopback(gens: list):
+    """Drive G frame generators (virtual ranks, one process) in lockstep."""
+    G = len(gens)
+    ops = [next(g) for g in gens]
+    results = [None] * G
+    while True:
+        kinds = {type(o) for o in ops}
+        if len(kinds) != 1:
+            raise RuntimeError(f"ranks disagree on the collective: {kinds}")
+        if isinstance(ops[0], Exchange):
+            outs = []
+            for r in range(G):
+                parts = []
+                for p in range(G):
+                    if int(ops[r].recv_rows[p]) != int(ops[p].send_rows[r]):
+                        raise RuntimeError("exchange row counts disagree")
+                    off = int(sum(ops[p].send_rows[:r]))
+                    parts.append(ops[p].tensor[off:off + int(ops[p].send_rows[r])])
+                outs.append(torch.cat(parts) if parts else ops[r].tensor[:0])
+        else:
+            total = torch.stack([o.tensor for o in ops]).sum(0)
+            rows = total.shape[0] // G
+            outs = [total[r * rows:(r + 1) * rows].clone() for r in range(G)]
+        nxt, done = [], 0
+        for r, g in enumerate(gens):
+            try:
+                nxt.append(g.send(outs[r]))
+            except StopIteration as e:
+                results[r] = e.value
+                nxt.append(None)
+                done += 1
+        if done == G:
+            return results
+        if done:
+            raise RuntimeError("ranks finished at different collectives")
+        ops = nxt
