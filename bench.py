@@ -9,8 +9,12 @@ begin_frame on both tables, accumulate_phase (keys + insert), resolve_phase
 
     python bench.py [--gpus N] [--steps K] [--warmup W] [--impl b200|reference]
 
-Prints ONE JSON line (rank 0).  N>1 (torchrun) runs one independent frame per rank
-(replicas: no data-path exchange).
+Prints ONE JSON line (rank 0).  N>1 (torchrun, NCCL) runs the key-sharded frame
+(paper_1902_05942_b200/sharded.py): rank r traces its own sample of every
+pixel (1 spp per GPU, spp = N for the image), the global fine/coarse tables of
+capacity 2^22 are split into N owner slices, records / lookups / answers move by
+all-to-all and the flat image by reduce-scatter.  Weak scaling: 8.29 M vertices per
+GPU per frame.
 """
 
 from __future__ import annotations
@@ -277,13 +281,21 @@ def run_b200(args):
 
     cfg = make_config(pf)
     stream, base = closed_box_stream(W_PIX, H_PIX, BOUNCES, 1 + rank)
+    if world > 1:  # rank r traces sample r of every pixel: distinct jitter draws
+        stream["sample"] = stream["sample"] + rank * BOUNCES
+        base = closed_box_stream(W_PIX, H_PIX, 1, 1)[1]
     vs = pf.VertexStream(**stream)
     n = len(vs)
     n_pix = W_PIX * H_PIX
-    state = pf.FrameState.from_config(cfg)
+    if world > 1:
+        from paper_1902_05942_b200 import sharded
+        state = sharded.ShardedState(cfg, rank, world, agg_capacity=1 << 21)
+    else:
+        state = pf.FrameState.from_config(cfg)
 
     ev = lambda: torch.cuda.Event(enable_timing=True)  # noqa: E731
-    phases = {"begin_check": [], "insert": [], "resolve": []}
+    phases = ({"begin_check": [], "insert": [], "resolve": []} if world == 1 else
+              {"begin_keys": [], "exchange_apply_rung1": [], "fallback_image": []})
 
     def step(f, timing=None):
         # one frame = ONE pf_filter_frame call; its phase events (recorded inside the C
@@ -295,7 +307,12 @@ def run_b200(args):
             for e in evs:  # materialise the cudaEvent_t handles
                 e.record()
             timing.append(tuple(evs))
-        pf.filter_frame(vs, base, cfg, state, 1, seed, want_means=False, phase_events=evs)
+        if world > 1:
+            sharded.run_dist(sharded.filter_frame_sharded(
+                vs, base, cfg, state, world, seed, composite="reduce", want_means=False,
+                phase_events=evs))
+        else:
+            pf.filter_frame(vs, base, cfg, state, 1, seed, want_means=False, phase_events=evs)
 
     clocks = ClockSampler(local)
     clocks.__enter__()
@@ -326,17 +343,21 @@ def run_b200(args):
         t = torch.tensor([elapsed], device="cuda", dtype=torch.float64)
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         t_max = float(t.item())
+    names = list(phases)
     for e0, e1, e2, e3 in marks:
-        phases["begin_check"].append(e0.elapsed_time(e1))
-        phases["insert"].append(e1.elapsed_time(e2))
-        phases["resolve"].append(e2.elapsed_time(e3))
+        phases[names[0]].append(e0.elapsed_time(e1))
+        phases[names[1]].append(e1.elapsed_time(e2))
+        phases[names[2]].append(e2.elapsed_time(e3))
     ph = {k: float(np.mean(v)) for k, v in phases.items()}
     value = n * world * args.steps / t_max
     ms_per_step = t_max / args.steps * 1e3
 
     # roofline of the dominant phase kernel (bytes per launch / mean launch time)
     peak, peak_kind = _peaks()
-    if ph["insert"] >= ph["resolve"]:
+    if world > 1:  # the round-1 key + pre-aggregation kernel reads the insert inputs
+        kname, kbytes = "shard_keys_kernel", INSERT_BYTES_PER_VERTEX * n
+        kms = ph["begin_keys"]
+    elif ph["insert"] >= ph["resolve"]:
         kname, kbytes, kms = "insert_frame_kernel", INSERT_BYTES_PER_VERTEX * n, ph["insert"]
     else:
         kname, kbytes, kms = ("resolve_phase", QUERY_BYTES_PER_VERTEX * n +
@@ -349,7 +370,7 @@ def run_b200(args):
     # end to end through the public API with host buffers
     e2e = None
     if not args.no_e2e:
-        e2e = run_e2e(pf, rng, cfg, stream, base, args, n)
+        e2e = run_e2e(pf, rng, cfg, stream, base, args, n, rank, world)
 
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu:
@@ -363,8 +384,10 @@ def run_b200(args):
                          f"fine+coarse), best of 2 frames, backend={setup['backend']}"}
 
     if rank == 0:
-        # begin x2, check, insert, effective records, resolve main, fallback, finalize
-        launches = 8 * args.steps
+        # single: begin x2, check, insert, effective records, resolve main, fallback,
+        # finalize.  sharded: begin x2, check, keys, emit, apply, answer, resolve, reset,
+        # fallback keys, emit, answer, ladder, reset, finalize (NCCL kernels not counted)
+        launches = (8 if world == 1 else 15) * args.steps
         line = {
             "metric": METRIC, "value": value, "unit": "vertices/s", "n_gpus": world,
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms_per_step,
@@ -373,7 +396,8 @@ def run_b200(args):
             "config": {"workload": WORKLOAD, "vertices_per_frame": n, "pixels": n_pix,
                        "capacity": cfg.capacity, "tables": "fine+coarse",
                        "temporal_mode": cfg.temporal_mode, "sum_mode": cfg.sum_mode,
-                       "parallelism": f"replicas x{world}" if world > 1 else "single",
+                       "parallelism": (f"key-sharded tables x{world} (NCCL all-to-all), "
+                                       f"1 spp per GPU" if world > 1 else "single"),
                        "l2": "inputs 1.0 GB per frame > 126 MB L2 (no flush needed)"},
             "phases_ms": ph, "roofline": roofline, "cpu_baseline": cpu, "e2e": e2e,
             "gpu_launches": launches, "clocks": clocks.summary(),
@@ -384,10 +408,12 @@ def run_b200(args):
     return 0
 
 
-def run_e2e(pf, rng, cfg, stream, base, args, n):
+def run_e2e(pf, rng, cfg, stream, base, args, n, rank=0, world=1):
     """Same frame through the public API from pinned host buffers: H2D of every
-    input the frame reads, filter_frame, D2H of the filtered image -- all timed."""
+    input the frame reads, the frame, D2H of the filtered image (this rank's rows for
+    N > 1) -- all timed; max over ranks."""
     import torch
+    import torch.distributed as dist
     fields = ("position", "normal", "contribution", "throughput", "pixel", "sample",
               "camera_distance")
     host = {f: stream[f].cpu().pin_memory() for f in fields}
@@ -397,7 +423,12 @@ def run_e2e(pf, rng, cfg, stream, base, args, n):
     dbase = torch.empty_like(base)
     unused = {"omega_r": torch.zeros_like(stream["position"]),
               "layer_id": torch.zeros_like(stream["pixel"])}
-    state = pf.FrameState.from_config(cfg)
+    if world > 1:
+        from paper_1902_05942_b200 import sharded
+        state = sharded.ShardedState(cfg, rank, world, agg_capacity=1 << 21)
+        himg = himg[: himg.shape[0] // world]
+    else:
+        state = pf.FrameState.from_config(cfg)
     h2d = sum(t.numel() * t.element_size() for t in host.values()) + hbase.numel() * 8
     d2h = himg.numel() * 8
 
@@ -406,12 +437,18 @@ def run_e2e(pf, rng, cfg, stream, base, args, n):
             dev[k].copy_(host[k], non_blocking=True)
         dbase.copy_(hbase, non_blocking=True)
         vs = pf.VertexStream(**dev, **unused)
-        image, _, _ = pf.filter_frame(vs, dbase, cfg, state, 1, rng.frame_seed(1, f))
+        if world > 1:
+            image, _, _ = sharded.run_dist(sharded.filter_frame_sharded(
+                vs, dbase, cfg, state, world, rng.frame_seed(1, f), composite="reduce"))
+        else:
+            image, _, _ = pf.filter_frame(vs, dbase, cfg, state, 1, rng.frame_seed(1, f))
         himg.copy_(image, non_blocking=True)
 
     for f in range(max(1, min(args.warmup, 3))):
         frame(f)
     torch.cuda.synchronize()
+    if world > 1:
+        dist.barrier()
     s, e = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     k = max(1, min(args.steps, 10))
     s.record()
@@ -420,7 +457,11 @@ def run_e2e(pf, rng, cfg, stream, base, args, n):
     e.record()
     torch.cuda.synchronize()
     t = s.elapsed_time(e) / 1e3
-    return {"value": n * k / t, "unit": "vertices/s", "h2d_bytes_per_step": h2d,
+    if world > 1:
+        tt = torch.tensor([t], device="cuda", dtype=torch.float64)
+        dist.all_reduce(tt, op=dist.ReduceOp.MAX)
+        t = float(tt.item())
+    return {"value": n * world * k / t, "unit": "vertices/s", "h2d_bytes_per_step": h2d,
             "d2h_bytes_per_step": d2h, "ms_per_step": t / k * 1e3, "steps": k}
 
 

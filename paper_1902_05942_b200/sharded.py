@@ -161,7 +161,7 @@ def _stats_message(st: ShardedState, records: bool) -> torch.Tensor:
 
 def filter_frame_sharded(vertices, base_image, cfg: FilterConfig, st: ShardedState, spp: int,
                          seed: int, pixel_base: int = 0, composite: str = "band",
-                         validate: bool = True, want_means: bool = True):
+                         validate: bool = True, want_means: bool = True, phase_events=None):
     """One frame on this rank (generator: yields Exchange / ReduceScatter).
 
     composite="band": the rank's vertices all land in its pixel band
@@ -169,6 +169,9 @@ def filter_frame_sharded(vertices, base_image, cfg: FilterConfig, st: ShardedSta
     composite="reduce": every rank's vertices address the whole image of H x W
     pixels (pixel_base 0) -- e.g. each rank traced other samples -- and the result is
     this rank's block of rows of the final image (H divisible by world).
+
+    phase_events: optional 4 torch.cuda.Events recorded at frame start, after the
+    round-1 key kernel, after the fine rung and at frame end.
 
     Returns (image, ResolveReport, FrameStats) via StopIteration.value."""
     if composite not in ("band", "reduce"):
@@ -197,6 +200,11 @@ def filter_frame_sharded(vertices, base_image, cfg: FilterConfig, st: ShardedSta
     coarse_seed = rng.stream_base(seed, rng.STREAM_JITTER_LOOKUP if cfg.jitter
                                   else rng.STREAM_JITTER_ACCUM)
 
+    def mark(k):
+        if phase_events is not None:
+            phase_events[k].record()
+
+    mark(0)
     # temporal update on the local slices (src/pipeline.py:331-333)
     st.fine.begin_frame(frame, cfg)
     if st.coarse is not None:
@@ -211,6 +219,7 @@ def filter_frame_sharded(vertices, base_image, cfg: FilterConfig, st: ShardedSta
         sh = st.c_shard(pixel_base)
         _lib.call("pf_shard_keys", ctypes.byref(cc), ctypes.byref(v), ctypes.byref(sh), has_coarse,
                   accum_seed, lookup_seed, st.bad_flag.data_ptr(), stream)
+        mark(1)
         _lib.call("pf_shard_emit", ctypes.byref(sh), st.send_records.data_ptr(),
                   st.send_requests.data_ptr(), stream)
         msg = _stats_message(st, True)
@@ -258,6 +267,7 @@ def filter_frame_sharded(vertices, base_image, cfg: FilterConfig, st: ShardedSta
     _lib.call("pf_shard_resolve", ctypes.byref(sh), ctypes.byref(cc), ctypes.byref(v),
               mine_ans.data_ptr(), flat.data_ptr(), n_pix, work.data_ptr(),
               work_count.data_ptr(), source.data_ptr(), _lib.ptr(chosen), res.data_ptr(), stream)
+    mark(2)
     _lib.call("pf_shard_reset", ctypes.byref(sh), stream)
 
     # ---- round 2: neighbourhood + coarse lookups of the work rows
@@ -308,6 +318,7 @@ def filter_frame_sharded(vertices, base_image, cfg: FilterConfig, st: ShardedSta
     image = torch.empty_like(base_band)
     _lib.call("pf_finalize_image", base_band.data_ptr(), band_flat.data_ptr(), image.data_ptr(),
               int(base_band.shape[0] * base_band.shape[1]), int(spp), stream)
+    mark(3)
     st.fine.frame = frame
     if st.coarse is not None:
         st.coarse.frame = frame

@@ -198,3 +198,54 @@ def test_shard_abi_rejects_bad_geometry(gpu):
     import ctypes
     with pytest.raises(ValueError):
         gpu._lib.call("pf_shard_reset", ctypes.byref(sh), gpu._lib.stream_handle())
+
+
+def _dist_worker(rank, world, port, out_dir):
+    import os
+    import sys
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+    import torch.distributed as dist
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        import paper_1902_05942_b200 as pf
+        from paper_1902_05942_b200 import sharded
+        w, h = 64, 32
+        s, base, fs = _box(w, h, 3, 40 + rank)
+        s["sample"] = s["sample"] + 3 * rank
+        base = _box(w, h, 1, 1)[1]
+        cfg = pf.FilterConfig(capacity=4096, footprint_scale=fs)
+        st = sharded.ShardedState(cfg, rank, world)
+        img, rep, _ = sharded.run_dist(sharded.filter_frame_sharded(
+            pf.VertexStream(**s), base, cfg, st, world, 7, composite="reduce"))
+        torch.save({"image": img.cpu(), "source": rep.source.cpu(), "means": rep.means.cpu()},
+                   os.path.join(out_dir, f"rank{rank}.pt"))
+    finally:
+        dist.destroy_process_group()
+
+
+def test_run_dist_gloo_two_processes(gpu, tmp_path):
+    """The torch.distributed driver with real frame tensors: two processes on one
+    device exchange through gloo (host memory; no kernel waits on another process)
+    and reproduce the single-GPU frame over both streams."""
+    import socket
+    import torch.multiprocessing as mp
+    with socket.socket() as sk:
+        sk.bind(("127.0.0.1", 0))
+        port = sk.getsockname()[1]
+    mp.start_processes(_dist_worker, args=(2, port, str(tmp_path)), nprocs=2, join=True,
+                       start_method="spawn")
+    res = [torch.load(tmp_path / f"rank{r}.pt") for r in range(2)]
+    w, h = 64, 32
+    parts = []
+    for r in range(2):
+        s, _, fs = _box(w, h, 3, 40 + r)
+        s["sample"] = s["sample"] + 3 * r
+        parts.append(s)
+    base = _box(w, h, 1, 1)[1]
+    cfg = gpu.FilterConfig(capacity=4096, footprint_scale=fs)
+    _, [(img1, rep1, _)] = _single(gpu, _cat(parts), base, cfg, 2, 7)
+    assert torch.equal(torch.cat([r["source"] for r in res]), rep1.source.cpu())
+    assert torch.equal(torch.cat([r["means"] for r in res]), rep1.means.cpu())
+    torch.testing.assert_close(torch.cat([r["image"] for r in res]), img1.cpu(), rtol=1e-12,
+                               atol=1e-14)

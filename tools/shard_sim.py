@@ -1,0 +1,85 @@
+"""Per-rank cost of the key-sharded frame, measured on ONE GPU.
+
+G virtual ranks (run_loopback: collectives served in-process, ranks run one after
+another on the same device, nothing waits on another rank's kernels) each render
+the full 1080p 4-bounce stream of their own sample, exactly the bench's N-GPU
+workload.  Reports the frame time of the fused single-GPU path, and for each G the
+loopback frame time / G = the compute a rank does per frame (the all-to-all
+transfer time over NVLink is not included; it is a few MB per rank per frame).
+
+    python tools/shard_sim.py [--worlds 1,2,4,8] [--frames 5]
+"""
+
+import argparse
+import json
+import os
+import sys
+import time
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+sys.path.insert(0, ROOT)
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--worlds", default="1,2,4,8")
+    ap.add_argument("--frames", type=int, default=5)
+    ap.add_argument("--width", type=int, default=1920)
+    ap.add_argument("--height", type=int, default=1080)
+    args = ap.parse_args()
+    import torch
+    import __graft_entry__
+    __graft_entry__.build()
+    import paper_1902_05942_b200 as pf
+    from paper_1902_05942_b200 import rng, sharded
+    from paper_1902_05942_b200.streams import camera_footprint, closed_box_stream
+
+    W, H = args.width, args.height
+    cap = 1 << (2 * W * H - 1).bit_length()
+    cfg = pf.FilterConfig(capacity=cap, footprint_scale=camera_footprint(H))
+    base = closed_box_stream(W, H, 1, 1)[1]
+    out = {"workload": f"{W}x{H} 4 bounces per rank", "capacity": cap}
+
+    def timed(fn, frames):
+        for f in range(2):
+            fn(f)
+        torch.cuda.synchronize()
+        s, e = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        t0 = time.perf_counter()
+        s.record()
+        for f in range(frames):
+            fn(10 + f)
+        e.record()
+        torch.cuda.synchronize()
+        return s.elapsed_time(e) / frames, (time.perf_counter() - t0) * 1e3 / frames
+
+    s0, _ = closed_box_stream(W, H, 4, 1)
+    vs0 = pf.VertexStream(**s0)
+    st0 = pf.FrameState.from_config(cfg)
+    ms, wall = timed(lambda f: pf.filter_frame(vs0, base, cfg, st0, 1, rng.frame_seed(1, f),
+                                               want_means=False), args.frames)
+    out["fused_single_ms"] = ms
+    del st0
+    for G in [int(x) for x in args.worlds.split(",")]:
+        streams = []
+        for r in range(G):
+            s, _ = closed_box_stream(W, H, 4, 1 + r)
+            s["sample"] = s["sample"] + 4 * r
+            streams.append(pf.VertexStream(**s))
+        states = [sharded.ShardedState(cfg, r, G, agg_capacity=1 << 21) for r in range(G)]
+
+        def frame(f):
+            sharded.run_loopback([sharded.filter_frame_sharded(
+                streams[r], base, cfg, states[r], G, rng.frame_seed(1, f), composite="reduce",
+                want_means=False) for r in range(G)])
+
+        ms, wall = timed(frame, args.frames)
+        out[f"world{G}"] = {"loopback_ms": ms, "per_rank_ms": ms / G, "wall_ms": wall,
+                            "regrows": sum(s.regrows for s in states)}
+        del states, streams
+        torch.cuda.empty_cache()
+    print(json.dumps(out))
+
+
+if __name__ == "__main__":
+    main()
