@@ -42,9 +42,10 @@ __device__ __forceinline__ uint64_t mix64(uint64_t x) {  // src/rng.py:51-59
     return x;
 }
 
-// numpy float64 -> int64 cast on x86 (cvttsd2si): NaN and out-of-range give INT64_MIN.
+// numpy float64 -> int64 cast on x86 (cvttsd2si): NaN and out-of-range give INT64_MIN
+// (-2^63 itself converts to INT64_MIN too, so one |x| < 2^63 test covers every case).
 __device__ __forceinline__ int64_t np_i64(double x) {
-    if (!(x >= -9223372036854775808.0 && x < 9223372036854775808.0))
+    if (!(fabs(x) < 0x1p63))
         return INT64_MIN;
     return static_cast<int64_t>(x);
 }
@@ -72,6 +73,28 @@ __device__ __forceinline__ double div_rcp(double x, double y, double r) {
     const double q0 = __dmul_rn(x, r);
     const double rem = __fma_rn(-q0, y, x);
     return __fma_rn(rem, r, q0);
+}
+
+// Three quotients by one divisor, branch-free on the common path: the Markstein
+// results are formed for all three (signed zeros selected), and one warp-wide test
+// sends any numerator outside the theorem's range to IEEE division.
+__device__ __forceinline__ void div3_rcp(const double x[3], double y, double r, double q[3]) {
+    bool slow = false;
+#pragma unroll
+    for (int c = 0; c < 3; ++c) {
+        const double ax = fabs(x[c]);
+        const double q0 = __dmul_rn(x[c], r);
+        const double rem = __fma_rn(-q0, y, x[c]);
+        q[c] = ax == 0.0 ? q0 : __fma_rn(rem, r, q0);
+        slow |= ax != 0.0 && !(ax > 0x1p-900 && ax < 0x1p+900);
+    }
+    if (slow) {
+#pragma unroll
+        for (int c = 0; c < 3; ++c) {
+            const double ax = fabs(x[c]);
+            if (ax != 0.0 && !(ax > 0x1p-900 && ax < 0x1p+900)) q[c] = ddiv_cold(x[c], y);
+        }
+    }
 }
 
 // np.maximum / np.minimum propagate NaN from either side.
@@ -138,15 +161,18 @@ __device__ __forceinline__ int64_t clamp_level(int64_t lv, int32_t delta) {
     return l < kMaxLevel ? l : kMaxLevel;
 }
 
-// 2^e as a double for |e| <= 1022, built from its exponent bits.
 // exp2(e) for integer e, as numpy computes it: normal powers from the exponent field,
-// subnormals below 2^-1022, 0 below 2^-1074 and +inf above 2^1023 -- bit ops, no branch.
+// subnormals below 2^-1022, 0 below 2^-1074 and +inf above 2^1023.
+static __device__ __noinline__ double pow2i_cold(int64_t e) {
+    if (e > 1023) return __longlong_as_double(0x7FF0000000000000ll);
+    const int64_t sh = e + 1074;  // subnormal bit index
+    return __longlong_as_double((sh >= 0 && sh < 52) ? (1ll << sh) : 0ll);
+}
+
 __device__ __forceinline__ double pow2i(int64_t e) {
-    const int64_t en = e < -1022 ? -1022 : (e > 1024 ? 1024 : e);
-    const uint64_t normal = static_cast<uint64_t>(en + 1023) << 52;  // e = 1024 -> inf bits
-    const int64_t sh = e + 1074;                                      // subnormal bit index
-    const uint64_t sub = (sh >= 0 && sh < 52) ? (1ull << sh) : 0ull;
-    return __longlong_as_double(e >= -1022 ? normal : sub);
+    if (e >= -1022 && e <= 1023)  // every level the key recipe produces
+        return __longlong_as_double(static_cast<long long>(e + 1023) << 52);
+    return pow2i_cold(e);
 }
 
 // base_voxel * exp2(level): exact power-of-two scaling.
@@ -177,7 +203,10 @@ __device__ __forceinline__ Frame3 tangent_frame(double x, double y, double z) {
 __device__ __forceinline__ int64_t octa_bin(double x, double y, double z, int bins) {
     const double s = np_max(dadd(dadd(fabs(x), fabs(y)), fabs(z)), 1e-300);
     const double rs = __drcp_rn(s);
-    const double px = div_rcp(x, s, rs), py = div_rcp(y, s, rs), pz = div_rcp(z, s, rs);
+    const double n3[3] = {x, y, z};
+    double p3[3];
+    div3_rcp(n3, s, rs, p3);
+    const double px = p3[0], py = p3[1], pz = p3[2];
     double fx = px, fy = py;
     if (pz < 0.0) {
         fx = dmul(dsub(1.0, fabs(py)), px >= 0.0 ? 1.0 : -1.0);
@@ -372,8 +401,10 @@ __device__ __forceinline__ CellKey make_key(const pf_config &cfg, const VertexIn
     const double rstep = dmul(ks.rbv, pow2i(-lv));
     CellKey k;
     // IEEE x / step (not a reciprocal multiply: base_voxel is inexact), via Markstein
+    double qd[3];
+    div3_rcp(jittered, step, rstep, qd);
 #pragma unroll
-    for (int c = 0; c < 3; ++c) k.q[c] = np_i64(floor(div_rcp(jittered[c], step, rstep)));
+    for (int c = 0; c < 3; ++c) k.q[c] = np_i64(floor(qd[c]));
     k.level = lv;
     k.aux = ks.aux;
     return k;

@@ -374,7 +374,7 @@ check_contributions_kernel(const double *__restrict__ vals, int64_t count, int32
     if (__any_sync(kFull, any) && (threadIdx.x & 31) == 0) atomicExch(bad, 1);
 }
 
-// Self-test of div_rcp against IEEE division: random numerators and divisors over a
+// Self-test of div_rcp / div3_rcp against IEEE division: random numerators and divisors over a
 // wide exponent range, plus the quantiser's divisors base_voxel * 2^level with the
 // reciprocal scaled by 2^-level (mismatches[0] and [1]).
 __global__ void __launch_bounds__(kThreads)
@@ -393,12 +393,22 @@ selftest_division_kernel(uint64_t seed, int64_t n, double base_voxel, unsigned l
         const double y = ((h2 >> 51) & 1 ? -my : my) * pow2i(ey);
         if (__double_as_longlong(div_rcp(x, y, __drcp_rn(y))) != __double_as_longlong(__ddiv_rn(x, y)))
             ++b0;
+        // div3_rcp: a regular numerator, a signed zero and one scaled far out of the
+        // Markstein range (IEEE fallback), by one divisor
+        const int ez = static_cast<int>((h1 >> 8) % 2001) - 1000;
+        const double x3[3] = {x, (h2 & 1) ? -0.0 : 0.0, x * pow2i(ez)};
+        double q3[3];
+        div3_rcp(x3, y, __drcp_rn(y), q3);
+        for (int c = 0; c < 3; ++c)
+            if (__double_as_longlong(q3[c]) != __double_as_longlong(__ddiv_rn(x3[c], y))) ++b0;
         const int64_t lv = static_cast<int64_t>(h2 % 32);
         const double step = voxel_step(base_voxel, lv);
         const double xs = (static_cast<double>(static_cast<int64_t>(h1 >> 20)) - 8.0e12) * 0x1p-30;
-        const double q = div_rcp(xs, step, dmul(rbv, pow2i(-lv)));
-        if (__double_as_longlong(q) != __double_as_longlong(__ddiv_rn(xs, step)))
-            ++b1;
+        const double xq[3] = {xs, -xs * 0.5, xs * 3.0};
+        double q[3];
+        div3_rcp(xq, step, dmul(rbv, pow2i(-lv)), q);
+        for (int c = 0; c < 3; ++c)
+            if (__double_as_longlong(q[c]) != __double_as_longlong(__ddiv_rn(xq[c], step))) ++b1;
     }
     if (b0) atomicAdd(bad, b0);
     if (b1) atomicAdd(bad + 1, b1);
