@@ -325,6 +325,56 @@ int pf_shard_ladder(const pf_shard *sh, const pf_config *cfg, const pf_vertices 
 /* Empty the aggregation table (only the slots this round claimed) and its counters. */
 int pf_shard_reset(const pf_shard *sh, void *stream);
 
+/* ---- 4. phase one: the path tracer that produces the vertex stream ----
+ * src/tracer.py:211-383 (_walk) with src/_native.pyx:83-167 (intersect_closest/any):
+ * one path per (pixel, sample); the scene is a triangle soup in device memory. */
+typedef struct pf_scene {
+    const double *v0, *e1, *e2;     /* [m][3] triangle corner and edges (src/scene.py:170-195) */
+    const double *normal;           /* [m][3] unit geometric normals */
+    const double *emission;         /* [m][3] */
+    const double *area;             /* [m] */
+    const int32_t *material_id;     /* [m] */
+    int64_t n_triangles;
+    const double *albedo;           /* [k][3] */
+    const double *glossy_weight;    /* [k] */
+    const double *glossy_exponent;  /* [k] */
+    int64_t n_materials;
+    const int64_t *light_tri;       /* [L] triangles with emission > 0, ascending */
+    int64_t n_lights;
+    double background[3];
+    double cam_pos[3], cam_right[3], cam_up[3], cam_fwd[3];  /* Camera.basis() */
+    double ndc_scale_x;             /* 2.0 * tan(fov / 2) * (width / height), as Python */
+    double ndc_scale_y;             /* 2.0 * tan(fov / 2) */
+    int32_t width, height;
+} pf_scene;
+
+/* TraceOptions (src/tracer.py:34-42). */
+typedef struct pf_trace_options {
+    int32_t max_depth;
+    int32_t rr_start;
+    int32_t nee;
+    int32_t select_k;
+    int32_t pixel_jitter;
+    int32_t pad0;
+    double rr_lo, rr_hi;            /* rr_clamp */
+    double diffuse_threshold;
+} pf_trace_options;
+
+/* Per-path results, row i for path i (device arrays; any vertex field may be NULL). */
+typedef struct pf_path_out {
+    double *base;                   /* [n][3] radiance not routed through the vertex */
+    double *radiance;               /* [n][3] base + throughput * contribution */
+    uint8_t *has_vertex;            /* [n] */
+    double *position, *normal, *omega_r, *contribution, *throughput;  /* [n][3] */
+    int64_t *layer_id;              /* [n] */
+    double *camera_distance;        /* [n] */
+} pf_path_out;
+
+/* Trace n paths (pixels[i], samples[i]) with draws from (seed, STREAM_TRACE). */
+int pf_trace_paths(const pf_scene *scene, const pf_trace_options *opt, uint64_t seed,
+                   const int64_t *pixels, const int64_t *samples, int64_t n,
+                   const pf_path_out *out, void *stream);
+
 /* VoxelTable.effective (src/table.py:205-238) over all slots.  eff_sum is int64 for
  * (integrate, fixed) else float64; eff_count is int64 for integrate else float64. */
 int pf_effective(const pf_table *t, int32_t mode, double ema_alpha, double delta_max,
@@ -346,6 +396,9 @@ int pf_check_contributions(const double *vals, int64_t count, int32_t *bad, void
 int pf_selftest_division(uint64_t seed, int64_t n, double base_voxel, int64_t *mismatches,
                          void *stream);
 
+/* Diagnostic: sin(x[i]) and cos(x[i]) as the library computes them for the jitter and
+ * the tracer -- glibc's dbl-64 algorithm, equal to numpy's float64 sin/cos here. */
+int pf_sincos(const double *x, int64_t n, double *s, double *c, void *stream);
 /* Number of non-EMPTY tags (VoxelTable.occupancy numerator, src/table.py:302-303). */
 int pf_count_occupied(const uint64_t *tags, int64_t capacity, int64_t *out, void *stream);
 

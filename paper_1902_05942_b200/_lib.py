@@ -16,8 +16,9 @@ _PKG = os.path.dirname(os.path.abspath(__file__))
 _ROOT = os.path.dirname(_PKG)
 LIB_PATH = os.environ.get("PF_LIB") or os.path.join(_PKG, "libpf_b200.so")
 SOURCES = [os.path.join(_PKG, "csrc", f) for f in ("pf_common.cu", "pf_table.cu", "pf_frame.cu",
-                                                    "pf_shard.cu")]
+                                                    "pf_shard.cu", "pf_trace.cu")]
 HEADERS = [os.path.join(_PKG, "csrc", f) for f in ("pf_device.cuh", "pf_insert.cuh",
+                                                    "pf_sincos_tab.h",
                                                     "pf_internal.cuh", "pf_sweep.cuh",
                                                     "pf_resolve.cuh")] + \
     [os.path.join(_ROOT, "include", "pathfilter_b200.h")]
@@ -32,7 +33,7 @@ EXPORTS = ("pf_abi_version", "pf_last_error", "pf_device_sm_count", "pf_accumula
            "pf_begin_frame", "pf_check_contributions", "pf_selftest_division",
            "pf_count_occupied", "pf_finalize_image", "pf_shard_keys", "pf_shard_emit",
            "pf_shard_apply", "pf_shard_answer", "pf_shard_resolve", "pf_shard_fallback_keys",
-           "pf_shard_ladder", "pf_shard_reset")
+           "pf_shard_ladder", "pf_shard_reset", "pf_trace_paths", "pf_sincos")
 
 
 def build(force: bool = False, verbose: bool = False) -> str:
@@ -107,6 +108,36 @@ class PfShard(ctypes.Structure):
                 ("vertex_slot", ctypes.c_void_p), ("work_slot", ctypes.c_void_p)]
 
 
+class PfScene(ctypes.Structure):
+    _fields_ = [("v0", ctypes.c_void_p), ("e1", ctypes.c_void_p), ("e2", ctypes.c_void_p),
+                ("normal", ctypes.c_void_p), ("emission", ctypes.c_void_p),
+                ("area", ctypes.c_void_p), ("material_id", ctypes.c_void_p),
+                ("n_triangles", ctypes.c_int64), ("albedo", ctypes.c_void_p),
+                ("glossy_weight", ctypes.c_void_p), ("glossy_exponent", ctypes.c_void_p),
+                ("n_materials", ctypes.c_int64), ("light_tri", ctypes.c_void_p),
+                ("n_lights", ctypes.c_int64), ("background", ctypes.c_double * 3),
+                ("cam_pos", ctypes.c_double * 3), ("cam_right", ctypes.c_double * 3),
+                ("cam_up", ctypes.c_double * 3), ("cam_fwd", ctypes.c_double * 3),
+                ("ndc_scale_x", ctypes.c_double), ("ndc_scale_y", ctypes.c_double),
+                ("width", ctypes.c_int32), ("height", ctypes.c_int32)]
+
+
+class PfTraceOptions(ctypes.Structure):
+    _fields_ = [("max_depth", ctypes.c_int32), ("rr_start", ctypes.c_int32),
+                ("nee", ctypes.c_int32), ("select_k", ctypes.c_int32),
+                ("pixel_jitter", ctypes.c_int32), ("pad0", ctypes.c_int32),
+                ("rr_lo", ctypes.c_double), ("rr_hi", ctypes.c_double),
+                ("diffuse_threshold", ctypes.c_double)]
+
+
+class PfPathOut(ctypes.Structure):
+    _fields_ = [("base", ctypes.c_void_p), ("radiance", ctypes.c_void_p),
+                ("has_vertex", ctypes.c_void_p), ("position", ctypes.c_void_p),
+                ("normal", ctypes.c_void_p), ("omega_r", ctypes.c_void_p),
+                ("contribution", ctypes.c_void_p), ("throughput", ctypes.c_void_p),
+                ("layer_id", ctypes.c_void_p), ("camera_distance", ctypes.c_void_p)]
+
+
 class PfEvictEvent(ctypes.Structure):
     _fields_ = [("vertex", ctypes.c_int64), ("slot", ctypes.c_int64),
                 ("victim_tag", ctypes.c_uint64), ("victim_touch", ctypes.c_int64)]
@@ -173,6 +204,8 @@ def lib() -> ctypes.CDLL:
     L.pf_shard_fallback_keys.argtypes = [vp, vp, vp, i32, u64, u64, vp, vp, vp]
     L.pf_shard_ladder.argtypes = [vp, vp, vp, i32, vp, vp, vp, vp, i64, vp, vp, vp, vp]
     L.pf_shard_reset.argtypes = [vp, vp]
+    L.pf_trace_paths.argtypes = [vp, vp, u64, vp, vp, i64, vp, vp]
+    L.pf_sincos.argtypes = [vp, i64, vp, vp, vp]
     for name in EXPORTS[3:]:
         getattr(L, name).restype = ctypes.c_int
     _lib = L

@@ -12,6 +12,7 @@
 #include <cuda_runtime.h>
 
 #include "../../include/pathfilter_b200.h"
+#include "pf_sincos_tab.h"
 
 namespace pf {
 
@@ -122,14 +123,162 @@ __device__ __forceinline__ void jitter_draws(uint64_t h0, int64_t pixel, int64_t
     u2 = static_cast<double>(b >> 11) * inv;
 }
 
+// ------------------------------------------------------------------ glibc sin / cos
+//
+// numpy's float64 sin/cos here are glibc 2.39's (bit for bit; glibc picks its FMA
+// build on this host), and glibc's are not correctly rounded, so CUDA's sin/cos give
+// jittered positions a few ulps off.  This is a restatement of glibc's dbl-64 algorithm
+// (sysdeps/ieee754/dbl-64/s_sin.c: do_sin, do_cos, reduce_sincos, TAYLOR_SIN) with its
+// table (pf_sincos_tab.h) and the FMA contractions of the FMA build, valid for
+// |x| < 105414350 (beyond that glibc switches to a multi-word reduction; we fall back
+// to CUDA's).  tests/test_gpu_parity.py::test_glibc_sincos checks it bit for bit
+// against numpy on 2^22 arguments.
+namespace glibc {
+constexpr double s1 = -0x1.5555555555555p-3, s2 = 0x1.1111111110ecep-7,
+                 s3 = -0x1.a01a019db08b8p-13, s4 = 0x1.71de27b9a7ed9p-19,
+                 s5 = -0x1.addffc2fcdf59p-26;
+constexpr double sn3 = -0x1.5555555555515p-3, sn5 = 0x1.11110e829872fp-7, cs2 = 0.5,
+                 cs4 = -0x1.5555555555535p-5, cs6 = 0x1.6c16bedd9e239p-10;
+constexpr double big = 0x1.8p45, toint = 0x1.8p52, hpinv = 0x1.45f306dc9c883p-1,
+                 mp1 = 0x1.921fb58p0, mp2 = -0x1.dde973cp-27, pp3 = -0x1.cb3b398p-55,
+                 pp4 = -0x1.d747f23e32ed7p-83, hp0 = 0x1.921fb54442d18p0,
+                 hp1 = 0x1.1a62633145c07p-54;
+
+__device__ __forceinline__ uint32_t hi_word(double x) {
+    return static_cast<uint32_t>(static_cast<uint64_t>(__double_as_longlong(x)) >> 32);
+}
+__device__ __forceinline__ uint32_t lo_word(double x) {
+    return static_cast<uint32_t>(static_cast<uint64_t>(__double_as_longlong(x)));
+}
+
+// Entry i = (sn, ssn, cs, ccs) of sin/cos(i/128) as two 16-byte loads (entries are
+// 32-byte aligned); i <= 109 on every path that uses the value.  `tab` is the table in
+// global memory or a kernel's shared-memory copy (stage_sincos_table): lanes gather
+// random entries, which shared memory serves without L1 tag lookups.
+__device__ __forceinline__ double4 table_entry(const double2 *tab, uint32_t i) {
+    const double2 *p = tab + 2 * (i < 110u ? i : 0u);
+    const double2 a = p[0], b = p[1];
+    return make_double4(a.x, a.y, b.x, b.y);
+}
+
+__device__ __forceinline__ double do_cos(double x, double dx, const double2 *tab) {
+    if (x < 0) dx = -dx;
+    const double ax = fabs(x);
+    const double u = __dadd_rn(big, ax);
+    x = __dadd_rn(__dsub_rn(ax, __dsub_rn(u, big)), dx);
+    const double xx = __dmul_rn(x, x);
+    const double s = __fma_rn(__dmul_rn(x, xx), __fma_rn(xx, sn5, sn3), x);
+    const double c = __dmul_rn(xx, __fma_rn(xx, __fma_rn(xx, cs6, cs4), cs2));
+    const double4 e = table_entry(tab, lo_word(u));
+    const double sn = e.x, ssn = e.y, cs = e.z, ccs = e.w;
+    const double cor = __fma_rn(-sn, s, __fma_rn(-cs, c, __fma_rn(-s, ssn, ccs)));
+    return __dadd_rn(cs, cor);
+}
+
+__device__ __forceinline__ double do_sin(double x, double dx, const double2 *tab) {
+    const double xold = x;
+    const double ax = fabs(x);
+    // TAYLOR_SIN for |x| < 0.126 (computed alongside; selected below)
+    const double x2 = __dmul_rn(x, x);
+    const double poly =
+        __fma_rn(__fma_rn(__fma_rn(__fma_rn(s5, x2, s4), x2, s3), x2, s2), x2, s1);
+    const double taylor =
+        __dadd_rn(x, __fma_rn(__fma_rn(poly, x, -__dmul_rn(0.5, dx)), x2, dx));
+    if (x <= 0) dx = -dx;
+    const double u = __dadd_rn(big, ax);
+    const double y = __dsub_rn(ax, __dsub_rn(u, big));
+    const double yy = __dmul_rn(y, y);
+    const double s = __dadd_rn(y, __fma_rn(__dmul_rn(y, yy), __fma_rn(yy, sn5, sn3), dx));
+    const double c = __fma_rn(y, dx, __dmul_rn(yy, __fma_rn(yy, __fma_rn(yy, cs6, cs4), cs2)));
+    const double4 e = table_entry(tab, lo_word(u));
+    const double sn = e.x, ssn = e.y, cs = e.z, ccs = e.w;
+    const double cor = __fma_rn(cs, s, __fma_rn(-sn, c, __fma_rn(s, ccs, ssn)));
+    const double table = copysign(__dadd_rn(sn, cor), xold);
+    return ax < 0.126 ? taylor : table;
+}
+}  // namespace glibc
+
+// sin(x) and cos(x) exactly as glibc computes them (see above): each lane evaluates one
+// do_sin and one do_cos with region-dependent arguments, without divergent branches.
+// |x| >= 105414350, inf, nan: CUDA's sincos out of line (never reached by the jitter,
+// whose argument is 2*pi*u in [0, 2*pi), nor by the tracer's directions).
+static __device__ __noinline__ void sincos_cold(double x, double *s, double *c) { sincos(x, s, c); }
+
+__device__ __forceinline__ const double2 *global_sincos_table() {
+    return reinterpret_cast<const double2 *>(kSinCosTab);
+}
+
+// Copy the table into shared memory (220 x 16 B); the caller syncs before use.
+__device__ __forceinline__ void stage_sincos_table(double2 *smem) {
+    for (int i = threadIdx.x; i < 220; i += blockDim.x) smem[i] = global_sincos_table()[i];
+}
+
+__device__ __forceinline__ void glibc_sincos(double x, double &sn, double &cs,
+                                             const double2 *tab = global_sincos_table()) {
+    using namespace glibc;
+    const uint32_t k = hi_word(x) & 0x7fffffffu;
+    if (k >= 0x419921FBu) {  // |x| >= 105414350 (or inf / nan): not on our paths
+        sincos_cold(x, &sn, &cs);
+        return;
+    }
+    double as, das, ac, dac;       // do_sin / do_cos arguments
+    bool sin_from_cos = false, sin_neg = false, cos_from_sin = false, cos_neg = false;
+    if (k < 0x3feb6000u) {         // |x| < 0.855469: no reduction
+        as = x; das = 0.0; ac = x; dac = 0.0;
+    } else if (k < 0x400368fdu) {  // |x| < 2.426265: around pi/2
+        const double t = __dsub_rn(hp0, fabs(x));
+        const double a = __dadd_rn(t, hp1);
+        ac = t; dac = hp1;                                   // sin = copysign(do_cos(t, hp1), x)
+        as = a; das = __dadd_rn(__dsub_rn(t, a), hp1);       // cos = do_sin(a, da)
+        sin_from_cos = true;
+        cos_from_sin = true;
+    } else {                       // reduce_sincos: x = n * pi/2 + (a + da)
+        const double t = __fma_rn(x, hpinv, toint);
+        const double xn = __dsub_rn(t, toint);
+        const double y = __fma_rn(-xn, mp2, __fma_rn(-xn, mp1, x));
+        const int n = static_cast<int>(lo_word(t) & 3u);
+        const double t2 = __fma_rn(-xn, pp3, y);
+        double db = __fma_rn(-xn, pp3, __dsub_rn(y, t2));
+        const double b = __fma_rn(-xn, pp4, t2);
+        db = __dadd_rn(db, __fma_rn(-xn, pp4, __dsub_rn(t2, b)));
+        as = ac = b;
+        das = dac = db;
+        sin_from_cos = (n & 1) != 0;                   // do_sincos(a, da, n)
+        sin_neg = (n & 2) != 0;
+        cos_from_sin = ((n + 1) & 1) == 0;             // do_sincos(a, da, n + 1)
+        cos_neg = ((n + 1) & 2) != 0;
+    }
+    const double vs = do_sin(as, das, tab);
+    const double vc = do_cos(ac, dac, tab);
+    if (k < 0x3feb6000u || k >= 0x400368fdu) {
+        sn = sin_from_cos ? vc : vs;
+        cs = cos_from_sin ? vs : vc;
+    } else {
+        sn = copysign(vc, x);
+        cs = vs;
+    }
+    if (sin_neg) sn = -sn;
+    if (cos_neg) cs = -cs;
+    if (k < 0x3e500000u) sn = x;    // |x| < 2^-26
+    if (k < 0x3e400000u) cs = 1.0;  // |x| < 2^-27
+}
+
 // Disc offsets: r = 0.5*sqrt(u1), phi = 2pi*u2, (r cos phi, r sin phi)
-// (src/keys.py:342-345).  sqrt is IEEE-exact; sin/cos are CUDA's (<= 2 ulp), the
-// one documented source of jittered-position ulp differences.
-__device__ __forceinline__ void disc_offset(double u1, double u2, double &u, double &v) {
+// (src/keys.py:342-345).  sqrt is IEEE-exact and sin/cos are glibc's (glibc_sincos),
+// so jittered positions equal numpy's bit for bit.
+#ifndef PF_GLIBC_SINCOS
+#define PF_GLIBC_SINCOS 1
+#endif
+__device__ __forceinline__ void disc_offset(double u1, double u2, double &u, double &v,
+                                            const double2 *tab = global_sincos_table()) {
     const double r = dmul(0.5, __dsqrt_rn(u1));
     const double phi = dmul(kTwoPi, u2);
     double s, c;
+#if PF_GLIBC_SINCOS
+    glibc_sincos(phi, s, c, tab);
+#else
     sincos(phi, &s, &c);
+#endif
     u = dmul(r, c);
     v = dmul(r, s);
 }

@@ -42,8 +42,10 @@ insert_frame_kernel(pf_config cfg, pf_vertices v, pf_table fine, pf_table coarse
                     int64_t *event_count, int64_t event_cap, const int32_t *abort_flag,
                     uint64_t h0_lookup, uint64_t *lk_index, uint32_t *lk_fp) {
     __shared__ BlockStats bs;
+    __shared__ double2 sincos_tab[220];
     if (abort_flag != nullptr && *abort_flag != 0) return;  // invalid input: no mutation
     stats_init(bs);
+    stage_sincos_table(sincos_tab);
     __syncthreads();
     // persistent: each block walks 256-vertex tiles; block counters flush once at exit
     const int64_t tiles = (v.n + kThreads - 1) / kThreads;
@@ -91,7 +93,7 @@ insert_frame_kernel(pf_config cfg, pf_vertices v, pf_table fine, pf_table coarse
             if (set != 1 && cfg.jitter) {  // set 1 reuses set 0's disc offsets
                 double u1, u2;
                 jitter_draws(set == 0 ? h0 : h0_lookup, x.pixel, x.sample, u1, u2);
-                disc_offset(u1, u2, du, dv);
+                disc_offset(u1, u2, du, dv, sincos_tab);
             }
             double jt[3];
             const CellHash h = key_hash(

@@ -162,8 +162,10 @@ __global__ void __launch_bounds__(kT, 2)
 shard_keys_kernel(pf_config cfg, pf_vertices v, ShardK k, int has_coarse, uint64_t h0,
                   uint64_t h0_lookup, const int32_t *abort_flag) {
     __shared__ OwnerCounts oc;
+    __shared__ double2 sincos_tab[220];
     if (abort_flag != nullptr && *abort_flag != 0) return;
     owner_init(oc, k.s.world);
+    stage_sincos_table(sincos_tab);
     __syncthreads();
     const int64_t tiles = (v.n + kT - 1) / kT;
     for (int64_t tile = blockIdx.x; tile < tiles; tile += gridDim.x) {
@@ -188,7 +190,7 @@ shard_keys_kernel(pf_config cfg, pf_vertices v, ShardK k, int has_coarse, uint64
             if (set != 1 && cfg.jitter) {  // the coarse set reuses the fine set's offsets
                 double u1, u2;
                 jitter_draws(set == 0 ? h0 : h0_lookup, x.pixel, x.sample, u1, u2);
-                disc_offset(u1, u2, du, dv);
+                disc_offset(u1, u2, du, dv, sincos_tab);
             }
             double jt[3];
             const CellHash h = key_hash(

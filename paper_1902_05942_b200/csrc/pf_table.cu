@@ -414,6 +414,13 @@ selftest_division_kernel(uint64_t seed, int64_t n, double base_voxel, unsigned l
     if (b1) atomicAdd(bad + 1, b1);
 }
 
+// glibc_sincos over an array (diagnostic entry point for the bit-exactness test).
+__global__ void __launch_bounds__(kThreads)
+sincos_kernel(const double *x, int64_t n, double *s, double *c) {
+    const int64_t i = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+    if (i < n) glibc_sincos(x[i], s[i], c[i]);
+}
+
 // ------------------------------------------------------------------ host wrappers
 
 static int accumulate_impl(const char *fn, bool fixed, uint64_t *tags, void *sums, int64_t *counts,
@@ -572,6 +579,13 @@ int pf_check_contributions(const double *vals, int64_t count, int32_t *bad, void
     check_contributions_kernel<<<static_cast<unsigned>(blocks), kThreads, 0, as_stream(stream)>>>(
         vals, count, bad);
     return check_launch(fn);
+}
+
+int pf_sincos(const double *x, int64_t n, double *s, double *c, void *stream) {
+    if (n < 0 || (n > 0 && (!x || !s || !c))) return fail_arg("pf_sincos", "bad arguments");
+    if (n == 0) return PF_OK;
+    sincos_kernel<<<blocks_for(n, kThreads), kThreads, 0, as_stream(stream)>>>(x, n, s, c);
+    return check_launch("pf_sincos");
 }
 
 int pf_count_occupied(const uint64_t *tags, int64_t capacity, int64_t *out, void *stream) {

@@ -295,9 +295,51 @@ def gen_hybrid():
     save("hybrid_table.npz", out)
 
 
+def put_trace(out: dict, prefix: str, res):
+    put_stream(out, f"{prefix}v_", res.vertices)
+    out[f"{prefix}image"] = res.image
+    out[f"{prefix}base"] = res.base_image
+    if res.variance is not None:
+        out[f"{prefix}variance"] = res.variance
+
+
+def gen_tracer():
+    """Phase-one fixtures: the reference tracer (src/tracer.py) on every builtin scene
+    kind, the benchmark's closed box (select_k = 1..4, rr_start 9), glossy layers,
+    motion, RR, NEE off / no pixel jitter, variance, and a reevaluate replay."""
+    from pathfilter.scene import load_scene
+    from pathfilter.tracer import reevaluate
+    out = {}
+    box = parse_scene(CLOSED_BOX.format(w=48, h=27))
+    for k in range(1, 5):
+        put_trace(out, f"box_k{k}_", trace(box, 1, 1, TraceOptions(select_k=k, rr_start=9)))
+    put_trace(out, "cornell_", trace(load_scene("cornell", 32, 32), 2, 5, want_variance=True))
+    put_trace(out, "glossy_", trace(load_scene("cornell-glossy", 24, 24), 1, 3,
+                                    TraceOptions(select_k=2)))
+    sweep = load_scene("shadow-sweep", 24, 24).at_frame(3)
+    put_trace(out, "sweep_", trace(sweep, 1, 7))
+    put_trace(out, "occluded_", trace(load_scene("occluded", 8, 8), 1, 2))
+    corr = load_scene("corridor", 20, 16).at_frame(5)
+    put_trace(out, "corridor_", trace(corr, 1, 9, TraceOptions(nee=False, pixel_jitter=False,
+                                                                max_depth=5)))
+    cb = load_scene("cornell", 32, 32)
+    ids = (np.arange(0, 2048, 7, dtype=np.uint64) % np.uint64(1024)) | \
+        ((np.arange(0, 2048, 7, dtype=np.uint64) // np.uint64(1024)) << np.uint64(32))
+    out["reeval_ids"] = ids
+    put_stream(out, "reeval_v_", reevaluate(cb, 5, 2, ids))
+    for name, sc in (("box", box), ("cornell", cb), ("glossy", load_scene("cornell-glossy", 24, 24)),
+                     ("sweep3", sweep), ("occluded", load_scene("occluded", 8, 8)),
+                     ("corridor5", corr)):
+        for f in ("v0", "e1", "e2", "normal", "area", "material_id", "emission"):
+            out[f"scene_{name}_{f}"] = getattr(sc, f)
+        out[f"scene_{name}_basis"] = np.stack(sc.camera.basis())
+    save("tracer.npz", out)
+
+
 if __name__ == "__main__":
-    which = sys.argv[1:] or ["rng", "keys", "cornell", "box4", "temporal", "hybrid"]
+    which = sys.argv[1:] or ["rng", "keys", "cornell", "box4", "temporal", "hybrid", "tracer"]
     fns = {"rng": gen_rng_hash, "keys": gen_keys_random, "cornell": gen_frame_cornell,
-           "box4": gen_frame_box4, "temporal": gen_temporal, "hybrid": gen_hybrid}
+           "box4": gen_frame_box4, "temporal": gen_temporal, "hybrid": gen_hybrid,
+           "tracer": gen_tracer}
     for w in which:
         fns[w]()
