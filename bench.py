@@ -1,8 +1,11 @@
 """Benchmark: filtered path vertices/s (insert + query) for one HD 1 spp 4-bounce frame.
 
 Workload (BASELINE.json configs[2]): 1920x1080, 1 spp, all
-vertices of 4-bounce paths in the closed Cornell box (8,294,400 synthetic vertices,
-streams.closed_box_stream), capacity next_pow2(2*W*H) = 2^22, fine + coarse tables,
+vertices of 4-bounce paths in the closed Cornell box of SURVEY App. B, traced on the
+device by the repo's path tracer exactly as the reference's recipe does (select_k =
+1..4, rr_start 9, seed 1, sample += k-1: 8,184,972 vertices, bit-identical to the
+reference tracer's stream); `--stream synthetic` uses streams.closed_box_stream
+instead.  Capacity next_pow2(2*W*H) = 2^22, fine + coarse tables,
 FilterConfig defaults (jitter, fixed-point sums, integrate).  One step = one frame:
 begin_frame on both tables, accumulate_phase (keys + insert), resolve_phase
 (ladder + composite), with the animated-scene seed schedule (src/pipeline.py:329).
@@ -35,6 +38,28 @@ sys.path.insert(0, ROOT)
 W_PIX, H_PIX, BOUNCES = 1920, 1080, 4
 METRIC = "filtered path vertices/sec (insert+query); ms/frame at 1080p 1spp 4 bounces"
 WORKLOAD = "1920x1080 1spp, all vertices of 4-bounce paths (closed Cornell box, synthetic)"
+WORKLOAD_TRACED = ("1920x1080 1spp, all vertices of 4-bounce paths: SURVEY App. B closed box "
+                   "traced on device (select_k 1..4, rr_start 9, seed 1)")
+
+
+def make_stream(kind: str, rank: int = 0, device=None):
+    """(stream dict of CUDA tensors, base image) of the benchmark workload for a rank:
+    rank r traces sample r of every pixel (distinct path ids and jitter draws)."""
+    from paper_1902_05942_b200.streams import closed_box_stream
+    if kind == "synthetic":
+        stream, base = closed_box_stream(W_PIX, H_PIX, BOUNCES, 1 + rank, device=device)
+        if rank:
+            stream["sample"] = stream["sample"] + rank * BOUNCES
+            base = closed_box_stream(W_PIX, H_PIX, 1, 1, device=device)[1]
+        return stream, base
+    from paper_1902_05942_b200.scene import closed_box
+    from paper_1902_05942_b200.tracer import multi_bounce_stream
+    vs, base = multi_bounce_stream(closed_box(W_PIX, H_PIX), BOUNCES, 1,
+                                   sample_offset=BOUNCES * rank)
+    if rank:  # the image's base term: the k = 1 trace of sample 0, identical on every rank
+        base = multi_bounce_stream(closed_box(W_PIX, H_PIX), 1, 1)[1]
+    stream = {f: getattr(vs, f).contiguous() for f in FIELDS}
+    return stream, base.contiguous()
 # SURVEY §8(d): algorithmic HBM bytes
 INSERT_BYTES_PER_VERTEX = 96      # position 24 + normal 24 + distance 8 + pixel 8 + sample 8 + contribution 24
 QUERY_BYTES_PER_VERTEX = 120      # + throughput 24
@@ -227,9 +252,11 @@ def run_reference_arm(args):
     if rank != 0:
         return 0
     import torch
-    from paper_1902_05942_b200.streams import camera_footprint, closed_box_stream, stream_to_numpy
+    from paper_1902_05942_b200.streams import camera_footprint, stream_to_numpy
     dev = "cuda" if torch.cuda.is_available() else "cpu"
-    stream, base = closed_box_stream(W_PIX, H_PIX, BOUNCES, 1, device=dev)
+    if dev == "cpu" and args.stream != "synthetic":
+        raise SystemExit("the traced stream needs a CUDA device; use --stream synthetic")
+    stream, base = make_stream(args.stream, 0, device=dev)
     stream_np = stream_to_numpy(stream)
     base_np = base.cpu().numpy()
     cap = 1 << (2 * W_PIX * H_PIX - 1).bit_length()
@@ -245,7 +272,8 @@ def run_reference_arm(args):
         "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
         "ms_per_step": per * 1e3, "higher_is_better": True, "scaling": "weak",
         "vs_baseline": None, "dtype": "f64", "data": "synthetic",
-        "config": {"workload": WORKLOAD, "vertices_per_frame": len(stream_np.pixel),
+        "config": {"workload": WORKLOAD if args.stream == "synthetic" else WORKLOAD_TRACED,
+                   "vertices_per_frame": len(stream_np.pixel),
                    "sample_vertices_per_step": n, "capacity": cap, "tables": "fine+coarse"},
         "cpu_baseline": {"value": value, "unit": "vertices/s", "cores": cores,
                          "kind": setup["kind"],
@@ -277,13 +305,10 @@ def run_b200(args):
         dist.barrier()
     import paper_1902_05942_b200 as pf
     from paper_1902_05942_b200 import rng
-    from paper_1902_05942_b200.streams import closed_box_stream, stream_to_numpy
+    from paper_1902_05942_b200.streams import stream_to_numpy
 
     cfg = make_config(pf)
-    stream, base = closed_box_stream(W_PIX, H_PIX, BOUNCES, 1 + rank)
-    if world > 1:  # rank r traces sample r of every pixel: distinct jitter draws
-        stream["sample"] = stream["sample"] + rank * BOUNCES
-        base = closed_box_stream(W_PIX, H_PIX, 1, 1)[1]
+    stream, base = make_stream(args.stream, rank)
     vs = pf.VertexStream(**stream)
     n = len(vs)
     n_pix = W_PIX * H_PIX
@@ -393,7 +418,8 @@ def run_b200(args):
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms_per_step,
             "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
             "data": "synthetic",
-            "config": {"workload": WORKLOAD, "vertices_per_frame": n, "pixels": n_pix,
+            "config": {"workload": WORKLOAD if args.stream == "synthetic" else WORKLOAD_TRACED,
+                       "vertices_per_frame": n, "pixels": n_pix,
                        "capacity": cfg.capacity, "tables": "fine+coarse",
                        "temporal_mode": cfg.temporal_mode, "sum_mode": cfg.sum_mode,
                        "parallelism": (f"key-sharded tables x{world} (NCCL all-to-all), "
@@ -473,6 +499,9 @@ def main():
     ap.add_argument("--impl", default="b200", choices=["b200", "reference"])
     ap.add_argument("--no-cpu", action="store_true", help="skip the cpu_baseline leg")
     ap.add_argument("--no-e2e", action="store_true", help="skip the host-buffer e2e leg")
+    ap.add_argument("--stream", default="traced", choices=["traced", "synthetic"],
+                    help="benchmark input: App. B scene traced on device, or the synthetic "
+                         "closed-box generator")
     args = ap.parse_args()
     if args.impl == "reference":
         return run_reference_arm(args)

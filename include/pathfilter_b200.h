@@ -23,7 +23,7 @@
 extern "C" {
 #endif
 
-#define PF_ABI_VERSION 1
+#define PF_ABI_VERSION 2
 
 enum pf_status {
     PF_OK = 0,
@@ -196,14 +196,17 @@ int pf_insert_frame(const pf_config *cfg, const pf_vertices *v, const pf_table *
  * stream_base_lookup, or NULL to build them here.
  * eff_records (may be NULL): scratch of 4 * fine->capacity uint64; when given, the
  * fine table's effective (sum, count) is computed once per occupied slot into one
- * 32-byte record that every lookup then reads. */
+ * 32-byte record that every lookup then reads.
+ * fallback_keys (may be NULL): scratch of 8 * n int64; when given, the lookup key and
+ * coarse hash of every row that leaves the fine rung are built one row per thread
+ * before the 3x3x3 pool instead of by one lane per row. */
 int pf_resolve_frame(const pf_config *cfg, const pf_vertices *v, const pf_table *fine,
                      const pf_table *coarse, uint64_t stream_base_lookup,
                      uint64_t stream_base_coarse, int64_t spp, const double *base_image,
                      int64_t n_pixels, double *image, double *flat, int64_t *work,
                      int64_t *work_count, uint8_t *source, double *chosen, int64_t *stats,
                      const uint64_t *lookup_index, const uint32_t *lookup_fp,
-                     uint64_t *eff_records, void *stream);
+                     uint64_t *eff_records, int64_t *fallback_keys, void *stream);
 
 /* Device scratch and outputs of pf_filter_frame (all device pointers). */
 typedef struct pf_frame_buffers {
@@ -221,6 +224,7 @@ typedef struct pf_frame_buffers {
     double *flat;                   /* [n_pixels][3] */
     int64_t *work;                  /* n */
     int64_t *work_count;            /* 1 */
+    int64_t *fallback_keys;         /* 8 * n, or NULL (see pf_resolve_frame) */
     void *phase_events[4];          /* optional cudaEvent_t recorded at frame start, just
                                        before the insert kernel, after it, at frame end */
 } pf_frame_buffers;

@@ -94,7 +94,8 @@ class PfFrameBuffers(ctypes.Structure):
                 ("horizon_clears_coarse", ctypes.c_void_p), ("lookup_index", ctypes.c_void_p),
                 ("lookup_fp", ctypes.c_void_p), ("eff_records", ctypes.c_void_p),
                 ("flat", ctypes.c_void_p), ("work", ctypes.c_void_p),
-                ("work_count", ctypes.c_void_p), ("phase_events", ctypes.c_void_p * 4)]
+                ("work_count", ctypes.c_void_p), ("fallback_keys", ctypes.c_void_p),
+                ("phase_events", ctypes.c_void_p * 4)]
 
 
 class PfShard(ctypes.Structure):
@@ -187,7 +188,7 @@ def lib() -> ctypes.CDLL:
     L.pf_insert_frame.argtypes = [vp, vp, vp, vp, u64, i64, vp, vp, vp, i64, vp, u64, vp, vp,
                                   vp]
     L.pf_resolve_frame.argtypes = [vp, vp, vp, vp, u64, u64, i64, vp, i64, vp, vp, vp, vp,
-                                   vp, vp, vp, vp, vp, vp, vp]
+                                   vp, vp, vp, vp, vp, vp, vp, vp]
     L.pf_filter_frame.argtypes = [vp, vp, vp, vp, i64, u64, u64, u64, i64, vp, i64, vp, vp, vp,
                                   vp, vp]
     L.pf_effective.argtypes = [vp, i32, dbl, dbl, vp, vp, vp]

@@ -173,6 +173,7 @@ struct ResolveArgs {
     const uint32_t *lk_fp;
     const ulonglong4 *rec;     // per-slot effective records of the fine table (or NULL)
     int64_t n_pixels;          // flat holds pixels [0, n_pixels)
+    int64_t *fb_keys;          // [work row][8] lookup key + coarse hash (or NULL)
 };
 
 // The fine table's effective value of slot s: its record when the effective pass ran.
@@ -312,6 +313,44 @@ __global__ void __launch_bounds__(kThreads) resolve_main_kernel(ResolveArgs a) {
     stats_flush(bs, a.stats, false);
 }
 
+// The work rows' lookup keys (q, level, aux; stream 3) and coarse hashes, one row per
+// thread -- the FP64 key recipe runs SIMT-wide instead of on one lane of a warp.
+// Record per row: q0, q1, q2, level, aux, coarse index, coarse fp, unused.
+__global__ void __launch_bounds__(kThreads) fallback_keys_kernel(ResolveArgs a) {
+    __shared__ double2 sincos_tab[220];
+    stage_sincos_table(sincos_tab);
+    __syncthreads();
+    const pf_config &cfg = a.cfg;
+    const int64_t n_work = *a.work_count;
+    for (int64_t w = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x; w < n_work;
+         w += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+        const int64_t row = a.work[w];
+        const VertexIn x = load_vertex(a.v, row, cfg);
+        const KeyShared ks = key_shared(cfg, x);
+        double du = 0.0, dv = 0.0, cdu = 0.0, cdv = 0.0;
+        if (cfg.jitter) {  // the coarse key uses stream 3 too when jitter is on (:255)
+            double u1, u2;
+            jitter_draws(a.h0_lookup, x.pixel, x.sample, u1, u2);
+            disc_offset(u1, u2, du, dv, sincos_tab);
+            cdu = du;
+            cdv = dv;
+            if (a.h0_coarse != a.h0_lookup) {
+                jitter_draws(a.h0_coarse, x.pixel, x.sample, u1, u2);
+                disc_offset(u1, u2, cdu, cdv, sincos_tab);
+            }
+        }
+        double jt[3];
+        const CellKey k = make_key(cfg, x, ks, cfg.jitter, du, dv, 0, jt);
+        CellHash hc{0ull, 0u};
+        if (a.has_coarse)
+            hc = key_hash(make_key(cfg, x, ks, cfg.jitter, cdu, cdv, cfg.coarse_delta, jt), ks);
+        longlong4 *o = reinterpret_cast<longlong4 *>(a.fb_keys + 8 * w);
+        o[0] = make_longlong4(k.q[0], k.q[1], k.q[2], k.level);
+        o[1] = make_longlong4(static_cast<long long>(k.aux), static_cast<long long>(hc.index),
+                              static_cast<long long>(hc.fp), 0);
+    }
+}
+
 // Rungs 2-5 for one work row per warp: lanes 0..26 probe the 3x3x3 neighbourhood in
 // (dx, dy, dz) nested order; lane 0 sums them in that order (numpy's order for the
 // float64 pools), then runs the coarse rung, the ladder and the composite.
@@ -330,9 +369,17 @@ __global__ void __launch_bounds__(kThreads) resolve_fallback_kernel(ResolveArgs 
     const uint64_t fmask = static_cast<uint64_t>(a.fine.capacity) - 1;
     for (int64_t w = warp0; w < n_work; w += nwarps) {
         const int64_t row = a.work[w];
-        // the row's lookup key (rebuilt by lane 0, broadcast to the 27 probing lanes)
-        int64_t kq[3] = {0, 0, 0}, klev = 0, kaux = 0;
-        if (lane == 0) {
+        // the row's lookup key: from fallback_keys_kernel (lanes 0..7 load the record),
+        // else rebuilt by lane 0; broadcast to the 27 probing lanes
+        int64_t kq[3] = {0, 0, 0}, klev = 0, kaux = 0, krec = 0;
+        if (a.fb_keys != nullptr) {
+            if (lane < 8) krec = a.fb_keys[8 * w + lane];
+            kq[0] = __shfl_sync(kFull, static_cast<long long>(krec), 0);
+            kq[1] = __shfl_sync(kFull, static_cast<long long>(krec), 1);
+            kq[2] = __shfl_sync(kFull, static_cast<long long>(krec), 2);
+            klev = __shfl_sync(kFull, static_cast<long long>(krec), 3);
+            kaux = __shfl_sync(kFull, static_cast<long long>(krec), 4);
+        } else if (lane == 0) {
             const CellKey k = lookup_key(a, row).first;
             kq[0] = k.q[0];
             kq[1] = k.q[1];
@@ -360,11 +407,17 @@ __global__ void __launch_bounds__(kThreads) resolve_fallback_kernel(ResolveArgs 
         // every lane now holds the same pooled sums; lane 0 finishes the row
         const bool ok_n = ((mode == PF_INTEGRATE) ? static_cast<double>(pool.icnt) : pool.fcnt) >= a.thr;
         if (lane == 0) {
-        const VertexIn x = load_vertex(a.v, row, cfg);
+        const int64_t pixel = __ldg(a.v.pixel + row);
         bool coarse_found = false;
         Effective ce{};
         if (!ok_n && a.has_coarse) {
-            const CellHash h = vertex_key(cfg, a.v, a.h0_coarse, row, cfg.coarse_delta).second;
+            CellHash h;
+            if (a.fb_keys != nullptr) {
+                h.index = static_cast<uint64_t>(a.fb_keys[8 * w + 5]);
+                h.fp = static_cast<uint32_t>(a.fb_keys[8 * w + 6]);
+            } else {
+                h = vertex_key(cfg, a.v, a.h0_coarse, row, cfg.coarse_delta).second;
+            }
             const int64_t s = probe_lookup(a.coarse.tags, static_cast<uint64_t>(a.coarse.capacity) - 1,
                                            a.coarse.probe_limit, h.index, h.fp);
             if (s >= 0) {
@@ -377,8 +430,8 @@ __global__ void __launch_bounds__(kThreads) resolve_fallback_kernel(ResolveArgs 
         for (int c = 0; c < 3; ++c) contrib[c] = __ldg(a.v.contribution + 3 * row + c);
         const int src = ladder_choose(pool, as_int, mode, fixed, a.thr, coarse_found, ce,
                                       eff_is_int(a.coarse, mode), contrib, ch);
-        composite(a, row, x.pixel, ch, src);
-        if (!(x.pixel >= 0 && x.pixel < a.n_pixels)) atomicAdd(&bs.v[PF_STAT_BAD_PIXELS], 1u);
+        composite(a, row, pixel, ch, src);
+        if (!(pixel >= 0 && pixel < a.n_pixels)) atomicAdd(&bs.v[PF_STAT_BAD_PIXELS], 1u);
         atomicAdd(&bs.v[PF_STAT_SOURCE_FINE + src], 1u);
         }
         __syncwarp();
@@ -444,7 +497,7 @@ int pf_resolve_frame(const pf_config *cfg, const pf_vertices *v, const pf_table 
                      int64_t n_pixels, double *image, double *flat, int64_t *work,
                      int64_t *work_count, uint8_t *source, double *chosen, int64_t *stats,
                      const uint64_t *lookup_index, const uint32_t *lookup_fp,
-                     uint64_t *eff_records, void *stream) {
+                     uint64_t *eff_records, int64_t *fallback_keys, void *stream) {
     const char *fn = "pf_resolve_frame";
     if ((lookup_index == nullptr) != (lookup_fp == nullptr))
         return fail_arg(fn, "lookup_index and lookup_fp go together");
@@ -484,6 +537,7 @@ int pf_resolve_frame(const pf_config *cfg, const pf_vertices *v, const pf_table 
         a.lk_fp = lookup_fp;
         a.rec = reinterpret_cast<const ulonglong4 *>(eff_records);
         a.n_pixels = n_pixels;
+        a.fb_keys = fallback_keys;
         if (eff_records != nullptr) {
             effective_records_kernel<<<sweep_blocks<kThreads>(fine->capacity, sm_count()), kThreads,
                                        0, st>>>(*fine, kc.temporal_mode, kc.ema_alpha,
@@ -497,6 +551,14 @@ int pf_resolve_frame(const pf_config *cfg, const pf_vertices *v, const pf_table 
         else
             resolve_main_kernel<1, false><<<blocks_for(v->n, kThreads), kThreads, 0, st>>>(a);
         if (int rc = check_launch(fn)) return rc;
+        if (fallback_keys != nullptr) {
+            static const int per_sm = resident_blocks(fallback_keys_kernel, kThreads);
+            int64_t kb = (v->n + kThreads - 1) / kThreads;
+            const int64_t kcap = static_cast<int64_t>(sm_count()) * per_sm;
+            if (kb > kcap) kb = kcap;
+            fallback_keys_kernel<<<static_cast<unsigned>(kb), kThreads, 0, st>>>(a);
+            if (int rc = check_launch(fn)) return rc;
+        }
         int64_t fb_blocks = (v->n + kWarps - 1) / kWarps;
         const int64_t cap = static_cast<int64_t>(sm_count()) * 8;
         if (fb_blocks > cap) fb_blocks = cap;
@@ -579,7 +641,7 @@ int pf_filter_frame(const pf_config *cfg, const pf_vertices *v, const pf_table *
     const int rc = pf_resolve_frame(cfg, v, fine, coarse, stream_base_lookup, stream_base_coarse,
                                     spp, base_image, n_pixels, image, b->flat, b->work,
                                     b->work_count, source, chosen, b->res_stats, b->lookup_index,
-                                    b->lookup_fp, b->eff_records, stream);
+                                    b->lookup_fp, b->eff_records, b->fallback_keys, stream);
     mark(3);
     return rc;
 }

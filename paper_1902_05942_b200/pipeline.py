@@ -409,6 +409,7 @@ def resolve_phase(vertices, cfg: FilterConfig, state: FrameState, frame: int, se
               counters.data_ptr(), lk[3].data_ptr() if lk_ok else None,
               lk[4].data_ptr() if lk_ok else None,
               state.buffer("eff_records", (state.fine.capacity, 4), torch.int64).data_ptr(),
+              state.buffer("fallback_keys", (max(n, 1), 8), torch.int64).data_ptr(),
               _lib.stream_handle())
     del keep
     report = ResolveReport(source, image, chosen)
@@ -446,6 +447,7 @@ def _fused_frame(vs: VertexStream, base_image, cfg: FilterConfig, state: FrameSt
     b.flat = state.buffer("flat", (h * w, 3), torch.float64).data_ptr()
     b.work = state.buffer("work", (max(n, 1),), torch.int64).data_ptr()
     b.work_count = state.buffer("work_count", (1,), torch.int64).data_ptr()
+    b.fallback_keys = state.buffer("fallback_keys", (max(n, 1), 8), torch.int64).data_ptr()
     if phase_events is not None:  # torch.cuda.Events recorded inside the C call
         for k, e in enumerate(phase_events):
             b.phase_events[k] = e.cuda_event

@@ -184,14 +184,15 @@ def reevaluate(scene: Scene, seed: int, spp: int, path_ids, options: TraceOption
 
 
 def multi_bounce_stream(scene: Scene, bounces: int, seed: int, rr_start: int = 9,
-                        options: TraceOptions | None = None) -> tuple:
+                        options: TraceOptions | None = None, sample_offset: int = 0) -> tuple:
     """The benchmark stream of SURVEY App. B: select_k = 1..bounces traces at 1 spp,
-    `sample += k - 1`, concatenated.  Returns (VertexStream, base image of k = 1)."""
+    `sample += k - 1`, concatenated.  Returns (VertexStream, base image of k = 1).
+    sample_offset traces another sample of every pixel (distinct path ids)."""
     streams, base = [], None
     for k in range(1, bounces + 1):
         opt = TraceOptions(**{**(options.__dict__ if options else {}), "select_k": k,
                               "rr_start": rr_start})
-        res = trace(scene, 1, seed, opt)
+        res = trace(scene, 1, seed, opt, sample_offset=sample_offset)
         v = res.vertices
         v.sample = v.sample + (k - 1)
         streams.append(v)

@@ -44,7 +44,10 @@ def test_library_exports_every_declared_symbol(lib):
 
 def test_abi_version_without_gpu(lib):
     lib.pf_abi_version.restype = ctypes.c_int
-    assert lib.pf_abi_version() == 1
+    import re
+    with open(os.path.join(ROOT, "include", "pathfilter_b200.h")) as fh:
+        want = int(re.search(r"#define PF_ABI_VERSION (\d+)", fh.read()).group(1))
+    assert lib.pf_abi_version() == want
 
 
 def test_argument_errors_are_status_codes(lib):
