@@ -400,6 +400,13 @@ int pf_check_contributions(const double *vals, int64_t count, int32_t *bad, void
 int pf_selftest_division(uint64_t seed, int64_t n, double base_voxel, int64_t *mismatches,
                          void *stream);
 
+/* temporal.reevaluation_deltas (src/temporal.py:60-92) after the host grouped the
+ * replayed rows by voxel: voxel v owns rows order[offsets[v] .. offsets[v+1]) (stream
+ * order); delta[v] = |mean_new - mean_old|_1 / (|mean_old|_1 + delta_eps) with the sums
+ * in np.add.at's order.  c_old / c_new: [rows][3] contributions. */
+int pf_segment_deltas(const int64_t *order, const int64_t *offsets, int64_t n_vox,
+                      const double *c_old, const double *c_new, double delta_eps, double *delta,
+                      void *stream);
 /* Diagnostic: sin(x[i]) and cos(x[i]) as the library computes them for the jitter and
  * the tracer -- glibc's dbl-64 algorithm, equal to numpy's float64 sin/cos here. */
 int pf_sincos(const double *x, int64_t n, double *s, double *c, void *stream);

@@ -1,26 +1,51 @@
 """B200-native hashed path-space filtering (arXiv 1902.05942).
 
-Drop-in for the filter API of the reference package `pathfilter`
-(src/__init__.py:10-33): build keys, insert vertices, query averages, temporal
-update.  All compute runs in hand-written sm_100a CUDA kernels
-(libpf_b200.so, C ABI in include/pathfilter_b200.h); there is no CPU fallback.
+Drop-in for the reference package `pathfilter` (src/__init__.py:10-33): build keys,
+insert vertices, query averages, temporal update -- plus the on-device path tracer
+that produces the vertex stream, whole frames (render_frame / run_sequence, all three
+temporal modes) and the key-sharded multi-GPU frame.  All compute runs in hand-written
+sm_100a CUDA kernels (libpf_b200.so, C ABI in include/pathfilter_b200.h); there is no
+CPU fallback.  The scalar key helpers and brute-force partition utilities the
+reference also exports are host code by design (one vertex at a time).
 """
 
 from . import rng
+from .images import read_ppm, tonemap, write_ppm
 from .keys import CellHashes, CellKey, FilterConfig, KeyArrays, hash_arrays, hashes, \
     make_key_arrays, pack_aux
+from .partition import ball_average, brute_voxel_average, derive_key, image_mse, \
+    neighborhood_mean
 from .pipeline import FrameState, FrameStats, ResolveReport, VertexStream, accumulate_phase, \
     filter_frame, resolve_phase, vertex_keys
+from .render import FrameResult, render_frame, run_sequence
+from .scalar import jitter_position, level_of_detail, make_cell_key
+from .scene import Camera, Material, Motion, Scene, SceneBuilder, SceneError, closed_box, \
+    cornell_box, load_scene, parse_scene
 from .table import EMPTY_TAG, EvictionEvent, InsertOutcome, Outcome, VoxelTable, \
     fixed_to_float, pack_priority, quantize_fixed
+from .temporal import blend, migrate_resolution, reevaluation_deltas, select_replay_ids, \
+    temporal_difference
+from .tracer import TraceOptions, TraceResult, reevaluate, trace
 
 BACKEND = "b200"
 __version__ = "0.1.0"
 
+
+def available_backends() -> list:
+    """src/_backend.py: the kernel backends this build provides."""
+    return [BACKEND]
+
+
 __all__ = [
-    "BACKEND", "rng", "CellHashes", "CellKey", "FilterConfig", "KeyArrays", "hash_arrays",
-    "hashes", "make_key_arrays", "pack_aux", "FrameState", "FrameStats", "ResolveReport",
+    "BACKEND", "available_backends", "rng", "CellHashes", "CellKey", "FilterConfig",
+    "KeyArrays", "hash_arrays", "hashes", "make_key_arrays", "pack_aux", "jitter_position",
+    "level_of_detail", "make_cell_key", "ball_average", "brute_voxel_average", "derive_key",
+    "image_mse", "neighborhood_mean", "FrameState", "FrameStats", "ResolveReport",
     "VertexStream", "accumulate_phase", "filter_frame", "resolve_phase", "vertex_keys",
+    "FrameResult", "render_frame", "run_sequence", "Camera", "Material", "Motion", "Scene",
+    "SceneBuilder", "SceneError", "closed_box", "cornell_box", "load_scene", "parse_scene",
     "EMPTY_TAG", "EvictionEvent", "InsertOutcome", "Outcome", "VoxelTable", "fixed_to_float",
-    "pack_priority", "quantize_fixed",
+    "pack_priority", "quantize_fixed", "blend", "migrate_resolution", "reevaluation_deltas",
+    "select_replay_ids", "temporal_difference", "TraceOptions", "TraceResult", "reevaluate",
+    "trace", "read_ppm", "tonemap", "write_ppm",
 ]

@@ -33,7 +33,7 @@ EXPORTS = ("pf_abi_version", "pf_last_error", "pf_device_sm_count", "pf_accumula
            "pf_begin_frame", "pf_check_contributions", "pf_selftest_division",
            "pf_count_occupied", "pf_finalize_image", "pf_shard_keys", "pf_shard_emit",
            "pf_shard_apply", "pf_shard_answer", "pf_shard_resolve", "pf_shard_fallback_keys",
-           "pf_shard_ladder", "pf_shard_reset", "pf_trace_paths", "pf_sincos")
+           "pf_shard_ladder", "pf_shard_reset", "pf_trace_paths", "pf_sincos", "pf_segment_deltas")
 
 
 def build(force: bool = False, verbose: bool = False) -> str:
@@ -207,6 +207,7 @@ def lib() -> ctypes.CDLL:
     L.pf_shard_reset.argtypes = [vp, vp]
     L.pf_trace_paths.argtypes = [vp, vp, u64, vp, vp, i64, vp, vp]
     L.pf_sincos.argtypes = [vp, i64, vp, vp, vp]
+    L.pf_segment_deltas.argtypes = [vp, vp, i64, vp, vp, dbl, vp, vp]
     for name in EXPORTS[3:]:
         getattr(L, name).restype = ctypes.c_int
     _lib = L

@@ -414,6 +414,33 @@ selftest_division_kernel(uint64_t seed, int64_t n, double base_voxel, unsigned l
     if (b1) atomicAdd(bad + 1, b1);
 }
 
+// temporal.reevaluation_deltas per voxel (src/temporal.py:80-92): voxel v's rows are
+// order[offsets[v] .. offsets[v+1]) in stream order, so the float sums follow np.add.at.
+__global__ void __launch_bounds__(kThreads)
+segment_deltas_kernel(const int64_t *order, const int64_t *offsets, int64_t n_vox,
+                      const double *c_old, const double *c_new, double eps, double *delta) {
+    const int64_t v = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+    if (v >= n_vox) return;
+    double so[3] = {0.0, 0.0, 0.0}, sn[3] = {0.0, 0.0, 0.0}, cnt = 0.0;
+    for (int64_t j = offsets[v]; j < offsets[v + 1]; ++j) {
+        const int64_t r = order[j];
+#pragma unroll
+        for (int c = 0; c < 3; ++c) {
+            so[c] = dadd(so[c], c_old[3 * r + c]);
+            sn[c] = dadd(sn[c], c_new[3 * r + c]);
+        }
+        cnt = dadd(cnt, 1.0);
+    }
+    double num = 0.0, den = 0.0;
+#pragma unroll
+    for (int c = 0; c < 3; ++c) {
+        const double mo = ddiv(so[c], cnt), mn = ddiv(sn[c], cnt);
+        num = c == 0 ? fabs(dsub(mn, mo)) : dadd(num, fabs(dsub(mn, mo)));
+        den = c == 0 ? fabs(mo) : dadd(den, fabs(mo));
+    }
+    delta[v] = ddiv(num, dadd(den, eps));
+}
+
 // glibc_sincos over an array (diagnostic entry point for the bit-exactness test).
 __global__ void __launch_bounds__(kThreads)
 sincos_kernel(const double *x, int64_t n, double *s, double *c) {
@@ -579,6 +606,17 @@ int pf_check_contributions(const double *vals, int64_t count, int32_t *bad, void
     check_contributions_kernel<<<static_cast<unsigned>(blocks), kThreads, 0, as_stream(stream)>>>(
         vals, count, bad);
     return check_launch(fn);
+}
+
+int pf_segment_deltas(const int64_t *order, const int64_t *offsets, int64_t n_vox,
+                      const double *c_old, const double *c_new, double delta_eps, double *delta,
+                      void *stream) {
+    if (n_vox < 0 || (n_vox > 0 && (!order || !offsets || !c_old || !c_new || !delta)))
+        return fail_arg("pf_segment_deltas", "bad arguments");
+    if (n_vox == 0) return PF_OK;
+    segment_deltas_kernel<<<blocks_for(n_vox, kThreads), kThreads, 0, as_stream(stream)>>>(
+        order, offsets, n_vox, c_old, c_new, delta_eps, delta);
+    return check_launch("pf_segment_deltas");
 }
 
 int pf_sincos(const double *x, int64_t n, double *s, double *c, void *stream) {

@@ -169,6 +169,7 @@ class FrameState:
     scratch: dict = field(default_factory=dict)
     lookup_keys: tuple | None = None
     pending_validation: list = field(default_factory=list)
+    prev_vertices: object = None  # last rendered frame's VertexStream (hybrid replay)
 
     def poll_validation(self, wait: bool = False, parity: int | None = None):
         """Raise for a frame whose device input check failed (its kernels were guarded:

@@ -169,7 +169,10 @@ def reevaluate(scene: Scene, seed: int, spp: int, path_ids, options: TraceOption
                ) -> VertexStream:
     """Replay paths by id under the current scene state (src/tracer.py:464-486)."""
     scene.validate()
-    ids = torch.as_tensor(np.asarray(path_ids, np.uint64).view(np.int64))
+    if isinstance(path_ids, torch.Tensor):
+        ids = path_ids.to(torch.int64)
+    else:
+        ids = torch.as_tensor(np.asarray(path_ids, np.uint64).view(np.int64))
     npix = scene.camera.width * scene.camera.height
     pixels = ids & 0xFFFFFFFF
     samples = (ids >> 32) & 0xFFFFFFFF

@@ -336,10 +336,120 @@ def gen_tracer():
     save("tracer.npz", out)
 
 
+def gen_render():
+    """render_frame sequences (src/pipeline.py:321-380): trace + temporal update +
+    accumulate (+ hybrid replay) + resolve, per temporal mode."""
+    from pathfilter.pipeline import run_sequence
+    from pathfilter.scene import load_scene
+    out = {}
+    runs = {
+        "integrate": ("cornell", 24, 24, 2, dict()),
+        "filter": ("corridor", 20, 16, 4, dict(temporal_mode="filter")),
+        "hybrid": ("shadow-sweep", 24, 24, 4, dict(temporal_mode="hybrid",
+                                                   reevaluate_fraction=0.25)),
+    }
+    for name, (scene_name, w, h, frames, kw) in runs.items():
+        sc = load_scene(scene_name, w, h)
+        cfg = FilterConfig(capacity=next_pow2(2 * w * h), **kw)
+        res = run_sequence(sc, cfg, 1, 13, frames=frames)
+        out[f"{name}_cfg"] = np.array(cfg_dict(cfg))
+        out[f"{name}_meta"] = np.array(json.dumps([scene_name, w, h, frames]))
+        for f, r in enumerate(res):
+            out[f"{name}_f{f}_filtered"] = r.filtered
+            out[f"{name}_f{f}_unfiltered"] = r.unfiltered
+            out[f"{name}_f{f}_source"] = r.report.source
+            out[f"{name}_f{f}_stats"] = np.array("\n".join(r.stats.lines()))
+    save("render.npz", out)
+
+
+def gen_formats():
+    """Output formats and the keyed temporal helpers: tonemap / PPM
+    bytes (src/images.py), VoxelTable.export_csv / dump bytes, blend /
+    temporal_difference / migrate_resolution (src/temporal.py)."""
+    import io
+    import tempfile
+    from pathfilter.images import tonemap, write_ppm
+    from pathfilter.keys import CellKey
+    from pathfilter.table import VoxelTable
+    from pathfilter.temporal import blend, migrate_resolution, temporal_difference
+    r = np.random.default_rng(5)
+    out = {}
+    img = r.uniform(-0.2, 1.4, (7, 9, 3))
+    out["img"] = img
+    out["tonemap"] = tonemap(img)
+    with tempfile.TemporaryDirectory() as td:
+        write_ppm(os.path.join(td, "a.ppm"), img)
+        out["ppm"] = np.frombuffer(open(os.path.join(td, "a.ppm"), "rb").read(), np.uint8)
+        t = VoxelTable(64, sum_mode="fixed")
+        vs = random_stream(200, 3, n_keys=20, spread=2.0)
+        k = make_key_arrays(vs.position, vs.normal, vs.omega_r, vs.layer_id, vs.camera_distance,
+                            FilterConfig(capacity=64), None, None, 0)
+        t.accumulate_batch(k.index, k.fingerprint, vs.contribution, 0)
+        put_table(out, "csvtab_", t)
+        t.export_csv(os.path.join(td, "t.csv"))
+        out["csv"] = np.array(open(os.path.join(td, "t.csv")).read())
+        t.dump(os.path.join(td, "t.bin"))
+        out["dump"] = np.frombuffer(open(os.path.join(td, "t.bin"), "rb").read(), np.uint8)
+    rows = []
+    for mode in ("integrate", "filter", "hybrid"):
+        for (no, nn, dl) in ((0, 3, 0.0), (5, 0, 0.1), (4, 2, 0.3), (7, 5, 0.9)):
+            m, n = blend([0.1, 0.2, 0.3], no, [0.5, 0.25, 0.0], nn, mode, dl)
+            rows.append(list(m) + [n])
+    out["blend"] = np.array(rows)
+    out["tdiff"] = np.array([temporal_difference([0.1, 0.2, 0.3], [0.2, 0.1, 0.35]),
+                             temporal_difference([0, 0, 0], [1e-5, 0, 0])])
+    cells = {CellKey(3, -2, 5, 4, 7): (np.array([6.0, 3.0, 1.5]), 6),
+             CellKey(2, -2, 5, 4, 7): (np.array([1.0, 1.0, 1.0]), 2),
+             CellKey(1, 1, 1, 3, 0): (np.array([2.0, 2.0, 2.0]), 4)}
+    for name, (lo, ln, fixed) in {"up": (4, 5, False), "down": (4, 3, False),
+                                  "downfix": (4, 2, True)}.items():
+        mig = migrate_resolution({k: (np.floor(v * 65536).astype(np.int64) if fixed else v, c)
+                                  for k, (v, c) in cells.items()}, lo, ln, 0.25, fixed)
+        out[f"mig_{name}"] = np.array(sorted(
+            [k.qx, k.qy, k.qz, k.level, k.aux, c] + [float(x) for x in v]
+            for k, (v, c) in mig.items()))
+    # scalar key path + brute-force partition utilities (src/keys.py:100-240, src/oracle.py)
+    from pathfilter.keys import jitter_position, level_of_detail, make_cell_key
+    from pathfilter.oracle import ball_average, brute_voxel_average, image_mse, \
+        neighborhood_mean
+    vs = random_stream(300, 11, n_keys=40, spread=3.0)
+    cfgs = {"default": FilterConfig(capacity=1024, footprint_scale=0.002),
+            "aux": FilterConfig(capacity=1024, footprint_scale=0.002, include_incident_angle=True,
+                                include_layer=True)}
+    for name, cfg in cfgs.items():
+        draws = r.random((len(vs), 2))
+        keys = [make_cell_key(vs.descriptor(i), cfg, draws[i], d) for i in range(len(vs))
+                for d in (0, 2)]
+        out[f"scalar_{name}_draws"] = draws
+        out[f"scalar_{name}_keys"] = np.array([[k.qx, k.qy, k.qz, k.level, k.aux] for k in keys])
+        out[f"scalar_{name}_lod"] = np.array([level_of_detail(float(d), cfg)
+                                              for d in vs.camera_distance])
+        out[f"scalar_{name}_jit"] = np.array([jitter_position(vs.position[i], vs.normal[i], 3,
+                                                              draws[i], cfg)
+                                              for i in range(len(vs))])
+        ka = make_key_arrays(vs.position, vs.normal, vs.omega_r, vs.layer_id, vs.camera_distance,
+                             cfg, draws[:, 0], draws[:, 1], 0)
+        out[f"part_{name}_jittered"] = ka.jittered
+        for sm in ("fixed", "float"):
+            part = brute_voxel_average(vs, cfg, ka.jittered, sm)
+            with tempfile.TemporaryDirectory() as td:
+                part.to_csv(os.path.join(td, "p.csv"))
+                out[f"part_{name}_{sm}_csv"] = np.array(open(os.path.join(td, "p.csv")).read())
+            some = sorted(part.cells)[::7]
+            out[f"part_{name}_{sm}_nbr"] = np.array([neighborhood_mean(part, k) for k in some])
+    put_stream(out, "part_v_", vs)
+    out["ball"] = np.array([ball_average(vs, vs.position[5], 1.5),
+                            ball_average(vs, vs.position[9], 0.8,
+                                         lambda c, p: 1.0 / (1.0 + float(((p - c) ** 2).sum())))])
+    out["mse"] = np.array(image_mse(img, img * 0.9))
+    save("formats.npz", out)
+
+
 if __name__ == "__main__":
-    which = sys.argv[1:] or ["rng", "keys", "cornell", "box4", "temporal", "hybrid", "tracer"]
+    which = sys.argv[1:] or ["rng", "keys", "cornell", "box4", "temporal", "hybrid", "tracer",
+                             "render", "formats"]
     fns = {"rng": gen_rng_hash, "keys": gen_keys_random, "cornell": gen_frame_cornell,
            "box4": gen_frame_box4, "temporal": gen_temporal, "hybrid": gen_hybrid,
-           "tracer": gen_tracer}
+           "tracer": gen_tracer, "render": gen_render, "formats": gen_formats}
     for w in which:
         fns[w]()
