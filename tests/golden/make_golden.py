@@ -442,6 +442,27 @@ def gen_formats():
                             ball_average(vs, vs.position[9], 0.8,
                                          lambda c, p: 1.0 / (1.0 + float(((p - c) ** 2).sum())))])
     out["mse"] = np.array(image_mse(img, img * 0.9))
+    # probe_scan over structured fingerprints (normal_in_fingerprint, src/table.py:186-203)
+    from pathfilter.keys import fingerprint_spatial_bits, hashes as ref_hashes
+    t = VoxelTable(256, sum_mode="fixed", probe_limit=8)
+    key = CellKey(4, -3, 9, 2, 0)
+    idx, fps, vals = [], [], []
+    for nb in range(6):
+        h = ref_hashes(key, nb)
+        idx.append(h.index)
+        fps.append(h.fingerprint)
+        vals.append([0.1 * nb, 0.2, 0.3 + nb])
+    other = ref_hashes(CellKey(5, -3, 9, 2, 0), 1)
+    idx.append(other.index)
+    fps.append(other.fingerprint)
+    vals.append([9.0, 9.0, 9.0])
+    t.accumulate_batch(np.array(idx, np.uint64), np.array(fps, np.uint32), np.array(vals), 0)
+    sp = fingerprint_spatial_bits(ref_hashes(key, 0).fingerprint)
+    res = t.probe_scan(ref_hashes(key, 0), lambda fp: fingerprint_spatial_bits(fp) == sp)
+    out["scan_idx"], out["scan_fp"] = np.array(idx, np.uint64), np.array(fps, np.uint32)
+    out["scan_vals"] = np.array(vals)
+    out["scan_means"] = np.array([m for m, _ in res])
+    out["scan_counts"] = np.array([c for _, c in res])
     save("formats.npz", out)
 
 

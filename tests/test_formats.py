@@ -125,3 +125,19 @@ def test_ball_average_and_mse():
                                  lambda c, p: 1.0 / (1.0 + float(((p - c) ** 2).sum())))])
     assert np.array_equal(got, d["ball"])
     assert image_mse(d["img"], d["img"] * 0.9) == float(d["mse"])
+
+
+@pytest.mark.gpu
+def test_probe_scan_structured_fingerprints(gpu):
+    """normal_in_fingerprint keys share the index hash; probe_scan finds every normal
+    variant of a voxel by the fingerprint's spatial bits (src/table.py:186-203)."""
+    from paper_1902_05942_b200.scalar import fingerprint_spatial_bits
+    d = load_golden("formats.npz")
+    t = gpu.VoxelTable(256, sum_mode="fixed", probe_limit=8, ordered=True)
+    t.accumulate_batch(d["scan_idx"], d["scan_fp"], d["scan_vals"], 0)
+    h = gpu.hashes(gpu.CellKey(4, -3, 9, 2, 0), 0)
+    assert h.index == int(d["scan_idx"][0]) and h.fingerprint == int(d["scan_fp"][0])
+    sp = fingerprint_spatial_bits(h.fingerprint)
+    res = t.probe_scan(h, lambda fp: fingerprint_spatial_bits(fp) == sp)
+    assert np.array_equal(np.array([c for _, c in res]), d["scan_counts"])
+    assert np.array_equal(np.array([np.asarray(m) for m, _ in res]), d["scan_means"])
