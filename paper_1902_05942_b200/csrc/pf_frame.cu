@@ -597,40 +597,16 @@ int pf_filter_frame(const pf_config *cfg, const pf_vertices *v, const pf_table *
         if (b->phase_events[k]) cudaEventRecord(static_cast<cudaEvent_t>(b->phase_events[k]), st);
     };
     mark(0);
-    // The input check reads only the vertex buffer and begin_frame only the tables:
-    // run the check on a side stream so the two overlap, joined before the insert.
-    SideStream &side = side_stream();
-    const bool fork = b->bad_flag != nullptr && v->n > 0 && side.ok;
-    if (b->bad_flag) {
-        if (cudaMemsetAsync(b->bad_flag, 0, sizeof(int32_t), st) != cudaSuccess)
-            return check_launch(fn);
-        if (fork) {
-            cudaEventRecord(side.fork, st);
-            cudaStreamWaitEvent(side.stream, side.fork, 0);
-            if (int rc = pf_check_contributions(v->contribution, 3 * v->n, b->bad_flag,
-                                                side.stream))
-                return rc;
-            cudaEventRecord(side.join, side.stream);
-        } else if (v->n > 0) {
-            if (int rc = pf_check_contributions(v->contribution, 3 * v->n, b->bad_flag, stream))
-                return rc;
-        }
-    }
-    // generation fold on both tables (src/pipeline.py:331-333)
-    if (int rc = pf_begin_frame(fine, frame, cfg->temporal_mode, cfg->ema_alpha, cfg->delta_max,
-                                cfg->sample_cap, b->horizon_clears_fine, stream))
-        return rc;
-    if (coarse)
-        if (int rc = pf_begin_frame(coarse, frame, cfg->temporal_mode, cfg->ema_alpha,
-                                    cfg->delta_max, cfg->sample_cap, b->horizon_clears_coarse,
-                                    stream))
-            return rc;
-    if (cudaMemsetAsync(b->acc_stats, 0, sizeof(int64_t) * PF_STAT_COUNT, st) != cudaSuccess ||
-        cudaMemsetAsync(b->res_stats, 0, sizeof(int64_t) * PF_STAT_COUNT, st) != cudaSuccess ||
-        (b->event_count &&
-         cudaMemsetAsync(b->event_count, 0, sizeof(int64_t), st) != cudaSuccess))
+    // prologue in one launch: generation fold on both tables (src/pipeline.py:331-333),
+    // the input check and the counter resets, side by side over the grid
+    if (b->bad_flag && cudaMemsetAsync(b->bad_flag, 0, sizeof(int32_t), st) != cudaSuccess)
         return check_launch(fn);
-    if (fork && cudaStreamWaitEvent(st, side.join, 0) != cudaSuccess) return check_launch(fn);
+    if (int rc = frame_prologue(fine, coarse, frame, cfg->temporal_mode, cfg->ema_alpha,
+                                cfg->delta_max, cfg->sample_cap, b->horizon_clears_fine,
+                                b->horizon_clears_coarse, v->n > 0 ? v->contribution : nullptr,
+                                3 * v->n, b->bad_flag, b->acc_stats, PF_STAT_COUNT, b->res_stats,
+                                PF_STAT_COUNT, b->event_count, st))
+        return rc;
     // accumulate_phase (fused, flag-guarded) + the resolve phase's lookup keys
     mark(1);
     if (int rc = pf_insert_frame(cfg, v, fine, coarse, stream_base_accum, frame, b->acc_stats,

@@ -72,6 +72,14 @@ inline int prepare_config(const char *fn, const pf_config *in, pf_config *out) {
     return PF_OK;
 }
 
+// pf_filter_frame's prologue in one launch (pf_table.cu): begin_frame on both tables,
+// the input check (vals/bad may be NULL) and the zeroing of three counter arrays.
+int frame_prologue(const pf_table *fine, const pf_table *coarse, int64_t frame, int32_t mode,
+                   double ema, double delta_max, int32_t sample_cap, int64_t *clears_fine,
+                   int64_t *clears_coarse, const double *vals, int64_t count, int32_t *bad,
+                   int64_t *zero0, int64_t n0, int64_t *zero1, int64_t n1, int64_t *zero2,
+                   cudaStream_t st);
+
 inline unsigned blocks_for(int64_t n, int threads) {
     return static_cast<unsigned>((n + threads - 1) / threads);
 }

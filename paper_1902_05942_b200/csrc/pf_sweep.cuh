@@ -19,16 +19,17 @@ struct SweepSmem {
     int n;
 };
 
-// f(slot, tag) runs once per occupied slot, spread over the CTA's threads.
+// f(slot, tag) runs once per occupied slot, spread over the CTA's threads.  The CTA is
+// block `blk` of `nblk` sweeping this table (a kernel may split its grid over jobs).
 template <int THREADS, typename F>
 __device__ __forceinline__ void for_each_occupied(const uint64_t *tags, int64_t capacity,
-                                                  SweepSmem<THREADS> &q, F &&f) {
+                                                  SweepSmem<THREADS> &q, int64_t blk,
+                                                  int64_t nblk, F &&f) {
     constexpr int kP = SweepSmem<THREADS>::kPairsPerThread;
     constexpr int kChunk = SweepSmem<THREADS>::kChunk;
     const int lane = threadIdx.x & 31;
     const ulonglong2 *tags2 = reinterpret_cast<const ulonglong2 *>(tags);
-    for (int64_t base = static_cast<int64_t>(blockIdx.x) * kChunk; base < capacity;
-         base += static_cast<int64_t>(gridDim.x) * kChunk) {
+    for (int64_t base = blk * kChunk; base < capacity; base += nblk * kChunk) {
         if (threadIdx.x == 0) q.n = 0;
         __syncthreads();
         ulonglong2 tg[kP];
@@ -62,6 +63,12 @@ __device__ __forceinline__ void for_each_occupied(const uint64_t *tags, int64_t 
         for (int k = threadIdx.x; k < n_q; k += THREADS) f(q.slot[k], q.tag[k]);
         __syncthreads();
     }
+}
+
+template <int THREADS, typename F>
+__device__ __forceinline__ void for_each_occupied(const uint64_t *tags, int64_t capacity,
+                                                  SweepSmem<THREADS> &q, F &&f) {
+    for_each_occupied<THREADS>(tags, capacity, q, blockIdx.x, gridDim.x, f);
 }
 
 // CTAs for a sweep over `capacity` slots (each CTA step covers kChunk slots).

@@ -414,6 +414,61 @@ selftest_division_kernel(uint64_t seed, int64_t n, double base_voxel, unsigned l
     if (b1) atomicAdd(bad + 1, b1);
 }
 
+// The frame prologue of pf_filter_frame in one launch: begin_frame on the fine and the
+// coarse table and the input check, interleaved over the grid (job = block % jobs) so
+// the three sweeps run side by side; block 0 also clears the frame's counters.
+template <bool FIXED>
+__global__ void __launch_bounds__(kThreads)
+frame_prologue_kernel(pf_table fine, pf_table coarse, int jobs, int64_t frame, int mode,
+                      double ema, double delta_max, int32_t sample_cap, int64_t *clears_fine,
+                      int64_t *clears_coarse, const double *vals, int64_t count, int32_t *bad,
+                      int64_t *zero0, int64_t n0, int64_t *zero1, int64_t n1, int64_t *zero2) {
+    __shared__ SweepSmem<kThreads> q;
+    __shared__ int block_clears;
+    if (blockIdx.x == 0) {
+        for (int64_t k = threadIdx.x; k < n0; k += blockDim.x) zero0[k] = 0;
+        for (int64_t k = threadIdx.x; k < n1; k += blockDim.x) zero1[k] = 0;
+        if (zero2 && threadIdx.x == 0) *zero2 = 0;
+    }
+    const int job = static_cast<int>(blockIdx.x % jobs);
+    const int64_t blk = blockIdx.x / jobs, nblk = gridDim.x / jobs;
+    const bool check = vals != nullptr && job == jobs - 1;
+    if (check) {  // NaN, +-inf or negative contributions; 16-byte loads, 4 per thread in flight
+        const double2 *v2 = reinterpret_cast<const double2 *>(vals);
+        const int64_t n2 = count / 2;
+        bool any = false;
+        const int64_t stride = nblk * blockDim.x;
+        for (int64_t k = blk * blockDim.x + threadIdx.x; k < n2; k += 4 * stride) {
+            double2 x[4];
+#pragma unroll
+            for (int u = 0; u < 4; ++u)
+                x[u] = k + u * stride < n2 ? __ldg(v2 + k + u * stride) : make_double2(0.0, 0.0);
+#pragma unroll
+            for (int u = 0; u < 4; ++u)
+                any |= !(x[u].x >= 0.0 && x[u].x <= 1.7976931348623157e308) ||
+                       !(x[u].y >= 0.0 && x[u].y <= 1.7976931348623157e308);
+        }
+        if (blk == 0 && threadIdx.x == 0 && (count & 1)) {
+            const double x = __ldg(vals + count - 1);
+            any |= !(x >= 0.0 && x <= 1.7976931348623157e308);
+        }
+        if (__any_sync(kFull, any) && (threadIdx.x & 31) == 0) atomicExch(bad, 1);
+        return;
+    }
+    const pf_table &t = job == 0 ? fine : coarse;
+    if (threadIdx.x == 0) block_clears = 0;
+    int cleared = 0;
+    for_each_occupied<kThreads>(t.tags, t.capacity, q, blk, nblk, [&](int64_t s, uint64_t tag) {
+        cleared += fold_slot<FIXED>(t, s, tag, frame, mode, ema, delta_max, sample_cap);
+    });
+    if (cleared) atomicAdd(&block_clears, cleared);
+    __syncthreads();
+    int64_t *clears = job == 0 ? clears_fine : clears_coarse;
+    if (threadIdx.x == 0 && block_clears && clears)
+        atomicAdd(reinterpret_cast<unsigned long long *>(clears),
+                  static_cast<unsigned long long>(block_clears));
+}
+
 // temporal.reevaluation_deltas per voxel (src/temporal.py:80-92): voxel v's rows are
 // order[offsets[v] .. offsets[v+1]) in stream order, so the float sums follow np.add.at.
 __global__ void __launch_bounds__(kThreads)
@@ -584,6 +639,42 @@ int pf_begin_frame(const pf_table *t, int64_t frame, int32_t mode, double ema_al
             *t, frame, mode, ema_alpha, delta_max, sample_cap, horizon_clears);
     return check_launch(fn);
 }
+
+}  // extern "C"
+
+namespace pf {
+
+int frame_prologue(const pf_table *fine, const pf_table *coarse, int64_t frame, int32_t mode,
+                   double ema, double delta_max, int32_t sample_cap, int64_t *clears_fine,
+                   int64_t *clears_coarse, const double *vals, int64_t count, int32_t *bad,
+                   int64_t *zero0, int64_t n0, int64_t *zero1, int64_t n1, int64_t *zero2,
+                   cudaStream_t st) {
+    const char *fn = "pf_filter_frame";
+    if (int rc = validate_table(fn, fine)) return rc;
+    if (coarse) {
+        if (int rc = validate_table(fn, coarse)) return rc;
+        if (coarse->sum_mode != fine->sum_mode) return fail_arg(fn, "fine/coarse sum_mode differ");
+    }
+    if (mode < PF_INTEGRATE || mode > PF_HYBRID) return fail_arg(fn, "unknown temporal mode");
+    const bool checking = vals != nullptr && bad != nullptr && count > 0;
+    const int jobs = (coarse ? 2 : 1) + (checking ? 1 : 0);
+    const unsigned per_job = sweep_blocks<kThreads>(fine->capacity, sm_count());
+    const pf_table c = coarse ? *coarse : *fine;
+    const unsigned g = per_job * static_cast<unsigned>(jobs);
+    if (fine->sum_mode == PF_SUM_FIXED)
+        frame_prologue_kernel<true><<<g, kThreads, 0, st>>>(
+            *fine, c, jobs, frame, mode, ema, delta_max, sample_cap, clears_fine, clears_coarse,
+            checking ? vals : nullptr, count, bad, zero0, n0, zero1, n1, zero2);
+    else
+        frame_prologue_kernel<false><<<g, kThreads, 0, st>>>(
+            *fine, c, jobs, frame, mode, ema, delta_max, sample_cap, clears_fine, clears_coarse,
+            checking ? vals : nullptr, count, bad, zero0, n0, zero1, n1, zero2);
+    return check_launch(fn);
+}
+
+}  // namespace pf
+
+extern "C" {
 
 int pf_selftest_division(uint64_t seed, int64_t n, double base_voxel, int64_t *mismatches,
                          void *stream) {
