@@ -440,6 +440,103 @@ __global__ void __launch_bounds__(kThreads) resolve_fallback_kernel(ResolveArgs 
     stats_flush(bs, a.stats, false);
 }
 
+// Rungs 2-5 with the neighbourhood probes spread over the whole CTA: a pass takes
+// kPoolRows work rows (keys from fallback_keys_kernel), their 27 x kPoolRows cell
+// probes run 3-4 per thread back to back (independent loads in flight), the found
+// cells' effective values land in shared memory, and one thread per row then pools
+// them in (dx, dy, dz) order, runs the coarse rung and the ladder and composites.
+constexpr int kPoolRows = 32;
+constexpr int kPoolCells = 27 * kPoolRows;
+
+struct PoolSmem {
+    int64_t key[kPoolRows][8];
+    uint64_t word[kPoolCells][4];   // sum x3 (int64 or float64 bits), count (same dtype)
+    uint8_t found[kPoolCells];
+};
+
+__global__ void __launch_bounds__(kThreads) resolve_pool_kernel(ResolveArgs a) {
+    __shared__ BlockStats bs;
+    __shared__ PoolSmem ps;
+    stats_init(bs);
+    __syncthreads();
+    const pf_config &cfg = a.cfg;
+    const int mode = cfg.temporal_mode;
+    const bool as_int = eff_is_int(a.fine, mode);
+    const bool int_cnt = mode == PF_INTEGRATE;
+    const bool fixed = a.fine.sum_mode == PF_SUM_FIXED;
+    const uint64_t fmask = static_cast<uint64_t>(a.fine.capacity) - 1;
+    const int64_t n_work = *a.work_count;
+    for (int64_t base = static_cast<int64_t>(blockIdx.x) * kPoolRows; base < n_work;
+         base += static_cast<int64_t>(gridDim.x) * kPoolRows) {
+        const int rows = static_cast<int>(n_work - base < kPoolRows ? n_work - base : kPoolRows);
+        {  // stage the pass's key records (8 words per row)
+            const int r = threadIdx.x >> 3, k = threadIdx.x & 7;
+            if (r < rows) ps.key[r][k] = a.fb_keys[8 * (base + r) + k];
+        }
+        __syncthreads();
+        for (int p = threadIdx.x; p < 27 * rows; p += kThreads) {
+            const int r = p / 27, j = p - 27 * (p / 27);
+            const CellHash h = cell_hash(ps.key[r][0] + neighbour_dx(j), ps.key[r][1] + neighbour_dy(j),
+                                         ps.key[r][2] + neighbour_dz(j), ps.key[r][3],
+                                         static_cast<uint64_t>(ps.key[r][4]), 0, 0u);
+            const int64_t s = probe_lookup(a.fine.tags, fmask, a.fine.probe_limit, h.index, h.fp);
+            ps.found[p] = s >= 0;
+            if (s >= 0) {
+                const Effective e = fine_effective(a, s);
+#pragma unroll
+                for (int c = 0; c < 3; ++c)
+                    ps.word[p][c] = as_int ? static_cast<uint64_t>(e.isum[c])
+                                           : static_cast<uint64_t>(__double_as_longlong(e.fsum[c]));
+                ps.word[p][3] = int_cnt ? static_cast<uint64_t>(e.icnt)
+                                        : static_cast<uint64_t>(__double_as_longlong(e.fcnt));
+            }
+        }
+        __syncthreads();
+        if (threadIdx.x < rows) {
+            const int r = threadIdx.x;
+            const int64_t w = base + r;
+            const int64_t row = a.work[w];
+            Pool pool{{0, 0, 0}, 0, {0.0, 0.0, 0.0}, 0.0};
+            for (int j = 0; j < 27; ++j) {  // numpy's order for the float64 pools
+                const int p = 27 * r + j;
+                if (!ps.found[p]) continue;
+#pragma unroll
+                for (int c = 0; c < 3; ++c) {
+                    if (as_int) pool.isum[c] += static_cast<int64_t>(ps.word[p][c]);
+                    else pool.fsum[c] = dadd(pool.fsum[c], __longlong_as_double(ps.word[p][c]));
+                }
+                if (int_cnt) pool.icnt += static_cast<int64_t>(ps.word[p][3]);
+                else pool.fcnt = dadd(pool.fcnt, __longlong_as_double(ps.word[p][3]));
+            }
+            const bool ok_n = (int_cnt ? static_cast<double>(pool.icnt) : pool.fcnt) >= a.thr;
+            bool coarse_found = false;
+            Effective ce{};
+            if (!ok_n && a.has_coarse) {
+                const int64_t s = probe_lookup(a.coarse.tags, static_cast<uint64_t>(a.coarse.capacity) - 1,
+                                               a.coarse.probe_limit,
+                                               static_cast<uint64_t>(ps.key[r][5]),
+                                               static_cast<uint32_t>(ps.key[r][6]));
+                if (s >= 0) {
+                    coarse_found = true;
+                    ce = effective_at(a.coarse, s, mode, cfg.ema_alpha, cfg.delta_max);
+                }
+            }
+            double contrib[3], ch[3];
+#pragma unroll
+            for (int c = 0; c < 3; ++c) contrib[c] = __ldg(a.v.contribution + 3 * row + c);
+            const int src = ladder_choose(pool, as_int, mode, fixed, a.thr, coarse_found, ce,
+                                          eff_is_int(a.coarse, mode), contrib, ch);
+            const int64_t pixel = __ldg(a.v.pixel + row);
+            composite(a, row, pixel, ch, src);
+            if (!(pixel >= 0 && pixel < a.n_pixels)) atomicAdd(&bs.v[PF_STAT_BAD_PIXELS], 1u);
+            atomicAdd(&bs.v[PF_STAT_SOURCE_FINE + src], 1u);
+        }
+        __syncthreads();
+    }
+    __syncthreads();
+    stats_flush(bs, a.stats, false);
+}
+
 __global__ void __launch_bounds__(kThreads)
 finalize_image_kernel(const double *__restrict__ base, const double *__restrict__ flat,
                       double *__restrict__ image, int64_t n, double spp) {
@@ -559,10 +656,18 @@ int pf_resolve_frame(const pf_config *cfg, const pf_vertices *v, const pf_table 
             fallback_keys_kernel<<<static_cast<unsigned>(kb), kThreads, 0, st>>>(a);
             if (int rc = check_launch(fn)) return rc;
         }
-        int64_t fb_blocks = (v->n + kWarps - 1) / kWarps;
-        const int64_t cap = static_cast<int64_t>(sm_count()) * 8;
-        if (fb_blocks > cap) fb_blocks = cap;
-        resolve_fallback_kernel<<<static_cast<unsigned>(fb_blocks), kThreads, 0, st>>>(a);
+        if (fallback_keys != nullptr) {
+            static const int per_sm_pool = resident_blocks(resolve_pool_kernel, kThreads);
+            int64_t pb = (v->n + kPoolRows - 1) / kPoolRows;
+            const int64_t pcap = static_cast<int64_t>(sm_count()) * per_sm_pool;
+            if (pb > pcap) pb = pcap;
+            resolve_pool_kernel<<<static_cast<unsigned>(pb), kThreads, 0, st>>>(a);
+        } else {
+            int64_t fb_blocks = (v->n + kWarps - 1) / kWarps;
+            const int64_t cap = static_cast<int64_t>(sm_count()) * 8;
+            if (fb_blocks > cap) fb_blocks = cap;
+            resolve_fallback_kernel<<<static_cast<unsigned>(fb_blocks), kThreads, 0, st>>>(a);
+        }
         if (int rc = check_launch(fn)) return rc;
     }
     const int64_t m = 3 * n_pixels;
