@@ -295,7 +295,12 @@ def run_b200(args):
     world = _env_int("WORLD_SIZE", 1)
     local = _env_int("LOCAL_RANK", 0)
     if world > 1:
-        dist.init_process_group("nccl")
+        # PF_BENCH_BACKEND=gloo + PF_BENCH_ONE_DEVICE=1: exercise the N-rank code path on a
+        # single GPU (exchanges through host memory, no kernel waits on another rank);
+        # numbers from such a run are not multi-GPU measurements
+        dist.init_process_group(os.environ.get("PF_BENCH_BACKEND", "nccl"))
+    if os.environ.get("PF_BENCH_ONE_DEVICE") == "1":
+        local = 0
     torch.cuda.set_device(local)
 
     import __graft_entry__
