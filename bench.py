@@ -319,7 +319,7 @@ def run_b200(args):
     n_pix = W_PIX * H_PIX
     if world > 1:
         from paper_1902_05942_b200 import sharded
-        state = sharded.ShardedState(cfg, rank, world, agg_capacity=1 << 21)
+        state = sharded.ShardedState(cfg, rank, world, agg_capacity=1 << 20)
     else:
         state = pf.FrameState.from_config(cfg)
 
@@ -456,7 +456,7 @@ def run_e2e(pf, rng, cfg, stream, base, args, n, rank=0, world=1):
               "layer_id": torch.zeros_like(stream["pixel"])}
     if world > 1:
         from paper_1902_05942_b200 import sharded
-        state = sharded.ShardedState(cfg, rank, world, agg_capacity=1 << 21)
+        state = sharded.ShardedState(cfg, rank, world, agg_capacity=1 << 20)
         himg = himg[: himg.shape[0] // world]
     else:
         state = pf.FrameState.from_config(cfg)

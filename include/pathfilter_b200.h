@@ -286,6 +286,7 @@ typedef struct pf_shard {
     int64_t *owner_cursor;          /* [2][world] emit cursors */
     int32_t *vertex_slot;           /* [n] aggregation slot of each vertex's fine lookup */
     int32_t *work_slot;             /* [n][28] slots of each work row's 27 neighbour + coarse lookups */
+    int64_t *row_keys;              /* [n][8] each work row's lookup key + coarse hash (scratch) */
 } pf_shard;
 
 /* Round 1 keys: every vertex's fine and coarse keys (jitter stream 2) are

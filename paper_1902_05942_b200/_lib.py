@@ -106,7 +106,8 @@ class PfShard(ctypes.Structure):
                 ("agg_capacity", ctypes.c_int64), ("distinct", ctypes.c_void_p),
                 ("n_distinct", ctypes.c_void_p), ("overflow", ctypes.c_void_p),
                 ("owner_counts", ctypes.c_void_p), ("owner_cursor", ctypes.c_void_p),
-                ("vertex_slot", ctypes.c_void_p), ("work_slot", ctypes.c_void_p)]
+                ("vertex_slot", ctypes.c_void_p), ("work_slot", ctypes.c_void_p),
+                ("row_keys", ctypes.c_void_p)]
 
 
 class PfScene(ctypes.Structure):

@@ -420,9 +420,47 @@ shard_resolve_kernel(ShardK k, pf_config cfg, pf_vertices v, const ulonglong4 *a
     stats_flush(bs, stats, false);
 }
 
-// One work row per warp.  Lanes 0 and 1 build the row's fine lookup key and coarse
-// key side by side (same instructions, different stream/level), lanes 0..26 hash
-// the neighbourhood cells and lane 27 carries the coarse cell.
+// Each work row's lookup key (stream 3) and coarse hash, one row per thread (the FP64
+// key recipe SIMT-wide); record: q0, q1, q2, level, aux, coarse index, coarse fp, 0.
+__global__ void __launch_bounds__(kT)
+shard_row_keys_kernel(pf_config cfg, pf_vertices v, ShardK k, int has_coarse, uint64_t h0_lookup,
+                      uint64_t h0_coarse, const int64_t *work, const int64_t *work_count) {
+    __shared__ double2 sincos_tab[220];
+    stage_sincos_table(sincos_tab);
+    __syncthreads();
+    const int64_t n_work = *work_count;
+    for (int64_t w = static_cast<int64_t>(blockIdx.x) * kT + threadIdx.x; w < n_work;
+         w += static_cast<int64_t>(gridDim.x) * kT) {
+        const int64_t row = work[w];
+        const VertexIn x = load_vertex(v, row, cfg);
+        const KeyShared ks = key_shared(cfg, x);
+        double du = 0.0, dv = 0.0, cdu = 0.0, cdv = 0.0;
+        if (cfg.jitter) {  // the coarse key shares the lookup draws when jitter is on
+            double u1, u2;
+            jitter_draws(h0_lookup, x.pixel, x.sample, u1, u2);
+            disc_offset(u1, u2, du, dv, sincos_tab);
+            cdu = du;
+            cdv = dv;
+            if (h0_coarse != h0_lookup) {
+                jitter_draws(h0_coarse, x.pixel, x.sample, u1, u2);
+                disc_offset(u1, u2, cdu, cdv, sincos_tab);
+            }
+        }
+        double jt[3];
+        const CellKey lk = make_key(cfg, x, ks, cfg.jitter, du, dv, 0, jt);
+        CellHash hc{0ull, 0u};
+        if (has_coarse)
+            hc = key_hash(make_key(cfg, x, ks, cfg.jitter, cdu, cdv, cfg.coarse_delta, jt), ks);
+        longlong4 *o = reinterpret_cast<longlong4 *>(k.s.row_keys + 8 * w);
+        o[0] = make_longlong4(lk.q[0], lk.q[1], lk.q[2], lk.level);
+        o[1] = make_longlong4(static_cast<long long>(lk.aux), static_cast<long long>(hc.index),
+                              static_cast<long long>(hc.fp), 0);
+    }
+}
+
+// One work row per warp: lanes 0..26 hash the neighbourhood cells of the row's lookup key
+// (shard_row_keys_kernel) and lane 27 carries the coarse cell; all 28 go into the
+// aggregation table as deduplicated requests.
 __global__ void __launch_bounds__(kT)
 shard_fallback_keys_kernel(pf_config cfg, pf_vertices v, ShardK k, int has_coarse,
                            uint64_t h0_lookup, uint64_t h0_coarse, const int64_t *work,
@@ -435,18 +473,14 @@ shard_fallback_keys_kernel(pf_config cfg, pf_vertices v, ShardK k, int has_coars
     const int64_t nwarps = static_cast<int64_t>(gridDim.x) * kTW;
     for (int64_t w = static_cast<int64_t>(blockIdx.x) * kTW + (threadIdx.x >> 5); w < n_work;
          w += nwarps) {
-        const int64_t row = work[w];
-        KeyAndHash kh{};
-        if (lane < 2)
-            kh = vertex_key(cfg, v, lane == 0 ? h0_lookup : h0_coarse, row,
-                            lane == 0 ? 0 : cfg.coarse_delta);
-        const long long q0 = __shfl_sync(kFull, static_cast<long long>(kh.first.q[0]), 0);
-        const long long q1 = __shfl_sync(kFull, static_cast<long long>(kh.first.q[1]), 0);
-        const long long q2 = __shfl_sync(kFull, static_cast<long long>(kh.first.q[2]), 0);
-        const long long lev = __shfl_sync(kFull, static_cast<long long>(kh.first.level), 0);
-        const unsigned long long aux = __shfl_sync(kFull, static_cast<unsigned long long>(kh.first.aux), 0);
-        const unsigned long long cidx = __shfl_sync(kFull, static_cast<unsigned long long>(kh.second.index), 1);
-        const unsigned cfp = __shfl_sync(kFull, kh.second.fp, 1);
+        const long long rec = lane < 8 ? k.s.row_keys[8 * w + lane] : 0;
+        const long long q0 = __shfl_sync(kFull, rec, 0);
+        const long long q1 = __shfl_sync(kFull, rec, 1);
+        const long long q2 = __shfl_sync(kFull, rec, 2);
+        const long long lev = __shfl_sync(kFull, rec, 3);
+        const unsigned long long aux = static_cast<unsigned long long>(__shfl_sync(kFull, rec, 4));
+        const unsigned long long cidx = static_cast<unsigned long long>(__shfl_sync(kFull, rec, 5));
+        const unsigned cfp = static_cast<unsigned>(__shfl_sync(kFull, rec, 6));
         uint64_t key = kAggEmpty;
         bool valid = false;
         if (lane < 27) {
@@ -699,7 +733,14 @@ int pf_shard_fallback_keys(const pf_config *cfg, const pf_vertices *v, const pf_
     pf_config kc;
     if (int rc = prepare_config(fn, cfg, &kc)) return rc;
     if (v->n == 0) return PF_OK;
-    if (!work || !work_count || !sh->work_slot) return fail_arg(fn, "work/work_slot is NULL");
+    if (!work || !work_count || !sh->work_slot || !sh->row_keys)
+        return fail_arg(fn, "work/work_slot/row_keys is NULL");
+    int64_t kb = (v->n + kT - 1) / kT;
+    const int64_t kcap = static_cast<int64_t>(sm_count()) * 4;
+    if (kb > kcap) kb = kcap;
+    shard_row_keys_kernel<<<static_cast<unsigned>(kb), kT, 0, as_stream(stream)>>>(
+        kc, *v, k, has_coarse != 0, stream_base_lookup, stream_base_coarse, work, work_count);
+    if (int rc = check_launch(fn)) return rc;
     int64_t blocks = (v->n + kTW - 1) / kTW;
     const int64_t cap = static_cast<int64_t>(sm_count()) * 8;
     if (blocks > cap) blocks = cap;

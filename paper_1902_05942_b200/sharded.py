@@ -98,6 +98,7 @@ class ShardedState:
         self._alloc_agg(_next_pow2(max(int(agg_capacity), 64)))
         self.vertex_slot = torch.empty(0, dtype=torch.int32, device=dev)
         self.work_slot = torch.empty(0, dtype=torch.int32, device=dev)
+        self.row_keys = torch.empty(0, dtype=torch.int64, device=dev)
         self.scratch: dict = {}
         self.regrows = 0
 
@@ -133,6 +134,7 @@ class ShardedState:
         if self.vertex_slot.numel() < n:
             self.vertex_slot = torch.empty(n, dtype=torch.int32, device=self._dev)
             self.work_slot = torch.empty((n, WORK_KEYS), dtype=torch.int32, device=self._dev)
+            self.row_keys = torch.empty((n, 8), dtype=torch.int64, device=self._dev)
 
     def c_shard(self, pixel_base: int) -> _lib.PfShard:
         s = _lib.PfShard()
@@ -147,6 +149,7 @@ class ShardedState:
         s.owner_counts, s.owner_cursor = self.owner_counts.data_ptr(), self.owner_cursor.data_ptr()
         s.vertex_slot = self.vertex_slot.data_ptr()
         s.work_slot = self.work_slot.data_ptr()
+        s.row_keys = self.row_keys.data_ptr()
         return s
 
 

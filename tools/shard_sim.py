@@ -26,6 +26,7 @@ def main():
     ap.add_argument("--frames", type=int, default=5)
     ap.add_argument("--width", type=int, default=1920)
     ap.add_argument("--height", type=int, default=1080)
+    ap.add_argument("--stream", default="traced", choices=["traced", "synthetic"])
     args = ap.parse_args()
     import torch
     import __graft_entry__
@@ -38,7 +39,7 @@ def main():
     cap = 1 << (2 * W * H - 1).bit_length()
     cfg = pf.FilterConfig(capacity=cap, footprint_scale=camera_footprint(H))
     base = closed_box_stream(W, H, 1, 1)[1]
-    out = {"workload": f"{W}x{H} 4 bounces per rank", "capacity": cap}
+    out = {"workload": f"{W}x{H} 4 bounces per rank ({args.stream})", "capacity": cap}
 
     def timed(fn, frames):
         for f in range(2):
@@ -53,20 +54,25 @@ def main():
         torch.cuda.synchronize()
         return s.elapsed_time(e) / frames, (time.perf_counter() - t0) * 1e3 / frames
 
-    s0, _ = closed_box_stream(W, H, 4, 1)
-    vs0 = pf.VertexStream(**s0)
+    from paper_1902_05942_b200.scene import closed_box
+    from paper_1902_05942_b200.tracer import multi_bounce_stream
+
+    def rank_stream(r):
+        if args.stream == "synthetic":
+            s, _ = closed_box_stream(W, H, 4, 1 + r)
+            s["sample"] = s["sample"] + 4 * r
+            return pf.VertexStream(**s)
+        return multi_bounce_stream(closed_box(W, H), 4, 1, sample_offset=4 * r)[0]
+
+    vs0 = rank_stream(0)
     st0 = pf.FrameState.from_config(cfg)
     ms, wall = timed(lambda f: pf.filter_frame(vs0, base, cfg, st0, 1, rng.frame_seed(1, f),
                                                want_means=False), args.frames)
     out["fused_single_ms"] = ms
     del st0
     for G in [int(x) for x in args.worlds.split(",")]:
-        streams = []
-        for r in range(G):
-            s, _ = closed_box_stream(W, H, 4, 1 + r)
-            s["sample"] = s["sample"] + 4 * r
-            streams.append(pf.VertexStream(**s))
-        states = [sharded.ShardedState(cfg, r, G, agg_capacity=1 << 21) for r in range(G)]
+        streams = [rank_stream(r) for r in range(G)]
+        states = [sharded.ShardedState(cfg, r, G, agg_capacity=1 << 20) for r in range(G)]
 
         def frame(f):
             sharded.run_loopback([sharded.filter_frame_sharded(
