@@ -15,9 +15,9 @@ begin_frame on both tables, accumulate_phase (keys + insert), resolve_phase
 Prints ONE JSON line (rank 0).  N>1 (torchrun, NCCL) runs the key-sharded frame
 (paper_1902_05942_b200/sharded.py): rank r traces its own sample of every
 pixel (1 spp per GPU, spp = N for the image), the global fine/coarse tables of
-capacity 2^22 are split into N owner slices, records / lookups / answers move by
-all-to-all and the flat image by reduce-scatter.  Weak scaling: 8.29 M vertices per
-GPU per frame.
+capacity 2^22 are split into N owner slices, pre-aggregated records move by
+all-to-all, the owners' cells by all-gather into a per-rank replica, and the flat
+image by reduce-scatter.  Weak scaling: 8.18 M vertices per GPU per frame.
 """
 
 from __future__ import annotations
@@ -325,7 +325,7 @@ def run_b200(args):
 
     ev = lambda: torch.cuda.Event(enable_timing=True)  # noqa: E731
     phases = ({"begin_check": [], "insert": [], "resolve": []} if world == 1 else
-              {"begin_keys": [], "exchange_apply_rung1": [], "fallback_image": []})
+              {"begin_keys": [], "exchange_apply_publish": [], "resolve_image": []})
 
     def step(f, timing=None):
         # one frame = ONE pf_filter_frame call; its phase events (recorded inside the C
@@ -414,10 +414,11 @@ def run_b200(args):
                          f"fine+coarse), best of 2 frames, backend={setup['backend']}"}
 
     if rank == 0:
-        # single: begin x2, check, insert, effective records, resolve main, fallback,
-        # finalize.  sharded: begin x2, check, keys, emit, apply, answer, resolve, reset,
-        # fallback keys, emit, answer, ladder, reset, finalize (NCCL kernels not counted)
-        launches = (8 if world == 1 else 15) * args.steps
+        # single: prologue, insert, effective records, resolve main, fallback keys, pool,
+        # finalize.  sharded: begin x2, check, keys, emit, apply, reset, publish x2,
+        # replica clear + write, resolve main, fallback keys, pool, finalize (NCCL kernels
+        # not counted)
+        launches = (7 if world == 1 else 15) * args.steps
         line = {
             "metric": METRIC, "value": value, "unit": "vertices/s", "n_gpus": world,
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms_per_step,

@@ -247,58 +247,63 @@ int pf_finalize_image(const double *base_image, const double *flat, double *imag
 /* ---- 3. key-sharded multi-GPU frame --------------------------------
  * G ranks (one per GPU, G a power of two <= 64) hold the global fine and coarse
  * tables of capacity C = 2^log2_capacity as G contiguous slices of S = C/G home
- * slots: owner(home) = home >> (log2 C - log2 G), so home slots and probe order are
- * the single-GPU table's.  The owner keeps its slice in a local pf_table of capacity
- * 2S (C when G == 1) indexed by home - rank*S: a probe chain that would leave the
- * slice continues in the slice's private tail instead of the next owner's slots.
+ * slots: owner(home) = home >> (log2 C - log2 G).  The owner keeps its slice in a local
+ * pf_table of capacity S indexed by home - rank*S; probe windows wrap within the slice
+ * (with G == 1 this is exactly the single-GPU table).
  *
- * One frame, per rank (the exchanges are the caller's all-to-alls, e.g. NCCL):
- *   pf_begin_frame (both local tables) ; pf_shard_keys ; pf_shard_emit
- *   -> all-to-all records (int64[5]) and requests (uint64)
- *   pf_shard_apply(records) ; pf_shard_answer(requests) -> all-to-all answers back
- *   pf_shard_resolve(answers) ; pf_shard_reset ; pf_shard_fallback_keys ; pf_shard_emit
- *   -> all-to-all requests ; pf_shard_answer -> all-to-all answers back
- *   pf_shard_ladder(answers) ; pf_finalize_image ; pf_shard_reset
+ * One frame, per rank (the exchanges are the caller's collectives, e.g. NCCL):
+ *   pf_begin_frame (both local slices) ; pf_shard_keys ; pf_shard_emit
+ *   -> all-to-all of the records (int64[5]) ; pf_shard_apply ; pf_shard_reset
+ *   pf_shard_publish -> all-gather of the entries (uint64[6]) into a replica of the
+ *   whole table ; pf_replica_update (clear last frame's entries, write this frame's)
+ *   pf_resolve_replica (the single-GPU resolve against the replica) ; pf_finalize_image
  * Every rank pre-aggregates its vertices per distinct key before sending (fixed-point
- * sums are exactly associative) and deduplicates its lookups, so the exchanges carry
- * one record per distinct key per rank, not one per vertex.
+ * sums are exactly associative), so the record exchange carries one record per
+ * distinct key per rank; the published entries are the occupied cells only.
  *
  * Aggregation table key: kind << 61 | home << 32 | fingerprint (home < 2^29), EMPTY
- * = ~0.  kinds: 0 fine record, 1 coarse record, 2 fine lookup, 3 neighbourhood lookup
- * (fine table), 4 coarse lookup.  Wire formats: record = int64[5] {key, sum[3],
- * weight} with sums in the table's sum_mode; request = uint64 key; answer =
- * uint64[4] {sum[3] (int64 or float64 bits, as VoxelTable.effective), count as
- * float64 bits, or all ones when the cell is absent}. */
+ * = ~0; kinds 0 fine record, 1 coarse record.  Record = int64[5] {key, sum[3], weight}
+ * with sums in the tables' sum_mode.  Entry = uint64[6] {global slot | coarse << 62,
+ * tag, effective sum[3] (int64 or float64 bits, as VoxelTable.effective), effective
+ * count as float64 bits}. */
 typedef struct pf_shard {
     int32_t rank;
     int32_t world;                  /* power of two, <= 64 */
     int32_t log2_capacity;          /* global C of both tables, C >= world, <= 2^29 */
     int32_t sum_mode;               /* pf_sum_mode of both tables */
-    int64_t pixel_base;             /* first pixel id of this rank's image band */
     uint64_t *agg_keys;             /* [agg_capacity], EMPTY = ~0 */
     int64_t *agg_sums;              /* [agg_capacity][3] */
-    int64_t *agg_counts;            /* [agg_capacity] weight (records) / send position (lookups) */
+    int64_t *agg_counts;            /* [agg_capacity] record weights */
     int64_t agg_capacity;           /* power of two >= 64; at most agg_capacity/2 keys a round */
     int32_t *distinct;              /* [agg_capacity/2] claimed slots in claim order (-1 hole) */
     int64_t *n_distinct;            /* [1] slot reservations of the current round */
     int32_t *overflow;              /* [1] set when a round needed more than agg_capacity/2 keys */
-    int64_t *owner_counts;          /* [2][world] keys per owner: records, requests */
+    int64_t *owner_counts;          /* [2][world] records per owner (row 1 unused) */
     int64_t *owner_cursor;          /* [2][world] emit cursors */
-    int32_t *vertex_slot;           /* [n] aggregation slot of each vertex's fine lookup */
-    int32_t *work_slot;             /* [n][28] slots of each work row's 27 neighbour + coarse lookups */
-    int64_t *row_keys;              /* [n][8] each work row's lookup key + coarse hash (scratch) */
 } pf_shard;
 
-/* Round 1 keys: every vertex's fine and coarse keys (jitter stream 2) are
- * pre-aggregated as records, its fine lookup key (stream 3) deduplicated as a request.
- * abort_flag as in pf_insert_frame. */
+/* Read-only replica of the global tables for the resolve (device arrays of C slots). */
+typedef struct pf_replica {
+    uint64_t *fine_tags;            /* [C] EMPTY where no owner published a cell */
+    uint64_t *fine_records;         /* [C][4] effective records */
+    uint64_t *coarse_tags;          /* [C] or NULL (no coarse table) */
+    uint64_t *coarse_records;
+    int64_t capacity;               /* C */
+    int32_t slice_log2;             /* log2(C / world): probe windows wrap within slices */
+    int32_t probe_limit;
+    int32_t sum_mode;
+    int32_t pad0;
+} pf_replica;
+
+/* Keys of every local vertex: the fine and coarse keys (jitter stream 2) go into the
+ * aggregation table as records, the fine lookup key (stream 3) to lookup_index /
+ * lookup_fp (n each) for pf_resolve_replica.  abort_flag as in pf_insert_frame. */
 int pf_shard_keys(const pf_config *cfg, const pf_vertices *v, const pf_shard *sh,
                   int32_t has_coarse, uint64_t stream_base_accum, uint64_t stream_base_lookup,
-                  const int32_t *abort_flag, void *stream);
-/* Write the round's records (kinds 0-1) and requests (kinds 2-4) grouped by owner:
- * owner o's records start at row sum(owner_counts[0][:o]) of send_records, its
- * requests at sum(owner_counts[1][:o]) of send_requests.  Each request's position is
- * remembered for the answers.  No-op when overflow is set. */
+                  const int32_t *abort_flag, uint64_t *lookup_index, uint32_t *lookup_fp,
+                  void *stream);
+/* Write the round's records grouped by owner: owner o's records start at row
+ * sum(owner_counts[0][:o]) of send_records.  No-op when overflow is set. */
 int pf_shard_emit(const pf_shard *sh, int64_t *send_records, uint64_t *send_requests,
                   void *stream);
 /* Owner side: insert received records into the local slices (warp-merged, weighted),
@@ -306,29 +311,27 @@ int pf_shard_emit(const pf_shard *sh, int64_t *send_records, uint64_t *send_requ
 int pf_shard_apply(const pf_shard *sh, const pf_table *fine, const pf_table *coarse,
                    const int64_t *records, int64_t n_records, int64_t frame, int64_t *stats,
                    void *stream);
-/* Owner side: answer received requests with the effective (sum, count) of the cell. */
-int pf_shard_answer(const pf_shard *sh, const pf_config *cfg, const pf_table *fine,
-                    const pf_table *coarse, const uint64_t *requests, int64_t n_requests,
-                    uint64_t *answers, int64_t *stats, void *stream);
-/* Fine rung from the answers to this rank's round-1 requests; rows below the
- * threshold go to the work list.  flat holds this rank's pixels [pixel_base,
- * pixel_base + n_pixels). */
-int pf_shard_resolve(const pf_shard *sh, const pf_config *cfg, const pf_vertices *v,
-                     const uint64_t *answers, double *flat, int64_t n_pixels, int64_t *work,
-                     int64_t *work_count, uint8_t *source, double *chosen, int64_t *stats,
-                     void *stream);
-/* Round 2 keys: the 27 neighbourhood cells and the coarse cell of every work row. */
-int pf_shard_fallback_keys(const pf_config *cfg, const pf_vertices *v, const pf_shard *sh,
-                           int32_t has_coarse, uint64_t stream_base_lookup,
-                           uint64_t stream_base_coarse, const int64_t *work,
-                           const int64_t *work_count, void *stream);
-/* Rungs 2-5 and the composite of every work row from the round-2 answers. */
-int pf_shard_ladder(const pf_shard *sh, const pf_config *cfg, const pf_vertices *v,
-                    int32_t has_coarse, const uint64_t *answers, const int64_t *work,
-                    const int64_t *work_count, double *flat, int64_t n_pixels, uint8_t *source,
-                    double *chosen, int64_t *stats, void *stream);
+/* Owner side: one entry per occupied local slot of both slices into `entries`
+ * (capacity: occupied slots), their number into *count. */
+int pf_shard_publish(const pf_shard *sh, const pf_config *cfg, const pf_table *fine,
+                     const pf_table *coarse, uint64_t *entries, int64_t *count, void *stream);
+/* Apply all-gathered entries to a replica: rank r's entries are rows
+ * [r * stride, r * stride + counts[r]) of `entries` (counts: device int64[world]);
+ * clear != 0 empties their slots instead (last frame's entries). */
+int pf_replica_update(const pf_replica *replica, const uint64_t *entries, const int64_t *counts,
+                      int32_t world, int64_t stride, int32_t clear, void *stream);
 /* Empty the aggregation table (only the slots this round claimed) and its counters. */
 int pf_shard_reset(const pf_shard *sh, void *stream);
+/* resolve_phase (src/pipeline.py:207-283) of this rank's vertices against a replica:
+ * the fine rung from lookup_index / lookup_fp (pf_shard_keys), the neighbourhood and
+ * coarse rungs, the ladder, the composite into flat (pixels [pixel_base, pixel_base +
+ * n_pixels), zeroed here).  work: n int64, fallback_keys: 8 * n int64 scratch. */
+int pf_resolve_replica(const pf_config *cfg, const pf_vertices *v, const pf_replica *replica,
+                       uint64_t stream_base_lookup, uint64_t stream_base_coarse,
+                       const uint64_t *lookup_index, const uint32_t *lookup_fp, double *flat,
+                       int64_t n_pixels, int64_t pixel_base, int64_t *work,
+                       int64_t *work_count, int64_t *fallback_keys, uint8_t *source,
+                       double *chosen, int64_t *stats, void *stream);
 
 /* ---- 4. phase one: the path tracer that produces the vertex stream ----
  * src/tracer.py:211-383 (_walk) with src/_native.pyx:83-167 (intersect_closest/any):

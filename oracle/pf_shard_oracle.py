@@ -3,13 +3,14 @@ over the sequential CPU oracle (oracle/pf_oracle.py).  Never imported by the pro
 
 `ShardedTable` stands in for one global VoxelTable (src/table.py:80-340) of capacity C
 but stores it as G owner slices: owner(home) = home >> (log2 C - log2 G), each owner a
-plain oracle Table of capacity 2S (S = C/G; C when G == 1) addressed by home - owner*S,
-so a probe chain never leaves its owner.  Feeding oracle.filter_frame a State of
+plain oracle Table of capacity S = C/G addressed by home - owner*S, whose probe windows
+wrap within the slice, so a probe chain never leaves its owner.  Feeding oracle.filter_frame a State of
 ShardedTables shows on the reference's own fixtures that the partition the GPU ranks
 use (paper_1902_05942_b200/sharded.py) leaves every per-key sum, count, source and
 mean of src/pipeline.py:152-283 unchanged.
 
-Slot ids seen by the pipeline are owner * 2S + local slot.
+Slot ids seen by the pipeline are owner * S + local slot (the global slot when no
+chain wraps).
 """
 
 from __future__ import annotations
@@ -27,7 +28,7 @@ class ShardedTable:
         self.capacity = capacity
         self.world = world
         self.slice = capacity // world
-        self.local = capacity if world == 1 else 2 * self.slice
+        self.local = self.slice
         self.shift = (capacity.bit_length() - 1) - (world.bit_length() - 1)
         self.sum_mode = sum_mode
         self.owners = [Table(self.local, probe_limit, sum_mode, evict_horizon, evict_min_age)

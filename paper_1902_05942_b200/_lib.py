@@ -32,8 +32,8 @@ EXPORTS = ("pf_abi_version", "pf_last_error", "pf_device_sm_count", "pf_accumula
            "pf_effective",
            "pf_begin_frame", "pf_check_contributions", "pf_selftest_division",
            "pf_count_occupied", "pf_finalize_image", "pf_shard_keys", "pf_shard_emit",
-           "pf_shard_apply", "pf_shard_answer", "pf_shard_resolve", "pf_shard_fallback_keys",
-           "pf_shard_ladder", "pf_shard_reset", "pf_trace_paths", "pf_sincos", "pf_segment_deltas")
+           "pf_shard_apply", "pf_shard_publish", "pf_replica_update", "pf_shard_reset",
+           "pf_resolve_replica", "pf_trace_paths", "pf_sincos", "pf_segment_deltas")
 
 
 def build(force: bool = False, verbose: bool = False) -> str:
@@ -101,13 +101,19 @@ class PfFrameBuffers(ctypes.Structure):
 class PfShard(ctypes.Structure):
     _fields_ = [("rank", ctypes.c_int32), ("world", ctypes.c_int32),
                 ("log2_capacity", ctypes.c_int32), ("sum_mode", ctypes.c_int32),
-                ("pixel_base", ctypes.c_int64), ("agg_keys", ctypes.c_void_p),
-                ("agg_sums", ctypes.c_void_p), ("agg_counts", ctypes.c_void_p),
-                ("agg_capacity", ctypes.c_int64), ("distinct", ctypes.c_void_p),
-                ("n_distinct", ctypes.c_void_p), ("overflow", ctypes.c_void_p),
-                ("owner_counts", ctypes.c_void_p), ("owner_cursor", ctypes.c_void_p),
-                ("vertex_slot", ctypes.c_void_p), ("work_slot", ctypes.c_void_p),
-                ("row_keys", ctypes.c_void_p)]
+                ("agg_keys", ctypes.c_void_p), ("agg_sums", ctypes.c_void_p),
+                ("agg_counts", ctypes.c_void_p), ("agg_capacity", ctypes.c_int64),
+                ("distinct", ctypes.c_void_p), ("n_distinct", ctypes.c_void_p),
+                ("overflow", ctypes.c_void_p), ("owner_counts", ctypes.c_void_p),
+                ("owner_cursor", ctypes.c_void_p)]
+
+
+class PfReplica(ctypes.Structure):
+    _fields_ = [("fine_tags", ctypes.c_void_p), ("fine_records", ctypes.c_void_p),
+                ("coarse_tags", ctypes.c_void_p), ("coarse_records", ctypes.c_void_p),
+                ("capacity", ctypes.c_int64), ("slice_log2", ctypes.c_int32),
+                ("probe_limit", ctypes.c_int32), ("sum_mode", ctypes.c_int32),
+                ("pad0", ctypes.c_int32)]
 
 
 class PfScene(ctypes.Structure):
@@ -198,13 +204,13 @@ def lib() -> ctypes.CDLL:
     L.pf_check_contributions.argtypes = [vp, i64, vp, vp]
     L.pf_selftest_division.argtypes = [u64, i64, dbl, vp, vp]
     L.pf_finalize_image.argtypes = [vp, vp, vp, i64, i64, vp]
-    L.pf_shard_keys.argtypes = [vp, vp, vp, i32, u64, u64, vp, vp]
+    L.pf_shard_keys.argtypes = [vp, vp, vp, i32, u64, u64, vp, vp, vp, vp]
     L.pf_shard_emit.argtypes = [vp, vp, vp, vp]
     L.pf_shard_apply.argtypes = [vp, vp, vp, vp, i64, i64, vp, vp]
-    L.pf_shard_answer.argtypes = [vp, vp, vp, vp, vp, i64, vp, vp, vp]
-    L.pf_shard_resolve.argtypes = [vp, vp, vp, vp, vp, i64, vp, vp, vp, vp, vp, vp]
-    L.pf_shard_fallback_keys.argtypes = [vp, vp, vp, i32, u64, u64, vp, vp, vp]
-    L.pf_shard_ladder.argtypes = [vp, vp, vp, i32, vp, vp, vp, vp, i64, vp, vp, vp, vp]
+    L.pf_shard_publish.argtypes = [vp, vp, vp, vp, vp, vp, vp]
+    L.pf_replica_update.argtypes = [vp, vp, vp, i32, i64, i32, vp]
+    L.pf_resolve_replica.argtypes = [vp, vp, vp, u64, u64, vp, vp, vp, i64, i64, vp, vp, vp, vp,
+                                     vp, vp, vp]
     L.pf_shard_reset.argtypes = [vp, vp]
     L.pf_trace_paths.argtypes = [vp, vp, u64, vp, vp, i64, vp, vp]
     L.pf_sincos.argtypes = [vp, i64, vp, vp, vp]

@@ -172,9 +172,19 @@ struct ResolveArgs {
     const uint64_t *lk_index;  // precomputed lookup keys (or NULL)
     const uint32_t *lk_fp;
     const ulonglong4 *rec;     // per-slot effective records of the fine table (or NULL)
-    int64_t n_pixels;          // flat holds pixels [0, n_pixels)
+    int64_t n_pixels;          // flat holds pixels [pixel_base, pixel_base + n_pixels)
     int64_t *fb_keys;          // [work row][8] lookup key + coarse hash (or NULL)
+    int64_t pixel_base;        // first pixel of flat (0 unless a rank composites a band)
+    uint64_t seg_mask;         // probe-window segment (~0: plain table; replica: slice - 1)
+    const ulonglong4 *crec;    // per-slot effective records of the coarse table (or NULL)
 };
+
+// The coarse table's effective value of slot s.
+__device__ __forceinline__ Effective coarse_effective(const ResolveArgs &a, int64_t s) {
+    const int mode = a.cfg.temporal_mode;
+    if (a.crec != nullptr) return unpack_effective(load_record(a.crec, s), eff_is_int(a.coarse, mode));
+    return effective_at(a.coarse, s, mode, a.cfg.ema_alpha, a.cfg.delta_max);
+}
 
 // The fine table's effective value of slot s: its record when the effective pass ran.
 __device__ __forceinline__ Effective fine_effective(const ResolveArgs &a, int64_t s) {
@@ -204,6 +214,7 @@ __device__ __forceinline__ KeyAndHash lookup_key(const ResolveArgs &a, int64_t r
 
 __device__ __forceinline__ void composite(const ResolveArgs &a, int64_t i, int64_t pixel,
                                           const double chosen[3], int source) {
+    pixel -= a.pixel_base;
     const uint64_t stream = l2_evict_first(), keep = l2_evict_last();
     if (pixel >= 0 && pixel < a.n_pixels) {
 #pragma unroll
@@ -257,7 +268,8 @@ __global__ void __launch_bounds__(kThreads) resolve_main_kernel(ResolveArgs a) {
         // first probe from the prefetched home tag; longer chains are rare
         if (tag[k] == kEmptyTag) slot[k] = -1;
         else if ((tag[k] & kFpMask) == h[k].fp) slot[k] = static_cast<int64_t>(h[k].index & fmask);
-        else slot[k] = probe_lookup(a.fine.tags, fmask, a.fine.probe_limit, h[k].index, h[k].fp);
+        else slot[k] = probe_lookup(a.fine.tags, fmask, a.fine.probe_limit, h[k].index, h[k].fp,
+                                    a.seg_mask);
     }
     Effective ef[KV];
     int64_t pixel[KV];
@@ -265,7 +277,7 @@ __global__ void __launch_bounds__(kThreads) resolve_main_kernel(ResolveArgs a) {
 #pragma unroll
     for (int k = 0; k < KV; ++k) {
         if (slot[k] >= 0) ef[k] = fine_effective(a, slot[k]);
-        pixel[k] = ld_stream(a.v.pixel + row[k], stream);
+        pixel[k] = ld_stream(a.v.pixel + row[k], stream) - a.pixel_base;
 #pragma unroll
         for (int c = 0; c < 3; ++c) tp[k][c] = ld_stream(a.v.throughput + 3 * row[k] + c, stream);
     }
@@ -397,7 +409,8 @@ __global__ void __launch_bounds__(kThreads) resolve_fallback_kernel(ResolveArgs 
             const CellHash h = cell_hash(kq[0] + neighbour_dx(lane), kq[1] + neighbour_dy(lane),
                                          kq[2] + neighbour_dz(lane), klev,
                                          static_cast<uint64_t>(kaux), 0, 0u);
-            const int64_t s = probe_lookup(a.fine.tags, fmask, a.fine.probe_limit, h.index, h.fp);
+            const int64_t s = probe_lookup(a.fine.tags, fmask, a.fine.probe_limit, h.index, h.fp,
+                                           a.seg_mask);
             if (s >= 0) {
                 found = true;
                 e = fine_effective(a, s);
@@ -419,10 +432,10 @@ __global__ void __launch_bounds__(kThreads) resolve_fallback_kernel(ResolveArgs 
                 h = vertex_key(cfg, a.v, a.h0_coarse, row, cfg.coarse_delta).second;
             }
             const int64_t s = probe_lookup(a.coarse.tags, static_cast<uint64_t>(a.coarse.capacity) - 1,
-                                           a.coarse.probe_limit, h.index, h.fp);
+                                           a.coarse.probe_limit, h.index, h.fp, a.seg_mask);
             if (s >= 0) {
                 coarse_found = true;
-                ce = effective_at(a.coarse, s, mode, cfg.ema_alpha, cfg.delta_max);
+                ce = coarse_effective(a, s);
             }
         }
         double contrib[3], ch[3];
@@ -431,7 +444,8 @@ __global__ void __launch_bounds__(kThreads) resolve_fallback_kernel(ResolveArgs 
         const int src = ladder_choose(pool, as_int, mode, fixed, a.thr, coarse_found, ce,
                                       eff_is_int(a.coarse, mode), contrib, ch);
         composite(a, row, pixel, ch, src);
-        if (!(pixel >= 0 && pixel < a.n_pixels)) atomicAdd(&bs.v[PF_STAT_BAD_PIXELS], 1u);
+        if (!(pixel - a.pixel_base >= 0 && pixel - a.pixel_base < a.n_pixels))
+            atomicAdd(&bs.v[PF_STAT_BAD_PIXELS], 1u);
         atomicAdd(&bs.v[PF_STAT_SOURCE_FINE + src], 1u);
         }
         __syncwarp();
@@ -479,7 +493,8 @@ __global__ void __launch_bounds__(kThreads) resolve_pool_kernel(ResolveArgs a) {
             const CellHash h = cell_hash(ps.key[r][0] + neighbour_dx(j), ps.key[r][1] + neighbour_dy(j),
                                          ps.key[r][2] + neighbour_dz(j), ps.key[r][3],
                                          static_cast<uint64_t>(ps.key[r][4]), 0, 0u);
-            const int64_t s = probe_lookup(a.fine.tags, fmask, a.fine.probe_limit, h.index, h.fp);
+            const int64_t s = probe_lookup(a.fine.tags, fmask, a.fine.probe_limit, h.index, h.fp,
+                                           a.seg_mask);
             ps.found[p] = s >= 0;
             if (s >= 0) {
                 const Effective e = fine_effective(a, s);
@@ -515,10 +530,10 @@ __global__ void __launch_bounds__(kThreads) resolve_pool_kernel(ResolveArgs a) {
                 const int64_t s = probe_lookup(a.coarse.tags, static_cast<uint64_t>(a.coarse.capacity) - 1,
                                                a.coarse.probe_limit,
                                                static_cast<uint64_t>(ps.key[r][5]),
-                                               static_cast<uint32_t>(ps.key[r][6]));
+                                               static_cast<uint32_t>(ps.key[r][6]), a.seg_mask);
                 if (s >= 0) {
                     coarse_found = true;
-                    ce = effective_at(a.coarse, s, mode, cfg.ema_alpha, cfg.delta_max);
+                    ce = coarse_effective(a, s);
                 }
             }
             double contrib[3], ch[3];
@@ -528,7 +543,8 @@ __global__ void __launch_bounds__(kThreads) resolve_pool_kernel(ResolveArgs a) {
                                           eff_is_int(a.coarse, mode), contrib, ch);
             const int64_t pixel = __ldg(a.v.pixel + row);
             composite(a, row, pixel, ch, src);
-            if (!(pixel >= 0 && pixel < a.n_pixels)) atomicAdd(&bs.v[PF_STAT_BAD_PIXELS], 1u);
+            if (!(pixel - a.pixel_base >= 0 && pixel - a.pixel_base < a.n_pixels))
+                atomicAdd(&bs.v[PF_STAT_BAD_PIXELS], 1u);
             atomicAdd(&bs.v[PF_STAT_SOURCE_FINE + src], 1u);
         }
         __syncthreads();
@@ -542,6 +558,38 @@ finalize_image_kernel(const double *__restrict__ base, const double *__restrict_
                       double *__restrict__ image, int64_t n, double spp) {
     const int64_t k = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
     if (k < n) image[k] = dadd(base[k], ddiv(flat[k], spp));
+}
+
+// The resolve rungs after the effective records exist: the fine rung (keys from the
+// insert pass, or rebuilt), the work rows' keys, the neighbourhood pool + coarse rung +
+// ladder + composite.
+static int launch_rungs(const char *fn, const ResolveArgs &a, int64_t n, bool have_keys,
+                        bool have_fb_keys, cudaStream_t st) {
+    if (have_keys)
+        resolve_main_kernel<kResolveKV, true>
+            <<<blocks_for(n, kThreads * kResolveKV), kThreads, 0, st>>>(a);
+    else
+        resolve_main_kernel<1, false><<<blocks_for(n, kThreads), kThreads, 0, st>>>(a);
+    if (int rc = check_launch(fn)) return rc;
+    if (have_fb_keys) {
+        static const int per_sm = resident_blocks(fallback_keys_kernel, kThreads);
+        int64_t kb = (n + kThreads - 1) / kThreads;
+        const int64_t kcap = static_cast<int64_t>(sm_count()) * per_sm;
+        if (kb > kcap) kb = kcap;
+        fallback_keys_kernel<<<static_cast<unsigned>(kb), kThreads, 0, st>>>(a);
+        if (int rc = check_launch(fn)) return rc;
+        static const int per_sm_pool = resident_blocks(resolve_pool_kernel, kThreads);
+        int64_t pb = (n + kPoolRows - 1) / kPoolRows;
+        const int64_t pcap = static_cast<int64_t>(sm_count()) * per_sm_pool;
+        if (pb > pcap) pb = pcap;
+        resolve_pool_kernel<<<static_cast<unsigned>(pb), kThreads, 0, st>>>(a);
+    } else {
+        int64_t fb_blocks = (n + kWarps - 1) / kWarps;
+        const int64_t cap = static_cast<int64_t>(sm_count()) * 8;
+        if (fb_blocks > cap) fb_blocks = cap;
+        resolve_fallback_kernel<<<static_cast<unsigned>(fb_blocks), kThreads, 0, st>>>(a);
+    }
+    return check_launch(fn);
 }
 
 }  // namespace pf
@@ -635,6 +683,9 @@ int pf_resolve_frame(const pf_config *cfg, const pf_vertices *v, const pf_table 
         a.rec = reinterpret_cast<const ulonglong4 *>(eff_records);
         a.n_pixels = n_pixels;
         a.fb_keys = fallback_keys;
+        a.pixel_base = 0;
+        a.seg_mask = ~0ull;
+        a.crec = nullptr;
         if (eff_records != nullptr) {
             effective_records_kernel<<<sweep_blocks<kThreads>(fine->capacity, sm_count()), kThreads,
                                        0, st>>>(*fine, kc.temporal_mode, kc.ema_alpha,
@@ -642,39 +693,70 @@ int pf_resolve_frame(const pf_config *cfg, const pf_vertices *v, const pf_table 
                                                 reinterpret_cast<ulonglong4 *>(eff_records));
             if (int rc = check_launch(fn)) return rc;
         }
-        if (lookup_index != nullptr)
-            resolve_main_kernel<kResolveKV, true>
-                <<<blocks_for(v->n, kThreads * kResolveKV), kThreads, 0, st>>>(a);
-        else
-            resolve_main_kernel<1, false><<<blocks_for(v->n, kThreads), kThreads, 0, st>>>(a);
-        if (int rc = check_launch(fn)) return rc;
-        if (fallback_keys != nullptr) {
-            static const int per_sm = resident_blocks(fallback_keys_kernel, kThreads);
-            int64_t kb = (v->n + kThreads - 1) / kThreads;
-            const int64_t kcap = static_cast<int64_t>(sm_count()) * per_sm;
-            if (kb > kcap) kb = kcap;
-            fallback_keys_kernel<<<static_cast<unsigned>(kb), kThreads, 0, st>>>(a);
-            if (int rc = check_launch(fn)) return rc;
-        }
-        if (fallback_keys != nullptr) {
-            static const int per_sm_pool = resident_blocks(resolve_pool_kernel, kThreads);
-            int64_t pb = (v->n + kPoolRows - 1) / kPoolRows;
-            const int64_t pcap = static_cast<int64_t>(sm_count()) * per_sm_pool;
-            if (pb > pcap) pb = pcap;
-            resolve_pool_kernel<<<static_cast<unsigned>(pb), kThreads, 0, st>>>(a);
-        } else {
-            int64_t fb_blocks = (v->n + kWarps - 1) / kWarps;
-            const int64_t cap = static_cast<int64_t>(sm_count()) * 8;
-            if (fb_blocks > cap) fb_blocks = cap;
-            resolve_fallback_kernel<<<static_cast<unsigned>(fb_blocks), kThreads, 0, st>>>(a);
-        }
-        if (int rc = check_launch(fn)) return rc;
+        if (int rc = launch_rungs(fn, a, v->n, lookup_index != nullptr, fallback_keys != nullptr, st))
+            return rc;
     }
     const int64_t m = 3 * n_pixels;
     if (m > 0)
         finalize_image_kernel<<<blocks_for(m, kThreads), kThreads, 0, st>>>(
             base_image, flat, image, m, static_cast<double>(spp));
     return check_launch(fn);
+}
+
+int pf_resolve_replica(const pf_config *cfg, const pf_vertices *v, const pf_replica *rp,
+                       uint64_t stream_base_lookup, uint64_t stream_base_coarse,
+                       const uint64_t *lookup_index, const uint32_t *lookup_fp, double *flat,
+                       int64_t n_pixels, int64_t pixel_base, int64_t *work,
+                       int64_t *work_count, int64_t *fallback_keys, uint8_t *source,
+                       double *chosen, int64_t *stats, void *stream) {
+    const char *fn = "pf_resolve_replica";
+    if (int rc = validate_vertices(fn, v, cfg)) return rc;
+    pf_config kc;
+    if (int rc = prepare_config(fn, cfg, &kc)) return rc;
+    if (rp == nullptr || !rp->fine_tags || !rp->fine_records || !is_pow2(rp->capacity) ||
+        rp->probe_limit < 1 || rp->slice_log2 < 1 || (1ll << rp->slice_log2) > rp->capacity ||
+        (rp->coarse_tags == nullptr) != (rp->coarse_records == nullptr))
+        return fail_arg(fn, "bad replica");
+    if (n_pixels < 0 || !flat || !stats) return fail_arg(fn, "flat / stats are NULL");
+    if (v->n > 0 && (!v->throughput || !v->contribution || !work || !work_count ||
+                     !fallback_keys || !lookup_index || !lookup_fp))
+        return fail_arg(fn, "throughput/contribution/work/keys is NULL");
+    cudaStream_t st = as_stream(stream);
+    if (cudaMemsetAsync(flat, 0, sizeof(double) * 3 * n_pixels, st) != cudaSuccess)
+        return check_launch(fn);
+    if (v->n == 0) return PF_OK;
+    if (cudaMemsetAsync(work_count, 0, sizeof(int64_t), st) != cudaSuccess) return check_launch(fn);
+    pf_table view{};
+    view.tags = rp->fine_tags;
+    view.capacity = rp->capacity;
+    view.sum_mode = rp->sum_mode;
+    view.probe_limit = rp->probe_limit;
+    pf_table cview = view;
+    cview.tags = rp->coarse_tags ? rp->coarse_tags : rp->fine_tags;
+    ResolveArgs a;
+    a.cfg = kc;
+    a.v = *v;
+    a.fine = view;
+    a.coarse = cview;
+    a.has_coarse = rp->coarse_tags != nullptr;
+    a.h0_lookup = stream_base_lookup;
+    a.h0_coarse = stream_base_coarse;
+    a.flat = flat;
+    a.work = work;
+    a.work_count = work_count;
+    a.source = source;
+    a.chosen = chosen;
+    a.stats = stats;
+    a.thr = static_cast<double>(cfg->low_count_threshold > 1 ? cfg->low_count_threshold : 1);
+    a.lk_index = lookup_index;
+    a.lk_fp = lookup_fp;
+    a.rec = reinterpret_cast<const ulonglong4 *>(rp->fine_records);
+    a.n_pixels = n_pixels;
+    a.fb_keys = fallback_keys;
+    a.pixel_base = pixel_base;
+    a.seg_mask = (1ull << rp->slice_log2) - 1;
+    a.crec = reinterpret_cast<const ulonglong4 *>(rp->coarse_records);
+    return launch_rungs(fn, a, v->n, true, true, st);
 }
 
 int pf_finalize_image(const double *base_image, const double *flat, double *image,

@@ -1,13 +1,16 @@
 // Key-sharded multi-GPU frame: each rank owns a contiguous slice of
-// the global tables' home slots; vertices are pre-aggregated per distinct key on the
-// rank that traced them, shipped to the owner as records, and lookups go to the owner
-// as deduplicated requests answered with the cell's effective (sum, count).
+// the global tables' home slots.  Inserts: vertices are pre-aggregated per distinct key
+// on the rank that traced them and shipped to the owner as records (one all-to-all).
+// Queries: after the inserts every owner publishes its occupied cells' effective
+// (sum, count) records, the ranks all-gather them into a read-only replica of the whole
+// global table (a few MB: ~4 % of the slots are occupied), and each rank resolves its
+// own vertices against the replica with the single-GPU resolve kernels
+// (pf_resolve_replica) -- no per-lookup round trips.
 //
-// The per-rank kernels here do everything but the exchanges, which the host runs as
-// all-to-alls between them (NCCL over NVLink/NVSwitch; pipeline_sharded.py).  The
-// results equal the single-GPU frame: every key's records reach the one rank that
-// owns its home slot, fixed-point sums are exactly associative, and the resolve
-// ladder consumes the same effective values in the same order (src/pipeline.py:152-283).
+// The host runs the collectives between the kernels (sharded.py).  Results equal the
+// single-GPU frame: each key's records reach exactly one owner, 16.16 fixed-point sums
+// are exactly associative, and the replica holds the owners' cells verbatim
+// (src/pipeline.py:152-283).
 #include "pf_resolve.cuh"
 #include "pf_sweep.cuh"
 #include "pf_internal.cuh"
@@ -17,9 +20,7 @@ namespace pf {
 namespace {
 
 constexpr int kT = 256;
-constexpr int kTW = kT / 32;
 constexpr int kMaxWorld = 64;
-constexpr int kWorkKeys = 28;  // 27 neighbourhood cells + the coarse cell
 constexpr int kHomeBits = 29;
 constexpr uint64_t kAggEmpty = ~0ull;
 
@@ -160,7 +161,8 @@ __device__ __forceinline__ int64_t warp_agg_insert(const ShardK &k, OwnerCounts 
 template <bool FIXED>
 __global__ void __launch_bounds__(kT, 2)
 shard_keys_kernel(pf_config cfg, pf_vertices v, ShardK k, int has_coarse, uint64_t h0,
-                  uint64_t h0_lookup, const int32_t *abort_flag) {
+                  uint64_t h0_lookup, const int32_t *abort_flag, uint64_t *lk_index,
+                  uint32_t *lk_fp) {
     __shared__ OwnerCounts oc;
     __shared__ double2 sincos_tab[220];
     if (abort_flag != nullptr && *abort_flag != 0) return;
@@ -195,15 +197,14 @@ shard_keys_kernel(pf_config cfg, pf_vertices v, ShardK k, int has_coarse, uint64
             double jt[3];
             const CellHash h = key_hash(
                 make_key(cfg, x, ks, cfg.jitter, du, dv, set == 1 ? cfg.coarse_delta : 0, jt), ks);
-            const uint64_t key = agg_key(set, h.index & k.home_mask, h.fp);
             if (set < 2) {
+                const uint64_t key = agg_key(set, h.index & k.home_mask, h.fp);
                 int64_t qs[3] = {q[0], q[1], q[2]};
                 double fs[3] = {f[0], f[1], f[2]};
                 warp_agg_insert<true, FIXED>(k, oc, valid, key, qs, fs, 1);
-            } else {
-                const int64_t slot = warp_agg_insert<false, FIXED>(k, oc, valid, key, nullptr,
-                                                                   nullptr, 0);
-                if (valid) k.s.vertex_slot[i] = static_cast<int32_t>(slot);
+            } else if (valid) {  // the resolve phase's lookup key (stream 3)
+                lk_index[i] = h.index;
+                lk_fp[i] = h.fp;
             }
         }
     }
@@ -266,7 +267,7 @@ shard_emit_kernel(ShardK k, int64_t *send_rec, uint64_t *send_req) {
 // ------------------------------------------------------------------ owner side
 
 __device__ __forceinline__ uint64_t local_index(const ShardK &k, uint64_t home) {
-    return home - k.slice_base;
+    return home - k.slice_base;  // < S: the local table's home slot
 }
 
 template <bool FIXED>
@@ -319,236 +320,54 @@ shard_apply_kernel(ShardK k, pf_table fine, pf_table coarse, int has_coarse, con
     stats_flush(bs, stats, true);
 }
 
+// ------------------------------------------------------------------ replica
+
+// Owner side: every occupied slot of the local slice -> one 48-byte entry
+// {global slot | table bit 62, tag, effective record (4 words)}.
 __global__ void __launch_bounds__(kT)
-shard_answer_kernel(ShardK k, pf_config cfg, pf_table fine, pf_table coarse, int has_coarse,
-                    const uint64_t *req, int64_t n, ulonglong4 *ans, int64_t *stats) {
-    const int64_t j = static_cast<int64_t>(blockIdx.x) * kT + threadIdx.x;
-    if (j == 0) atomicAdd(reinterpret_cast<unsigned long long *>(stats + PF_STAT_SHARD_REQUESTS),
-                          static_cast<unsigned long long>(n));
-    if (j >= n) return;
-    const uint64_t key = __ldg(reinterpret_cast<const unsigned long long *>(req) + j);
-    const bool to_coarse = key_kind(key) == kKindCoarseLookup;
-    ulonglong4 out = absent_record();
-    if (!to_coarse || has_coarse) {
-        const pf_table &t = to_coarse ? coarse : fine;
-        const int64_t s = probe_lookup(t.tags, static_cast<uint64_t>(t.capacity) - 1, t.probe_limit,
-                                       local_index(k, key_home(key)), key_fp(key));
-        if (s >= 0)
-            out = pack_effective(effective_at(t, s, cfg.temporal_mode, cfg.ema_alpha, cfg.delta_max),
-                                 eff_is_int(t, cfg.temporal_mode));
-    }
-    ulonglong2 *o = reinterpret_cast<ulonglong2 *>(ans + j);
-    o[0] = make_ulonglong2(out.x, out.y);
-    o[1] = make_ulonglong2(out.z, out.w);
+shard_publish_kernel(ShardK k, pf_table t, int table_bit, int mode, double ema, double delta_max,
+                     uint64_t *out, int64_t *count) {
+    __shared__ SweepSmem<kT> q;
+    const bool fixed = t.sum_mode == PF_SUM_FIXED;
+    const bool as_int = eff_is_int(t, mode);
+    for_each_occupied<kT>(t.tags, t.capacity, q, [&](int64_t s, uint64_t tag) {
+        const ulonglong4 r = pack_effective(effective_of(load_cell(t, s, true), fixed, mode, ema,
+                                                         delta_max), as_int);
+        const unsigned long long j = atomicAdd(reinterpret_cast<unsigned long long *>(count), 1ull);
+        uint64_t *e = out + 6 * j;
+        e[0] = (k.slice_base + static_cast<uint64_t>(s)) | (static_cast<uint64_t>(table_bit) << 62);
+        e[1] = tag;
+        e[2] = r.x;
+        e[3] = r.y;
+        e[4] = r.z;
+        e[5] = r.w;
+    });
 }
 
-// ------------------------------------------------------------------ requester side
-
-__device__ __forceinline__ bool as_int_mode(int sum_mode, int mode) {
-    return mode == PF_INTEGRATE && sum_mode == PF_SUM_FIXED;
-}
-
-// The answer to the request held in aggregation slot `slot` (its send position was
-// stored there by the emit kernel).
-__device__ __forceinline__ ulonglong4 answer_of(const ShardK &k, const ulonglong4 *ans,
-                                                int32_t slot) {
-    if (slot < 0) return absent_record();
-    const int64_t pos = __ldg(k.s.agg_counts + slot);
-    return load_record(ans, pos);
-}
-
-__device__ __forceinline__ void composite_local(double *flat, int64_t n_pixels, int64_t pixel,
-                                                const double *throughput, const double chosen[3],
-                                                BlockStats &bs, bool count_bad) {
-    const uint64_t stream = l2_evict_first(), keep = l2_evict_last();
-    if (pixel >= 0 && pixel < n_pixels) {
-#pragma unroll
-        for (int c = 0; c < 3; ++c)
-            red_add_f64(flat + 3 * pixel + c, dmul(ld_stream(throughput + c, stream), chosen[c]), keep);
-    } else if (count_bad) {
-        atomicAdd(&bs.v[PF_STAT_BAD_PIXELS], 1u);
-    }
-}
-
+// All-gathered entries: rank r's rows are [r * stride, r * stride + counts[r]).  clear=1
+// empties the entries' slots (last frame's replica), clear=0 writes tags and records.
 __global__ void __launch_bounds__(kT)
-shard_resolve_kernel(ShardK k, pf_config cfg, pf_vertices v, const ulonglong4 *ans, double *flat,
-                     int64_t n_pixels, double thr, int64_t *work, int64_t *work_count,
-                     uint8_t *source, double *chosen, int64_t *stats) {
-    __shared__ BlockStats bs;
-    stats_init(bs);
-    __syncthreads();
-    const int mode = cfg.temporal_mode;
-    const bool as_int = as_int_mode(k.s.sum_mode, mode);
-    const bool fixed = k.s.sum_mode == PF_SUM_FIXED;
-    const int lane = threadIdx.x & 31;
-    const uint64_t stream = l2_evict_first();
-    const int64_t tiles = (v.n + kT - 1) / kT;
-    for (int64_t tile = blockIdx.x; tile < tiles; tile += gridDim.x) {
-        const int64_t i0 = tile * kT + threadIdx.x;
-        const bool valid = i0 < v.n;
-        const int64_t i = valid ? i0 : v.n - 1;
-        const ulonglong4 rec = answer_of(k, ans, k.s.vertex_slot[i]);
-        const bool found = rec.w != kAbsentCount;
-        const Effective e = unpack_effective(rec, as_int);
-        const bool fine_ok = valid && found && e.fcnt >= thr;
-        if (fine_ok) {
-            double m[3];
-#pragma unroll
-            for (int c = 0; c < 3; ++c) m[c] = row_mean(eff_sum_f64(e, as_int, c), e.fcnt, fixed);
-            const int64_t pixel = ld_stream(v.pixel + i, stream) - k.s.pixel_base;
-            composite_local(flat, n_pixels, pixel, v.throughput + 3 * i, m, bs, true);
-            if (source) source[i] = 0;
-            if (chosen) {
-#pragma unroll
-                for (int c = 0; c < 3; ++c) chosen[3 * i + c] = m[c];
-            }
+replica_update_kernel(pf_replica rp, const uint64_t *entries, const int64_t *counts, int world,
+                      int64_t stride, int clear) {
+    const int64_t n = stride * world;
+    for (int64_t i = static_cast<int64_t>(blockIdx.x) * kT + threadIdx.x; i < n;
+         i += static_cast<int64_t>(gridDim.x) * kT) {
+        const int r = static_cast<int>(i / stride);
+        if (i - r * stride >= counts[r]) continue;
+        const uint64_t *e = entries + 6 * i;
+        const bool coarse = (e[0] >> 62) & 1u;
+        const uint64_t slot = e[0] & ((1ull << 62) - 1);
+        uint64_t *tags = coarse ? rp.coarse_tags : rp.fine_tags;
+        uint64_t *rec = coarse ? rp.coarse_records : rp.fine_records;
+        if (tags == nullptr) continue;
+        if (clear) {
+            tags[slot] = kEmptyTag;
+        } else {
+            tags[slot] = e[1];
+            reinterpret_cast<ulonglong2 *>(rec + 4 * slot)[0] = make_ulonglong2(e[2], e[3]);
+            reinterpret_cast<ulonglong2 *>(rec + 4 * slot)[1] = make_ulonglong2(e[4], e[5]);
         }
-        const bool need = valid && !fine_ok;
-        const unsigned mk = __ballot_sync(kFull, need);
-        if (mk) {
-            unsigned long long wb = 0;
-            if (lane == __ffs(mk) - 1)
-                wb = atomicAdd(reinterpret_cast<unsigned long long *>(work_count),
-                               static_cast<unsigned long long>(__popc(mk)));
-            wb = __shfl_sync(kFull, wb, __ffs(mk) - 1);
-            if (need) work[static_cast<int64_t>(wb) + __popc(mk & ((1u << lane) - 1u))] = i;
-        }
-        warp_count(bs, PF_STAT_SOURCE_FINE, fine_ok);
-        warp_count(bs, PF_STAT_FALLBACK_ROWS, need);
     }
-    __syncthreads();
-    stats_flush(bs, stats, false);
-}
-
-// Each work row's lookup key (stream 3) and coarse hash, one row per thread (the FP64
-// key recipe SIMT-wide); record: q0, q1, q2, level, aux, coarse index, coarse fp, 0.
-__global__ void __launch_bounds__(kT)
-shard_row_keys_kernel(pf_config cfg, pf_vertices v, ShardK k, int has_coarse, uint64_t h0_lookup,
-                      uint64_t h0_coarse, const int64_t *work, const int64_t *work_count) {
-    __shared__ double2 sincos_tab[220];
-    stage_sincos_table(sincos_tab);
-    __syncthreads();
-    const int64_t n_work = *work_count;
-    for (int64_t w = static_cast<int64_t>(blockIdx.x) * kT + threadIdx.x; w < n_work;
-         w += static_cast<int64_t>(gridDim.x) * kT) {
-        const int64_t row = work[w];
-        const VertexIn x = load_vertex(v, row, cfg);
-        const KeyShared ks = key_shared(cfg, x);
-        double du = 0.0, dv = 0.0, cdu = 0.0, cdv = 0.0;
-        if (cfg.jitter) {  // the coarse key shares the lookup draws when jitter is on
-            double u1, u2;
-            jitter_draws(h0_lookup, x.pixel, x.sample, u1, u2);
-            disc_offset(u1, u2, du, dv, sincos_tab);
-            cdu = du;
-            cdv = dv;
-            if (h0_coarse != h0_lookup) {
-                jitter_draws(h0_coarse, x.pixel, x.sample, u1, u2);
-                disc_offset(u1, u2, cdu, cdv, sincos_tab);
-            }
-        }
-        double jt[3];
-        const CellKey lk = make_key(cfg, x, ks, cfg.jitter, du, dv, 0, jt);
-        CellHash hc{0ull, 0u};
-        if (has_coarse)
-            hc = key_hash(make_key(cfg, x, ks, cfg.jitter, cdu, cdv, cfg.coarse_delta, jt), ks);
-        longlong4 *o = reinterpret_cast<longlong4 *>(k.s.row_keys + 8 * w);
-        o[0] = make_longlong4(lk.q[0], lk.q[1], lk.q[2], lk.level);
-        o[1] = make_longlong4(static_cast<long long>(lk.aux), static_cast<long long>(hc.index),
-                              static_cast<long long>(hc.fp), 0);
-    }
-}
-
-// One work row per warp: lanes 0..26 hash the neighbourhood cells of the row's lookup key
-// (shard_row_keys_kernel) and lane 27 carries the coarse cell; all 28 go into the
-// aggregation table as deduplicated requests.
-__global__ void __launch_bounds__(kT)
-shard_fallback_keys_kernel(pf_config cfg, pf_vertices v, ShardK k, int has_coarse,
-                           uint64_t h0_lookup, uint64_t h0_coarse, const int64_t *work,
-                           const int64_t *work_count) {
-    __shared__ OwnerCounts oc;
-    owner_init(oc, k.s.world);
-    __syncthreads();
-    const int lane = threadIdx.x & 31;
-    const int64_t n_work = *work_count;
-    const int64_t nwarps = static_cast<int64_t>(gridDim.x) * kTW;
-    for (int64_t w = static_cast<int64_t>(blockIdx.x) * kTW + (threadIdx.x >> 5); w < n_work;
-         w += nwarps) {
-        const long long rec = lane < 8 ? k.s.row_keys[8 * w + lane] : 0;
-        const long long q0 = __shfl_sync(kFull, rec, 0);
-        const long long q1 = __shfl_sync(kFull, rec, 1);
-        const long long q2 = __shfl_sync(kFull, rec, 2);
-        const long long lev = __shfl_sync(kFull, rec, 3);
-        const unsigned long long aux = static_cast<unsigned long long>(__shfl_sync(kFull, rec, 4));
-        const unsigned long long cidx = static_cast<unsigned long long>(__shfl_sync(kFull, rec, 5));
-        const unsigned cfp = static_cast<unsigned>(__shfl_sync(kFull, rec, 6));
-        uint64_t key = kAggEmpty;
-        bool valid = false;
-        if (lane < 27) {
-            const CellHash h = cell_hash(q0 + neighbour_dx(lane), q1 + neighbour_dy(lane),
-                                         q2 + neighbour_dz(lane), lev, aux, 0, 0u);
-            key = agg_key(kKindNeighbour, h.index & k.home_mask, h.fp);
-            valid = true;
-        } else if (lane == 27 && has_coarse) {
-            key = agg_key(kKindCoarseLookup, cidx & k.home_mask, cfp);
-            valid = true;
-        }
-        const int64_t slot = warp_agg_insert<false, true>(k, oc, valid, key, nullptr, nullptr, 0);
-        if (lane < kWorkKeys) k.s.work_slot[w * kWorkKeys + lane] = valid ? static_cast<int32_t>(slot) : -1;
-    }
-    __syncthreads();
-    owner_flush(oc, k);
-}
-
-__global__ void __launch_bounds__(kT)
-shard_ladder_kernel(ShardK k, pf_config cfg, pf_vertices v, int has_coarse, const ulonglong4 *ans,
-                    const int64_t *work, const int64_t *work_count, double *flat, int64_t n_pixels,
-                    double thr, uint8_t *source, double *chosen, int64_t *stats) {
-    __shared__ BlockStats bs;
-    stats_init(bs);
-    __syncthreads();
-    const int lane = threadIdx.x & 31;
-    const int mode = cfg.temporal_mode;
-    const bool as_int = as_int_mode(k.s.sum_mode, mode);
-    const bool fixed = k.s.sum_mode == PF_SUM_FIXED;
-    const int64_t n_work = *work_count;
-    const int64_t nwarps = static_cast<int64_t>(gridDim.x) * kTW;
-    for (int64_t w = static_cast<int64_t>(blockIdx.x) * kTW + (threadIdx.x >> 5); w < n_work;
-         w += nwarps) {
-        const int64_t row = work[w];
-        bool found = false;
-        Effective e{};
-        if (lane < 27) {
-            const ulonglong4 rec = answer_of(k, ans, k.s.work_slot[w * kWorkKeys + lane]);
-            found = rec.w != kAbsentCount;
-            if (found) e = unpack_effective(rec, as_int);
-        }
-        const Pool pool = pool_neighbours(found, e, as_int, mode);
-        if (lane == 0) {
-            bool coarse_found = false;
-            Effective ce{};
-            if (has_coarse) {
-                const ulonglong4 rec = answer_of(k, ans, k.s.work_slot[w * kWorkKeys + 27]);
-                coarse_found = rec.w != kAbsentCount;
-                if (coarse_found) ce = unpack_effective(rec, as_int);
-            }
-            double contrib[3], ch[3];
-#pragma unroll
-            for (int c = 0; c < 3; ++c) contrib[c] = __ldg(v.contribution + 3 * row + c);
-            const int src = ladder_choose(pool, as_int, mode, fixed, thr, coarse_found, ce, as_int,
-                                          contrib, ch);
-            const int64_t pixel = __ldg(v.pixel + row) - k.s.pixel_base;
-            composite_local(flat, n_pixels, pixel, v.throughput + 3 * row, ch, bs, true);
-            if (source) source[row] = static_cast<uint8_t>(src);
-            if (chosen) {
-#pragma unroll
-                for (int c = 0; c < 3; ++c) chosen[3 * row + c] = ch[c];
-            }
-            atomicAdd(&bs.v[PF_STAT_SOURCE_FINE + src], 1u);
-        }
-        __syncwarp();
-    }
-    __syncthreads();
-    stats_flush(bs, stats, false);
 }
 
 __global__ void __launch_bounds__(kT) shard_reset_kernel(ShardK k) {
@@ -593,15 +412,12 @@ int prepare_shard(const char *fn, const pf_shard *sh, ShardK *out) {
     return PF_OK;
 }
 
-// The local slice table: capacity C for one rank, 2S otherwise (see the header).
+// The local slice table: capacity S = C / world, probe windows wrap within it.
 int check_slice(const char *fn, const ShardK &k, const pf_table *t) {
     if (int rc = validate_table(fn, t)) return rc;
-    const int64_t c = 1ll << k.s.log2_capacity;
-    const int64_t want = k.s.world == 1 ? c : 2 * (c / k.s.world);
-    if (t->capacity != want) return fail_arg(fn, "local table capacity must be C (world 1) or 2C/world");
+    const int64_t want = (1ll << k.s.log2_capacity) / k.s.world;
+    if (t->capacity != want) return fail_arg(fn, "local table capacity must be C / world");
     if (t->sum_mode != k.s.sum_mode) return fail_arg(fn, "table sum_mode differs from the shard's");
-    if (k.s.world > 1 && t->probe_limit > c / k.s.world)
-        return fail_arg(fn, "probe_limit exceeds the slice size");
     return PF_OK;
 }
 
@@ -625,7 +441,8 @@ extern "C" {
 
 int pf_shard_keys(const pf_config *cfg, const pf_vertices *v, const pf_shard *sh,
                   int32_t has_coarse, uint64_t stream_base_accum, uint64_t stream_base_lookup,
-                  const int32_t *abort_flag, void *stream) {
+                  const int32_t *abort_flag, uint64_t *lookup_index, uint32_t *lookup_fp,
+                  void *stream) {
     const char *fn = "pf_shard_keys";
     ShardK k;
     if (int rc = prepare_shard(fn, sh, &k)) return rc;
@@ -633,14 +450,17 @@ int pf_shard_keys(const pf_config *cfg, const pf_vertices *v, const pf_shard *sh
     pf_config kc;
     if (int rc = prepare_config(fn, cfg, &kc)) return rc;
     if (v->n == 0) return PF_OK;
-    if (!v->contribution || !sh->vertex_slot) return fail_arg(fn, "contribution/vertex_slot is NULL");
+    if (!v->contribution || !lookup_index || !lookup_fp)
+        return fail_arg(fn, "contribution/lookup_index/lookup_fp is NULL");
     cudaStream_t st = as_stream(stream);
     if (sh->sum_mode == PF_SUM_FIXED)
         shard_keys_kernel<true><<<grid_for(shard_keys_kernel<true>, v->n, 8), kT, 0, st>>>(
-            kc, *v, k, has_coarse != 0, stream_base_accum, stream_base_lookup, abort_flag);
+            kc, *v, k, has_coarse != 0, stream_base_accum, stream_base_lookup, abort_flag,
+            lookup_index, lookup_fp);
     else
         shard_keys_kernel<false><<<grid_for(shard_keys_kernel<false>, v->n, 8), kT, 0, st>>>(
-            kc, *v, k, has_coarse != 0, stream_base_accum, stream_base_lookup, abort_flag);
+            kc, *v, k, has_coarse != 0, stream_base_accum, stream_base_lookup, abort_flag,
+            lookup_index, lookup_fp);
     return check_launch(fn);
 }
 
@@ -682,93 +502,39 @@ int pf_shard_apply(const pf_shard *sh, const pf_table *fine, const pf_table *coa
     return check_launch(fn);
 }
 
-int pf_shard_answer(const pf_shard *sh, const pf_config *cfg, const pf_table *fine,
-                    const pf_table *coarse, const uint64_t *requests, int64_t n_requests,
-                    uint64_t *answers, int64_t *stats, void *stream) {
-    const char *fn = "pf_shard_answer";
+int pf_shard_publish(const pf_shard *sh, const pf_config *cfg, const pf_table *fine,
+                     const pf_table *coarse, uint64_t *entries, int64_t *count, void *stream) {
+    const char *fn = "pf_shard_publish";
     ShardK k;
     if (int rc = prepare_shard(fn, sh, &k)) return rc;
-    if (cfg == nullptr) return fail_arg(fn, "config is NULL");
+    if (cfg == nullptr || !entries || !count) return fail_arg(fn, "config/entries/count is NULL");
     if (int rc = check_slice(fn, k, fine)) return rc;
     if (coarse)
         if (int rc = check_slice(fn, k, coarse)) return rc;
-    if (!stats) return fail_arg(fn, "stats is NULL");
-    if (n_requests < 0) return fail_arg(fn, "negative request count");
-    if (n_requests == 0) return PF_OK;
-    if (!requests || !answers) return fail_arg(fn, "requests/answers is NULL");
-    shard_answer_kernel<<<blocks_for(n_requests, kT), kT, 0, as_stream(stream)>>>(
-        k, *cfg, *fine, coarse ? *coarse : *fine, coarse != nullptr, requests, n_requests,
-        reinterpret_cast<ulonglong4 *>(answers), stats);
-    return check_launch(fn);
+    cudaStream_t st = as_stream(stream);
+    if (cudaMemsetAsync(count, 0, sizeof(int64_t), st) != cudaSuccess) return check_launch(fn);
+    const pf_table *tabs[2] = {fine, coarse};
+    for (int tb = 0; tb < 2; ++tb) {
+        if (!tabs[tb]) continue;
+        shard_publish_kernel<<<sweep_blocks<kT>(tabs[tb]->capacity, sm_count()), kT, 0, st>>>(
+            k, *tabs[tb], tb, cfg->temporal_mode, cfg->ema_alpha, cfg->delta_max, entries, count);
+        if (int rc = check_launch(fn)) return rc;
+    }
+    return PF_OK;
 }
 
-int pf_shard_resolve(const pf_shard *sh, const pf_config *cfg, const pf_vertices *v,
-                     const uint64_t *answers, double *flat, int64_t n_pixels, int64_t *work,
-                     int64_t *work_count, uint8_t *source, double *chosen, int64_t *stats,
-                     void *stream) {
-    const char *fn = "pf_shard_resolve";
-    ShardK k;
-    if (int rc = prepare_shard(fn, sh, &k)) return rc;
-    if (int rc = validate_vertices(fn, v, cfg)) return rc;
-    if (!flat || !work || !work_count || !stats || n_pixels < 0)
-        return fail_arg(fn, "flat/work/work_count/stats is NULL");
-    if (v->n == 0) return PF_OK;
-    if (!v->throughput || !sh->vertex_slot) return fail_arg(fn, "throughput/vertex_slot is NULL");
-    if (!answers) return fail_arg(fn, "answers is NULL");
-    const double thr = static_cast<double>(cfg->low_count_threshold > 1 ? cfg->low_count_threshold : 1);
-    shard_resolve_kernel<<<grid_for(shard_resolve_kernel, v->n, 8), kT, 0, as_stream(stream)>>>(
-        k, *cfg, *v, reinterpret_cast<const ulonglong4 *>(answers), flat, n_pixels, thr, work,
-        work_count, source, chosen, stats);
-    return check_launch(fn);
-}
-
-int pf_shard_fallback_keys(const pf_config *cfg, const pf_vertices *v, const pf_shard *sh,
-                           int32_t has_coarse, uint64_t stream_base_lookup,
-                           uint64_t stream_base_coarse, const int64_t *work,
-                           const int64_t *work_count, void *stream) {
-    const char *fn = "pf_shard_fallback_keys";
-    ShardK k;
-    if (int rc = prepare_shard(fn, sh, &k)) return rc;
-    if (int rc = validate_vertices(fn, v, cfg)) return rc;
-    pf_config kc;
-    if (int rc = prepare_config(fn, cfg, &kc)) return rc;
-    if (v->n == 0) return PF_OK;
-    if (!work || !work_count || !sh->work_slot || !sh->row_keys)
-        return fail_arg(fn, "work/work_slot/row_keys is NULL");
-    int64_t kb = (v->n + kT - 1) / kT;
-    const int64_t kcap = static_cast<int64_t>(sm_count()) * 4;
-    if (kb > kcap) kb = kcap;
-    shard_row_keys_kernel<<<static_cast<unsigned>(kb), kT, 0, as_stream(stream)>>>(
-        kc, *v, k, has_coarse != 0, stream_base_lookup, stream_base_coarse, work, work_count);
-    if (int rc = check_launch(fn)) return rc;
-    int64_t blocks = (v->n + kTW - 1) / kTW;
+int pf_replica_update(const pf_replica *rp, const uint64_t *entries, const int64_t *counts,
+                      int32_t world, int64_t stride, int32_t clear, void *stream) {
+    const char *fn = "pf_replica_update";
+    if (!rp || !rp->fine_tags || !rp->fine_records || world < 1 || stride < 0)
+        return fail_arg(fn, "bad replica / sizes");
+    if (stride == 0) return PF_OK;
+    if (!entries || !counts) return fail_arg(fn, "entries/counts is NULL");
+    int64_t blocks = (stride * world + kT - 1) / kT;
     const int64_t cap = static_cast<int64_t>(sm_count()) * 8;
     if (blocks > cap) blocks = cap;
-    shard_fallback_keys_kernel<<<static_cast<unsigned>(blocks), kT, 0, as_stream(stream)>>>(
-        kc, *v, k, has_coarse != 0, stream_base_lookup, stream_base_coarse, work, work_count);
-    return check_launch(fn);
-}
-
-int pf_shard_ladder(const pf_shard *sh, const pf_config *cfg, const pf_vertices *v,
-                    int32_t has_coarse, const uint64_t *answers, const int64_t *work,
-                    const int64_t *work_count, double *flat, int64_t n_pixels, uint8_t *source,
-                    double *chosen, int64_t *stats, void *stream) {
-    const char *fn = "pf_shard_ladder";
-    ShardK k;
-    if (int rc = prepare_shard(fn, sh, &k)) return rc;
-    if (int rc = validate_vertices(fn, v, cfg)) return rc;
-    if (!flat || !work || !work_count || !stats || n_pixels < 0)
-        return fail_arg(fn, "flat/work/work_count/stats is NULL");
-    if (v->n == 0) return PF_OK;
-    if (!v->throughput || !v->contribution || !sh->work_slot || !answers)
-        return fail_arg(fn, "throughput/contribution/work_slot/answers is NULL");
-    const double thr = static_cast<double>(cfg->low_count_threshold > 1 ? cfg->low_count_threshold : 1);
-    int64_t blocks = (v->n + kTW - 1) / kTW;
-    const int64_t cap = static_cast<int64_t>(sm_count()) * 8;
-    if (blocks > cap) blocks = cap;
-    shard_ladder_kernel<<<static_cast<unsigned>(blocks), kT, 0, as_stream(stream)>>>(
-        k, *cfg, *v, has_coarse != 0, reinterpret_cast<const ulonglong4 *>(answers), work,
-        work_count, flat, n_pixels, thr, source, chosen, stats);
+    replica_update_kernel<<<static_cast<unsigned>(blocks), kT, 0, as_stream(stream)>>>(
+        *rp, entries, counts, world, stride, clear);
     return check_launch(fn);
 }
 

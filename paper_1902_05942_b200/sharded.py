@@ -2,30 +2,31 @@
 
 One process per GPU.  The global fine and coarse tables (capacity C each, the
 single-GPU layout) are split into G contiguous slices of home slots; rank r owns
-homes [r*S, (r+1)*S), S = C/G, and keeps them in a local table of capacity 2S
-(C when G == 1) so probe chains stay on the owner (include/pathfilter_b200.h, section 3).
+homes [r*S, (r+1)*S), S = C/G, in a local table of capacity S whose probe windows wrap
+within the slice (include/pathfilter_b200.h, section 3).
 
 A frame is a generator that yields its collectives and receives their results:
 
-    round 1   keys of every local vertex; pre-aggregated records (fine, coarse) and
-              deduplicated fine lookups, bucketed by owner            (pf_shard_keys/emit)
-              -> all-to-all of counts (+ overflow / bad-input flags), records, requests
-              owner applies the records, answers the lookups        (pf_shard_apply/answer)
-              -> all-to-all of answers; fine rung + work list       (pf_shard_resolve)
-    round 2   27 neighbourhood + coarse lookups of the work rows     (pf_shard_fallback_keys)
-              -> counts, requests; owner answers; answers back; ladder (pf_shard_ladder)
+    insert    keys of every local vertex; fine/coarse records pre-aggregated per
+              distinct key and bucketed by owner              (pf_shard_keys / emit)
+              -> all-to-all of counts (+ overflow / bad-input flags) and records
+              owners apply the records                          (pf_shard_apply)
+    publish   owners emit their occupied cells' effective records (pf_shard_publish)
+              -> all-gather into a replica of the whole table   (pf_replica_update)
+    resolve   every rank resolves its own vertices against the replica with the
+              single-GPU rungs                                  (pf_resolve_replica)
     image     composite local to the rank's pixels ("band"), or summed over ranks with
               a reduce-scatter of the flat buffer ("reduce": ranks trace different
-              samples of the same pixels), then base + flat / spp    (pf_finalize_image)
+              samples of the same pixels), then base + flat / spp (pf_finalize_image)
 
 `run_dist` drives a frame with torch.distributed (NCCL on B200; gloo copies through
 host memory); `run_loopback` drives G virtual ranks in one process (tests).
 
 Results equal the single-GPU frame over the ranks' concatenated vertex streams: each
 key's records reach exactly one owner, 16.16 fixed-point sums are exactly associative,
-and every rung consumes the same effective (sum, count) values in the reference's
-order.  Only the slot a key occupies can differ (chains never cross slices), which
-matters only when a chain reaches probe_limit.
+and the replica holds the owners' cells verbatim, so every rung sees the same
+effective (sum, count) values.  Only the slot a key occupies can differ (probe windows
+wrap within a slice), which matters only when a chain reaches probe_limit.
 """
 
 from __future__ import annotations
@@ -41,8 +42,8 @@ from .keys import FilterConfig, as_f64, device
 from .pipeline import FrameStats, ResolveReport, VertexStream
 from .table import VoxelTable
 
-WORK_KEYS = 28
 _AGG_EMPTY = -1  # ~0 as int64
+_EMPTY_TAG = 0xFFFFFFFF00000000 - (1 << 64)  # as int64
 
 
 @dataclass
@@ -53,6 +54,13 @@ class Exchange:
     tensor: torch.Tensor
     send_rows: list
     recv_rows: list
+
+
+@dataclass
+class AllGather:
+    """Concatenate every rank's `tensor` (same shape on all ranks) in rank order."""
+
+    tensor: torch.Tensor
 
 
 @dataclass
@@ -67,26 +75,27 @@ def _next_pow2(x: int) -> int:
 
 
 class ShardedState:
-    """This rank's slices of the fine/coarse tables plus the aggregation scratch."""
+    """This rank's slices of the fine/coarse tables, the aggregation scratch and the
+    replica of the global tables used by the resolve."""
 
     def __init__(self, cfg: FilterConfig, rank: int, world: int, agg_capacity: int = 1 << 20):
         _lib.require_cuda()
         C = int(cfg.capacity)
         if world < 1 or world & (world - 1) or world > 64:
             raise ValueError("world must be a power of two <= 64")
-        if C < world or C & (C - 1):
-            raise ValueError("capacity must be a power of two >= world")
+        if C < 2 * world or C & (C - 1):
+            raise ValueError("capacity must be a power of two >= 2 * world")
         if not 0 <= rank < world:
             raise ValueError("rank out of range")
         self.cfg_capacity = C
         self.rank, self.world = int(rank), int(world)
         self.slice = C // world
-        local = C if world == 1 else 2 * self.slice
-        self.fine = VoxelTable(local, cfg.probe_limit, cfg.sum_mode, cfg.evict_horizon,
+        self.fine = VoxelTable(self.slice, cfg.probe_limit, cfg.sum_mode, cfg.evict_horizon,
                                cfg.evict_min_age)
-        self.coarse = (VoxelTable(local, cfg.probe_limit, cfg.sum_mode, cfg.evict_horizon,
+        self.coarse = (VoxelTable(self.slice, cfg.probe_limit, cfg.sum_mode, cfg.evict_horizon,
                                   cfg.evict_min_age) if cfg.multi_level else None)
         self.sum_mode = cfg.sum_mode
+        self.probe_limit = int(cfg.probe_limit)
         self.frame = 0
         dev = device()
         self._dev = dev
@@ -96,9 +105,17 @@ class ShardedState:
         self.owner_cursor = torch.zeros((2, world), dtype=torch.int64, device=dev)
         self.bad_flag = torch.zeros(1, dtype=torch.int32, device=dev)
         self._alloc_agg(_next_pow2(max(int(agg_capacity), 64)))
-        self.vertex_slot = torch.empty(0, dtype=torch.int32, device=dev)
-        self.work_slot = torch.empty(0, dtype=torch.int32, device=dev)
-        self.row_keys = torch.empty(0, dtype=torch.int64, device=dev)
+        # replica of the global tables (tags EMPTY until published), published entries
+        empty = torch.full((C,), _EMPTY_TAG, dtype=torch.int64, device=dev)
+        self.rep_fine_tags = empty
+        self.rep_fine_rec = torch.zeros((C, 4), dtype=torch.int64, device=dev)
+        self.rep_coarse_tags = empty.clone() if self.coarse is not None else None
+        self.rep_coarse_rec = (torch.zeros((C, 4), dtype=torch.int64, device=dev)
+                               if self.coarse is not None else None)
+        n_local = self.slice * (2 if self.coarse is not None else 1)
+        self.entries = torch.empty((n_local, 6), dtype=torch.int64, device=dev)
+        self.entry_count = torch.zeros(1, dtype=torch.int64, device=dev)
+        self.prev_gathered = None  # (entries [world * stride, 6], counts [world], stride)
         self.scratch: dict = {}
         self.regrows = 0
 
@@ -112,7 +129,7 @@ class ShardedState:
         self.agg_counts = torch.zeros(cap, dtype=torch.int64, device=dev)
         self.distinct = torch.empty(cap // 2, dtype=torch.int32, device=dev)
         self.send_records = torch.empty((cap // 2, 5), dtype=torch.int64, device=dev)
-        self.send_requests = torch.empty(cap // 2, dtype=torch.int64, device=dev)
+        self.send_requests = torch.empty(1, dtype=torch.int64, device=dev)
 
     def grow_agg(self, need: int):
         """Re-allocate the aggregation table for `need` distinct keys (empty)."""
@@ -130,34 +147,33 @@ class ShardedState:
             self.scratch[name] = b
         return b[:n].view(*shape)
 
-    def ensure_rows(self, n: int):
-        if self.vertex_slot.numel() < n:
-            self.vertex_slot = torch.empty(n, dtype=torch.int32, device=self._dev)
-            self.work_slot = torch.empty((n, WORK_KEYS), dtype=torch.int32, device=self._dev)
-            self.row_keys = torch.empty((n, 8), dtype=torch.int64, device=self._dev)
-
-    def c_shard(self, pixel_base: int) -> _lib.PfShard:
+    def c_shard(self) -> _lib.PfShard:
         s = _lib.PfShard()
         s.rank, s.world = self.rank, self.world
         s.log2_capacity = self.cfg_capacity.bit_length() - 1
         s.sum_mode = 0 if self.sum_mode == "fixed" else 1
-        s.pixel_base = int(pixel_base)
         s.agg_keys, s.agg_sums = self.agg_keys.data_ptr(), self.agg_sums.data_ptr()
         s.agg_counts, s.agg_capacity = self.agg_counts.data_ptr(), self.agg_capacity
         s.distinct, s.n_distinct = self.distinct.data_ptr(), self.n_distinct.data_ptr()
         s.overflow = self.overflow.data_ptr()
         s.owner_counts, s.owner_cursor = self.owner_counts.data_ptr(), self.owner_cursor.data_ptr()
-        s.vertex_slot = self.vertex_slot.data_ptr()
-        s.work_slot = self.work_slot.data_ptr()
-        s.row_keys = self.row_keys.data_ptr()
         return s
 
+    def c_replica(self) -> _lib.PfReplica:
+        r = _lib.PfReplica()
+        r.fine_tags, r.fine_records = self.rep_fine_tags.data_ptr(), self.rep_fine_rec.data_ptr()
+        r.coarse_tags = _lib.ptr(self.rep_coarse_tags)
+        r.coarse_records = _lib.ptr(self.rep_coarse_rec)
+        r.capacity = self.cfg_capacity
+        r.slice_log2 = self.slice.bit_length() - 1
+        r.probe_limit = self.probe_limit
+        r.sum_mode = 0 if self.sum_mode == "fixed" else 1
+        return r
 
-def _stats_message(st: ShardedState, records: bool) -> torch.Tensor:
-    """[world, 4] int64 per destination: records, requests, overflow, bad input."""
-    oc = st.owner_counts
-    cols = [oc[0] if records else torch.zeros_like(oc[0]), oc[1],
-            st.overflow.to(torch.int64).expand(st.world),
+
+def _stats_message(st: ShardedState) -> torch.Tensor:
+    """[world, 3] int64 per destination: records, overflow, bad input."""
+    cols = [st.owner_counts[0], st.overflow.to(torch.int64).expand(st.world),
             st.bad_flag.to(torch.int64).expand(st.world)]
     return torch.stack(cols, dim=1).contiguous()
 
@@ -165,16 +181,15 @@ def _stats_message(st: ShardedState, records: bool) -> torch.Tensor:
 def filter_frame_sharded(vertices, base_image, cfg: FilterConfig, st: ShardedState, spp: int,
                          seed: int, pixel_base: int = 0, composite: str = "band",
                          validate: bool = True, want_means: bool = True, phase_events=None):
-    """One frame on this rank (generator: yields Exchange / ReduceScatter).
+    """One frame on this rank (generator: yields Exchange / AllGather / ReduceScatter).
 
     composite="band": the rank's vertices all land in its pixel band
     [pixel_base, pixel_base + H*W) and `base_image` is that band (H x W x 3).
     composite="reduce": every rank's vertices address the whole image of H x W
     pixels (pixel_base 0) -- e.g. each rank traced other samples -- and the result is
     this rank's block of rows of the final image (H divisible by world).
-
-    phase_events: optional 4 torch.cuda.Events recorded at frame start, after the
-    round-1 key kernel, after the fine rung and at frame end.
+    phase_events: optional 4 torch.cuda.Events recorded at frame start, after the key
+    kernel, after the replica is built and at frame end.
 
     Returns (image, ResolveReport, FrameStats) via StopIteration.value."""
     if composite not in ("band", "reduce"):
@@ -189,7 +204,6 @@ def filter_frame_sharded(vertices, base_image, cfg: FilterConfig, st: ShardedSta
         raise ValueError("reduce composite needs H divisible by world and pixel_base 0")
     n_pix = H * W
     dev = base.device
-    st.ensure_rows(max(n, 1))
     cc = cfg.to_c()
     v, keep = vs.c_struct()
     ft = st.fine.c_table()
@@ -202,6 +216,8 @@ def filter_frame_sharded(vertices, base_image, cfg: FilterConfig, st: ShardedSta
     lookup_seed = rng.stream_base(seed, rng.STREAM_JITTER_LOOKUP)
     coarse_seed = rng.stream_base(seed, rng.STREAM_JITTER_LOOKUP if cfg.jitter
                                   else rng.STREAM_JITTER_ACCUM)
+    lk_index = st.buffer("lk_index", (max(n, 1),), torch.int64)
+    lk_fp = st.buffer("lk_fp", (max(n, 1),), torch.int32)
 
     def mark(k):
         if phase_events is not None:
@@ -213,102 +229,74 @@ def filter_frame_sharded(vertices, base_image, cfg: FilterConfig, st: ShardedSta
     if st.coarse is not None:
         st.coarse.begin_frame(frame, cfg)
 
-    # ---- round 1: records + fine lookups
+    # ---- insert: pre-aggregated records to their owners
     st.bad_flag.zero_()
     if validate and n:
         _lib.call("pf_check_contributions", vs.contribution.data_ptr(), 3 * n,
                   st.bad_flag.data_ptr(), stream)
     while True:
-        sh = st.c_shard(pixel_base)
+        sh = st.c_shard()
         _lib.call("pf_shard_keys", ctypes.byref(cc), ctypes.byref(v), ctypes.byref(sh), has_coarse,
-                  accum_seed, lookup_seed, st.bad_flag.data_ptr(), stream)
+                  accum_seed, lookup_seed, st.bad_flag.data_ptr(), lk_index.data_ptr(),
+                  lk_fp.data_ptr(), stream)
         mark(1)
         _lib.call("pf_shard_emit", ctypes.byref(sh), st.send_records.data_ptr(),
                   st.send_requests.data_ptr(), stream)
-        msg = _stats_message(st, True)
+        msg = _stats_message(st)
         recv = yield Exchange(msg, [1] * G, [1] * G)
         mine, theirs = msg.cpu().numpy(), recv.cpu().numpy()
-        if theirs[:, 3].any():
+        if theirs[:, 2].any():
             _lib.call("pf_shard_reset", ctypes.byref(sh), stream)
             raise ValueError("contributions must be finite and non-negative "
                              "(frame rejected on every rank; tables unchanged)")
-        if not theirs[:, 2].any():
+        if not theirs[:, 1].any():
             break
-        if mine[0, 2]:  # this rank overflowed: grow and redo its round-1 keys
+        if mine[0, 1]:  # this rank overflowed: grow and redo its keys
             st.grow_agg(int(st.n_distinct.item()))
         else:  # a peer overflowed: keep this rank's round, repeat the count exchange
             st.overflow.zero_()
             while True:
                 recv = yield Exchange(msg, [1] * G, [1] * G)
-                if not recv.cpu().numpy()[:, 2].any():
+                if not recv.cpu().numpy()[:, 1].any():
                     break
             theirs = recv.cpu().numpy()
             break
-    send_rec, send_req = mine[:, 0].tolist(), mine[:, 1].tolist()
-    recv_rec, recv_req = theirs[:, 0].tolist(), theirs[:, 1].tolist()
+    send_rec, recv_rec = mine[:, 0].tolist(), theirs[:, 0].tolist()
     records = yield Exchange(st.send_records[:sum(send_rec)], send_rec, recv_rec)
-    requests = yield Exchange(st.send_requests[:sum(send_req)], send_req, recv_req)
     _lib.call("pf_shard_apply", ctypes.byref(sh), ctypes.byref(ft),
               ctypes.byref(ct) if ct is not None else None, records.data_ptr(),
               int(records.shape[0]), int(frame), acc.data_ptr(), stream)
-    answers = st.buffer("answers1", (max(int(requests.shape[0]), 1), 4), torch.int64)
-    _lib.call("pf_shard_answer", ctypes.byref(sh), ctypes.byref(cc), ctypes.byref(ft),
-              ctypes.byref(ct) if ct is not None else None, requests.data_ptr(),
-              int(requests.shape[0]), answers.data_ptr(), res.data_ptr(), stream)
-    mine_ans = yield Exchange(answers[:int(requests.shape[0])], recv_req, send_req)
+    _lib.call("pf_shard_reset", ctypes.byref(sh), stream)
 
-    # fine rung
+    # ---- publish the owners' cells into every rank's replica
+    _lib.call("pf_shard_publish", ctypes.byref(sh), ctypes.byref(cc), ctypes.byref(ft),
+              ctypes.byref(ct) if ct is not None else None, st.entries.data_ptr(),
+              st.entry_count.data_ptr(), stream)
+    counts = yield AllGather(st.entry_count)
+    stride = int(counts.max().item()) if counts.numel() else 0
+    gathered = yield AllGather(st.entries[:stride])
+    rp = st.c_replica()
+    if st.prev_gathered is not None:
+        pg, pc, ps = st.prev_gathered
+        _lib.call("pf_replica_update", ctypes.byref(rp), pg.data_ptr(), pc.data_ptr(), G, ps, 1,
+                  stream)
+    counts_dev = counts.to(dev).contiguous()
+    _lib.call("pf_replica_update", ctypes.byref(rp), _lib.ptr(gathered) if stride else None,
+              counts_dev.data_ptr(), G, stride, 0, stream)
+    st.prev_gathered = (gathered, counts_dev, stride)
+    mark(2)
+
+    # ---- resolve this rank's vertices against the replica
     source = torch.empty(n, dtype=torch.uint8, device=dev)
     chosen = torch.empty((n, 3), dtype=torch.float64, device=dev) if want_means else None
     flat = st.buffer("flat", (n_pix, 3), torch.float64)
-    flat.zero_()
     work = st.buffer("work", (max(n, 1),), torch.int64)
     work_count = st.buffer("work_count", (1,), torch.int64)
-    work_count.zero_()
-    if mine_ans.shape[0] == 0:
-        mine_ans = st.buffer("answers_none", (1, 4), torch.int64)
-    _lib.call("pf_shard_resolve", ctypes.byref(sh), ctypes.byref(cc), ctypes.byref(v),
-              mine_ans.data_ptr(), flat.data_ptr(), n_pix, work.data_ptr(),
-              work_count.data_ptr(), source.data_ptr(), _lib.ptr(chosen), res.data_ptr(), stream)
-    mark(2)
-    _lib.call("pf_shard_reset", ctypes.byref(sh), stream)
-
-    # ---- round 2: neighbourhood + coarse lookups of the work rows
-    while True:
-        sh = st.c_shard(pixel_base)
-        _lib.call("pf_shard_fallback_keys", ctypes.byref(cc), ctypes.byref(v), ctypes.byref(sh),
-                  has_coarse, lookup_seed, coarse_seed, work.data_ptr(), work_count.data_ptr(),
-                  stream)
-        _lib.call("pf_shard_emit", ctypes.byref(sh), st.send_records.data_ptr(),
-                  st.send_requests.data_ptr(), stream)
-        msg = _stats_message(st, False)
-        recv = yield Exchange(msg, [1] * G, [1] * G)
-        mine, theirs = msg.cpu().numpy(), recv.cpu().numpy()
-        if not theirs[:, 2].any():
-            break
-        if mine[0, 2]:
-            st.grow_agg(int(st.n_distinct.item()))
-        else:
-            st.overflow.zero_()
-            while True:
-                recv = yield Exchange(msg, [1] * G, [1] * G)
-                if not recv.cpu().numpy()[:, 2].any():
-                    break
-            theirs = recv.cpu().numpy()
-            break
-    send_req, recv_req = mine[:, 1].tolist(), theirs[:, 1].tolist()
-    requests = yield Exchange(st.send_requests[:sum(send_req)], send_req, recv_req)
-    answers = st.buffer("answers2", (max(int(requests.shape[0]), 1), 4), torch.int64)
-    _lib.call("pf_shard_answer", ctypes.byref(sh), ctypes.byref(cc), ctypes.byref(ft),
-              ctypes.byref(ct) if ct is not None else None, requests.data_ptr(),
-              int(requests.shape[0]), answers.data_ptr(), res.data_ptr(), stream)
-    mine_ans = yield Exchange(answers[:int(requests.shape[0])], recv_req, send_req)
-    if mine_ans.shape[0] == 0:
-        mine_ans = st.buffer("answers_none", (1, 4), torch.int64)
-    _lib.call("pf_shard_ladder", ctypes.byref(sh), ctypes.byref(cc), ctypes.byref(v), has_coarse,
-              mine_ans.data_ptr(), work.data_ptr(), work_count.data_ptr(), flat.data_ptr(),
-              n_pix, source.data_ptr(), _lib.ptr(chosen), res.data_ptr(), stream)
-    _lib.call("pf_shard_reset", ctypes.byref(sh), stream)
+    fb_keys = st.buffer("fallback_keys", (max(n, 1), 8), torch.int64)
+    _lib.call("pf_resolve_replica", ctypes.byref(cc), ctypes.byref(v), ctypes.byref(rp),
+              lookup_seed, coarse_seed, lk_index.data_ptr(), lk_fp.data_ptr(), flat.data_ptr(),
+              n_pix, int(pixel_base), work.data_ptr(), work_count.data_ptr(), fb_keys.data_ptr(),
+              source.data_ptr(), _lib.ptr(chosen), res.data_ptr(), stream)
     del keep
 
     # ---- image
@@ -361,6 +349,21 @@ def _reduce_scatter_dist(rs: ReduceScatter, group=None) -> torch.Tensor:
     return out
 
 
+def _all_gather_dist(ag: AllGather, group=None) -> torch.Tensor:
+    import torch.distributed as dist
+    t = ag.tensor.contiguous()
+    g = dist.get_world_size(group)
+    via_host = t.is_cuda and dist.get_backend(group) == "gloo"
+    src = t.cpu() if via_host else t
+    if via_host:
+        parts = [torch.empty_like(src) for _ in range(g)]
+        dist.all_gather(parts, src, group=group)
+        return torch.cat(parts).to(t.device)
+    out = torch.empty((g * t.shape[0],) + tuple(t.shape[1:]), dtype=t.dtype, device=t.device)
+    dist.all_gather_into_tensor(out, src, group=group)
+    return out
+
+
 def run_dist(gen, group=None):
     """Drive one rank's frame generator with torch.distributed collectives."""
     try:
@@ -368,6 +371,8 @@ def run_dist(gen, group=None):
         while True:
             if isinstance(op, Exchange):
                 op = gen.send(_a2a_dist(op, group))
+            elif isinstance(op, AllGather):
+                op = gen.send(_all_gather_dist(op, group))
             elif isinstance(op, ReduceScatter):
                 op = gen.send(_reduce_scatter_dist(op, group))
             else:
@@ -385,7 +390,10 @@ def run_loopback(gens: list):
         kinds = {type(o) for o in ops}
         if len(kinds) != 1:
             raise RuntimeError(f"ranks disagree on the collective: {kinds}")
-        if isinstance(ops[0], Exchange):
+        if isinstance(ops[0], AllGather):
+            total = torch.cat([o.tensor for o in ops])
+            outs = [total.clone() for _ in range(G)]
+        elif isinstance(ops[0], Exchange):
             outs = []
             for r in range(G):
                 parts = []

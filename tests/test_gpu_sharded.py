@@ -145,8 +145,8 @@ def test_reduce_frame_multi_sample_matches_single(gpu, world):
 
 
 def test_aggregation_overflow_regrows(gpu):
-    """A tiny aggregation table overflows in both rounds; the ranks grow it, redo the
-    round in lockstep and still match the single-GPU frame."""
+    """A tiny aggregation table overflows; the rank grows it, the ranks redo the count
+    exchange in lockstep and still match the single-GPU frame."""
     from paper_1902_05942_b200 import sharded
     w, h = 64, 32
     s, base, fs = _box(w, h, 2, 9)
@@ -160,7 +160,7 @@ def test_aggregation_overflow_regrows(gpu):
                                          base[r * 16:(r + 1) * 16].contiguous(), cfg, states[r],
                                          1, 4, pixel_base=r * 16 * w) for r in range(2)]
     outs = sharded.run_loopback(gens)
-    assert states[0].regrows >= 2  # both rounds outgrew 64 slots
+    assert states[0].regrows >= 1  # the records outgrew 64 slots
     order = _band_order(s, w, h, 2)
     assert torch.equal(torch.cat([o[1].source for o in outs]), rep1.source[order])
     assert torch.equal(torch.cat([o[1].means for o in outs]), rep1.means[order])
@@ -193,7 +193,7 @@ def test_shard_abi_rejects_bad_geometry(gpu):
         sharded.ShardedState(cfg, 2, 2)
     st = sharded.ShardedState(cfg, 1, 2)
     st.world = 2
-    sh = st.c_shard(0)
+    sh = st.c_shard()
     sh.log2_capacity = 30
     import ctypes
     with pytest.raises(ValueError):

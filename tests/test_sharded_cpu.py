@@ -76,7 +76,7 @@ def protocol(rank: int, world: int, overflow_once: bool):
     """A frame-shaped collective sequence (sharded.filter_frame_sharded's exchanges
     with host tensors): counts + flags, records and requests with ragged splits, an
     overflow retry, answers back, a reduce-scatter.  Returns what it received."""
-    from paper_1902_05942_b200.sharded import Exchange, ReduceScatter
+    from paper_1902_05942_b200.sharded import AllGather, Exchange, ReduceScatter
     G = world
     got = {}
     overflowed = overflow_once and rank == 0
@@ -103,6 +103,7 @@ def protocol(rank: int, world: int, overflow_once: bool):
     back = yield Exchange(answers, recv_req, send_req)
     got["answers"] = back.clone()
     got["reqs_sent"] = reqs
+    got["gathered"] = (yield AllGather(torch.full((3, 6), 7 + rank, dtype=torch.int64))).clone()
     flat = torch.arange(8 * G * 3, dtype=torch.float64).reshape(8 * G, 3) * (rank + 1)
     got["band"] = (yield ReduceScatter(flat)).clone()
     return got
@@ -150,5 +151,7 @@ def test_gloo_world2_drivers_match_loopback(tmp_path, overflow_once):
         full = sum(torch.arange(8 * world * 3, dtype=torch.float64).reshape(8 * world, 3) * (p + 1)
                    for p in range(world))
         assert torch.equal(got["band"], full[8 * r:8 * (r + 1)])
+        assert torch.equal(got["gathered"], torch.cat([torch.full((3, 6), 7 + p, dtype=torch.int64)
+                                                       for p in range(world)]))
         if overflow_once:
             assert got["retries"] == 1
