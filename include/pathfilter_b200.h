@@ -57,6 +57,7 @@ typedef struct pf_config {
     int32_t sample_cap;
     uint64_t lod_ulps[2];    /* filled by the library from lod_threshold (callers leave 0):
                                 4-bit count of doubles between T[k] and 2^k, k = 0..31 */
+    double inv_base_voxel;   /* filled by the library: RN(1 / base_voxel) */
 } pf_config;
 
 /* VertexStream (src/tracer.py:732-767): row-major [n][3] float64 triples. */

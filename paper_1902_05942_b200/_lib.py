@@ -61,7 +61,7 @@ class PfConfig(ctypes.Structure):
                 ("jitter", ctypes.c_int32), ("multi_level", ctypes.c_int32),
                 ("coarse_delta", ctypes.c_int32), ("low_count_threshold", ctypes.c_int32),
                 ("temporal_mode", ctypes.c_int32), ("sample_cap", ctypes.c_int32),
-                ("lod_ulps", ctypes.c_uint64 * 2)]
+                ("lod_ulps", ctypes.c_uint64 * 2), ("inv_base_voxel", ctypes.c_double)]
 
 
 class PfVertices(ctypes.Structure):

@@ -508,11 +508,13 @@ struct KeyShared {
     uint32_t fp_bin;
     int has_fp_bin;
     double rbv;  // RN(1 / base_voxel): RN(1/step) = rbv * 2^-level exactly
+    int64_t lv0; // LOD of the unjittered vertex (before any level_delta)
 };
 
 __device__ __forceinline__ KeyShared key_shared(const pf_config &cfg, const VertexIn &x) {
     KeyShared k;
-    k.rbv = __drcp_rn(cfg.base_voxel);
+    k.rbv = cfg.inv_base_voxel;  // prepare_config: RN(1 / base_voxel)
+    k.lv0 = lod_level(x.dist, cfg);
     k.frame = tangent_frame(x.nrm[0], x.nrm[1], x.nrm[2]);
     k.aux = aux_word(cfg, x.nrm[0], x.nrm[1], x.nrm[2], x.omega, x.layer);
     k.has_fp_bin = cfg.include_normal && cfg.normal_in_fingerprint;
@@ -526,7 +528,7 @@ __device__ __forceinline__ KeyShared key_shared(const pf_config &cfg, const Vert
 __device__ __forceinline__ CellKey make_key(const pf_config &cfg, const VertexIn &x,
                                             const KeyShared &ks, int jit, double u, double v,
                                             int32_t level_delta, double jittered[3]) {
-    int64_t lv = clamp_level(lod_level(x.dist, cfg), level_delta);
+    int64_t lv = clamp_level(ks.lv0, level_delta);
     if (jit) {
         const double step = voxel_step(cfg.base_voxel, lv);
         double d2 = 0.0;

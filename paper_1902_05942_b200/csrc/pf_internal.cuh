@@ -69,6 +69,7 @@ inline int prepare_config(const char *fn, const pf_config *in, pf_config *out) {
         if (m < 0 || m > 15) return fail_arg(fn, "lod_threshold[k] must be within 15 ulps below 2^k");
         out->lod_ulps[k >> 4] |= static_cast<uint64_t>(m) << ((k & 15) * 4);
     }
+    out->inv_base_voxel = 1.0 / in->base_voxel;  // IEEE division: RN(1/base_voxel)
     return PF_OK;
 }
 

@@ -68,7 +68,7 @@ def test_cubin_is_sm100a():
 
 def test_struct_layouts():
     from paper_1902_05942_b200 import _lib
-    assert ctypes.sizeof(_lib.PfConfig) == 4 * 8 + 32 * 8 + 12 * 4 + 2 * 8
+    assert ctypes.sizeof(_lib.PfConfig) == 4 * 8 + 32 * 8 + 12 * 4 + 2 * 8 + 8
     assert ctypes.sizeof(_lib.PfVertices) == 10 * 8
     assert ctypes.sizeof(_lib.PfTable) == 8 * 8 + 4 * 4
     assert ctypes.sizeof(_lib.PfEvictEvent) == 32
