@@ -547,3 +547,37 @@ def test_filter_frame_rejects_invalid_contributions(gpu):
                 state.poll_validation(wait=True)
         st = state.fine.state()
         assert st["counts"].sum() == 0 and st["hist_counts"].sum() == len(vs)
+
+
+def test_empty_stream_frame(gpu):
+    """A frame with no vertices leaves the image at the base and every counter at 0
+    (the reference's empty-input handling, src/pipeline.py:157-160, 212-214)."""
+    import torch
+    cfg = gpu.FilterConfig(capacity=1024)
+    state = gpu.FrameState.from_config(cfg)
+    e3 = torch.zeros((0, 3), dtype=torch.float64, device="cuda")
+    e1 = torch.zeros(0, dtype=torch.int64, device="cuda")
+    vs = gpu.VertexStream(e3, e3, e3, e3, e3, e1, e1, e1, e1.to(torch.float64))
+    base = torch.rand((4, 5, 3), dtype=torch.float64, device="cuda")
+    for _ in range(2):
+        image, report, stats = gpu.filter_frame(vs, base, cfg, state, 1, 3)
+        assert torch.equal(image, base)
+        assert report.source.numel() == 0 and stats.probe_failures == 0
+    assert state.fine.occupied_count() == 0
+
+
+def test_probe_limit_failures_conserve_vertices(gpu):
+    """A table far too small for the frame: keys that find no slot are counted as
+    probe failures, every other vertex lands in exactly one cell."""
+    import torch
+    from paper_1902_05942_b200.streams import camera_footprint, closed_box_stream
+    s, base = closed_box_stream(64, 48, 2, 8)
+    cfg = gpu.FilterConfig(capacity=256, probe_limit=4, footprint_scale=camera_footprint(48))
+    state = gpu.FrameState.from_config(cfg)
+    vs = gpu.VertexStream(**s)
+    _, report, stats = gpu.filter_frame(vs, base, cfg, state, 1, 5)
+    n = len(vs)
+    assert stats.probe_failures > 0
+    assert state.fine.total_counts() + stats.probe_failures == n
+    assert state.coarse.total_counts() + stats.coarse_probe_failures == n
+    assert int(torch.bincount(report.source.to(torch.int64), minlength=4).sum()) == n

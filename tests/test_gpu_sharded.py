@@ -249,3 +249,22 @@ def test_run_dist_gloo_two_processes(gpu, tmp_path):
     assert torch.equal(torch.cat([r["means"] for r in res]), rep1.means.cpu())
     torch.testing.assert_close(torch.cat([r["image"] for r in res]), img1.cpu(), rtol=1e-12,
                                atol=1e-14)
+
+
+def test_rank_without_vertices(gpu):
+    """A rank whose band traced nothing still takes part in every collective."""
+    from paper_1902_05942_b200 import sharded
+    w, h = 32, 16
+    s, base, fs = _box(w, h, 2, 6)
+    cfg = gpu.FilterConfig(capacity=2048, footprint_scale=fs)
+    parts = _split_rows(s, w, h, 2)
+    parts[1] = {k: v[:0] for k, v in parts[1].items()}
+    single, [(img1, rep1, _)] = _single(gpu, parts[0], base, cfg, 1, 2)
+    states = [sharded.ShardedState(cfg, r, 2) for r in range(2)]
+    gens = [sharded.filter_frame_sharded(gpu.VertexStream(**parts[r]),
+                                         base[r * 8:(r + 1) * 8].contiguous(), cfg, states[r], 1,
+                                         2, pixel_base=r * 8 * w) for r in range(2)]
+    outs = sharded.run_loopback(gens)
+    assert torch.equal(outs[0][1].source, rep1.source)
+    assert torch.equal(outs[1][0], base[8:])
+    torch.testing.assert_close(outs[0][0], img1[:8], rtol=1e-12, atol=1e-14)
