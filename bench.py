@@ -36,6 +36,15 @@ ROOT = os.path.dirname(os.path.abspath(__file__))
 sys.path.insert(0, ROOT)
 
 W_PIX, H_PIX, BOUNCES = 1920, 1080, 4
+TEMPORAL = "integrate"
+# --workload: the default is the metric's configuration (BASELINE.json configs[2]); the
+# others are the remaining configs of BASELINE.json, for the record
+WORKLOADS = {
+    "hd4": (1920, 1080, 4, "integrate", "configs[2]"),
+    "hd1": (1920, 1080, 1, "integrate", "configs[1]"),
+    "hd-temporal": (1920, 1080, 1, "filter", "configs[3]: EMA blend + aging, one step = one frame"),
+    "uhd4": (3840, 2160, 4, "integrate", "configs[4] on one GPU"),
+}
 METRIC = "filtered path vertices/sec (insert+query); ms/frame at 1080p 1spp 4 bounces"
 WORKLOAD = "1920x1080 1spp, all vertices of 4-bounce paths (closed Cornell box, synthetic)"
 WORKLOAD_TRACED = ("1920x1080 1spp, all vertices of 4-bounce paths: SURVEY App. B closed box "
@@ -166,7 +175,16 @@ def _traffic(kernel: str):
 def make_config(pf):
     from paper_1902_05942_b200.streams import camera_footprint
     cap = 1 << (2 * W_PIX * H_PIX - 1).bit_length()
-    return pf.FilterConfig(capacity=cap, footprint_scale=camera_footprint(H_PIX))
+    return pf.FilterConfig(capacity=cap, footprint_scale=camera_footprint(H_PIX),
+                           temporal_mode=TEMPORAL)
+
+
+def workload_text(kind: str) -> str:
+    if kind == "synthetic":
+        return WORKLOAD
+    return (f"{W_PIX}x{H_PIX} 1spp, all vertices of {BOUNCES}-bounce paths: SURVEY App. B closed "
+            f"box traced on device (select_k 1..{BOUNCES}, rr_start 9, seed 1), "
+            f"temporal_mode {TEMPORAL}")
 
 
 def cpu_reference_frame(sample_stream, base, cfg_kwargs, seed, frame, state):
@@ -260,7 +278,7 @@ def run_reference_arm(args):
     stream_np = stream_to_numpy(stream)
     base_np = base.cpu().numpy()
     cap = 1 << (2 * W_PIX * H_PIX - 1).bit_length()
-    cfg_kwargs = dict(capacity=cap, footprint_scale=camera_footprint(H_PIX))
+    cfg_kwargs = dict(capacity=cap, footprint_scale=camera_footprint(H_PIX), temporal_mode=TEMPORAL)
     stride = 4
     total = args.warmup + args.steps
     setup, n, times, cores = cpu_baseline(stream_np, base_np, cfg_kwargs, total, stride)
@@ -272,7 +290,7 @@ def run_reference_arm(args):
         "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
         "ms_per_step": per * 1e3, "higher_is_better": True, "scaling": "weak",
         "vs_baseline": None, "dtype": "f64", "data": "synthetic",
-        "config": {"workload": WORKLOAD if args.stream == "synthetic" else WORKLOAD_TRACED,
+        "config": {"workload": workload_text(args.stream), "bench_workload": args.workload,
                    "vertices_per_frame": len(stream_np.pixel),
                    "sample_vertices_per_step": n, "capacity": cap, "tables": "fine+coarse"},
         "cpu_baseline": {"value": value, "unit": "vertices/s", "cores": cores,
@@ -405,7 +423,8 @@ def run_b200(args):
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu:
         stream_np = stream_to_numpy(stream)
-        kwargs = dict(capacity=cfg.capacity, footprint_scale=cfg.footprint_scale)
+        kwargs = dict(capacity=cfg.capacity, footprint_scale=cfg.footprint_scale,
+                      temporal_mode=cfg.temporal_mode)
         stride = 4
         setup, ns, times, cores = cpu_baseline(stream_np, base.cpu().numpy(), kwargs, 2, stride)
         cpu = {"value": ns / min(times), "unit": "vertices/s", "cores": cores,
@@ -424,7 +443,7 @@ def run_b200(args):
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms_per_step,
             "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
             "data": "synthetic",
-            "config": {"workload": WORKLOAD if args.stream == "synthetic" else WORKLOAD_TRACED,
+            "config": {"workload": workload_text(args.stream), "bench_workload": args.workload,
                        "vertices_per_frame": n, "pixels": n_pix,
                        "capacity": cfg.capacity, "tables": "fine+coarse",
                        "temporal_mode": cfg.temporal_mode, "sum_mode": cfg.sum_mode,
@@ -505,10 +524,14 @@ def main():
     ap.add_argument("--impl", default="b200", choices=["b200", "reference"])
     ap.add_argument("--no-cpu", action="store_true", help="skip the cpu_baseline leg")
     ap.add_argument("--no-e2e", action="store_true", help="skip the host-buffer e2e leg")
+    ap.add_argument("--workload", default="hd4", choices=list(WORKLOADS),
+                    help="BASELINE.json configuration (default: the metric's, configs[2])")
     ap.add_argument("--stream", default="traced", choices=["traced", "synthetic"],
                     help="benchmark input: App. B scene traced on device, or the synthetic "
                          "closed-box generator")
     args = ap.parse_args()
+    global W_PIX, H_PIX, BOUNCES, TEMPORAL
+    W_PIX, H_PIX, BOUNCES, TEMPORAL, _ = WORKLOADS[args.workload]
     if args.impl == "reference":
         return run_reference_arm(args)
     return run_b200(args)
