@@ -395,6 +395,13 @@ int pf_begin_frame(const pf_table *t, int64_t frame, int32_t mode, double ema_al
                    double delta_max, int32_t sample_cap, int64_t *horizon_clears,
                    void *stream);
 
+/* begin_frame on a fine and (optionally) a coarse table plus the input check of
+ * `count` contributions (vals/bad may be NULL: no check; *bad is cleared first), in one
+ * launch -- the prologue of a frame (pf_filter_frame, the sharded frame). */
+int pf_begin_frame_checked(const pf_table *fine, const pf_table *coarse, int64_t frame,
+                           int32_t mode, double ema_alpha, double delta_max, int32_t sample_cap,
+                           int64_t *clears_fine, int64_t *clears_coarse, const double *vals,
+                           int64_t count, int32_t *bad, void *stream);
 /* Input validation of accumulate_batch (src/table.py:127-129): *bad (int32, device) is
  * set to 1 when any of the `count` float64 values is NaN, infinite or negative. */
 int pf_check_contributions(const double *vals, int64_t count, int32_t *bad, void *stream);

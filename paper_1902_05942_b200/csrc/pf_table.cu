@@ -676,6 +676,18 @@ int frame_prologue(const pf_table *fine, const pf_table *coarse, int64_t frame, 
 
 extern "C" {
 
+int pf_begin_frame_checked(const pf_table *fine, const pf_table *coarse, int64_t frame,
+                           int32_t mode, double ema_alpha, double delta_max, int32_t sample_cap,
+                           int64_t *clears_fine, int64_t *clears_coarse, const double *vals,
+                           int64_t count, int32_t *bad, void *stream) {
+    cudaStream_t st = as_stream(stream);
+    if (bad && cudaMemsetAsync(bad, 0, sizeof(int32_t), st) != cudaSuccess)
+        return check_launch("pf_begin_frame_checked");
+    return frame_prologue(fine, coarse, frame, mode, ema_alpha, delta_max, sample_cap,
+                          clears_fine, clears_coarse, vals, count, bad, nullptr, 0, nullptr, 0,
+                          nullptr, st);
+}
+
 int pf_selftest_division(uint64_t seed, int64_t n, double base_voxel, int64_t *mismatches,
                          void *stream) {
     const char *fn = "pf_selftest_division";

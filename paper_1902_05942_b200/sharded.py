@@ -38,7 +38,7 @@ import numpy as np
 import torch
 
 from . import _lib, rng
-from .keys import FilterConfig, as_f64, device
+from .keys import FilterConfig, as_f64, device, temporal_code
 from .pipeline import FrameStats, ResolveReport, VertexStream
 from .table import VoxelTable
 
@@ -224,16 +224,20 @@ def filter_frame_sharded(vertices, base_image, cfg: FilterConfig, st: ShardedSta
             phase_events[k].record()
 
     mark(0)
-    # temporal update on the local slices (src/pipeline.py:331-333)
-    st.fine.begin_frame(frame, cfg)
+    # temporal update on the local slices (src/pipeline.py:331-333) and the input check,
+    # side by side in one launch
+    check = validate and n > 0
+    _lib.call("pf_begin_frame_checked", ctypes.byref(ft), ctypes.byref(ct) if ct is not None
+              else None, int(frame), temporal_code(cfg.temporal_mode), float(cfg.ema_alpha),
+              float(cfg.delta_max), int(cfg.sample_cap), st.fine._clears.data_ptr(),
+              st.coarse._clears.data_ptr() if st.coarse is not None else None,
+              vs.contribution.data_ptr() if check else None, 3 * n,
+              st.bad_flag.data_ptr(), stream)
+    st.fine.frame = frame
     if st.coarse is not None:
-        st.coarse.begin_frame(frame, cfg)
+        st.coarse.frame = frame
 
     # ---- insert: pre-aggregated records to their owners
-    st.bad_flag.zero_()
-    if validate and n:
-        _lib.call("pf_check_contributions", vs.contribution.data_ptr(), 3 * n,
-                  st.bad_flag.data_ptr(), stream)
     while True:
         sh = st.c_shard()
         _lib.call("pf_shard_keys", ctypes.byref(cc), ctypes.byref(v), ctypes.byref(sh), has_coarse,
