@@ -164,7 +164,8 @@ def _peaks():
 
 
 def _traffic(kernel: str):
-    """dram bytes per launch from the committed ncu --set full summary, if any."""
+    """dram bytes (or, for "<kernel>_inst", warp instructions) per launch from the
+    committed ncu --set full summary, if any."""
     p = os.path.join(ROOT, "profiles", "ncu_traffic.json")
     if os.path.exists(p):
         with open(p) as fh:
@@ -415,6 +416,18 @@ def run_b200(args):
                 "peak_kind": peak_kind, "unit": "GB/s", "frac": achieved / peak,
                 "bytes_per_launch": kbytes, "traffic": _traffic(kname)}
 
+    # the insert kernel is issue-bound, not HBM-bound: its instruction issue rate against
+    # the SMs' peak (148 SMs x 4 schedulers x 1 warp-instruction per clock), with the
+    # per-launch instruction count from the committed ncu capture (same workload)
+    issue = None
+    inst = _traffic("insert_frame_kernel_inst") if kname == "insert_frame_kernel" else None
+    if inst and args.workload == "hd4" and args.stream == "traced":
+        sm_mhz = clocks.summary().get("sm_mhz") or 1965.0
+        ipeak = 148 * 4 * sm_mhz * 1e6
+        iach = inst / (kms / 1e3)
+        issue = {"bound": "issue", "kernel": kname, "achieved": iach, "peak": ipeak,
+                 "unit": "warp-inst/s", "frac": iach / ipeak, "inst_per_launch": inst}
+
     # end to end through the public API with host buffers
     e2e = None
     if not args.no_e2e:
@@ -450,7 +463,8 @@ def run_b200(args):
                        "parallelism": (f"key-sharded tables x{world} (NCCL all-to-all), "
                                        f"1 spp per GPU" if world > 1 else "single"),
                        "l2": "inputs 1.0 GB per frame > 126 MB L2 (no flush needed)"},
-            "phases_ms": ph, "roofline": roofline, "cpu_baseline": cpu, "e2e": e2e,
+            "phases_ms": ph, "roofline": roofline, "roofline_issue": issue, "cpu_baseline": cpu,
+            "e2e": e2e,
             "gpu_launches": launches, "clocks": clocks.summary(),
         }
         print(json.dumps(line), flush=True)
