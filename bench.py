@@ -173,6 +173,19 @@ def _traffic(kernel: str):
     return None
 
 
+def _l2_red_peak():
+    """Sustained random-address RED.U64 rate (ops/s) measured by tools/l2atomics.cu."""
+    p = os.path.join(ROOT, "profiles", "r1_l2atomics.log")
+    if not os.path.exists(p):
+        return None
+    with open(p) as fh:
+        for line in fh:
+            d = json.loads(line)
+            if d.get("pattern") == "red_u64_random":
+                return d["gops_per_s"] * 1e9
+    return None
+
+
 def make_config(pf):
     from paper_1902_05942_b200.streams import camera_footprint
     cap = 1 << (2 * W_PIX * H_PIX - 1).bit_length()
@@ -427,6 +440,15 @@ def run_b200(args):
         iach = inst / (kms / 1e3)
         issue = {"bound": "issue", "kernel": kname, "achieved": iach, "peak": ipeak,
                  "unit": "warp-inst/s", "frac": iach / ipeak, "inst_per_launch": inst}
+    # and its L2 reductions against the sustained random-address RED rate measured by
+    # tools/l2atomics.cu on this pool (profiles/r1_l2atomics.log)
+    atomics = None
+    reds = _traffic("insert_frame_kernel_red_sectors") if kname == "insert_frame_kernel" else None
+    red_peak = _l2_red_peak()
+    if reds and red_peak and args.workload == "hd4" and args.stream == "traced":
+        rach = reds / (kms / 1e3)
+        atomics = {"bound": "l2_atomics", "kernel": kname, "achieved": rach, "peak": red_peak,
+                   "unit": "red/s", "frac": rach / red_peak, "red_per_launch": reds}
 
     # end to end through the public API with host buffers
     e2e = None
@@ -463,7 +485,8 @@ def run_b200(args):
                        "parallelism": (f"key-sharded tables x{world} (NCCL all-to-all), "
                                        f"1 spp per GPU" if world > 1 else "single"),
                        "l2": "inputs 1.0 GB per frame > 126 MB L2 (no flush needed)"},
-            "phases_ms": ph, "roofline": roofline, "roofline_issue": issue, "cpu_baseline": cpu,
+            "phases_ms": ph, "roofline": roofline, "roofline_issue": issue,
+            "roofline_atomics": atomics, "cpu_baseline": cpu,
             "e2e": e2e,
             "gpu_launches": launches, "clocks": clocks.summary(),
         }
