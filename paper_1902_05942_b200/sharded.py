@@ -278,7 +278,8 @@ def filter_frame_sharded(vertices, base_image, cfg: FilterConfig, st: ShardedSta
               st.entry_count.data_ptr(), stream)
     counts = yield AllGather(st.entry_count)
     stride = int(counts.max().item()) if counts.numel() else 0
-    gathered = yield AllGather(st.entries[:stride])
+    # every rank saw the same counts, so all skip an empty gather together
+    gathered = (yield AllGather(st.entries[:stride])) if stride else st.entries[:0]
     rp = st.c_replica()
     if st.prev_gathered is not None:
         pg, pc, ps = st.prev_gathered
