@@ -47,8 +47,6 @@ WORKLOADS = {
 }
 METRIC = "filtered path vertices/sec (insert+query); ms/frame at 1080p 1spp 4 bounces"
 WORKLOAD = "1920x1080 1spp, all vertices of 4-bounce paths (closed Cornell box, synthetic)"
-WORKLOAD_TRACED = ("1920x1080 1spp, all vertices of 4-bounce paths: SURVEY App. B closed box "
-                   "traced on device (select_k 1..4, rr_start 9, seed 1)")
 
 
 def make_stream(kind: str, rank: int = 0, device=None):

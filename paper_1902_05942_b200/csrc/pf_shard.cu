@@ -27,9 +27,6 @@ constexpr uint64_t kAggEmpty = ~0ull;
 enum : int {
     kKindFineRecord = 0,
     kKindCoarseRecord = 1,
-    kKindFineLookup = 2,
-    kKindNeighbour = 3,
-    kKindCoarseLookup = 4,
 };
 
 // Per-launch constants derived from pf_shard on the host.
