@@ -37,12 +37,12 @@ enum pf_sum_mode { PF_SUM_FIXED = 0, PF_SUM_FLOAT = 1 };
 /* FilterConfig (src/keys.py:30-79) reduced to what the device reads. */
 typedef struct pf_config {
     double c_lod;            /* footprint_scale * s_pixels / base_voxel, evaluated on the host
-                                exactly as src/keys.py:324 does */
+                                exactly as src/keys.py:246 does */
     double base_voxel;
     double ema_alpha;
     double delta_max;
     double lod_threshold[32];/* [k] = smallest double r with floor(np.log2(r)) >= k, k=1..31
-                                (exact floor(log2) of src/keys.py:325; [0] unused) */
+                                (exact floor(log2) of src/keys.py:247; [0] unused) */
     int32_t normal_bins;
     int32_t incident_angle_bins;
     int32_t include_normal;
@@ -60,7 +60,7 @@ typedef struct pf_config {
     double inv_base_voxel;   /* filled by the library: RN(1 / base_voxel) */
 } pf_config;
 
-/* VertexStream (src/tracer.py:732-767): row-major [n][3] float64 triples. */
+/* VertexStream (src/tracer.py:66-104): row-major [n][3] float64 triples. */
 typedef struct pf_vertices {
     const double *position;
     const double *normal;
@@ -90,7 +90,7 @@ typedef struct pf_table {
     int32_t evict_horizon;
 } pf_table;
 
-/* KeyArrays (src/keys.py:380-398); every pointer may be NULL (not written). */
+/* KeyArrays (src/keys.py:302-320); every pointer may be NULL (not written). */
 typedef struct pf_key_out {
     int64_t *qx, *qy, *qz, *level;
     uint64_t *aux;
@@ -160,7 +160,7 @@ int pf_lookup_slots(const uint64_t *tags, int64_t capacity, const uint64_t *idx,
 
 /* ---- 2. filter API ---------------------------------------------------------------- */
 
-/* keys.make_key_arrays (src/keys.py:420-437) with explicit jitter draws u1/u2
+/* keys.make_key_arrays (src/keys.py:342-359) with explicit jitter draws u1/u2
  * (NULL = no jitter). */
 int pf_make_key_arrays(const pf_config *cfg, const pf_vertices *v, const double *u1,
                        const double *u2, int32_t level_delta, pf_key_out *out, void *stream);
@@ -168,7 +168,7 @@ int pf_make_key_arrays(const pf_config *cfg, const pf_vertices *v, const double 
  * src/rng.py:62-78 keyed by path id; stream_base = mix64(seed ^ stream_tag*G). */
 int pf_vertex_keys(const pf_config *cfg, const pf_vertices *v, uint64_t stream_base,
                    int32_t level_delta, pf_key_out *out, void *stream);
-/* keys.hash_arrays (src/keys.py:405-417); normal_fp_bins may be NULL. */
+/* keys.hash_arrays (src/keys.py:327-339); normal_fp_bins may be NULL. */
 int pf_hash_arrays(const int64_t *qx, const int64_t *qy, const int64_t *qz,
                    const int64_t *level, const uint64_t *aux, const uint32_t *normal_fp_bins,
                    int64_t n, uint64_t *index, uint32_t *fingerprint, void *stream);
@@ -357,7 +357,7 @@ typedef struct pf_scene {
     int32_t width, height;
 } pf_scene;
 
-/* TraceOptions (src/tracer.py:34-42). */
+/* TraceOptions (src/tracer.py:35-43). */
 typedef struct pf_trace_options {
     int32_t max_depth;
     int32_t rr_start;

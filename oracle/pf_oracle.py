@@ -170,7 +170,7 @@ def jitter_draws(seed: int, stream: int, pixel, sample):
 # ---------------------------------------------------------------- keys (src/keys.py)
 
 def lod(distance: np.ndarray, cfg: Config) -> np.ndarray:
-    """floor(log2(max(d * C, 1))) clamped to 31 (src/keys.py:323-326)."""
+    """floor(log2(max(d * C, 1))) clamped to 31 (src/keys.py:245-248)."""
     c_lod = cfg.footprint_scale * cfg.s_pixels / cfg.base_voxel
     ratio = distance * c_lod
     lv = np.floor(np.log2(np.maximum(ratio, 1.0))).astype(np.int64)
@@ -178,7 +178,7 @@ def lod(distance: np.ndarray, cfg: Config) -> np.ndarray:
 
 
 def tangent_frame(n: np.ndarray):
-    """Branchless ONB, evaluated left to right (src/keys.py:329-336)."""
+    """Branchless ONB, evaluated left to right (src/keys.py:251-258)."""
     x, y, z = n[:, 0], n[:, 1], n[:, 2]
     s = np.where(z >= 0.0, 1.0, -1.0)
     a = -1.0 / (s + z)
@@ -189,7 +189,7 @@ def tangent_frame(n: np.ndarray):
 
 
 def disc(u1, u2):
-    """Polar warp to the radius-1/2 disc (src/keys.py:342-345)."""
+    """Polar warp to the radius-1/2 disc (src/keys.py:264-267)."""
     r = 0.5 * np.sqrt(u1)
     phi = (2.0 * math.pi) * u2
     return r * np.cos(phi), r * np.sin(phi)
@@ -200,13 +200,13 @@ def voxel_step(level: np.ndarray, cfg: Config) -> np.ndarray:
 
 
 def jitter(pos, nrm, level, u, v, cfg: Config):
-    """x + (u t1 + v t2) * step (src/keys.py:339-348)."""
+    """x + (u t1 + v t2) * step (src/keys.py:261-270)."""
     t1, t2 = tangent_frame(nrm)
     return pos + (u[:, None] * t1 + v[:, None] * t2) * voxel_step(level, cfg)[:, None]
 
 
 def octa_bins(n: np.ndarray, bins: int) -> np.ndarray:
-    """Octahedral normal bin by*bins+bx (src/keys.py:351-361)."""
+    """Octahedral normal bin by*bins+bx (src/keys.py:273-283)."""
     s = np.maximum(np.abs(n).sum(axis=1), 1e-300)
     p = n / s[:, None]
     px, py, pz = p[:, 0], p[:, 1], p[:, 2]
@@ -219,7 +219,7 @@ def octa_bins(n: np.ndarray, bins: int) -> np.ndarray:
 
 
 def aux_word(nrm, omega_r, layer, cfg: Config) -> np.ndarray:
-    """Normal bin | angle bin << 16 | layer << 24 (src/keys.py:364-377)."""
+    """Normal bin | angle bin << 16 | layer << 24 (src/keys.py:286-299)."""
     aux = np.zeros(len(nrm), np.uint64)
     if cfg.include_normal and not cfg.normal_in_fingerprint:
         aux |= octa_bins(nrm, cfg.normal_bins).astype(np.uint64)
@@ -235,7 +235,7 @@ def aux_word(nrm, omega_r, layer, cfg: Config) -> np.ndarray:
 
 
 def cell_hashes(qx, qy, qz, level, aux, fp_bins=None):
-    """Index hash and fingerprint over (qx,qy,qz,level,aux) (src/keys.py:405-417)."""
+    """Index hash and fingerprint over (qx,qy,qz,level,aux) (src/keys.py:327-339)."""
     fields = [np.asarray(f).astype(np.uint64) for f in (qx, qy, qz, level, aux)]
     n = len(fields[0])
     h = np.full(n, INIT_INDEX, np.uint64)
@@ -265,7 +265,7 @@ class Keys:
 
 def keys(pos, nrm, omega_r, layer, dist, cfg: Config, u=None, v=None,
          level_delta: int = 0) -> Keys:
-    """make_key_arrays restated (src/keys.py:420-437); u, v are the disc offsets."""
+    """make_key_arrays restated (src/keys.py:342-359); u, v are the disc offsets."""
     lv = np.minimum(lod(dist, cfg) + level_delta, MAX_LEVEL)
     if cfg.jitter and u is not None:
         x = jitter(pos, nrm, lv, u, v, cfg)

@@ -27,13 +27,12 @@ from .temporal import blend, migrate_resolution, reevaluation_deltas, select_rep
     temporal_difference
 from .tracer import TraceOptions, TraceResult, reevaluate, trace
 
-BACKEND = "b200"
+from ._backend import BACKEND, available_backends
+from .keys import aux_bits_array, jittered_positions, levels_array, normal_bins_array, \
+    tangent_basis_array
+from .pipeline import VertexDescriptor
+
 __version__ = "0.1.0"
-
-
-def available_backends() -> list:
-    """src/_backend.py: the kernel backends this build provides."""
-    return [BACKEND]
 
 
 __all__ = [
@@ -47,5 +46,6 @@ __all__ = [
     "EMPTY_TAG", "EvictionEvent", "InsertOutcome", "Outcome", "VoxelTable", "fixed_to_float",
     "pack_priority", "quantize_fixed", "blend", "migrate_resolution", "reevaluation_deltas",
     "select_replay_ids", "temporal_difference", "TraceOptions", "TraceResult", "reevaluate",
-    "trace", "read_ppm", "tonemap", "write_ppm",
+    "trace", "read_ppm", "tonemap", "write_ppm", "VertexDescriptor", "levels_array",
+    "tangent_basis_array", "jittered_positions", "normal_bins_array", "aux_bits_array",
 ]

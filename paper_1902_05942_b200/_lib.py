@@ -231,6 +231,18 @@ def require_cuda() -> torch.device:
     return torch.device("cuda", torch.cuda.current_device())
 
 
+BACKEND = "b200"
+
+
+def check_backend(name: str | None) -> None:
+    """get_kernels (src/_backend.py:33-42): None or this build's name selects the device
+    kernels; "native" (the reference's compiled backend) is accepted as an alias.  The
+    reference's "python" backend is a CPU path and does not exist here."""
+    if name is None or name in (BACKEND, "native"):
+        return
+    raise ValueError(f"unknown backend {name!r}")
+
+
 def call(name: str, *args) -> None:
     """Invoke a C-ABI entry point and raise on a nonzero pf_status."""
     L = lib()

@@ -1,7 +1,7 @@
 // Device building blocks of the hashed path-space filter (sm_100a).
 //
 // Everything that must be bit-exact with the reference lives here: the counter
-// RNG (src/rng.py), the key recipe (src/keys.py:323-437) and the
+// RNG (src/rng.py), the key recipe (src/keys.py:245-359) and the
 // per-slot temporal math (src/table.py:205-298).  The whole library is compiled
 // with -fmad=false, and the FP64 key arithmetic additionally spells every
 // multiply/add with __dmul_rn/__dadd_rn so numpy's op order (no FMA contraction)
@@ -22,15 +22,15 @@ constexpr uint64_t kAgeMask = 0xFFFFFFull;              // src/_native.pyx:75 (p
 constexpr uint64_t kPrioAgeMask = 0xFFFFFEull;          // src/table.py:40 (packing side)
 constexpr uint64_t kFpMask = 0xFFFFFFFFull;
 // Transient tag held while an eviction wipes the victim cell.  Fingerprint bits are
-// the sentinel 0 (never a real key, src/keys.py:96) so nothing matches it, and it
+// the sentinel 0 (never a real key, src/keys.py:18, 214-215) so nothing matches it, and it
 // is never EMPTY; probers that meet it wait for the evictor to publish the new tag.
 constexpr uint64_t kBusyTag = 0ull;
 constexpr uint64_t kGolden = 0x9E3779B97F4A7C15ull;     // src/rng.py:16
 constexpr uint64_t kInitIndex = 0x9E3779B97F4A7C15ull;  // src/keys.py:22
 constexpr uint64_t kInitFp = 0xC2B2AE3D27D4EB4Full;     // src/keys.py:23
-constexpr double kTwoPi = 6.283185307179586;            // 2.0 * math.pi (src/keys.py:343)
+constexpr double kTwoPi = 6.283185307179586;            // 2.0 * math.pi (src/keys.py:265)
 constexpr double kFixedScale = 65536.0;                 // src/table.py:38
-constexpr int kMaxLevel = 31;                           // src/keys.py:97
+constexpr int kMaxLevel = 31;                           // src/keys.py:19
 
 // ------------------------------------------------------------------ integer helpers
 
@@ -264,7 +264,7 @@ __device__ __forceinline__ void glibc_sincos(double x, double &sn, double &cs,
 }
 
 // Disc offsets: r = 0.5*sqrt(u1), phi = 2pi*u2, (r cos phi, r sin phi)
-// (src/keys.py:342-345).  sqrt is IEEE-exact and sin/cos are glibc's (glibc_sincos),
+// (src/keys.py:264-267).  sqrt is IEEE-exact and sin/cos are glibc's (glibc_sincos),
 // so jittered positions equal numpy's bit for bit.
 #ifndef PF_GLIBC_SINCOS
 #define PF_GLIBC_SINCOS 1
@@ -285,7 +285,7 @@ __device__ __forceinline__ void disc_offset(double u1, double u2, double &u, dou
 
 // ------------------------------------------------------------------ keys (src/keys.py)
 
-// floor(log2(max(d * c_lod, 1))) clamped to 31 (src/keys.py:323-326).  numpy's log2
+// floor(log2(max(d * c_lod, 1))) clamped to 31 (src/keys.py:245-248).  numpy's log2
 // rounds up to k just below 2^k, so the exact floor is exponent + (r >= T[e+1]).
 // T[k] = 2^k - m_k ulps with m_k < 16 packed as 4-bit fields in cfg.lod_ulps, so
 // ratio >= T[e+1] <=> mantissa >= 2^52 - m_{e+1}: pure integer work on the bits
@@ -333,7 +333,7 @@ struct Frame3 {
     double t1[3], t2[3];
 };
 
-// Branchless ONB (src/keys.py:329-336) in numpy's left-to-right order.
+// Branchless ONB (src/keys.py:251-258) in numpy's left-to-right order.
 __device__ __forceinline__ Frame3 tangent_frame(double x, double y, double z) {
     const double s = (z >= 0.0) ? 1.0 : -1.0;
     const double a = -__drcp_rn(dadd(s, z));  // -1.0 / (s + z): negation is exact
@@ -348,7 +348,7 @@ __device__ __forceinline__ Frame3 tangent_frame(double x, double y, double z) {
     return f;
 }
 
-// Octahedral normal bin (src/keys.py:351-361).
+// Octahedral normal bin (src/keys.py:273-283).
 __device__ __forceinline__ int64_t octa_bin(double x, double y, double z, int bins) {
     const double s = np_max(dadd(dadd(fabs(x), fabs(y)), fabs(z)), 1e-300);
     const double rs = __drcp_rn(s);
@@ -369,7 +369,7 @@ __device__ __forceinline__ int64_t octa_bin(double x, double y, double z, int bi
     return by * bins + bx;
 }
 
-// aux word (src/keys.py:364-377).  The incident-angle dot product follows numpy's
+// aux word (src/keys.py:286-299).  The incident-angle dot product follows numpy's
 // einsum("ij,ij->i") reduction order for length 3: (n0*o0 + n2*o2) + n1*o1
 // (measured in this image; see tests/test_oracle_golden.py).
 __device__ __forceinline__ uint64_t aux_word(const pf_config &cfg, double nx, double ny,
@@ -401,7 +401,7 @@ struct CellHash {
     uint32_t fp;
 };
 
-// hash_arrays (src/keys.py:405-417).
+// hash_arrays (src/keys.py:327-339).
 __device__ __forceinline__ CellHash cell_hash(int64_t qx, int64_t qy, int64_t qz, int64_t level,
                                               uint64_t aux, int has_fp_bin, uint32_t fp_bin) {
     const uint64_t f[5] = {static_cast<uint64_t>(qx), static_cast<uint64_t>(qy),
@@ -523,7 +523,7 @@ __device__ __forceinline__ KeyShared key_shared(const pf_config &cfg, const Vert
     return k;
 }
 
-// make_key_arrays for one vertex and one level_delta (src/keys.py:420-437).
+// make_key_arrays for one vertex and one level_delta (src/keys.py:342-359).
 // jit = 0 disables jitter; (u, v) are the disc offsets.
 __device__ __forceinline__ CellKey make_key(const pf_config &cfg, const VertexIn &x,
                                             const KeyShared &ks, int jit, double u, double v,

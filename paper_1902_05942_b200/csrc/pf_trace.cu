@@ -19,8 +19,8 @@ namespace pf {
 
 namespace {
 
-constexpr double kTMin = 1e-7;                 // src/tracer.py:28
-constexpr double kShadowShrink = 1.0 - 1e-6;   // src/tracer.py:29
+constexpr double kTMin = 1e-7;                 // src/tracer.py:30
+constexpr double kShadowShrink = 1.0 - 1e-6;   // src/tracer.py:31
 constexpr double kDetEps = 1e-14;              // src/_native.pyx:72
 constexpr double kPi = 3.141592653589793;      // math.pi
 constexpr double kTwoPiT = 6.283185307179586;  // 2.0 * math.pi

@@ -84,14 +84,14 @@ class FilterConfig:
             raise ValueError("ema_alpha must be in [0, 1]")
 
     def for_camera(self, fov: float, image_height: int) -> "FilterConfig":
-        """Copy with footprint_scale derived from a camera (src/keys.py:152-154)."""
+        """Copy with footprint_scale derived from a camera (src/keys.py:74-76)."""
         return replace(self, footprint_scale=2.0 * math.tan(fov / 2.0) / image_height)
 
     def voxel_size(self, level: int) -> float:
         return self.base_voxel * float(2 ** level)
 
     def to_c(self) -> _lib.PfConfig:
-        """The pf_config the kernels read; c_lod evaluated as src/keys.py:324 does.
+        """The pf_config the kernels read; c_lod evaluated as src/keys.py:246 does.
         Cached per field values (it is rebuilt only when a knob changes)."""
         key = tuple(getattr(self, f) for f in self.__dataclass_fields__)
         cached = self.__dict__.get("_c_cache")
@@ -201,7 +201,7 @@ def u32_numpy(t: torch.Tensor) -> np.ndarray:
 
 @dataclass
 class KeyArrays:
-    """Struct-of-arrays CellKeys plus hashes (src/keys.py:380-398), on the device.
+    """Struct-of-arrays CellKeys plus hashes (src/keys.py:302-320), on the device.
 
     index holds uint64 bits in an int64 tensor and fingerprint uint32 bits in an
     int32 tensor; numpy() returns the reference dtypes."""
@@ -266,7 +266,7 @@ def vertices_c(position, normal, omega_r, layer_id, camera_distance, pixel=None,
 
 def make_key_arrays(position, normal, omega_r, layer_id, camera_distance,
                     cfg: FilterConfig, u1=None, u2=None, level_delta: int = 0) -> KeyArrays:
-    """Vectorised make_cell_key + hashes over a vertex stream (src/keys.py:420-437)."""
+    """Vectorised make_cell_key + hashes over a vertex stream (src/keys.py:342-359)."""
     pos = as_f64(position, 3)
     nrm = as_f64(normal, 3)
     om = as_f64(omega_r, 3)
@@ -285,9 +285,92 @@ def make_key_arrays(position, normal, omega_r, layer_id, camera_distance,
     return out
 
 
+# ------------------------------------------------------------------ vectorised stages
+# The reference's per-stage numpy helpers (src/keys.py:245-300).  levels / bins / aux come
+# from the key kernel itself (the fields it computes on the way to the hash), so they are
+# the exact values the filter uses; jittered_positions restates the numpy expression as
+# one device op per numpy op (no contraction across ops) with glibc-exact sin/cos.
+
+def _stage_keys(n_or_dist, cfg: FilterConfig, normal=None, omega_r=None, layer_id=None
+                ) -> KeyArrays:
+    dist = as_f64(n_or_dist).reshape(-1)
+    n = int(dist.shape[0])
+    z3 = torch.zeros((n, 3), dtype=torch.float64, device=dist.device)
+    nrm = as_f64(normal, 3) if normal is not None else z3
+    om = as_f64(omega_r, 3) if omega_r is not None else z3
+    lay = as_i64(layer_id).reshape(-1) if layer_id is not None else \
+        torch.zeros(n, dtype=torch.int64, device=dist.device)
+    return make_key_arrays(z3, nrm, om, lay, dist, replace(cfg, jitter=False))
+
+
+def levels_array(camera_distance, cfg: FilterConfig) -> torch.Tensor:
+    """LOD level per vertex, min(floor(log2(max(d * c_lod, 1))), 31) (src/keys.py:245-248)."""
+    return _stage_keys(camera_distance, cfg).level
+
+
+def normal_bins_array(n, bins: int) -> torch.Tensor:
+    """Octahedral normal bin per row (src/keys.py:273-284)."""
+    nrm = as_f64(n, 3)
+    if int(bins) < 1:
+        raise ValueError("bins must be >= 1")
+    cfg = FilterConfig(include_normal=True, normal_bins=int(bins), normal_in_fingerprint=False,
+                       include_incident_angle=False, include_layer=False, jitter=False)
+    return _stage_keys(torch.ones(nrm.shape[0], dtype=torch.float64, device=nrm.device), cfg,
+                       normal=nrm).aux
+
+
+def aux_bits_array(normal, omega_r, layer_id, cfg: FilterConfig) -> torch.Tensor:
+    """Packed aux field: normal bin | angle bin << 16 | layer << 24 (src/keys.py:286-300).
+    int64 tensor holding the reference's uint64 values (all < 2^32)."""
+    nrm = as_f64(normal, 3)
+    return _stage_keys(torch.ones(nrm.shape[0], dtype=torch.float64, device=nrm.device), cfg,
+                       normal=nrm, omega_r=omega_r, layer_id=layer_id).aux
+
+
+def tangent_basis_array(n) -> tuple[torch.Tensor, torch.Tensor]:
+    """Duff et al. orthonormal basis per row (src/keys.py:251-258)."""
+    nrm = as_f64(n, 3)
+    x, y, z = nrm[:, 0], nrm[:, 1], nrm[:, 2]
+    s = torch.where(z >= 0.0, 1.0, -1.0).to(torch.float64)
+    a = -1.0 / (s + z)
+    b = (x * y) * a
+    t1 = torch.stack([1.0 + ((s * x) * x) * a, s * b, -s * x], 1)
+    t2 = torch.stack([b, s + (y * y) * a, -y], 1)
+    return t1, t2
+
+
+def sincos_array(x) -> tuple[torch.Tensor, torch.Tensor]:
+    """glibc-exact (sin, cos) of a float64 array on the device (csrc pf_sincos)."""
+    t = as_f64(x).reshape(-1)
+    s = torch.empty_like(t)
+    c = torch.empty_like(t)
+    _lib.call("pf_sincos", _lib.ptr(t), int(t.shape[0]), _lib.ptr(s), _lib.ptr(c),
+              _lib.stream_handle())
+    return s, c
+
+
+def jittered_positions(position, normal, level, u1, u2, cfg: FilterConfig) -> torch.Tensor:
+    """Disc jitter of radius half a voxel in the tangent plane (src/keys.py:261-270)."""
+    pos = as_f64(position, 3)
+    if not cfg.jitter:
+        return pos
+    nrm = as_f64(normal, 3)
+    lv = as_i64(level).reshape(-1)
+    r = 0.5 * torch.sqrt(as_f64(u1).reshape(-1))
+    phi = (2.0 * math.pi) * as_f64(u2).reshape(-1)
+    sn, cs = sincos_array(phi)
+    u = r * cs
+    v = r * sn
+    t1, t2 = tangent_basis_array(nrm)
+    step = cfg.base_voxel * torch.ldexp(torch.ones_like(r), lv)
+    off = u[:, None] * t1
+    off = off + v[:, None] * t2
+    return pos + off * step[:, None]
+
+
 def hash_arrays(qx, qy, qz, level, aux, normal_fp_bins=None):
     """Index hash (uint64 bits, int64 tensor) and fingerprint (uint32 bits, int32 tensor)
-    of key fields (src/keys.py:405-417)."""
+    of key fields (src/keys.py:327-339)."""
     tx, ty, tz, tl, ta = (as_i64(a).reshape(-1) for a in (qx, qy, qz, level, aux))
     n = int(tx.shape[0])
     fb = as_u32_bits(normal_fp_bins).reshape(-1) if normal_fp_bins is not None else None
@@ -300,7 +383,7 @@ def hash_arrays(qx, qy, qz, level, aux, normal_fp_bins=None):
 
 
 def hashes(key: CellKey, normal_fp_bin: int | None = None) -> CellHashes:
-    """Index hash and fingerprint of one key (src/keys.py:297-312), on the device."""
+    """Index hash and fingerprint of one key (src/keys.py:219-234), on the device."""
     fb = None if normal_fp_bin is None else np.array([normal_fp_bin & 0x3F], np.uint32)
     u = lambda x: np.array([x & 0xFFFFFFFFFFFFFFFF], np.uint64)  # noqa: E731
     idx, fp = hash_arrays(u(key.qx), u(key.qy), u(key.qz), u(key.level), u(key.aux), fb)

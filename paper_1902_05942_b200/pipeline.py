@@ -32,8 +32,28 @@ _FIELDS = ("position", "normal", "omega_r", "contribution", "throughput", "pixel
 
 
 @dataclass
+class VertexDescriptor:
+    """One recorded path vertex, the scalar view of a stream row (src/tracer.py:46-62),
+    with numpy vectors and Python scalars as in the reference."""
+
+    position: np.ndarray
+    normal: np.ndarray
+    omega_r: np.ndarray
+    contribution: np.ndarray
+    throughput: np.ndarray
+    pixel: int
+    sample: int
+    layer_id: int
+    camera_distance: float
+
+    @property
+    def path_id(self) -> int:
+        return (self.sample << 32) | self.pixel
+
+
+@dataclass
 class VertexStream:
-    """Struct-of-arrays vertex record (src/tracer.py:732-767) as CUDA tensors."""
+    """Struct-of-arrays vertex record (src/tracer.py:66-104) as CUDA tensors."""
 
     position: torch.Tensor
     normal: torch.Tensor
@@ -63,8 +83,39 @@ class VertexStream:
                           as_i64(getattr(vs, f)).reshape(-1)) for f in _FIELDS})
 
     def select(self, rows) -> "VertexStream":
-        r = as_i64(rows).reshape(-1)
+        """Rows by index array or boolean mask (src/tracer.py:92-93)."""
+        if isinstance(rows, torch.Tensor) and rows.dtype == torch.bool:
+            r = rows.to(self.pixel.device)
+        elif not isinstance(rows, torch.Tensor) and np.asarray(rows).dtype == np.bool_:
+            r = torch.as_tensor(np.asarray(rows), device=self.pixel.device)
+        else:
+            r = as_i64(rows).reshape(-1)
         return VertexStream(*(getattr(self, f)[r] for f in _FIELDS))
+
+    def descriptor(self, i: int) -> VertexDescriptor:
+        """Row i as a host VertexDescriptor (src/tracer.py:86-90); one device read."""
+        row = [getattr(self, f)[i].cpu().numpy() for f in _FIELDS]
+        return VertexDescriptor(*row[:5], int(row[5]), int(row[6]), int(row[7]), float(row[8]))
+
+    @staticmethod
+    def concat(streams: list) -> "VertexStream":
+        """Row concatenation (src/tracer.py:95-101); an empty list gives an empty stream."""
+        if not streams:
+            return VertexStream.empty()
+        return VertexStream(*(torch.cat([getattr(VertexStream.from_any(s), f) for s in streams])
+                              for f in _FIELDS))
+
+    @staticmethod
+    def empty() -> "VertexStream":
+        dev = device()
+        e3 = torch.zeros((0, 3), dtype=torch.float64, device=dev)
+        e1 = torch.zeros(0, dtype=torch.int64, device=dev)
+        return VertexStream(e3, e3, e3, e3, e3, e1, e1, e1, e1.to(torch.float64))
+
+    def numpy(self):
+        """Host copy with the reference's field dtypes (a SimpleNamespace of arrays)."""
+        from types import SimpleNamespace
+        return SimpleNamespace(**{f: getattr(self, f).cpu().numpy() for f in _FIELDS})
 
     def c_struct(self):
         """pf_vertices view, cached while the field tensors stay the same objects."""

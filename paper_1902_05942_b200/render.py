@@ -80,15 +80,17 @@ def apply_temporal_differences(scene_f: Scene, cfg: FilterConfig, state: FrameSt
 
 
 def render_frame(scene: Scene, cfg: FilterConfig, state: FrameState, spp: int, seed: int,
-                 options: TraceOptions | None = None) -> FrameResult:
-    """Trace, begin the generation, accumulate, resolve, advance (src/pipeline.py:321-363)."""
+                 threads: int = 1, options: TraceOptions | None = None,
+                 backend: str | None = None) -> FrameResult:
+    """Trace, begin the generation, accumulate, resolve, advance (src/pipeline.py:321-363).
+    `threads` only names the reference's tracer parallelism (see tracer.trace)."""
     t0 = time.perf_counter()
     frame = state.frame
     scene_f = scene.at_frame(frame)
     cfg_f = cfg.for_camera(scene_f.camera.fov, scene_f.camera.height)
     frame_seed = rng.frame_seed(seed, frame) if scene.frames > 1 else seed
     t1 = time.perf_counter()
-    tr = trace(scene_f, spp, frame_seed, options)
+    tr = trace(scene_f, spp, frame_seed, options, backend=backend)
     t2 = time.perf_counter()
     if cfg.temporal_mode == "hybrid":
         state.fine.begin_frame(frame, cfg_f)
@@ -120,15 +122,15 @@ def render_frame(scene: Scene, cfg: FilterConfig, state: FrameState, spp: int, s
 
 
 def run_sequence(scene: Scene, cfg: FilterConfig, spp: int, seed: int, frames: int | None = None,
-                 options: TraceOptions | None = None, on_frame=None,
-                 ordered: bool = False) -> list:
+                 threads: int = 1, options: TraceOptions | None = None,
+                 backend: str | None = None, on_frame=None, ordered: bool = False) -> list:
     """`frames` frames with persistent temporal state (src/pipeline.py:366-380).
     ordered=True uses sequential-order tables (the reference's threads=1 slot layout)."""
     cfg = cfg.for_camera(scene.camera.fov, scene.camera.height)
     state = FrameState.from_config(cfg, ordered=ordered)
     out = []
     for _ in range(frames if frames is not None else scene.frames):
-        res = render_frame(scene, cfg, state, spp, seed, options)
+        res = render_frame(scene, cfg, state, spp, seed, threads, options, backend)
         out.append(res)
         if on_frame is not None:
             on_frame(res)

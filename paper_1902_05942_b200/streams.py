@@ -26,7 +26,7 @@ _GREEN = (0.12, 0.45, 0.15)
 
 
 def camera_footprint(height: int) -> float:
-    """footprint_scale of FilterConfig.for_camera (src/keys.py:152-154) for this camera."""
+    """footprint_scale of FilterConfig.for_camera (src/keys.py:74-76) for this camera."""
     return 2.0 * math.tan(FOV / 2.0) / height
 
 

@@ -19,7 +19,7 @@ import numpy as np
 import torch
 
 from . import _lib
-from .pipeline import VertexStream
+from .pipeline import VertexDescriptor, VertexStream  # noqa: F401  (src/tracer.py exports both)
 from .scene import Scene
 
 T_MIN = 1e-7
@@ -28,7 +28,7 @@ SHADOW_SHRINK = 1.0 - 1e-6
 
 @dataclass
 class TraceOptions:
-    """src/tracer.py:34-42."""
+    """src/tracer.py:35-43."""
 
     max_depth: int = 8
     rr_start: int = 3
@@ -127,12 +127,18 @@ def concat_streams(streams: list) -> VertexStream:
     """VertexStream.concat (src/tracer.py:95-101)."""
     fields = ("position", "normal", "omega_r", "contribution", "throughput", "pixel", "sample",
               "layer_id", "camera_distance")
-    return VertexStream(**{f: torch.cat([getattr(s, f) for s in streams]) for f in fields})
+    return VertexStream.concat(streams)
 
 
 def trace(scene: Scene, spp: int, seed: int, options: TraceOptions | None = None,
-          sample_offset: int = 0, want_variance: bool = False) -> TraceResult:
-    """Render `spp` samples per pixel and collect the vertex stream (src/tracer.py:411-461)."""
+          threads: int = 1, sample_offset: int = 0, want_variance: bool = False,
+          backend: str | None = None) -> TraceResult:
+    """Render `spp` samples per pixel and collect the vertex stream (src/tracer.py:411-461).
+
+    `threads` is accepted for signature compatibility: every pixel is one device thread,
+    and the stream is always in the reference's threads=1 order (pixel-major per sample),
+    which the reference documents as one valid ordering of the threads>1 stream."""
+    _lib.check_backend(backend)
     if spp < 1:
         raise ValueError("spp must be >= 1")
     scene.validate()
@@ -165,9 +171,10 @@ def trace(scene: Scene, spp: int, seed: int, options: TraceOptions | None = None
                        seed)
 
 
-def reevaluate(scene: Scene, seed: int, spp: int, path_ids, options: TraceOptions | None = None
-               ) -> VertexStream:
+def reevaluate(scene: Scene, seed: int, spp: int, path_ids, options: TraceOptions | None = None,
+               backend: str | None = None) -> VertexStream:
     """Replay paths by id under the current scene state (src/tracer.py:464-486)."""
+    _lib.check_backend(backend)
     scene.validate()
     if isinstance(path_ids, torch.Tensor):
         ids = path_ids.to(torch.int64)

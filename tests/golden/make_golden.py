@@ -466,11 +466,60 @@ def gen_formats():
     save("formats.npz", out)
 
 
+def gen_stages():
+    """The per-stage vectorised helpers (src/keys.py:245-300) on random and edge-case rows:
+    signed zeros, axis normals, the -z hemisphere seam, ratios around 1 and 2^k, huge
+    distances, unnormalised normals."""
+    from pathfilter.keys import aux_bits_array, jittered_positions, levels_array, \
+        normal_bins_array, tangent_basis_array
+    out = {}
+    r = np.random.default_rng(21)
+    n = 6000
+    nrm = r.normal(size=(n, 3))
+    nrm /= np.linalg.norm(nrm, axis=1, keepdims=True)
+    edge = np.array([[0, 0, 1], [0, 0, -1], [0, 0, 0.0], [0, 0, -0.0], [1, 0, 0], [-1, 0, 0],
+                     [0, 1, 0], [0, -1, 0], [0.6, 0.8, -0.0], [-0.6, 0.8, 0.0],
+                     [1e-300, -1e-300, -1], [3.0, -4.0, 12.0], [0.5, 0.5, -0.5],
+                     [-0.0, -0.0, -1.0], [1e-17, 1.0, -1e-17], [0, 0, 0]], np.float64)
+    nrm[:len(edge)] = edge
+    om = r.normal(size=(n, 3))
+    om /= np.linalg.norm(om, axis=1, keepdims=True)
+    om[:len(edge)] = edge[::-1]
+    lay = r.integers(0, 3, n)
+    dist = np.exp(r.uniform(np.log(1e-3), np.log(1e7), n))
+    cfg = FilterConfig(base_voxel=0.02, footprint_scale=0.003, include_incident_angle=True,
+                       include_layer=True, normal_bins=6)
+    c_lod = cfg.footprint_scale * cfg.s_pixels / cfg.base_voxel
+    ks = np.arange(32)
+    near = np.concatenate([2.0 ** ks, np.nextafter(2.0 ** ks, 0), np.nextafter(2.0 ** ks, 3e9)])
+    dist[:len(near)] = near / c_lod
+    dist[len(near):len(near) + 4] = [0.0, 1e-300, 1e300, 1.0 / c_lod]
+    u1 = r.uniform(0.0, 1.0, n)
+    u2 = r.uniform(0.0, 1.0, n)
+    u1[:4] = [0.0, 1.0, 0.5, np.nextafter(1.0, 0)]
+    u2[:4] = [0.0, 0.25, 0.999999999, 0.5]
+    pos = r.uniform(-100.0, 100.0, (n, 3))
+    lv = levels_array(dist, cfg)
+    t1, t2 = tangent_basis_array(nrm)
+    out.update(normal=nrm, omega_r=om, layer_id=lay, camera_distance=dist, u1=u1, u2=u2,
+               position=pos, cfg=np.array(cfg_dict(cfg)), levels=lv, t1=t1, t2=t2,
+               jittered=jittered_positions(pos, nrm, lv, u1, u2, cfg),
+               jittered_lv0=jittered_positions(pos, nrm, np.zeros(n, np.int64), u1, u2, cfg),
+               aux=aux_bits_array(nrm, om, lay, cfg))
+    for b in (1, 2, 6, 8, 16, 64):
+        out[f"bins_{b}"] = normal_bins_array(nrm, b)
+    cfg2 = FilterConfig(include_normal=True, normal_in_fingerprint=True, include_layer=True)
+    out["cfg_nfp"] = np.array(cfg_dict(cfg2))
+    out["aux_nfp"] = aux_bits_array(nrm, om, lay, cfg2)
+    save("stages.npz", out)
+
+
 if __name__ == "__main__":
     which = sys.argv[1:] or ["rng", "keys", "cornell", "box4", "temporal", "hybrid", "tracer",
-                             "render", "formats"]
+                             "render", "formats", "stages"]
     fns = {"rng": gen_rng_hash, "keys": gen_keys_random, "cornell": gen_frame_cornell,
            "box4": gen_frame_box4, "temporal": gen_temporal, "hybrid": gen_hybrid,
-           "tracer": gen_tracer, "render": gen_render, "formats": gen_formats}
+           "tracer": gen_tracer, "render": gen_render, "formats": gen_formats,
+           "stages": gen_stages}
     for w in which:
         fns[w]()

@@ -49,7 +49,7 @@ def test_equal_keys_hash_equally(gpu, qx, qy, qz, lv, aux):
     c = gpu.hashes(gpu.CellKey(qx + 1, qy, qz, lv, aux))
     assert (a.index, a.fingerprint) == (b.index, b.fingerprint)
     assert (a.index, a.fingerprint) != (c.index, c.fingerprint)
-    assert a.fingerprint != 0  # the sentinel is remapped (src/keys.py:96)
+    assert a.fingerprint != 0  # the sentinel is remapped (src/keys.py:214-215)
 
 
 def test_home_slots_are_uniform(gpu):

@@ -31,7 +31,7 @@ def test_reference_hash_vectors(oracle):
 
 
 def test_sentinel_remap(oracle):
-    # a fingerprint that hashes to the empty sentinel must come back as 1 (src/keys.py:292-294)
+    # a fingerprint that hashes to the empty sentinel must come back as 1 (src/keys.py:338)
     _, f = oracle.cell_hashes([0], [0], [0], [0], np.zeros(1, np.uint64),
                               fp_bins=np.zeros(1, np.uint32))
     assert int(f[0]) != 0
@@ -132,3 +132,24 @@ def test_effective_and_begin_frame(oracle, sm):
         c = oracle.Config(**{**cfg.__dict__, "temporal_mode": mode, "ema_alpha": 0.7})
         t.begin_frame(5, c)
         _assert_table(t, d, f"{sm}_post_{mode}_")
+
+
+def test_key_stages(oracle):
+    """The oracle's per-stage restatements against the reference's vectorised helpers
+    (src/keys.py:245-300) on random and edge-case rows (stages.npz)."""
+    d = load_golden("stages.npz")
+    cfg = _cfg(oracle, d, "cfg")
+    lv = oracle.lod(d["camera_distance"], cfg)
+    assert np.array_equal(lv, d["levels"])
+    t1, t2 = oracle.tangent_frame(d["normal"])
+    assert np.array_equal(t1, d["t1"], equal_nan=True)
+    assert np.array_equal(t2, d["t2"], equal_nan=True)
+    u, v = oracle.disc(d["u1"], d["u2"])
+    got = oracle.jitter(d["position"], d["normal"], lv, u, v, cfg)
+    assert np.array_equal(got, d["jittered"], equal_nan=True)
+    for b in (1, 2, 6, 8, 16, 64):
+        assert np.array_equal(oracle.octa_bins(d["normal"], b), d[f"bins_{b}"])
+    assert np.array_equal(oracle.aux_word(d["normal"], d["omega_r"], d["layer_id"], cfg), d["aux"])
+    cfg2 = _cfg(oracle, d, "cfg_nfp")
+    assert np.array_equal(oracle.aux_word(d["normal"], d["omega_r"], d["layer_id"], cfg2),
+                          d["aux_nfp"])
