@@ -23,7 +23,7 @@
 extern "C" {
 #endif
 
-#define PF_ABI_VERSION 2
+#define PF_ABI_VERSION 3
 
 enum pf_status {
     PF_OK = 0,
@@ -58,6 +58,10 @@ typedef struct pf_config {
     uint64_t lod_ulps[2];    /* filled by the library from lod_threshold (callers leave 0):
                                 4-bit count of doubles between T[k] and 2^k, k = 0..31 */
     double inv_base_voxel;   /* filled by the library: RN(1 / base_voxel) */
+    double lod_dist[32];     /* filled by the library: [k] = smallest distance d >= 0 with
+                                RN(d * c_lod) >= lod_threshold[k] for k = 1..31, and
+                                RN(d * c_lod) = +inf for k = 0; +inf when no finite d
+                                reaches it, NaN unless 0 < c_lod < inf */
 } pf_config;
 
 /* VertexStream (src/tracer.py:66-104): row-major [n][3] float64 triples. */
@@ -129,6 +133,9 @@ typedef struct pf_evict_event {
 int pf_abi_version(void);
 const char *pf_last_error(void);
 int pf_device_sm_count(void);
+/* Host only: the config every entry point actually runs with -- `in` plus the
+ * library-derived fields (lod_ulps, inv_base_voxel, lod_dist).  Validates thresholds. */
+int pf_prepare_config(const pf_config *in, pf_config *out);
 
 /* ---- 1. reference kernel-module ABI ------------------------------------------------ */
 

@@ -34,7 +34,7 @@ EXPORTS = ("pf_abi_version", "pf_last_error", "pf_device_sm_count", "pf_accumula
            "pf_count_occupied", "pf_finalize_image", "pf_shard_keys", "pf_shard_emit",
            "pf_shard_apply", "pf_shard_publish", "pf_replica_update", "pf_shard_reset",
            "pf_resolve_replica", "pf_trace_paths", "pf_sincos", "pf_segment_deltas",
-           "pf_begin_frame_checked")
+           "pf_begin_frame_checked", "pf_prepare_config")
 
 
 def build(force: bool = False, verbose: bool = False) -> str:
@@ -62,7 +62,8 @@ class PfConfig(ctypes.Structure):
                 ("jitter", ctypes.c_int32), ("multi_level", ctypes.c_int32),
                 ("coarse_delta", ctypes.c_int32), ("low_count_threshold", ctypes.c_int32),
                 ("temporal_mode", ctypes.c_int32), ("sample_cap", ctypes.c_int32),
-                ("lod_ulps", ctypes.c_uint64 * 2), ("inv_base_voxel", ctypes.c_double)]
+                ("lod_ulps", ctypes.c_uint64 * 2), ("inv_base_voxel", ctypes.c_double),
+                ("lod_dist", ctypes.c_double * 32)]
 
 
 class PfVertices(ctypes.Structure):
@@ -215,6 +216,7 @@ def lib() -> ctypes.CDLL:
     L.pf_shard_reset.argtypes = [vp, vp]
     L.pf_trace_paths.argtypes = [vp, vp, u64, vp, vp, i64, vp, vp]
     L.pf_sincos.argtypes = [vp, i64, vp, vp, vp]
+    L.pf_prepare_config.argtypes = [vp, vp]
     L.pf_segment_deltas.argtypes = [vp, vp, i64, vp, vp, dbl, vp, vp]
     L.pf_begin_frame_checked.argtypes = [vp, vp, i64, i32, dbl, dbl, i32, vp, vp, vp, i64, vp,
                                          vp]

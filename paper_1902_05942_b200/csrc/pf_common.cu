@@ -62,4 +62,9 @@ const char *pf_last_error(void) { return pf::g_last_error.c_str(); }
 
 int pf_device_sm_count(void) { return pf::sm_count(); }
 
+int pf_prepare_config(const pf_config *in, pf_config *out) {
+    if (in == nullptr || out == nullptr) return pf::fail_arg("pf_prepare_config", "NULL config");
+    return pf::prepare_config("pf_prepare_config", in, out);
+}
+
 }  // extern "C"

@@ -67,6 +67,8 @@ static __device__ __noinline__ double ddiv_cold(double x, double y) { return __d
 
 __device__ __forceinline__ double div_rcp(double x, double y, double r) {
     const double ax = fabs(x);
+    if (!(fabs(y) > 0x1p-900 && fabs(y) < 0x1p+900))
+        return ddiv_cold(x, y);
     if (ax == 0.0)
         return __dmul_rn(x, r);  // signed zero: sign(x) * sign(y), like IEEE division
     if (!(ax > 0x1p-900 && ax < 0x1p+900))
@@ -80,7 +82,10 @@ __device__ __forceinline__ double div_rcp(double x, double y, double r) {
 // results are formed for all three (signed zeros selected), and one warp-wide test
 // sends any numerator outside the theorem's range to IEEE division.
 __device__ __forceinline__ void div3_rcp(const double x[3], double y, double r, double q[3]) {
-    bool slow = false;
+    // a divisor outside the theorem's range (0, inf, NaN, subnormal: a level of INT64_MIN
+    // from an infinite distance gives step 0) sends all three to IEEE division
+    const bool y_bad = !(fabs(y) > 0x1p-900 && fabs(y) < 0x1p+900);
+    bool slow = y_bad;
 #pragma unroll
     for (int c = 0; c < 3; ++c) {
         const double ax = fabs(x[c]);
@@ -93,7 +98,8 @@ __device__ __forceinline__ void div3_rcp(const double x[3], double y, double r, 
 #pragma unroll
         for (int c = 0; c < 3; ++c) {
             const double ax = fabs(x[c]);
-            if (ax != 0.0 && !(ax > 0x1p-900 && ax < 0x1p+900)) q[c] = ddiv_cold(x[c], y);
+            if (y_bad || (ax != 0.0 && !(ax > 0x1p-900 && ax < 0x1p+900)))
+                q[c] = ddiv_cold(x[c], y);
         }
     }
 }
@@ -292,7 +298,7 @@ __device__ __forceinline__ void disc_offset(double u1, double u2, double &u, dou
 // (no dynamic indexing into the kernel-parameter array, which would spill it).
 __device__ __forceinline__ int64_t lod_level(double dist, const pf_config &cfg) {
     const double ratio = np_max(dmul(dist, cfg.c_lod), 1.0);
-    if (ratio != ratio)
+    if (!(ratio <= 1.7976931348623157e308))  // NaN or inf: floor(log2) casts to INT64_MIN
         return INT64_MIN;
     if (ratio >= 2147483648.0)
         return kMaxLevel;
@@ -509,12 +515,40 @@ struct KeyShared {
     int has_fp_bin;
     double rbv;  // RN(1 / base_voxel): RN(1/step) = rbv * 2^-level exactly
     int64_t lv0; // LOD of the unjittered vertex (before any level_delta)
+    double gmove;  // d2 < gmove => LOD(dist + |x' - x|) == lv0 (see moved_bound)
 };
 
-__device__ __forceinline__ KeyShared key_shared(const pf_config &cfg, const VertexIn &x) {
+// Copy cfg.lod_dist into shared memory (static indices: no local copy of the params).
+__device__ __forceinline__ void stage_lod_dist(double *smem, const pf_config &cfg) {
+    if (threadIdx.x == 0) {
+#pragma unroll
+        for (int j = 0; j < 32; ++j) smem[j] = cfg.lod_dist[j];
+    }
+}
+
+// Bound on the squared jitter length below which the jittered distance keeps the level:
+// moved = RN(d + RN(sqrt(d2))) >= d and LOD is monotone while the ratio is finite, so
+// LOD(moved) == lv0 whenever moved < D = lod_dist[lv0 + 1] (lod_dist[0] for level 31:
+// the distance whose ratio overflows to inf).  With e = D * 2^-50 covering the roundings
+// of D - d, of the sqrt and of the final sum, d2 < ((D - d) - e)^2 (1 - 2^-50) implies it.
+// -1 (never) for negative/NaN distances, huge D or a missing table.
+__device__ __forceinline__ double moved_bound(const double *lod_dist, double dist, int64_t lv0) {
+    if (lod_dist == nullptr || !(dist >= 0.0) || lv0 < 0) return -1.0;
+    const double inf = __longlong_as_double(0x7FF0000000000000ll);
+    const double dk = lod_dist[(lv0 + 1) & 31];
+    if (dk == inf) return dist <= 1e300 ? inf : -1.0;  // moved stays finite
+    if (!(dk >= 0x1p-900)) return -1.0;
+    const double g = dsub(dsub(dk, dist), dmul(dk, 0x1p-50));
+    if (!(g > 0.0)) return -1.0;
+    return dmul(dmul(g, g), 1.0 - 0x1p-50);
+}
+
+__device__ __forceinline__ KeyShared key_shared(const pf_config &cfg, const VertexIn &x,
+                                                const double *lod_dist = nullptr) {
     KeyShared k;
     k.rbv = cfg.inv_base_voxel;  // prepare_config: RN(1 / base_voxel)
     k.lv0 = lod_level(x.dist, cfg);
+    k.gmove = moved_bound(lod_dist, x.dist, k.lv0);
     k.frame = tangent_frame(x.nrm[0], x.nrm[1], x.nrm[2]);
     k.aux = aux_word(cfg, x.nrm[0], x.nrm[1], x.nrm[2], x.omega, x.layer);
     k.has_fp_bin = cfg.include_normal && cfg.normal_in_fingerprint;
@@ -542,8 +576,10 @@ __device__ __forceinline__ CellKey make_key(const pf_config &cfg, const VertexIn
         const double e1 = dsub(jittered[1], x.pos[1]);
         const double e2 = dsub(jittered[2], x.pos[2]);
         d2 = dadd(dadd(dmul(e0, e0), dmul(e1, e1)), dmul(e2, e2));
-        const double moved = dadd(x.dist, __dsqrt_rn(d2));
-        lv = clamp_level(lod_level(moved, cfg), level_delta);
+        if (!(d2 < ks.gmove)) {  // the jitter may cross a LOD threshold: exact recipe
+            const double moved = dadd(x.dist, __dsqrt_rn(d2));
+            lv = clamp_level(lod_level(moved, cfg), level_delta);
+        }
     } else {
 #pragma unroll
         for (int c = 0; c < 3; ++c) jittered[c] = x.pos[c];

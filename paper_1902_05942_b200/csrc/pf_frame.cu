@@ -43,9 +43,11 @@ insert_frame_kernel(pf_config cfg, pf_vertices v, pf_table fine, pf_table coarse
                     uint64_t h0_lookup, uint64_t *lk_index, uint32_t *lk_fp) {
     __shared__ BlockStats bs;
     __shared__ double2 sincos_tab[220];
+    __shared__ double lod_dist[32];
     if (abort_flag != nullptr && *abort_flag != 0) return;  // invalid input: no mutation
     stats_init(bs);
     stage_sincos_table(sincos_tab);
+    stage_lod_dist(lod_dist, cfg);
     __syncthreads();
     // persistent: each block walks 256-vertex tiles; block counters flush once at exit
     const int64_t tiles = (v.n + kThreads - 1) / kThreads;
@@ -80,7 +82,7 @@ insert_frame_kernel(pf_config cfg, pf_vertices v, pf_table fine, pf_table coarse
         const VertexIn x = load_vertex(v, i, cfg, stream);
 #pragma unroll
         for (int c = 0; c < 3; ++c) val[c] = ld_stream(v.contribution + 3 * i + c, stream);
-        const KeyShared ks = key_shared(cfg, x);
+        const KeyShared ks = key_shared(cfg, x, lod_dist);
         // Key sets in one rolled loop (one copy of the key code keeps the kernel's
         // instruction footprint inside the SM's instruction caches):
         //   0 fine (jitter stream 2), 1 coarse (stream 2, level + coarse_delta),
@@ -330,7 +332,9 @@ __global__ void __launch_bounds__(kThreads) resolve_main_kernel(ResolveArgs a) {
 // Record per row: q0, q1, q2, level, aux, coarse index, coarse fp, unused.
 __global__ void __launch_bounds__(kThreads) fallback_keys_kernel(ResolveArgs a) {
     __shared__ double2 sincos_tab[220];
+    __shared__ double lod_dist[32];
     stage_sincos_table(sincos_tab);
+    stage_lod_dist(lod_dist, a.cfg);
     __syncthreads();
     const pf_config &cfg = a.cfg;
     const int64_t n_work = *a.work_count;
@@ -338,7 +342,7 @@ __global__ void __launch_bounds__(kThreads) fallback_keys_kernel(ResolveArgs a) 
          w += static_cast<int64_t>(gridDim.x) * blockDim.x) {
         const int64_t row = a.work[w];
         const VertexIn x = load_vertex(a.v, row, cfg);
-        const KeyShared ks = key_shared(cfg, x);
+        const KeyShared ks = key_shared(cfg, x, lod_dist);
         double du = 0.0, dv = 0.0, cdu = 0.0, cdv = 0.0;
         if (cfg.jitter) {  // the coarse key uses stream 3 too when jitter is on (:255)
             double u1, u2;

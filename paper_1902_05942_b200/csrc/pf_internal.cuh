@@ -5,6 +5,7 @@
 
 #include <cstdint>
 #include <cstring>
+#include <limits>
 #include <string>
 
 #include "../../include/pathfilter_b200.h"
@@ -70,6 +71,28 @@ inline int prepare_config(const char *fn, const pf_config *in, pf_config *out) {
         out->lod_ulps[k >> 4] |= static_cast<uint64_t>(m) << ((k & 15) * 4);
     }
     out->inv_base_voxel = 1.0 / in->base_voxel;  // IEEE division: RN(1/base_voxel)
+    // lod_dist[k]: smallest non-negative double d with RN(d * c_lod) >= T[k], by bisection
+    // over the (monotone) bit patterns of non-negative doubles.  make_key skips the exact
+    // LOD of the jittered distance when the jitter cannot reach the next threshold.
+    const double c = in->c_lod;
+    for (int k = 0; k < 32; ++k) {
+        double dk = std::numeric_limits<double>::quiet_NaN();
+        if (c > 0.0 && c < std::numeric_limits<double>::infinity()) {
+            // [0]: the first distance whose ratio overflows (LOD(inf) is INT64_MIN)
+            const double t = k == 0 ? std::numeric_limits<double>::infinity()
+                                    : in->lod_threshold[k];
+            uint64_t lo = 0, hi = 0x7FF0000000000000ull;  // P(hi) holds: inf * c >= t
+            while (lo < hi) {                               // smallest bits with P
+                const uint64_t mid = lo + (hi - lo) / 2;
+                double d;
+                std::memcpy(&d, &mid, 8);
+                if (d * c >= t) hi = mid;
+                else lo = mid + 1;
+            }
+            std::memcpy(&dk, &lo, 8);
+        }
+        out->lod_dist[k] = dk;
+    }
     return PF_OK;
 }
 

@@ -162,9 +162,11 @@ shard_keys_kernel(pf_config cfg, pf_vertices v, ShardK k, int has_coarse, uint64
                   uint32_t *lk_fp) {
     __shared__ OwnerCounts oc;
     __shared__ double2 sincos_tab[220];
+    __shared__ double lod_dist[32];
     if (abort_flag != nullptr && *abort_flag != 0) return;
     owner_init(oc, k.s.world);
     stage_sincos_table(sincos_tab);
+    stage_lod_dist(lod_dist, cfg);
     __syncthreads();
     const int64_t tiles = (v.n + kT - 1) / kT;
     for (int64_t tile = blockIdx.x; tile < tiles; tile += gridDim.x) {
@@ -181,7 +183,7 @@ shard_keys_kernel(pf_config cfg, pf_vertices v, ShardK k, int has_coarse, uint64
             if (FIXED) q[c] = quantize_fixed(val);
             else f[c] = val;
         }
-        const KeyShared ks = key_shared(cfg, x);
+        const KeyShared ks = key_shared(cfg, x, lod_dist);
         double du = 0.0, dv = 0.0;
 #pragma unroll 1
         for (int set = 0; set < 3; ++set) {

@@ -185,10 +185,13 @@ __global__ void __launch_bounds__(kThreads)
 keys_kernel(pf_config cfg, pf_vertices v, const double *__restrict__ u1,
             const double *__restrict__ u2, int use_rng, uint64_t h0, int32_t level_delta,
             pf_key_out o) {
+    __shared__ double lod_dist[32];
+    stage_lod_dist(lod_dist, cfg);
+    __syncthreads();
     const int64_t i = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
     if (i >= v.n) return;
     const VertexIn x = load_vertex(v, i, cfg);
-    const KeyShared ks = key_shared(cfg, x);
+    const KeyShared ks = key_shared(cfg, x, lod_dist);
     int jit = 0;
     double du = 0.0, dv = 0.0;
     if (cfg.jitter) {

@@ -511,6 +511,26 @@ def gen_stages():
     cfg2 = FilterConfig(include_normal=True, normal_in_fingerprint=True, include_layer=True)
     out["cfg_nfp"] = np.array(cfg_dict(cfg2))
     out["aux_nfp"] = aux_bits_array(nrm, om, lay, cfg2)
+    # keys of vertices whose jittered distance straddles a LOD threshold: distances just
+    # below d_k = 2^k / c_lod (within the fine and coarse jitter radii) and around it
+    m = 12000
+    k = r.integers(1, 24, m)
+    rel = np.where(r.uniform(size=m) < 0.5, r.uniform(0.0, 0.004, m), r.uniform(0.0, 0.03, m))
+    near = (2.0 ** k / c_lod) * (1.0 - rel)
+    near[:64] = np.nextafter(2.0 ** k[:64] / c_lod, 0.0)
+    near[64:128] = 2.0 ** k[64:128] / c_lod
+    near[128:136] = [0.0, 1e-300, 1e300, np.inf, 31.9 / c_lod, 2.0 ** 31 / c_lod, 1e9, 5e8]
+    npos = r.uniform(-100.0, 100.0, (m, 3))
+    nn = r.normal(size=(m, 3))
+    nn /= np.linalg.norm(nn, axis=1, keepdims=True)
+    nl = r.integers(0, 3, m)
+    nu1, nu2 = r.uniform(0.0, 1.0, m), r.uniform(0.0, 1.0, m)
+    nu1[:512] = 1.0 - r.uniform(0.0, 1e-6, 512)  # the full jitter radius
+    out.update(near_position=npos, near_normal=nn, near_layer=nl, near_distance=near,
+               near_u1=nu1, near_u2=nu2)
+    for delta in (0, 2):
+        kk = make_key_arrays(npos, nn, nn, nl, near, cfg, nu1, nu2, delta)
+        put_keys(out, f"near{delta}_", kk)
     save("stages.npz", out)
 
 

@@ -68,7 +68,36 @@ def test_cubin_is_sm100a():
 
 def test_struct_layouts():
     from paper_1902_05942_b200 import _lib
-    assert ctypes.sizeof(_lib.PfConfig) == 4 * 8 + 32 * 8 + 12 * 4 + 2 * 8 + 8
+    assert ctypes.sizeof(_lib.PfConfig) == 4 * 8 + 32 * 8 + 12 * 4 + 2 * 8 + 8 + 32 * 8
     assert ctypes.sizeof(_lib.PfVertices) == 10 * 8
     assert ctypes.sizeof(_lib.PfTable) == 8 * 8 + 4 * 4
     assert ctypes.sizeof(_lib.PfEvictEvent) == 32
+
+
+@pytest.mark.parametrize("fs,sp,bv", [(0.003, 8.0, 0.02), (0.01, 8.0, 0.01), (1e-7, 3.0, 0.5),
+                                      (0.0, 8.0, 0.01), (1e300, 8.0, 1e-10),
+                                      (1e-310, 1.0, 1.0)])
+def test_prepare_config_lod_dist(fs, sp, bv):
+    """pf_prepare_config's lod_dist[k] is the smallest distance whose RN(d * c_lod)
+    reaches the LOD threshold T[k] -- the bound make_key uses to skip the exact LOD of
+    the jittered distance (checked in Python's own IEEE doubles)."""
+    import math
+    from paper_1902_05942_b200 import _lib
+    from paper_1902_05942_b200.keys import FilterConfig
+    cfg = FilterConfig(footprint_scale=fs, s_pixels=sp, base_voxel=bv)
+    cin = cfg.to_c()
+    out = _lib.PfConfig()
+    L = _lib.lib()
+    assert L.pf_prepare_config(ctypes.byref(cin), ctypes.byref(out)) == 0
+    c = cin.c_lod
+    assert out.inv_base_voxel == 1.0 / bv
+    for k in range(0, 32):
+        t = math.inf if k == 0 else cin.lod_threshold[k]  # [0]: where the ratio overflows
+        d = out.lod_dist[k]
+        if not 0.0 < c < math.inf:
+            assert math.isnan(d)
+        elif math.isinf(d):
+            assert not (1.7976931348623157e308 * c >= t)
+        else:
+            assert d * c >= t
+            assert d == 0.0 or math.nextafter(d, 0.0) * c < t

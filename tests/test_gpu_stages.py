@@ -97,3 +97,18 @@ def test_backend_names(gpu):
     a = gpu.trace(scene, 1, 1, threads=4)
     b = gpu.trace(scene, 1, 1, None, 1, 0, False, "native")
     assert torch.equal(a.image, b.image)
+
+
+@pytest.mark.parametrize("delta", [0, 2])
+def test_keys_across_lod_thresholds(gpu, stages, delta):
+    """Jittered distances that do and do not cross a LOD threshold (about half of the
+    rows change level): the kernel's threshold-distance shortcut (pf_config.lod_dist)
+    must give the reference's keys bit for bit, including at d_k itself, 0, 1e300, inf."""
+    cfg = _cfg(gpu, stages, "cfg")
+    k = gpu.make_key_arrays(stages["near_position"], stages["near_normal"],
+                            stages["near_normal"], stages["near_layer"],
+                            stages["near_distance"], cfg, stages["near_u1"], stages["near_u2"],
+                            delta).numpy()
+    for f in ("qx", "qy", "qz", "level", "aux", "index", "fingerprint"):
+        assert np.array_equal(k[f], stages[f"near{delta}_{f}"]), f
+    assert np.array_equal(k["jittered"], stages[f"near{delta}_jittered"], equal_nan=True)
