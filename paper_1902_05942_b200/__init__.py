@@ -30,6 +30,7 @@ from .tracer import TraceOptions, TraceResult, reevaluate, trace
 from ._backend import BACKEND, available_backends
 from .keys import aux_bits_array, jittered_positions, levels_array, normal_bins_array, \
     tangent_basis_array
+from .host import HostFrame, HostFramePipeline
 from .pipeline import VertexDescriptor
 
 __version__ = "0.1.0"
@@ -48,4 +49,5 @@ __all__ = [
     "select_replay_ids", "temporal_difference", "TraceOptions", "TraceResult", "reevaluate",
     "trace", "read_ppm", "tonemap", "write_ppm", "VertexDescriptor", "levels_array",
     "tangent_basis_array", "jittered_positions", "normal_bins_array", "aux_bits_array",
+    "HostFrame", "HostFramePipeline",
 ]

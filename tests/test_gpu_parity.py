@@ -581,3 +581,30 @@ def test_probe_limit_failures_conserve_vertices(gpu):
     assert state.fine.total_counts() + stats.probe_failures == n
     assert state.coarse.total_counts() + stats.coarse_probe_failures == n
     assert int(torch.bincount(report.source.to(torch.int64), minlength=4).sum()) == n
+
+
+@pytest.mark.parametrize("depth", [1, 2, 3])
+def test_host_pipeline_matches_device_frames(gpu, depth):
+    """HostFramePipeline (host buffers, copies on a side stream overlapping the previous
+    frame) gives the reference's frame-0 image and, frame after frame in filter mode,
+    exactly what filter_frame gives on device copies of the same inputs."""
+    from types import SimpleNamespace
+    d = load_golden("frame_cornell128.npz")
+    vs = golden_stream(d)
+    cfg = cfg_of(gpu, d, "fixed_cfg")
+    host = SimpleNamespace(**{f: torch.from_numpy(np.ascontiguousarray(getattr(vs, f)))
+                              .pin_memory() for f in ("position", "normal", "omega_r",
+                                                      "contribution", "throughput", "pixel",
+                                                      "sample", "layer_id", "camera_distance")})
+    spp, seed = int(d["spp"]), int(d["seed"])
+    pipe = gpu.HostFramePipeline(cfg, depth=depth)
+    imgs = pipe.run([(host, d["base"], spp, seed + 7 * f) for f in range(5)])
+    assert np.array_equal(imgs[0].numpy(), d["fixed_image"])
+    cfg_f = cfg_of(gpu, d, "fixed_cfg")
+    cfg_f.temporal_mode = "filter"
+    pipe_f = gpu.HostFramePipeline(cfg_f, depth=depth)
+    got = pipe_f.run([(host, d["base"], spp, seed + 7 * f) for f in range(5)])
+    st = gpu.FrameState.from_config(cfg_f)
+    for f in range(5):
+        img, _, _ = gpu.filter_frame(vs, d["base"], cfg_f, st, spp, seed + 7 * f)
+        assert np.array_equal(got[f].numpy(), _np(img)), f
