@@ -51,6 +51,15 @@ __device__ __forceinline__ int64_t np_i64(double x) {
     return static_cast<int64_t>(x);
 }
 
+// np_i64(floor(x)) as ONE F2I.FLOOR and a compare on x itself: floor(x) < 2^63 iff
+// x < 2^63; below -2^63 (and at it) the conversion saturates to INT64_MIN, which is
+// numpy's value there; NaN fails the compare.
+__device__ __forceinline__ int64_t np_floor_i64(double x) {
+    long long r;
+    asm("cvt.rmi.s64.f64 %0, %1;" : "=l"(r) : "d"(x));
+    return x < 0x1p63 ? static_cast<int64_t>(r) : INT64_MIN;
+}
+
 __device__ __forceinline__ double dmul(double a, double b) { return __dmul_rn(a, b); }
 __device__ __forceinline__ double dadd(double a, double b) { return __dadd_rn(a, b); }
 __device__ __forceinline__ double dsub(double a, double b) { return __dsub_rn(a, b); }
@@ -591,7 +600,7 @@ __device__ __forceinline__ CellKey make_key(const pf_config &cfg, const VertexIn
     double qd[3];
     div3_rcp(jittered, step, rstep, qd);
 #pragma unroll
-    for (int c = 0; c < 3; ++c) k.q[c] = np_i64(floor(qd[c]));
+    for (int c = 0; c < 3; ++c) k.q[c] = np_floor_i64(qd[c]);
     k.level = lv;
     k.aux = ks.aux;
     return k;

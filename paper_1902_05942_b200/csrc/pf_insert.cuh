@@ -10,7 +10,7 @@ constexpr unsigned kFull = 0xFFFFFFFFu;
 
 // 16.16 fixed point, half up (src/_native.pyx:251-253): floor(v*65536 + 0.5).
 __device__ __forceinline__ int64_t quantize_fixed(double v) {
-    return np_i64(floor(dadd(dmul(v, kFixedScale), 0.5)));
+    return np_floor_i64(dadd(dmul(v, kFixedScale), 0.5));
 }
 
 struct LaneInsert {

@@ -301,7 +301,7 @@ __device__ __forceinline__ int fold_slot(const pf_table &t, int64_t s, uint64_t 
 #pragma unroll
                 for (int c = 0; c < 3; ++c) {
                     const double nh = dmul(ddiv(e.fsum[c], denom), static_cast<double>(cnt));
-                    hist[c] = FIXED ? static_cast<uint64_t>(np_i64(floor(dadd(nh, 0.5))))
+                    hist[c] = FIXED ? static_cast<uint64_t>(np_floor_i64(dadd(nh, 0.5)))
                                     : static_cast<uint64_t>(__double_as_longlong(nh));
                 }
                 hc = cnt;
@@ -316,8 +316,8 @@ __device__ __forceinline__ int fold_slot(const pf_table &t, int64_t s, uint64_t 
 #pragma unroll
             for (int c = 0; c < 3; ++c) {
                 if (FIXED)
-                    hist[c] = static_cast<uint64_t>(np_i64(floor(dadd(
-                        dmul(static_cast<double>(static_cast<int64_t>(hist[c])), scale), 0.5))));
+                    hist[c] = static_cast<uint64_t>(np_floor_i64(dadd(
+                        dmul(static_cast<double>(static_cast<int64_t>(hist[c])), scale), 0.5)));
                 else
                     hist[c] = __double_as_longlong(dmul(__longlong_as_double(hist[c]), scale));
             }
