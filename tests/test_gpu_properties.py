@@ -120,3 +120,23 @@ def test_conservation_across_seeds(gpu, sum_mode):
             assert np.array_equal(t.sums.sum(0).cpu().numpy(), want)
         else:
             np.testing.assert_allclose(t.sums.sum(0).cpu().numpy(), vals.sum(0), rtol=1e-12)
+
+
+def test_conservation_large_fixed_values(gpu):
+    """Quanta at and above 2^27 (contributions >= 2048) take the pointer-jumping group sum
+    instead of the 32-bit warp reduction; sums stay exact, mixed per warp."""
+    r = np.random.default_rng(77)
+    n = 40000
+    idx = r.integers(0, 2**63, 300).astype(np.uint64)[r.integers(0, 300, n)]
+    fp = ((idx >> np.uint64(7)) & np.uint64(0xFFFFFFFF)).astype(np.uint32) | np.uint32(1)
+    vals = r.uniform(0.0, 3.0, (n, 3))
+    big = r.uniform(size=n) < 0.05
+    vals[big] = r.uniform(2047.0, 1e6, (int(big.sum()), 3))
+    vals[:32] = (2.0 ** 27 - 1) / 65536.0  # quanta 2^27 - 1 (fast path) and 2^27 (not)
+    vals[32:64] = 2048.0
+    t = gpu.VoxelTable(1024, sum_mode="fixed")
+    st_, _, _ = t.accumulate_batch(idx, fp, vals, 0)
+    assert int((st_ == 2).sum()) == 0
+    assert t.total_counts() == n
+    want = np.floor(vals * 65536.0 + 0.5).astype(np.int64).sum(0)
+    assert np.array_equal(t.sums.sum(0).cpu().numpy(), want)
