@@ -1,4 +1,5 @@
 #!/bin/bash
+# usage: bash tools/bench_variants.sh base mb4   (variant k = tools/_var/k.so, built with extra -D flags)
 # bench each variant library: prints label, ms/frame, phases
 for v in "$@"; do
   if [ "$v" = base ]; then lib=""; else lib="tools/_var/$v.so"; fi
