@@ -233,6 +233,46 @@ def gen_frame_box4():
     save("frame_box4.npz", out)
 
 
+FRAME_VARIANTS = {
+    "aux": dict(include_incident_angle=True, include_layer=True, normal_bins=6),
+    "nfp": dict(normal_in_fingerprint=True),
+    "nojit": dict(jitter=False),
+    "single": dict(multi_level=False),
+    "thr1": dict(low_count_threshold=1),
+    "thr64": dict(low_count_threshold=64),
+    "probe2": dict(capacity=512, probe_limit=2),
+    "delta3": dict(coarse_delta=3, sum_mode="float"),
+}
+
+
+def gen_frame_variants():
+    """One 4-bounce closed-box frame per key / ladder option (the resolve paths the
+    default config rarely takes: no coarse table, all-fallback rows, probe failures,
+    aux and fingerprint bins in the lookup and pool keys)."""
+    out = {}
+    w, h = 48, 27
+    scene, vs, base = box_stream(w, h, seed=3)
+    put_stream(out, "v_", vs)
+    out["base"] = base
+    seed = 5
+    for name, kw in FRAME_VARIANTS.items():
+        kw = {"capacity": next_pow2(2 * w * h), **kw}
+        cfg = FilterConfig(**kw).for_camera(scene.camera.fov, scene.camera.height)
+        state = FrameState.from_config(cfg)
+        state.fine.begin_frame(0, cfg)
+        if state.coarse is not None:
+            state.coarse.begin_frame(0, cfg)
+        fk, ck, stats = accumulate_phase(vs, cfg, state, 0, seed)
+        image, report = resolve_phase(vs, cfg, state, 0, seed, 1, base, fk)
+        stats.source_counts = report.counts
+        out[f"{name}_cfg"] = np.array(cfg_dict(cfg))
+        frame_outputs(out, f"{name}_", state, fk, ck, image, report, stats)
+    out["seed"] = np.uint64(seed)
+    out["spp"] = np.int64(1)
+    out["variants"] = np.array(sorted(FRAME_VARIANTS))
+    save("frame_variants.npz", out)
+
+
 def gen_temporal():
     """Corridor pan with a 128-slot table: claims, evictions and horizon clears."""
     out = {}
@@ -536,10 +576,10 @@ def gen_stages():
 
 if __name__ == "__main__":
     which = sys.argv[1:] or ["rng", "keys", "cornell", "box4", "temporal", "hybrid", "tracer",
-                             "render", "formats", "stages"]
+                             "render", "formats", "stages", "variants"]
     fns = {"rng": gen_rng_hash, "keys": gen_keys_random, "cornell": gen_frame_cornell,
            "box4": gen_frame_box4, "temporal": gen_temporal, "hybrid": gen_hybrid,
            "tracer": gen_tracer, "render": gen_render, "formats": gen_formats,
-           "stages": gen_stages}
+           "stages": gen_stages, "variants": gen_frame_variants}
     for w in which:
         fns[w]()

@@ -608,3 +608,45 @@ def test_host_pipeline_matches_device_frames(gpu, depth):
     for f in range(5):
         img, _, _ = gpu.filter_frame(vs, d["base"], cfg_f, st, spp, seed + 7 * f)
         assert np.array_equal(got[f].numpy(), _np(img)), f
+
+
+def _variant_cases():
+    import numpy as _np_
+    names = [str(x) for x in load_golden("frame_variants.npz")["variants"]]
+    # probe failures depend on which keys claim first: parallel tables are only
+    # comparable where nothing fails or gets evicted
+    return [(n, o) for n in names for o in (False, True) if o or n != "probe2"]
+
+
+@pytest.mark.parametrize("name,ordered", _variant_cases())
+def test_frame_variants_golden(gpu, name, ordered):
+    """One frame per key / ladder option against the reference (frame_variants.npz):
+    incident-angle + layer aux bins, fingerprint normal bins, no jitter, no coarse
+    table, thresholds 1 and 64, probe limit 2 on a 512-slot table, coarse_delta 3 in
+    float mode -- through the fused frame (parallel) or the sequential-order tables."""
+    d = load_golden("frame_variants.npz")
+    vs = golden_stream(d)
+    cfg = cfg_of(gpu, d, f"{name}_cfg")
+    state = gpu.FrameState.from_config(cfg, ordered=ordered)
+    image, report, stats = gpu.filter_frame(vs, d["base"], cfg, state, int(d["spp"]),
+                                            int(d["seed"]))
+    flt = cfg.sum_mode == "float"
+    rtol = 1e-12 if flt else 0.0
+    assert_tables_equal(state.fine.state(), golden_table(d, f"{name}_fine_"), ordered, rtol)
+    if state.coarse is not None:
+        assert_tables_equal(state.coarse.state(), golden_table(d, f"{name}_coarse_"), ordered,
+                            rtol)
+    else:
+        assert f"{name}_coarse_tags" not in d.files
+    assert np.array_equal(_np(report.source), d[f"{name}_source"])
+    if flt:
+        np.testing.assert_allclose(_np(report.means), d[f"{name}_chosen"], rtol=1e-12, atol=0)
+    else:
+        assert np.array_equal(_np(report.means), d[f"{name}_chosen"])
+    np.testing.assert_allclose(_np(image), d[f"{name}_image"], rtol=1e-12, atol=1e-300)
+    want = dict(l.split("=", 1) for l in str(d[f"{name}_stats"]).splitlines())
+    assert stats.probe_failures == int(want["probe_failures"])
+    assert stats.coarse_probe_failures == int(want["coarse_probe_failures"])
+    fk = state.prev_fine_keys.materialize().numpy()
+    for f in KEY_FIELDS:
+        assert np.array_equal(fk[f], d[f"{name}_fk_{f}"]), f

@@ -153,3 +153,24 @@ def test_key_stages(oracle):
     cfg2 = _cfg(oracle, d, "cfg_nfp")
     assert np.array_equal(oracle.aux_word(d["normal"], d["omega_r"], d["layer_id"], cfg2),
                           d["aux_nfp"])
+
+
+@pytest.mark.parametrize("name", ["aux", "delta3", "nfp", "nojit", "probe2", "single", "thr1",
+                                  "thr64"])
+def test_frame_variants_replay(oracle, name):
+    """The oracle frame under each key / ladder option (frame_variants.npz)."""
+    d = load_golden("frame_variants.npz")
+    vs = golden_stream(d)
+    cfg = _cfg(oracle, d, f"{name}_cfg")
+    state = oracle.State.from_config(cfg)
+    img, src, chosen, stats = oracle.filter_frame(vs, cfg, state, 0, int(d["seed"]),
+                                                  int(d["spp"]), d["base"])
+    _assert_table(state.fine, d, f"{name}_fine_")
+    if state.coarse is not None:
+        _assert_table(state.coarse, d, f"{name}_coarse_")
+    assert np.array_equal(src, d[f"{name}_source"])
+    assert np.array_equal(chosen, d[f"{name}_chosen"])
+    assert np.array_equal(img, d[f"{name}_image"])
+    want = dict(l.split("=", 1) for l in str(d[f"{name}_stats"]).splitlines())
+    assert int(want["probe_failures"]) == stats["probe_failures"]
+    assert int(want["collisions"]) == stats["collisions"]
