@@ -268,3 +268,45 @@ def test_rank_without_vertices(gpu):
     assert torch.equal(outs[0][1].source, rep1.source)
     assert torch.equal(outs[1][0], base[8:])
     torch.testing.assert_close(outs[0][0], img1[:8], rtol=1e-12, atol=1e-14)
+
+
+@pytest.mark.parametrize("name", ["aux", "delta3", "nfp", "nojit", "single", "thr1", "thr64"])
+def test_variants_sharded_match_reference(gpu, name):
+    """The key / ladder options of frame_variants.npz through the 2-rank sharded frame
+    (pixel row bands of 14 and 13 rows, band composite): the reference's sources,
+    means, image and per-key tables."""
+    from conftest import golden_cfg, golden_stream, golden_table, load_golden
+    from paper_1902_05942_b200 import sharded
+    d = load_golden("frame_variants.npz")
+    vs = gpu.VertexStream.from_any(golden_stream(d))
+    cfg = gpu.FilterConfig(**golden_cfg(d, f"{name}_cfg"))
+    base = torch.as_tensor(d["base"], device="cuda")
+    H, W = int(base.shape[0]), int(base.shape[1])
+    world, split = 2, 14
+    bands = [(0, split), (split, H)]
+    rows = [torch.nonzero((vs.pixel >= a * W) & (vs.pixel < b * W)).reshape(-1) for a, b in bands]
+    states = [sharded.ShardedState(cfg, r, world) for r in range(world)]
+    outs = sharded.run_loopback([sharded.filter_frame_sharded(
+        vs.select(rows[r]), base[a:b].contiguous(), cfg, states[r], int(d["spp"]),
+        int(d["seed"]), pixel_base=a * W) for r, (a, b) in enumerate(bands)])
+    order = torch.cat(rows).cpu().numpy()
+    assert np.array_equal(torch.cat([o[1].source for o in outs]).cpu().numpy(),
+                          d[f"{name}_source"][order])
+    means = torch.cat([o[1].means for o in outs]).cpu().numpy()
+    if cfg.sum_mode == "float":
+        np.testing.assert_allclose(means, d[f"{name}_chosen"][order], rtol=1e-12, atol=0)
+    else:
+        assert np.array_equal(means, d[f"{name}_chosen"][order])
+    img = torch.cat([o[0] for o in outs]).cpu().numpy()
+    np.testing.assert_allclose(img, d[f"{name}_image"], rtol=1e-12, atol=1e-300)
+    tables = ("fine", "coarse") if cfg.multi_level else ("fine",)
+    for table in tables:
+        a = _union_canon(states, table)
+        b = canon(golden_table(d, f"{name}_{table}_"))
+        assert len(a) == len(b)
+        for ra, rb in zip(a, b):
+            assert ra[:4] == rb[:4]
+            if cfg.sum_mode == "float":
+                np.testing.assert_allclose(ra[4] + ra[5], rb[4] + rb[5], rtol=1e-12, atol=0)
+            else:
+                assert ra[4:] == rb[4:]
