@@ -357,16 +357,10 @@ def run_b200(args):
     phases = ({"begin_check": [], "insert": [], "resolve": []} if world == 1 else
               {"begin_keys": [], "exchange_apply_publish": [], "resolve_image": []})
 
-    def step(f, timing=None):
+    def step(f, evs=None):
         # one frame = ONE pf_filter_frame call; its phase events (recorded inside the C
         # call on the launching stream) bracket begin+check, the insert kernel, resolve
         seed = rng.frame_seed(1, f)
-        evs = None
-        if timing is not None:
-            evs = [ev() for _ in range(4)]
-            for e in evs:  # materialise the cudaEvent_t handles
-                e.record()
-            timing.append(tuple(evs))
         if world > 1:
             sharded.run_dist(sharded.filter_frame_sharded(
                 vs, base, cfg, state, world, seed, composite="reduce", want_means=True,
@@ -383,12 +377,18 @@ def run_b200(args):
     if world > 1:
         dist.barrier()
     torch.cuda.synchronize()
-    marks = []
+    # the phase events of every timed frame, created and materialised (one record each)
+    # before the timed region, so inside it only the C call's own records remain
+    marks = [tuple(ev() for _ in range(4)) for _ in range(args.steps)]
+    for m in marks:
+        for e in m:
+            e.record()
+    torch.cuda.synchronize()
     start, stop = ev(), ev()
     t_wall0 = time.time()
     start.record()
     for k in range(args.steps):
-        step(args.warmup + k, marks)
+        step(args.warmup + k, marks[k])
     stop.record()
     torch.cuda.synchronize()
     t_wall1 = time.time()
