@@ -42,6 +42,8 @@ def build(force: bool = False, verbose: bool = False) -> str:
     newest = max(os.path.getmtime(p) for p in SOURCES + HEADERS)
     if not force and os.path.exists(LIB_PATH) and os.path.getmtime(LIB_PATH) >= newest:
         return LIB_PATH
+    if not force and os.environ.get("PF_LIB") and os.path.exists(LIB_PATH):
+        return LIB_PATH  # a prebuilt variant library (tools/build_variant.sh): never rebuilt
     nvcc = os.environ.get("NVCC", "nvcc")
     cmd = [nvcc, *NVCC_FLAGS, "-o", LIB_PATH, *SOURCES]
     if verbose:

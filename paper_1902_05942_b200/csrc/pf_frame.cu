@@ -12,7 +12,10 @@ constexpr int kThreads = 256;
 #ifndef PF_RESOLVE_KV
 #define PF_RESOLVE_KV 2
 #endif
-constexpr int kResolveKV = PF_RESOLVE_KV;  // vertices per thread in resolve_main
+constexpr int kResolveKV = PF_RESOLVE_KV;
+#ifndef PF_RESOLVE_HOIST
+#define PF_RESOLVE_HOIST 1
+#endif  // vertices per thread in resolve_main
 constexpr int kWarps = kThreads / 32;
 
 __device__ __forceinline__ void log_eviction(pf_evict_event *events, int64_t *count, int64_t cap,
@@ -236,10 +239,13 @@ __device__ __forceinline__ void composite(const ResolveArgs &a, int64_t i, int64
 // KV vertices per thread, each step issued for all KV rows before the next (key ->
 // home tag -> cell state -> composite), so a thread keeps KV independent L2/HBM
 // round trips in flight: the kernel is bound by memory latency, not arithmetic.
+#ifndef PF_RESOLVE_MIN_BLOCKS
+#define PF_RESOLVE_MIN_BLOCKS 4  // 4 x 256 threads per SM: <= 64 registers
+#endif
 template <int KV, bool HAVE_KEYS>
-__global__ void __launch_bounds__(kThreads) resolve_main_kernel(ResolveArgs a) {
+__global__ void __launch_bounds__(kThreads, PF_RESOLVE_MIN_BLOCKS) resolve_main_kernel(ResolveArgs a) {
     __shared__ BlockStats bs;
-    stats_init(bs);
+    stats_init(bs, false);
     __syncthreads();
     const pf_config &cfg = a.cfg;
     const uint64_t stream = l2_evict_first(), keep = l2_evict_last();
@@ -249,6 +255,8 @@ __global__ void __launch_bounds__(kThreads) resolve_main_kernel(ResolveArgs a) {
     bool valid[KV];
     CellHash h[KV];
     uint64_t tag[KV];
+    int64_t pixel[KV];
+    double tp[KV][3];
 #pragma unroll
     for (int k = 0; k < KV; ++k) {
         const int64_t i0 = base + static_cast<int64_t>(k) * blockDim.x;
@@ -261,6 +269,15 @@ __global__ void __launch_bounds__(kThreads) resolve_main_kernel(ResolveArgs a) {
             h[k] = lookup_key(a, row[k]).second;
         }
     }
+#if PF_RESOLVE_HOIST
+    // the composite's stream loads depend on nothing: in flight beside the key loads
+#pragma unroll
+    for (int k = 0; k < KV; ++k) {
+        pixel[k] = ld_stream(a.v.pixel + row[k], stream) - a.pixel_base;
+#pragma unroll
+        for (int c = 0; c < 3; ++c) tp[k][c] = ld_stream(a.v.throughput + 3 * row[k] + c, stream);
+    }
+#endif
 #pragma unroll
     for (int k = 0; k < KV; ++k) tag[k] = __ldg(reinterpret_cast<const unsigned long long *>(
                                       a.fine.tags) + (h[k].index & fmask));
@@ -274,14 +291,14 @@ __global__ void __launch_bounds__(kThreads) resolve_main_kernel(ResolveArgs a) {
                                     a.seg_mask);
     }
     Effective ef[KV];
-    int64_t pixel[KV];
-    double tp[KV][3];
 #pragma unroll
     for (int k = 0; k < KV; ++k) {
         if (slot[k] >= 0) ef[k] = fine_effective(a, slot[k]);
+#if !PF_RESOLVE_HOIST
         pixel[k] = ld_stream(a.v.pixel + row[k], stream) - a.pixel_base;
 #pragma unroll
         for (int c = 0; c < 3; ++c) tp[k][c] = ld_stream(a.v.throughput + 3 * row[k] + c, stream);
+#endif
     }
     const bool as_int = eff_is_int(a.fine, cfg.temporal_mode);
     const bool fixed = a.fine.sum_mode == PF_SUM_FIXED;
@@ -295,11 +312,12 @@ __global__ void __launch_bounds__(kThreads) resolve_main_kernel(ResolveArgs a) {
                 fine_ok = true;
                 double m[3];
                 const bool in_image = pixel[k] >= 0 && pixel[k] < a.n_pixels;
+                const double sums[3] = {eff_sum_f64(e, as_int, 0), eff_sum_f64(e, as_int, 1),
+                                        eff_sum_f64(e, as_int, 2)};
+                row_mean3(sums, cnt, fixed, m);
 #pragma unroll
-                for (int c = 0; c < 3; ++c) {
-                    m[c] = row_mean(eff_sum_f64(e, as_int, c), cnt, fixed);
+                for (int c = 0; c < 3; ++c)
                     if (in_image) red_add_f64(a.flat + 3 * pixel[k] + c, dmul(tp[k][c], m[c]), keep);
-                }
                 if (a.source) a.source[row[k]] = 0;
                 if (a.chosen) {
 #pragma unroll
@@ -372,7 +390,7 @@ __global__ void __launch_bounds__(kThreads) fallback_keys_kernel(ResolveArgs a) 
 // float64 pools), then runs the coarse rung, the ladder and the composite.
 __global__ void __launch_bounds__(kThreads) resolve_fallback_kernel(ResolveArgs a) {
     __shared__ BlockStats bs;
-    stats_init(bs);
+    stats_init(bs, false);
     __syncthreads();
     const pf_config &cfg = a.cfg;
     const int lane = threadIdx.x & 31;
@@ -475,7 +493,7 @@ struct PoolSmem {
 __global__ void __launch_bounds__(kThreads) resolve_pool_kernel(ResolveArgs a) {
     __shared__ BlockStats bs;
     __shared__ PoolSmem ps;
-    stats_init(bs);
+    stats_init(bs, false);
     __syncthreads();
     const pf_config &cfg = a.cfg;
     const int mode = cfg.temporal_mode;

@@ -15,9 +15,11 @@ struct BlockStats {
     unsigned hist[256];
 };
 
-__device__ __forceinline__ void stats_init(BlockStats &b) {
+// with_hist false: the kernel never counts probe lengths (and flushes without them)
+__device__ __forceinline__ void stats_init(BlockStats &b, bool with_hist = true) {
     for (int k = threadIdx.x; k < PF_STAT_HIST_BASE; k += blockDim.x) b.v[k] = 0;
-    for (int k = threadIdx.x; k < 256; k += blockDim.x) b.hist[k] = 0;
+    if (with_hist)
+        for (int k = threadIdx.x; k < 256; k += blockDim.x) b.hist[k] = 0;
 }
 
 // warp-aggregated add of a per-lane predicate into a block counter
@@ -81,6 +83,24 @@ __device__ __forceinline__ double row_mean(double sum, double cnt, bool fixed) {
     double d = np_max(cnt, 1e-300);
     if (fixed) d = dmul(d, kFixedScale);
     return ddiv(sum, d);
+}
+
+// The three channels of one row: one correctly rounded reciprocal of the shared
+// divisor and Markstein's correction per channel (div3_rcp), each quotient equal to
+// IEEE sum / d; a divisor outside the theorem's range (cnt 0 -> 1e-300) takes IEEE
+// division inside div3_rcp.
+#ifndef PF_ROW_MEAN_RCP
+#define PF_ROW_MEAN_RCP 1
+#endif
+__device__ __forceinline__ void row_mean3(const double sum[3], double cnt, bool fixed, double m[3]) {
+#if PF_ROW_MEAN_RCP
+    double d = np_max(cnt, 1e-300);
+    if (fixed) d = dmul(d, kFixedScale);
+    div3_rcp(sum, d, __drcp_rn(d), m);
+#else
+#pragma unroll
+    for (int c = 0; c < 3; ++c) m[c] = row_mean(sum[c], cnt, fixed);
+#endif
 }
 
 struct KeyAndHash {
@@ -152,17 +172,19 @@ __device__ __forceinline__ int ladder_choose(const Pool &p, bool as_int, int mod
     const bool ok_n = cnt_n >= thr;
     double mean_n[3] = {0.0, 0.0, 0.0};
     if (cnt_n > 0.0) {
-#pragma unroll
-        for (int c = 0; c < 3; ++c)
-            mean_n[c] = row_mean(as_int ? static_cast<double>(p.isum[c]) : p.fsum[c], cnt_n, fixed);
+        const double sums[3] = {as_int ? static_cast<double>(p.isum[0]) : p.fsum[0],
+                                as_int ? static_cast<double>(p.isum[1]) : p.fsum[1],
+                                as_int ? static_cast<double>(p.isum[2]) : p.fsum[2]};
+        row_mean3(sums, cnt_n, fixed, mean_n);
     }
     double cnt_c = 0.0;
     double mean_c[3] = {0.0, 0.0, 0.0};
     if (!ok_n && coarse_found) {
         cnt_c = ce.fcnt;
         if (cnt_c > 0.0) {
-#pragma unroll
-            for (int c = 0; c < 3; ++c) mean_c[c] = row_mean(eff_sum_f64(ce, c_int, c), cnt_c, fixed);
+            const double sums[3] = {eff_sum_f64(ce, c_int, 0), eff_sum_f64(ce, c_int, 1),
+                                    eff_sum_f64(ce, c_int, 2)};
+            row_mean3(sums, cnt_c, fixed, mean_c);
         }
     }
     const bool ok_c = !ok_n && cnt_c >= thr;
