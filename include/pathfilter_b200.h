@@ -23,7 +23,7 @@
 extern "C" {
 #endif
 
-#define PF_ABI_VERSION 3
+#define PF_ABI_VERSION 4
 
 enum pf_status {
     PF_OK = 0,
@@ -186,21 +186,21 @@ int pf_hash_arrays(const int64_t *qx, const int64_t *qy, const int64_t *qz,
  * events: optional eviction log of capacity `event_capacity` with its int64 counter.
  * abort_flag (device int32, may be NULL): when nonzero at launch the kernel leaves
  * the tables untouched (set by pf_check_contributions for invalid input).
- * lookup_index/lookup_fp (may be NULL): also emit the resolve phase's fine lookup
- * key (stream_base_lookup, level_delta 0) for every vertex, so pf_resolve_frame
- * does not rebuild it from the vertex buffer. */
+ * lookup_keys (may be NULL): also emit the resolve phase's fine lookup key
+ * (stream_base_lookup, level_delta 0) for every vertex as one packed word,
+ * fingerprint << 32 | (slot index & 0xFFFFFFFF) (fine capacity <= 2^32), so
+ * pf_resolve_frame does not rebuild it from the vertex buffer. */
 int pf_insert_frame(const pf_config *cfg, const pf_vertices *v, const pf_table *fine,
                     const pf_table *coarse, uint64_t stream_base_accum, int64_t frame,
                     int64_t *stats, pf_evict_event *events, int64_t *event_count,
                     int64_t event_capacity, const int32_t *abort_flag,
-                    uint64_t stream_base_lookup, uint64_t *lookup_index, uint32_t *lookup_fp,
-                    void *stream);
+                    uint64_t stream_base_lookup, uint64_t *lookup_keys, void *stream);
 
 /* Fused resolve_phase (src/pipeline.py:207-283): lookup keys, fine rung, 3x3x3
  * neighbourhood, coarse rung, ladder, composite.  flat: float64[n_pixels][3]
  * scratch; work: int64 scratch of n entries plus work_count (int64[1]);
  * image = base_image + flat/spp.  source (u8[n]) and chosen (f64[n][3]) may be NULL.
- * lookup_index/lookup_fp: the keys pf_insert_frame emitted for the same vertices and
+ * lookup_keys: the packed keys pf_insert_frame emitted for the same vertices and
  * stream_base_lookup, or NULL to build them here.
  * eff_records (may be NULL): scratch of 4 * fine->capacity uint64; when given, the
  * fine table's effective (sum, count) is computed once per occupied slot into one
@@ -213,8 +213,8 @@ int pf_resolve_frame(const pf_config *cfg, const pf_vertices *v, const pf_table 
                      uint64_t stream_base_coarse, int64_t spp, const double *base_image,
                      int64_t n_pixels, double *image, double *flat, int64_t *work,
                      int64_t *work_count, uint8_t *source, double *chosen, int64_t *stats,
-                     const uint64_t *lookup_index, const uint32_t *lookup_fp,
-                     uint64_t *eff_records, int64_t *fallback_keys, void *stream);
+                     const uint64_t *lookup_keys, uint64_t *eff_records,
+                     int64_t *fallback_keys, void *stream);
 
 /* Device scratch and outputs of pf_filter_frame (all device pointers). */
 typedef struct pf_frame_buffers {
@@ -226,8 +226,7 @@ typedef struct pf_frame_buffers {
     int32_t *bad_flag;              /* input check flag, or NULL to skip validation */
     int64_t *horizon_clears_fine;   /* int64[1] counters incremented by begin_frame */
     int64_t *horizon_clears_coarse;
-    uint64_t *lookup_index;         /* n: lookup keys handed from insert to resolve */
-    uint32_t *lookup_fp;
+    uint64_t *lookup_keys;          /* n: packed lookup keys handed from insert to resolve */
     uint64_t *eff_records;          /* 4 * fine->capacity */
     double *flat;                   /* [n_pixels][3] */
     int64_t *work;                  /* n */
@@ -304,12 +303,12 @@ typedef struct pf_replica {
 } pf_replica;
 
 /* Keys of every local vertex: the fine and coarse keys (jitter stream 2) go into the
- * aggregation table as records, the fine lookup key (stream 3) to lookup_index /
- * lookup_fp (n each) for pf_resolve_replica.  abort_flag as in pf_insert_frame. */
+ * aggregation table as records, the packed fine lookup key (stream 3; as
+ * pf_insert_frame's lookup_keys) to lookup_keys (n) for pf_resolve_replica.
+ * abort_flag as in pf_insert_frame. */
 int pf_shard_keys(const pf_config *cfg, const pf_vertices *v, const pf_shard *sh,
                   int32_t has_coarse, uint64_t stream_base_accum, uint64_t stream_base_lookup,
-                  const int32_t *abort_flag, uint64_t *lookup_index, uint32_t *lookup_fp,
-                  void *stream);
+                  const int32_t *abort_flag, uint64_t *lookup_keys, void *stream);
 /* Write the round's records grouped by owner: owner o's records start at row
  * sum(owner_counts[0][:o]) of send_records.  No-op when overflow is set. */
 int pf_shard_emit(const pf_shard *sh, int64_t *send_records, uint64_t *send_requests,
@@ -331,12 +330,12 @@ int pf_replica_update(const pf_replica *replica, const uint64_t *entries, const 
 /* Empty the aggregation table (only the slots this round claimed) and its counters. */
 int pf_shard_reset(const pf_shard *sh, void *stream);
 /* resolve_phase (src/pipeline.py:207-283) of this rank's vertices against a replica:
- * the fine rung from lookup_index / lookup_fp (pf_shard_keys), the neighbourhood and
+ * the fine rung from lookup_keys (pf_shard_keys), the neighbourhood and
  * coarse rungs, the ladder, the composite into flat (pixels [pixel_base, pixel_base +
  * n_pixels), zeroed here).  work: n int64, fallback_keys: 8 * n int64 scratch. */
 int pf_resolve_replica(const pf_config *cfg, const pf_vertices *v, const pf_replica *replica,
                        uint64_t stream_base_lookup, uint64_t stream_base_coarse,
-                       const uint64_t *lookup_index, const uint32_t *lookup_fp, double *flat,
+                       const uint64_t *lookup_keys, double *flat,
                        int64_t n_pixels, int64_t pixel_base, int64_t *work,
                        int64_t *work_count, int64_t *fallback_keys, uint8_t *source,
                        double *chosen, int64_t *stats, void *stream);

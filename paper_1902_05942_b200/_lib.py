@@ -95,8 +95,8 @@ class PfFrameBuffers(ctypes.Structure):
                 ("events", ctypes.c_void_p), ("event_count", ctypes.c_void_p),
                 ("event_capacity", ctypes.c_int64), ("bad_flag", ctypes.c_void_p),
                 ("horizon_clears_fine", ctypes.c_void_p),
-                ("horizon_clears_coarse", ctypes.c_void_p), ("lookup_index", ctypes.c_void_p),
-                ("lookup_fp", ctypes.c_void_p), ("eff_records", ctypes.c_void_p),
+                ("horizon_clears_coarse", ctypes.c_void_p), ("lookup_keys", ctypes.c_void_p),
+                ("eff_records", ctypes.c_void_p),
                 ("flat", ctypes.c_void_p), ("work", ctypes.c_void_p),
                 ("work_count", ctypes.c_void_p), ("fallback_keys", ctypes.c_void_p),
                 ("phase_events", ctypes.c_void_p * 4)]
@@ -196,10 +196,9 @@ def lib() -> ctypes.CDLL:
     L.pf_make_key_arrays.argtypes = [vp, vp, vp, vp, i32, vp, vp]
     L.pf_vertex_keys.argtypes = [vp, vp, u64, i32, vp, vp]
     L.pf_hash_arrays.argtypes = [vp, vp, vp, vp, vp, vp, i64, vp, vp, vp]
-    L.pf_insert_frame.argtypes = [vp, vp, vp, vp, u64, i64, vp, vp, vp, i64, vp, u64, vp, vp,
-                                  vp]
+    L.pf_insert_frame.argtypes = [vp, vp, vp, vp, u64, i64, vp, vp, vp, i64, vp, u64, vp, vp]
     L.pf_resolve_frame.argtypes = [vp, vp, vp, vp, u64, u64, i64, vp, i64, vp, vp, vp, vp,
-                                   vp, vp, vp, vp, vp, vp, vp, vp]
+                                   vp, vp, vp, vp, vp, vp, vp]
     L.pf_filter_frame.argtypes = [vp, vp, vp, vp, i64, u64, u64, u64, i64, vp, i64, vp, vp, vp,
                                   vp, vp]
     L.pf_effective.argtypes = [vp, i32, dbl, dbl, vp, vp, vp]
@@ -208,12 +207,12 @@ def lib() -> ctypes.CDLL:
     L.pf_check_contributions.argtypes = [vp, i64, vp, vp]
     L.pf_selftest_division.argtypes = [u64, i64, dbl, vp, vp]
     L.pf_finalize_image.argtypes = [vp, vp, vp, i64, i64, vp]
-    L.pf_shard_keys.argtypes = [vp, vp, vp, i32, u64, u64, vp, vp, vp, vp]
+    L.pf_shard_keys.argtypes = [vp, vp, vp, i32, u64, u64, vp, vp, vp]
     L.pf_shard_emit.argtypes = [vp, vp, vp, vp]
     L.pf_shard_apply.argtypes = [vp, vp, vp, vp, i64, i64, vp, vp]
     L.pf_shard_publish.argtypes = [vp, vp, vp, vp, vp, vp, vp]
     L.pf_replica_update.argtypes = [vp, vp, vp, i32, i64, i32, vp]
-    L.pf_resolve_replica.argtypes = [vp, vp, vp, u64, u64, vp, vp, vp, i64, i64, vp, vp, vp, vp,
+    L.pf_resolve_replica.argtypes = [vp, vp, vp, u64, u64, vp, vp, i64, i64, vp, vp, vp, vp,
                                      vp, vp, vp]
     L.pf_shard_reset.argtypes = [vp, vp]
     L.pf_trace_paths.argtypes = [vp, vp, u64, vp, vp, i64, vp, vp]

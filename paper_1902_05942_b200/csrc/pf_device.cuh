@@ -416,6 +416,19 @@ struct CellHash {
     uint32_t fp;
 };
 
+// A lookup key handed from the insert pass to the resolve pass in one word: the low 32
+// bits of the slot index (all a probe of a table with capacity <= 2^32 reads) and the
+// fingerprint.
+__device__ __forceinline__ uint64_t pack_lookup_key(const CellHash &h) {
+    return (static_cast<uint64_t>(h.fp) << 32) | (h.index & 0xFFFFFFFFull);
+}
+__device__ __forceinline__ CellHash unpack_lookup_key(uint64_t w) {
+    CellHash h;
+    h.index = w & 0xFFFFFFFFull;
+    h.fp = static_cast<uint32_t>(w >> 32);
+    return h;
+}
+
 // hash_arrays (src/keys.py:327-339).
 __device__ __forceinline__ CellHash cell_hash(int64_t qx, int64_t qy, int64_t qz, int64_t level,
                                               uint64_t aux, int has_fp_bin, uint32_t fp_bin) {

@@ -43,7 +43,7 @@ __global__ void __launch_bounds__(kThreads, PF_INSERT_MIN_BLOCKS)
 insert_frame_kernel(pf_config cfg, pf_vertices v, pf_table fine, pf_table coarse, int has_coarse,
                     uint64_t h0, int64_t frame, int64_t *stats, pf_evict_event *events,
                     int64_t *event_count, int64_t event_cap, const int32_t *abort_flag,
-                    uint64_t h0_lookup, uint64_t *lk_index, uint32_t *lk_fp) {
+                    uint64_t h0_lookup, uint64_t *lk_keys) {
     __shared__ BlockStats bs;
     __shared__ double2 sincos_tab[220];
     __shared__ double lod_dist[32];
@@ -90,7 +90,7 @@ insert_frame_kernel(pf_config cfg, pf_vertices v, pf_table fine, pf_table coarse
         // instruction footprint inside the SM's instruction caches):
         //   0 fine (jitter stream 2), 1 coarse (stream 2, level + coarse_delta),
         //   2 the resolve phase's fine lookup key (stream 3)
-        const int nsets = lk_index != nullptr ? 3 : (has_coarse ? 2 : 1);
+        const int nsets = lk_keys != nullptr ? 3 : (has_coarse ? 2 : 1);
         double du = 0.0, dv = 0.0;
 #pragma unroll 1
         for (int set = 0; set < nsets; ++set) {
@@ -113,8 +113,7 @@ insert_frame_kernel(pf_config cfg, pf_vertices v, pf_table fine, pf_table coarse
                 ht_c = ld_relaxed(coarse.tags +
                                   (h.index & static_cast<uint64_t>(coarse.capacity - 1)));
             } else if (valid) {
-                lk_index[i] = h.index;
-                lk_fp[i] = h.fp;
+                lk_keys[i] = pack_lookup_key(h);
             }
         }
     }
@@ -174,8 +173,7 @@ struct ResolveArgs {
     double *chosen;
     int64_t *stats;
     double thr;
-    const uint64_t *lk_index;  // precomputed lookup keys (or NULL)
-    const uint32_t *lk_fp;
+    const uint64_t *lk_keys;   // precomputed packed lookup keys (or NULL)
     const ulonglong4 *rec;     // per-slot effective records of the fine table (or NULL)
     int64_t n_pixels;          // flat holds pixels [pixel_base, pixel_base + n_pixels)
     int64_t *fb_keys;          // [work row][8] lookup key + coarse hash (or NULL)
@@ -263,8 +261,7 @@ __global__ void __launch_bounds__(kThreads, PF_RESOLVE_MIN_BLOCKS) resolve_main_
         valid[k] = i0 < a.v.n;
         row[k] = valid[k] ? i0 : a.v.n - 1;  // tail lanes shadow the last vertex
         if (HAVE_KEYS) {  // keys emitted by the insert pass
-            h[k].index = ld_stream(a.lk_index + row[k], stream);
-            h[k].fp = ld_stream(a.lk_fp + row[k], stream);
+            h[k] = unpack_lookup_key(ld_stream(a.lk_keys + row[k], stream));
         } else {
             h[k] = lookup_key(a, row[k]).second;
         }
@@ -624,11 +621,10 @@ int pf_insert_frame(const pf_config *cfg, const pf_vertices *v, const pf_table *
                     const pf_table *coarse, uint64_t stream_base_accum, int64_t frame,
                     int64_t *stats, pf_evict_event *events, int64_t *event_count,
                     int64_t event_capacity, const int32_t *abort_flag,
-                    uint64_t stream_base_lookup, uint64_t *lookup_index, uint32_t *lookup_fp,
-                    void *stream) {
+                    uint64_t stream_base_lookup, uint64_t *lookup_keys, void *stream) {
     const char *fn = "pf_insert_frame";
-    if ((lookup_index == nullptr) != (lookup_fp == nullptr))
-        return fail_arg(fn, "lookup_index and lookup_fp go together");
+    if (lookup_keys && fine && fine->capacity > (1ll << 32))
+        return fail_arg(fn, "packed lookup keys need a fine capacity <= 2^32");
     if (int rc = validate_vertices(fn, v, cfg)) return rc;
     pf_config kc;
     if (int rc = prepare_config(fn, cfg, &kc)) return rc;
@@ -650,11 +646,11 @@ int pf_insert_frame(const pf_config *cfg, const pf_vertices *v, const pf_table *
     if (fine->sum_mode == PF_SUM_FIXED)
         insert_frame_kernel<true><<<g, kThreads, 0, as_stream(stream)>>>(
             kc, *v, *fine, c, coarse != nullptr, stream_base_accum, frame, stats, events,
-            event_count, event_capacity, abort_flag, stream_base_lookup, lookup_index, lookup_fp);
+            event_count, event_capacity, abort_flag, stream_base_lookup, lookup_keys);
     else
         insert_frame_kernel<false><<<g, kThreads, 0, as_stream(stream)>>>(
             kc, *v, *fine, c, coarse != nullptr, stream_base_accum, frame, stats, events,
-            event_count, event_capacity, abort_flag, stream_base_lookup, lookup_index, lookup_fp);
+            event_count, event_capacity, abort_flag, stream_base_lookup, lookup_keys);
     return check_launch(fn);
 }
 
@@ -663,11 +659,9 @@ int pf_resolve_frame(const pf_config *cfg, const pf_vertices *v, const pf_table 
                      uint64_t stream_base_coarse, int64_t spp, const double *base_image,
                      int64_t n_pixels, double *image, double *flat, int64_t *work,
                      int64_t *work_count, uint8_t *source, double *chosen, int64_t *stats,
-                     const uint64_t *lookup_index, const uint32_t *lookup_fp,
-                     uint64_t *eff_records, int64_t *fallback_keys, void *stream) {
+                     const uint64_t *lookup_keys, uint64_t *eff_records,
+                     int64_t *fallback_keys, void *stream) {
     const char *fn = "pf_resolve_frame";
-    if ((lookup_index == nullptr) != (lookup_fp == nullptr))
-        return fail_arg(fn, "lookup_index and lookup_fp go together");
     if (int rc = validate_vertices(fn, v, cfg)) return rc;
     pf_config kc;
     if (int rc = prepare_config(fn, cfg, &kc)) return rc;
@@ -700,8 +694,7 @@ int pf_resolve_frame(const pf_config *cfg, const pf_vertices *v, const pf_table 
         a.chosen = chosen;
         a.stats = stats;
         a.thr = static_cast<double>(cfg->low_count_threshold > 1 ? cfg->low_count_threshold : 1);
-        a.lk_index = lookup_index;
-        a.lk_fp = lookup_fp;
+        a.lk_keys = lookup_keys;
         a.rec = reinterpret_cast<const ulonglong4 *>(eff_records);
         a.n_pixels = n_pixels;
         a.fb_keys = fallback_keys;
@@ -715,7 +708,7 @@ int pf_resolve_frame(const pf_config *cfg, const pf_vertices *v, const pf_table 
                                                 reinterpret_cast<ulonglong4 *>(eff_records));
             if (int rc = check_launch(fn)) return rc;
         }
-        if (int rc = launch_rungs(fn, a, v->n, lookup_index != nullptr, fallback_keys != nullptr, st))
+        if (int rc = launch_rungs(fn, a, v->n, lookup_keys != nullptr, fallback_keys != nullptr, st))
             return rc;
     }
     const int64_t m = 3 * n_pixels;
@@ -727,7 +720,7 @@ int pf_resolve_frame(const pf_config *cfg, const pf_vertices *v, const pf_table 
 
 int pf_resolve_replica(const pf_config *cfg, const pf_vertices *v, const pf_replica *rp,
                        uint64_t stream_base_lookup, uint64_t stream_base_coarse,
-                       const uint64_t *lookup_index, const uint32_t *lookup_fp, double *flat,
+                       const uint64_t *lookup_keys, double *flat,
                        int64_t n_pixels, int64_t pixel_base, int64_t *work,
                        int64_t *work_count, int64_t *fallback_keys, uint8_t *source,
                        double *chosen, int64_t *stats, void *stream) {
@@ -741,7 +734,7 @@ int pf_resolve_replica(const pf_config *cfg, const pf_vertices *v, const pf_repl
         return fail_arg(fn, "bad replica");
     if (n_pixels < 0 || !flat || !stats) return fail_arg(fn, "flat / stats are NULL");
     if (v->n > 0 && (!v->throughput || !v->contribution || !work || !work_count ||
-                     !fallback_keys || !lookup_index || !lookup_fp))
+                     !fallback_keys || !lookup_keys))
         return fail_arg(fn, "throughput/contribution/work/keys is NULL");
     cudaStream_t st = as_stream(stream);
     if (cudaMemsetAsync(flat, 0, sizeof(double) * 3 * n_pixels, st) != cudaSuccess)
@@ -770,8 +763,7 @@ int pf_resolve_replica(const pf_config *cfg, const pf_vertices *v, const pf_repl
     a.chosen = chosen;
     a.stats = stats;
     a.thr = static_cast<double>(cfg->low_count_threshold > 1 ? cfg->low_count_threshold : 1);
-    a.lk_index = lookup_index;
-    a.lk_fp = lookup_fp;
+    a.lk_keys = lookup_keys;
     a.rec = reinterpret_cast<const ulonglong4 *>(rp->fine_records);
     a.n_pixels = n_pixels;
     a.fb_keys = fallback_keys;
@@ -820,13 +812,13 @@ int pf_filter_frame(const pf_config *cfg, const pf_vertices *v, const pf_table *
     mark(1);
     if (int rc = pf_insert_frame(cfg, v, fine, coarse, stream_base_accum, frame, b->acc_stats,
                                  b->events, b->event_count, b->event_capacity, b->bad_flag,
-                                 stream_base_lookup, b->lookup_index, b->lookup_fp, stream))
+                                 stream_base_lookup, b->lookup_keys, stream))
         return rc;
     mark(2);
     const int rc = pf_resolve_frame(cfg, v, fine, coarse, stream_base_lookup, stream_base_coarse,
                                     spp, base_image, n_pixels, image, b->flat, b->work,
-                                    b->work_count, source, chosen, b->res_stats, b->lookup_index,
-                                    b->lookup_fp, b->eff_records, b->fallback_keys, stream);
+                                    b->work_count, source, chosen, b->res_stats, b->lookup_keys,
+                                    b->eff_records, b->fallback_keys, stream);
     mark(3);
     return rc;
 }

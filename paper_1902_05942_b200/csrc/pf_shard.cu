@@ -158,8 +158,7 @@ __device__ __forceinline__ int64_t warp_agg_insert(const ShardK &k, OwnerCounts 
 template <bool FIXED>
 __global__ void __launch_bounds__(kT, 2)
 shard_keys_kernel(pf_config cfg, pf_vertices v, ShardK k, int has_coarse, uint64_t h0,
-                  uint64_t h0_lookup, const int32_t *abort_flag, uint64_t *lk_index,
-                  uint32_t *lk_fp) {
+                  uint64_t h0_lookup, const int32_t *abort_flag, uint64_t *lk_keys) {
     __shared__ OwnerCounts oc;
     __shared__ double2 sincos_tab[220];
     __shared__ double lod_dist[32];
@@ -202,8 +201,7 @@ shard_keys_kernel(pf_config cfg, pf_vertices v, ShardK k, int has_coarse, uint64
                 double fs[3] = {f[0], f[1], f[2]};
                 warp_agg_insert<true, FIXED>(k, oc, valid, key, qs, fs, 1);
             } else if (valid) {  // the resolve phase's lookup key (stream 3)
-                lk_index[i] = h.index;
-                lk_fp[i] = h.fp;
+                lk_keys[i] = pack_lookup_key(h);
             }
         }
     }
@@ -440,8 +438,7 @@ extern "C" {
 
 int pf_shard_keys(const pf_config *cfg, const pf_vertices *v, const pf_shard *sh,
                   int32_t has_coarse, uint64_t stream_base_accum, uint64_t stream_base_lookup,
-                  const int32_t *abort_flag, uint64_t *lookup_index, uint32_t *lookup_fp,
-                  void *stream) {
+                  const int32_t *abort_flag, uint64_t *lookup_keys, void *stream) {
     const char *fn = "pf_shard_keys";
     ShardK k;
     if (int rc = prepare_shard(fn, sh, &k)) return rc;
@@ -449,17 +446,17 @@ int pf_shard_keys(const pf_config *cfg, const pf_vertices *v, const pf_shard *sh
     pf_config kc;
     if (int rc = prepare_config(fn, cfg, &kc)) return rc;
     if (v->n == 0) return PF_OK;
-    if (!v->contribution || !lookup_index || !lookup_fp)
-        return fail_arg(fn, "contribution/lookup_index/lookup_fp is NULL");
+    if (!v->contribution || !lookup_keys)
+        return fail_arg(fn, "contribution/lookup_keys is NULL");
     cudaStream_t st = as_stream(stream);
     if (sh->sum_mode == PF_SUM_FIXED)
         shard_keys_kernel<true><<<grid_for(shard_keys_kernel<true>, v->n, 8), kT, 0, st>>>(
             kc, *v, k, has_coarse != 0, stream_base_accum, stream_base_lookup, abort_flag,
-            lookup_index, lookup_fp);
+            lookup_keys);
     else
         shard_keys_kernel<false><<<grid_for(shard_keys_kernel<false>, v->n, 8), kT, 0, st>>>(
             kc, *v, k, has_coarse != 0, stream_base_accum, stream_base_lookup, abort_flag,
-            lookup_index, lookup_fp);
+            lookup_keys);
     return check_launch(fn);
 }
 

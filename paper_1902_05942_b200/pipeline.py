@@ -354,8 +354,7 @@ def accumulate_phase(vertices, cfg: FilterConfig, state: FrameState, frame: int,
         # check, then the flag-guarded insert (no mutation on bad input), then one sync
         flag = state.buffer("bad_flag", (1,), torch.int32)
         check_contributions(vs.contribution, flag, wait=False)
-    lk_index = state.buffer("lk_index", (n,), torch.int64)
-    lk_fp = state.buffer("lk_fp", (n,), torch.int32)
+    lk_keys = state.buffer("lk_keys", (n,), torch.int64)  # packed fp << 32 | slot index
     lookup_seed = rng.stream_base(seed, rng.STREAM_JITTER_LOOKUP)
     events = state.buffer(f"events{parity}", (n, 4), torch.int64)
     ev_count = state.buffer(f"event_count{parity}", (1,), torch.int64)
@@ -367,10 +366,10 @@ def accumulate_phase(vertices, cfg: FilterConfig, state: FrameState, frame: int,
               ctypes.byref(ct) if ct is not None else None,
               rng.stream_base(seed, rng.STREAM_JITTER_ACCUM), int(frame), counters.data_ptr(),
               events.data_ptr(), ev_count.data_ptr(), n, _lib.ptr(flag), lookup_seed,
-              lk_index.data_ptr(), lk_fp.data_ptr(), _lib.stream_handle())
+              lk_keys.data_ptr(), _lib.stream_handle())
     del keep
     # resolve_phase reuses these lookup keys when called for the same stream / seed / knobs
-    state.lookup_keys = (vs, lookup_seed, cfg.to_c(), lk_index, lk_fp)
+    state.lookup_keys = (vs, lookup_seed, cfg.to_c(), lk_keys)
     _register_event_drain(state, frame, events, ev_count, parity)
     if flag is not None:
         raise_if_bad(flag)  # the guarded kernel left the tables untouched
@@ -459,7 +458,6 @@ def resolve_phase(vertices, cfg: FilterConfig, state: FrameState, frame: int, se
               int(spp), base.data_ptr(), h * w, image.data_ptr(), flat.data_ptr(),
               work.data_ptr(), work_count.data_ptr(), source.data_ptr(), _lib.ptr(chosen),
               counters.data_ptr(), lk[3].data_ptr() if lk_ok else None,
-              lk[4].data_ptr() if lk_ok else None,
               state.buffer("eff_records", (state.fine.capacity, 4), torch.int64).data_ptr(),
               state.buffer("fallback_keys", (max(n, 1), 8), torch.int64).data_ptr(),
               _lib.stream_handle())
@@ -486,15 +484,14 @@ def _fused_frame(vs: VertexStream, base_image, cfg: FilterConfig, state: FrameSt
     events = state.buffer(f"events{parity}", (max(n, 1), 4), torch.int64)
     ev_count = state.buffer(f"event_count{parity}", (1,), torch.int64)
     flag = state.buffer("bad_flag", (1,), torch.int32) if validate else None
-    lk_index = state.buffer("lk_index", (max(n, 1),), torch.int64)
-    lk_fp = state.buffer("lk_fp", (max(n, 1),), torch.int32)
+    lk_keys = state.buffer("lk_keys", (max(n, 1),), torch.int64)
     b = _lib.PfFrameBuffers()
     b.acc_stats, b.res_stats = acc.data_ptr(), res.data_ptr()
     b.events, b.event_count, b.event_capacity = events.data_ptr(), ev_count.data_ptr(), n
     b.bad_flag = _lib.ptr(flag)
     b.horizon_clears_fine = state.fine._clears.data_ptr()
     b.horizon_clears_coarse = state.coarse._clears.data_ptr() if state.coarse is not None else None
-    b.lookup_index, b.lookup_fp = lk_index.data_ptr(), lk_fp.data_ptr()
+    b.lookup_keys = lk_keys.data_ptr()
     b.eff_records = state.buffer("eff_records", (state.fine.capacity, 4), torch.int64).data_ptr()
     b.flat = state.buffer("flat", (h * w, 3), torch.float64).data_ptr()
     b.work = state.buffer("work", (max(n, 1),), torch.int64).data_ptr()
@@ -519,7 +516,7 @@ def _fused_frame(vs: VertexStream, base_image, cfg: FilterConfig, state: FrameSt
     state.fine.frame = frame
     if state.coarse is not None:
         state.coarse.frame = frame
-    state.lookup_keys = (vs, lookup_seed, cc, lk_index[:n], lk_fp[:n])
+    state.lookup_keys = (vs, lookup_seed, cc, lk_keys[:n])
     if n:
         _register_event_drain(state, frame, events, ev_count, parity)
     stats = FrameStats(frame=frame, n_vertices=n, counters=acc)

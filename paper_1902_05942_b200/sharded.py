@@ -216,8 +216,7 @@ def filter_frame_sharded(vertices, base_image, cfg: FilterConfig, st: ShardedSta
     lookup_seed = rng.stream_base(seed, rng.STREAM_JITTER_LOOKUP)
     coarse_seed = rng.stream_base(seed, rng.STREAM_JITTER_LOOKUP if cfg.jitter
                                   else rng.STREAM_JITTER_ACCUM)
-    lk_index = st.buffer("lk_index", (max(n, 1),), torch.int64)
-    lk_fp = st.buffer("lk_fp", (max(n, 1),), torch.int32)
+    lk_keys = st.buffer("lk_keys", (max(n, 1),), torch.int64)  # packed fp << 32 | slot index
 
     def mark(k):
         if phase_events is not None:
@@ -241,8 +240,8 @@ def filter_frame_sharded(vertices, base_image, cfg: FilterConfig, st: ShardedSta
     while True:
         sh = st.c_shard()
         _lib.call("pf_shard_keys", ctypes.byref(cc), ctypes.byref(v), ctypes.byref(sh), has_coarse,
-                  accum_seed, lookup_seed, st.bad_flag.data_ptr(), lk_index.data_ptr(),
-                  lk_fp.data_ptr(), stream)
+                  accum_seed, lookup_seed, st.bad_flag.data_ptr(), lk_keys.data_ptr(),
+                  stream)
         mark(1)
         _lib.call("pf_shard_emit", ctypes.byref(sh), st.send_records.data_ptr(),
                   st.send_requests.data_ptr(), stream)
@@ -299,7 +298,7 @@ def filter_frame_sharded(vertices, base_image, cfg: FilterConfig, st: ShardedSta
     work_count = st.buffer("work_count", (1,), torch.int64)
     fb_keys = st.buffer("fallback_keys", (max(n, 1), 8), torch.int64)
     _lib.call("pf_resolve_replica", ctypes.byref(cc), ctypes.byref(v), ctypes.byref(rp),
-              lookup_seed, coarse_seed, lk_index.data_ptr(), lk_fp.data_ptr(), flat.data_ptr(),
+              lookup_seed, coarse_seed, lk_keys.data_ptr(), flat.data_ptr(),
               n_pix, int(pixel_base), work.data_ptr(), work_count.data_ptr(), fb_keys.data_ptr(),
               source.data_ptr(), _lib.ptr(chosen), res.data_ptr(), stream)
     del keep
