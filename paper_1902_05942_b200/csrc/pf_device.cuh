@@ -516,7 +516,9 @@ __device__ __forceinline__ VertexIn load_vertex(const pf_vertices &v, int64_t i,
     x.dist = ld_stream(v.camera_distance + i, pol);
     x.pixel = ld_stream(v.pixel + i, pol);
     x.sample = ld_stream(v.sample + i, pol);
-    x.layer = (v.layer_id != nullptr) ? ld_stream(v.layer_id + i, pol) : 0;
+    // the layer only enters the aux word (aux_word); the default key reads no layer ids
+    x.layer = (v.layer_id != nullptr && (cfg.include_incident_angle || cfg.include_layer))
+                  ? ld_stream(v.layer_id + i, pol) : 0;
     if (cfg.include_incident_angle && v.omega_r != nullptr) {
 #pragma unroll
         for (int c = 0; c < 3; ++c) x.omega[c] = ld_stream(v.omega_r + 3 * i + c, pol);
