@@ -34,6 +34,15 @@ __device__ __forceinline__ void log_eviction(pf_evict_event *events, int64_t *co
 
 // ------------------------------------------------------------------ insert
 
+// The fused insert does not warp-merge equal keys (bit 0: merge fine keys, bit 1:
+// coarse): after the merge only 1.21 (fine) / 1.29 (coarse) vertices share an update
+// on the 1080p 4-bounce stream (tools/merge_stats.py), and the two MATCH.ANY plus the
+// pointer-jumping rounds cost more issue slots than the extra REDs (insert 0.93 ->
+// 0.82 ms; merging one table only: 0.83-0.86 ms).  Lanes with equal keys probe side by
+// side and resolve to the same cell through probe_insert's claim / evict protocol.
+#ifndef PF_FRAME_MERGE
+#define PF_FRAME_MERGE 0
+#endif
 #ifndef PF_INSERT_MIN_BLOCKS
 #define PF_INSERT_MIN_BLOCKS 3  // 3 x 256 threads per SM: <= 85 registers
 #endif
@@ -124,7 +133,7 @@ insert_frame_kernel(pf_config cfg, pf_vertices v, pf_table fine, pf_table coarse
         const pf_table &t = tb == 0 ? fine : coarse;
         const CellHash h = tb == 0 ? hf : hc;
         const LaneInsert r = warp_insert<FIXED>(t, valid, h.index, h.fp, val, frame,
-                                                tb == 0 ? ht_f : ht_c);
+                                                tb == 0 ? ht_f : ht_c, (PF_FRAME_MERGE >> tb) & 1);
         warp_count(bs, tb == 0 ? PF_STAT_PROBE_FAILURES : PF_STAT_COARSE_PROBE_FAILURES,
                    valid && r.status == 2);
         warp_count(bs, tb == 0 ? PF_STAT_EVICTIONS : PF_STAT_COARSE_EVICTIONS,

@@ -35,10 +35,16 @@ template <bool FIXED, bool WEIGHTED>
 __device__ __forceinline__ LaneInsert warp_insert_sums(const pf_table &t, bool valid, uint64_t idx,
                                                        uint32_t fp, int64_t qsum[3],
                                                        double fsum[3], uint64_t weight,
-                                                       int64_t frame, uint64_t home_tag) {
+                                                       int64_t frame, uint64_t home_tag,
+                                                       bool merge = true) {
     const unsigned lane = threadIdx.x & 31u;
     const uint64_t k2 = static_cast<uint64_t>(fp) | (static_cast<uint64_t>(valid) << 32);
-    const unsigned peers = __match_any_sync(kFull, valid ? idx : 0ull) & __match_any_sync(kFull, k2);
+    // merge == false: every lane is its own group; lanes with the same key then probe
+    // side by side (the claim CAS / eviction protocol of probe_insert resolves them to
+    // one cell exactly as the merged path does) and each adds its own vertex
+    const unsigned peers = merge ? (__match_any_sync(kFull, valid ? idx : 0ull) &
+                                    __match_any_sync(kFull, k2))
+                                 : (1u << lane);
     const int leader = __ffs(peers) - 1;
     const bool is_leader = valid && static_cast<int>(lane) == leader;
     if (WEIGHTED && !valid) weight = 0;
@@ -115,7 +121,7 @@ __device__ __forceinline__ LaneInsert warp_insert_sums(const pf_table &t, bool v
 template <bool FIXED>
 __device__ __forceinline__ LaneInsert warp_insert(const pf_table &t, bool valid, uint64_t idx,
                                                   uint32_t fp, const double val[3], int64_t frame,
-                                                  uint64_t home_tag) {
+                                                  uint64_t home_tag, bool merge = true) {
     int64_t qsum[3];
     double fsum[3];
 #pragma unroll
@@ -123,7 +129,7 @@ __device__ __forceinline__ LaneInsert warp_insert(const pf_table &t, bool valid,
         if (FIXED) qsum[c] = valid ? quantize_fixed(val[c]) : 0;
         else fsum[c] = valid ? val[c] : 0.0;
     }
-    return warp_insert_sums<FIXED, false>(t, valid, idx, fp, qsum, fsum, 1, frame, home_tag);
+    return warp_insert_sums<FIXED, false>(t, valid, idx, fp, qsum, fsum, 1, frame, home_tag, merge);
 }
 
 }  // namespace pf
