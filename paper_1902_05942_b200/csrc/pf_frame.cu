@@ -132,8 +132,10 @@ insert_frame_kernel(pf_config cfg, pf_vertices v, pf_table fine, pf_table coarse
         if (tb == 1 && !has_coarse) break;
         const pf_table &t = tb == 0 ? fine : coarse;
         const CellHash h = tb == 0 ? hf : hc;
-        const LaneInsert r = warp_insert<FIXED>(t, valid, h.index, h.fp, val, frame,
-                                                tb == 0 ? ht_f : ht_c, (PF_FRAME_MERGE >> tb) & 1);
+        const uint64_t home_tag = tb == 0 ? ht_f : ht_c;
+        const LaneInsert r = ((PF_FRAME_MERGE >> tb) & 1)
+            ? warp_insert<FIXED>(t, valid, h.index, h.fp, val, frame, home_tag)
+            : lane_insert<FIXED>(t, valid, h.index, h.fp, val, frame, home_tag);
         warp_count(bs, tb == 0 ? PF_STAT_PROBE_FAILURES : PF_STAT_COARSE_PROBE_FAILURES,
                    valid && r.status == 2);
         warp_count(bs, tb == 0 ? PF_STAT_EVICTIONS : PF_STAT_COARSE_EVICTIONS,

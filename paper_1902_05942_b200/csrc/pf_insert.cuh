@@ -117,6 +117,45 @@ __device__ __forceinline__ LaneInsert warp_insert_sums(const pf_table &t, bool v
     return out;
 }
 
+// One vertex per lane, no warp collectives: every valid lane probes / claims for its own
+// key and adds its own quantised radiance and a count of 1 (lanes holding the same key
+// resolve to the same cell through probe_insert's claim CAS and eviction protocol).
+template <bool FIXED>
+__device__ __forceinline__ LaneInsert lane_insert(const pf_table &t, bool valid, uint64_t idx,
+                                                  uint32_t fp, const double val[3], int64_t frame,
+                                                  uint64_t home_tag) {
+    LaneInsert out;
+    out.slot = -1;
+    out.status = 2;
+    out.probe_len = 0;
+    out.victim_tag = 0;
+    out.victim_touch = 0;
+    out.leader = valid;
+    out.peers = 1u << (threadIdx.x & 31u);
+    if (!valid) return out;
+    const InsertResult r = probe_insert(t, idx, fp, home_tag);
+    if (r.status != 2) {
+        const int64_t s = r.slot;
+        const uint64_t keep = l2_evict_last();
+#pragma unroll
+        for (int c = 0; c < 3; ++c) {
+            if (FIXED)
+                red_add_u64(static_cast<int64_t *>(t.sums) + 3 * s + c,
+                            static_cast<uint64_t>(quantize_fixed(val[c])), keep);
+            else
+                red_add_f64(static_cast<double *>(t.sums) + 3 * s + c, val[c], keep);
+        }
+        red_add_u64(t.counts + s, 1ull, keep);
+        st_relaxed_u64(t.last_touch + s, static_cast<uint64_t>(frame));
+    }
+    out.slot = r.slot;
+    out.status = r.status;
+    out.probe_len = r.probe_len;
+    out.victim_tag = r.victim_tag;
+    out.victim_touch = r.victim_touch;
+    return out;
+}
+
 // One vertex per lane: quantise the lane's radiance and insert it (weight 1).
 template <bool FIXED>
 __device__ __forceinline__ LaneInsert warp_insert(const pf_table &t, bool valid, uint64_t idx,
