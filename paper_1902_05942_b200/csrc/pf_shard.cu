@@ -74,12 +74,14 @@ __device__ __forceinline__ void owner_flush(const OwnerCounts &oc, const ShardK 
 template <bool VALUES, bool FIXED>
 __device__ __forceinline__ int64_t warp_agg_insert(const ShardK &k, OwnerCounts &oc, bool valid,
                                                    uint64_t key, int64_t qsum[3], double fsum[3],
-                                                   uint64_t weight) {
+                                                   uint64_t weight, bool merge = true) {
     const unsigned lane = threadIdx.x & 31u;
-    const unsigned peers = __match_any_sync(kFull, valid ? key : kAggEmpty);
+    // merge == false: every lane adds its own key (equal keys racing for one empty slot
+    // resolve through the claim CAS; the loser leaves a hole in the distinct list)
+    const unsigned peers = merge ? __match_any_sync(kFull, valid ? key : kAggEmpty) : (1u << lane);
     const int leader = __ffs(peers) - 1;
     const bool is_leader = valid && static_cast<int>(lane) == leader;
-    if (VALUES) {
+    if (VALUES && merge) {
         if (!valid) weight = 0;
         // group totals by pointer jumping (as warp_insert_sums)
         const unsigned above = valid && lane < 31 ? (peers & (0xFFFFFFFFu << (lane + 1))) : 0u;
@@ -150,10 +152,15 @@ __device__ __forceinline__ int64_t warp_agg_insert(const ShardK &k, OwnerCounts 
             red_add_u64(s.agg_counts + slot, weight, keep);
         }
     }
-    return __shfl_sync(kFull, slot, leader);
+    return merge ? __shfl_sync(kFull, slot, leader) : slot;
 }
 
 // ------------------------------------------------------------------ round 1 keys
+
+#ifndef PF_SHARD_MERGE
+#define PF_SHARD_MERGE 1  // warp-merge equal keys before the aggregation table: without it racing
+                          // duplicates leave holes that overflow the distinct list (regrows)
+#endif
 
 template <bool FIXED>
 __global__ void __launch_bounds__(kT, 2)
@@ -199,7 +206,7 @@ shard_keys_kernel(pf_config cfg, pf_vertices v, ShardK k, int has_coarse, uint64
                 const uint64_t key = agg_key(set, h.index & k.home_mask, h.fp);
                 int64_t qs[3] = {q[0], q[1], q[2]};
                 double fs[3] = {f[0], f[1], f[2]};
-                warp_agg_insert<true, FIXED>(k, oc, valid, key, qs, fs, 1);
+                warp_agg_insert<true, FIXED>(k, oc, valid, key, qs, fs, 1, PF_SHARD_MERGE);
             } else if (valid) {  // the resolve phase's lookup key (stream 3)
                 lk_keys[i] = pack_lookup_key(h);
             }
