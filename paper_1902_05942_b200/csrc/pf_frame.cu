@@ -126,6 +126,9 @@ insert_frame_kernel(pf_config cfg, pf_vertices v, pf_table fine, pf_table coarse
             }
         }
     }
+    int64_t qval[3];  // quantised once for both tables
+#pragma unroll
+    for (int c = 0; c < 3; ++c) qval[c] = FIXED ? quantize_fixed(val[c]) : 0;
     // unrolled: each copy of warp_insert addresses its table's parameters directly
 #pragma unroll
     for (int tb = 0; tb < 2; ++tb) {
@@ -135,7 +138,7 @@ insert_frame_kernel(pf_config cfg, pf_vertices v, pf_table fine, pf_table coarse
         const uint64_t home_tag = tb == 0 ? ht_f : ht_c;
         const LaneInsert r = ((PF_FRAME_MERGE >> tb) & 1)
             ? warp_insert<FIXED>(t, valid, h.index, h.fp, val, frame, home_tag)
-            : lane_insert<FIXED>(t, valid, h.index, h.fp, val, frame, home_tag);
+            : lane_insert<FIXED>(t, valid, h.index, h.fp, qval, val, frame, home_tag);
         warp_count(bs, tb == 0 ? PF_STAT_PROBE_FAILURES : PF_STAT_COARSE_PROBE_FAILURES,
                    valid && r.status == 2);
         warp_count(bs, tb == 0 ? PF_STAT_EVICTIONS : PF_STAT_COARSE_EVICTIONS,

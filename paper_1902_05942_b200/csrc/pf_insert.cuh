@@ -120,9 +120,11 @@ __device__ __forceinline__ LaneInsert warp_insert_sums(const pf_table &t, bool v
 // One vertex per lane, no warp collectives: every valid lane probes / claims for its own
 // key and adds its own quantised radiance and a count of 1 (lanes holding the same key
 // resolve to the same cell through probe_insert's claim CAS and eviction protocol).
+// q: the lane's radiance already quantised (FIXED), val: as float64 (float mode).
 template <bool FIXED>
 __device__ __forceinline__ LaneInsert lane_insert(const pf_table &t, bool valid, uint64_t idx,
-                                                  uint32_t fp, const double val[3], int64_t frame,
+                                                  uint32_t fp, const int64_t q[3],
+                                                  const double val[3], int64_t frame,
                                                   uint64_t home_tag) {
     LaneInsert out;
     out.slot = -1;
@@ -141,7 +143,7 @@ __device__ __forceinline__ LaneInsert lane_insert(const pf_table &t, bool valid,
         for (int c = 0; c < 3; ++c) {
             if (FIXED)
                 red_add_u64(static_cast<int64_t *>(t.sums) + 3 * s + c,
-                            static_cast<uint64_t>(quantize_fixed(val[c])), keep);
+                            static_cast<uint64_t>(q[c]), keep);
             else
                 red_add_f64(static_cast<double *>(t.sums) + 3 * s + c, val[c], keep);
         }
