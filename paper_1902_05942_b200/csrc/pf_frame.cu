@@ -256,9 +256,8 @@ __device__ __forceinline__ void composite(const ResolveArgs &a, int64_t i, int64
 #endif
 template <int KV, bool HAVE_KEYS>
 __global__ void __launch_bounds__(kThreads, PF_RESOLVE_MIN_BLOCKS) resolve_main_kernel(ResolveArgs a) {
-    __shared__ BlockStats bs;
-    stats_init(bs, false);
-    __syncthreads();
+    // no CTA counters and no barriers: the fine / fallback row counts follow from the
+    // work list (main_row_counts in the next kernel), rows outside the image are rare
     const pf_config &cfg = a.cfg;
     const uint64_t stream = l2_evict_first(), keep = l2_evict_last();
     const uint64_t fmask = static_cast<uint64_t>(a.fine.capacity) - 1;
@@ -348,12 +347,23 @@ __global__ void __launch_bounds__(kThreads, PF_RESOLVE_MIN_BLOCKS) resolve_main_
             wb = __shfl_sync(kFull, wb, __ffs(m) - 1);
             if (need) a.work[static_cast<int64_t>(wb) + __popc(m & ((1u << lane) - 1u))] = row[k];
         }
-        warp_count(bs, PF_STAT_SOURCE_FINE, valid[k] && fine_ok);
-        warp_count(bs, PF_STAT_BAD_PIXELS, valid[k] && fine_ok && !(pixel[k] >= 0 && pixel[k] < a.n_pixels));
-        warp_count(bs, PF_STAT_FALLBACK_ROWS, need);
+        const bool bad = valid[k] && fine_ok && !(pixel[k] >= 0 && pixel[k] < a.n_pixels);
+        if (__any_sync(kFull, bad)) {
+            const unsigned b = __ballot_sync(kFull, bad);
+            if ((threadIdx.x & 31) == 0)
+                atomicAdd(reinterpret_cast<unsigned long long *>(a.stats + PF_STAT_BAD_PIXELS),
+                          static_cast<unsigned long long>(__popc(b)));
+        }
     }
-    __syncthreads();
-    stats_flush(bs, a.stats, false);
+}
+
+// resolve_main's row counters, once per resolve: every row it saw either took the fine
+// rung or went to the work list (called by one thread of the kernel that follows it).
+__device__ __forceinline__ void main_row_counts(const ResolveArgs &a, int64_t n_work) {
+    atomicAdd(reinterpret_cast<unsigned long long *>(a.stats + PF_STAT_FALLBACK_ROWS),
+              static_cast<unsigned long long>(n_work));
+    atomicAdd(reinterpret_cast<unsigned long long *>(a.stats + PF_STAT_SOURCE_FINE),
+              static_cast<unsigned long long>(a.v.n - n_work));
 }
 
 // The work rows' lookup keys (q, level, aux; stream 3) and coarse hashes, one row per
@@ -406,6 +416,7 @@ __global__ void __launch_bounds__(kThreads) resolve_fallback_kernel(ResolveArgs 
     const pf_config &cfg = a.cfg;
     const int lane = threadIdx.x & 31;
     const int64_t n_work = *a.work_count;
+    if (blockIdx.x == 0 && threadIdx.x == 0) main_row_counts(a, n_work);
     const int64_t warp0 = static_cast<int64_t>(blockIdx.x) * kWarps + (threadIdx.x >> 5);
     const int64_t nwarps = static_cast<int64_t>(gridDim.x) * kWarps;
     const int mode = cfg.temporal_mode;
@@ -513,6 +524,7 @@ __global__ void __launch_bounds__(kThreads) resolve_pool_kernel(ResolveArgs a) {
     const bool fixed = a.fine.sum_mode == PF_SUM_FIXED;
     const uint64_t fmask = static_cast<uint64_t>(a.fine.capacity) - 1;
     const int64_t n_work = *a.work_count;
+    if (blockIdx.x == 0 && threadIdx.x == 0) main_row_counts(a, n_work);
     for (int64_t base = static_cast<int64_t>(blockIdx.x) * kPoolRows; base < n_work;
          base += static_cast<int64_t>(gridDim.x) * kPoolRows) {
         const int rows = static_cast<int>(n_work - base < kPoolRows ? n_work - base : kPoolRows);
