@@ -581,20 +581,25 @@ __device__ __forceinline__ KeyShared key_shared(const pf_config &cfg, const Vert
     return k;
 }
 
-// make_key_arrays for one vertex and one level_delta (src/keys.py:342-359).
-// jit = 0 disables jitter; (u, v) are the disc offsets.
-__device__ __forceinline__ CellKey make_key(const pf_config &cfg, const VertexIn &x,
-                                            const KeyShared &ks, int jit, double u, double v,
-                                            int32_t level_delta, double jittered[3]) {
+// The level-independent jitter direction u*t1 + v*t2 (src/keys.py:268, before the
+// scaling by the voxel size), numpy's operation order.
+__device__ __forceinline__ void jitter_dir(double u, double v, const double t1[3],
+                                           const double t2[3], double w[3]) {
+#pragma unroll
+    for (int c = 0; c < 3; ++c) w[c] = dadd(dmul(u, t1[c]), dmul(v, t2[c]));
+}
+
+// make_key_arrays for one vertex and one level_delta (src/keys.py:342-359), given the
+// jitter direction w (jitter_dir; ignored when jit = 0).
+__device__ __forceinline__ CellKey make_key_w(const pf_config &cfg, const VertexIn &x,
+                                              const KeyShared &ks, int jit, const double w[3],
+                                              int32_t level_delta, double jittered[3]) {
     int64_t lv = clamp_level(ks.lv0, level_delta);
     if (jit) {
         const double step = voxel_step(cfg.base_voxel, lv);
         double d2 = 0.0;
 #pragma unroll
-        for (int c = 0; c < 3; ++c) {
-            const double off = dmul(dadd(dmul(u, ks.frame.t1[c]), dmul(v, ks.frame.t2[c])), step);
-            jittered[c] = dadd(x.pos[c], off);
-        }
+        for (int c = 0; c < 3; ++c) jittered[c] = dadd(x.pos[c], dmul(w[c], step));
         // np.linalg.norm(x' - x, axis=1): sqrt of the sequential sum of squares
         const double e0 = dsub(jittered[0], x.pos[0]);
         const double e1 = dsub(jittered[1], x.pos[1]);
@@ -619,6 +624,16 @@ __device__ __forceinline__ CellKey make_key(const pf_config &cfg, const VertexIn
     k.level = lv;
     k.aux = ks.aux;
     return k;
+}
+
+// make_key_arrays for one vertex and one level_delta (src/keys.py:342-359).
+// jit = 0 disables jitter; (u, v) are the disc offsets.
+__device__ __forceinline__ CellKey make_key(const pf_config &cfg, const VertexIn &x,
+                                            const KeyShared &ks, int jit, double u, double v,
+                                            int32_t level_delta, double jittered[3]) {
+    double w[3] = {0.0, 0.0, 0.0};
+    if (jit) jitter_dir(u, v, ks.frame.t1, ks.frame.t2, w);
+    return make_key_w(cfg, x, ks, jit, w, level_delta, jittered);
 }
 
 __device__ __forceinline__ CellHash key_hash(const CellKey &k, const KeyShared &ks) {
