@@ -126,9 +126,11 @@ __device__ __forceinline__ double np_min(double a, double b) {
 // draw_unit_array(seed, stream, path_id, 0, dim) for dims 0 and 1
 // (src/rng.py:62-78, src/pipeline.py:119-123); h0 = mix64(seed ^ stream*G) is a
 // host constant.
-__device__ __forceinline__ void jitter_draws(uint64_t h0, int64_t pixel, int64_t sample,
-                                             double &u1, double &u2) {
-    const uint64_t pid = (static_cast<uint64_t>(sample) << 32) | static_cast<uint64_t>(pixel);
+__device__ __forceinline__ uint64_t path_id(int64_t pixel, int64_t sample) {  // src/tracer.py:82-84
+    return (static_cast<uint64_t>(sample) << 32) | static_cast<uint64_t>(pixel);
+}
+
+__device__ __forceinline__ void jitter_draws_pid(uint64_t h0, uint64_t pid, double &u1, double &u2) {
     uint64_t h = mix64(h0 ^ (pid + kGolden));
     h = mix64(h ^ (0ull + kGolden));
     const uint64_t a = mix64(h ^ (0ull + kGolden));
@@ -136,6 +138,11 @@ __device__ __forceinline__ void jitter_draws(uint64_t h0, int64_t pixel, int64_t
     const double inv = 1.0 / 9007199254740992.0;  // 2^-53, exact
     u1 = static_cast<double>(a >> 11) * inv;
     u2 = static_cast<double>(b >> 11) * inv;
+}
+
+__device__ __forceinline__ void jitter_draws(uint64_t h0, int64_t pixel, int64_t sample,
+                                             double &u1, double &u2) {
+    jitter_draws_pid(h0, path_id(pixel, sample), u1, u2);
 }
 
 // ------------------------------------------------------------------ glibc sin / cos
