@@ -162,13 +162,26 @@ __device__ __forceinline__ int64_t warp_agg_insert(const ShardK &k, OwnerCounts 
                           // duplicates leave holes that overflow the distinct list (regrows)
 #endif
 
+// 3 CTAs per SM (80 registers): per-rank frame 1.58-1.68 -> 1.45 ms at G = 2 and
+// 1.50 -> 1.37 ms at G = 4 (tools/shard_sim.py); 4 CTAs or parking the frame and position
+// in shared memory (PF_SHARD_PARK) measured the same.
+#ifndef PF_SHARD_KEYS_MIN_BLOCKS
+#define PF_SHARD_KEYS_MIN_BLOCKS 3
+#endif
+#ifndef PF_SHARD_PARK
+#define PF_SHARD_PARK 0  // tangent frame and position wait in shared memory (as the fused insert)
+#endif
+
 template <bool FIXED>
-__global__ void __launch_bounds__(kT, 2)
+__global__ void __launch_bounds__(kT, PF_SHARD_KEYS_MIN_BLOCKS)
 shard_keys_kernel(pf_config cfg, pf_vertices v, ShardK k, int has_coarse, uint64_t h0,
                   uint64_t h0_lookup, const int32_t *abort_flag, uint64_t *lk_keys) {
     __shared__ OwnerCounts oc;
     __shared__ double2 sincos_tab[220];
     __shared__ double lod_dist[32];
+#if PF_SHARD_PARK
+    __shared__ double park[9][kT];  // t1, t2, position per thread
+#endif
     if (abort_flag != nullptr && *abort_flag != 0) return;
     owner_init(oc, k.s.world);
     stage_sincos_table(sincos_tab);
@@ -190,18 +203,45 @@ shard_keys_kernel(pf_config cfg, pf_vertices v, ShardK k, int has_coarse, uint64
             else f[c] = val;
         }
         const KeyShared ks = key_shared(cfg, x, lod_dist);
-        double du = 0.0, dv = 0.0;
+#if PF_SHARD_PARK
+#pragma unroll
+        for (int c = 0; c < 3; ++c) {
+            park[c][threadIdx.x] = ks.frame.t1[c];
+            park[3 + c][threadIdx.x] = ks.frame.t2[c];
+            park[6 + c][threadIdx.x] = x.pos[c];
+        }
+#endif
+        const uint64_t pid = path_id(x.pixel, x.sample);
+        double w[3] = {0.0, 0.0, 0.0};  // jitter direction u*t1 + v*t2
 #pragma unroll 1
         for (int set = 0; set < 3; ++set) {
             if (set == 1 && !has_coarse) continue;
             if (set != 1 && cfg.jitter) {  // the coarse set reuses the fine set's offsets
-                double u1, u2;
-                jitter_draws(set == 0 ? h0 : h0_lookup, x.pixel, x.sample, u1, u2);
+                double u1, u2, du, dv;
+                jitter_draws_pid(set == 0 ? h0 : h0_lookup, pid, u1, u2);
                 disc_offset(u1, u2, du, dv, sincos_tab);
+#if PF_SHARD_PARK
+                double t1[3], t2[3];
+#pragma unroll
+                for (int c = 0; c < 3; ++c) {
+                    t1[c] = park[c][threadIdx.x];
+                    t2[c] = park[3 + c][threadIdx.x];
+                }
+                jitter_dir(du, dv, t1, t2, w);
+#else
+                jitter_dir(du, dv, ks.frame.t1, ks.frame.t2, w);
+#endif
             }
             double jt[3];
+#if PF_SHARD_PARK
+            VertexIn xk = x;
+#pragma unroll
+            for (int c = 0; c < 3; ++c) xk.pos[c] = park[6 + c][threadIdx.x];
+#else
+            const VertexIn &xk = x;
+#endif
             const CellHash h = key_hash(
-                make_key(cfg, x, ks, cfg.jitter, du, dv, set == 1 ? cfg.coarse_delta : 0, jt), ks);
+                make_key_w(cfg, xk, ks, cfg.jitter, w, set == 1 ? cfg.coarse_delta : 0, jt), ks);
             if (set < 2) {
                 const uint64_t key = agg_key(set, h.index & k.home_mask, h.fp);
                 int64_t qs[3] = {q[0], q[1], q[2]};
