@@ -53,6 +53,9 @@ __device__ __forceinline__ void log_eviction(pf_evict_event *events, int64_t *co
 #define PF_POS_SMEM 1  // the position too (0.784 -> 0.775 ms)
 #endif
 
+#ifndef PF_INSERT_PREFETCH
+#define PF_INSERT_PREFETCH 0  // L2 prefetch of the CTA's next vertex tile: 5 us slower now
+#endif
 #ifndef PF_INSERT_MIN_BLOCKS
 #define PF_INSERT_MIN_BLOCKS 3  // 3 x 256 threads per SM: <= 85 registers
 #endif
@@ -94,7 +97,7 @@ insert_frame_kernel(pf_config cfg, pf_vertices v, pf_table fine, pf_table coarse
             const int64_t nxt = (tile + gridDim.x) * kThreads;
             const int64_t lines3 = 3 * kThreads * 8 / 128, lines1 = kThreads * 8 / 128;
             const int k = threadIdx.x;
-            if (nxt < v.n) {
+            if (PF_INSERT_PREFETCH && nxt < v.n) {
                 if (k < lines3) {
                     prefetch_l2(reinterpret_cast<const char *>(v.position + 3 * nxt) + 128 * k);
                     prefetch_l2(reinterpret_cast<const char *>(v.normal + 3 * nxt) + 128 * k);
