@@ -131,6 +131,9 @@ typedef struct pf_evict_event {
 } pf_evict_event;
 
 int pf_abi_version(void);
+/* Source id of the build: SHA-256 prefix of the CUDA sources, headers and nvcc flags
+ * (paper_1902_05942_b200/_lib.py: source_id).  Ties a binary to the tree it came from. */
+const char *pf_build_id(void);
 const char *pf_last_error(void);
 int pf_device_sm_count(void);
 /* Host only: the config every entry point actually runs with -- `in` plus the

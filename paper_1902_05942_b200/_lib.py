@@ -7,6 +7,7 @@ library, or calling one without a CUDA device, raises immediately.
 from __future__ import annotations
 
 import ctypes
+import hashlib
 import os
 import subprocess
 
@@ -34,22 +35,57 @@ EXPORTS = ("pf_abi_version", "pf_last_error", "pf_device_sm_count", "pf_accumula
            "pf_count_occupied", "pf_finalize_image", "pf_shard_keys", "pf_shard_emit",
            "pf_shard_apply", "pf_shard_publish", "pf_replica_update", "pf_shard_reset",
            "pf_resolve_replica", "pf_trace_paths", "pf_sincos", "pf_segment_deltas",
-           "pf_begin_frame_checked", "pf_prepare_config")
+           "pf_begin_frame_checked", "pf_prepare_config", "pf_build_id")
+
+_BUILD_TAG = b"PF_BUILD_ID="
+
+
+def source_id(extra_flags: tuple[str, ...] = ()) -> str:
+    """SHA-256 (first 16 hex digits) of every source and header plus the nvcc flags:
+    the identity a library built from this tree carries (pf_build_id)."""
+    h = hashlib.sha256()
+    for p in sorted(SOURCES + HEADERS):
+        h.update(os.path.relpath(p, _ROOT).encode())
+        with open(p, "rb") as f:
+            h.update(f.read())
+    h.update(" ".join(NVCC_FLAGS + list(extra_flags)).encode())
+    return h.hexdigest()[:16]
+
+
+def library_id(path: str = LIB_PATH) -> str | None:
+    """The build id embedded in a built library (read from the file, not loaded)."""
+    try:
+        with open(path, "rb") as f:
+            data = f.read()
+    except OSError:
+        return None
+    k = data.find(_BUILD_TAG)
+    if k < 0:
+        return None
+    return data[k + len(_BUILD_TAG):k + len(_BUILD_TAG) + 16].decode(errors="replace")
 
 
 def build(force: bool = False, verbose: bool = False) -> str:
-    """Compile the CUDA sources for sm_100a into the in-tree shared library."""
-    newest = max(os.path.getmtime(p) for p in SOURCES + HEADERS)
-    if not force and os.path.exists(LIB_PATH) and os.path.getmtime(LIB_PATH) >= newest:
-        return LIB_PATH
+    """Compile the CUDA sources for sm_100a into the in-tree shared library.  The
+    library is rebuilt whenever its embedded build id differs from the tree's."""
     if not force and os.environ.get("PF_LIB") and os.path.exists(LIB_PATH):
         return LIB_PATH  # a prebuilt variant library (tools/build_variant.sh): never rebuilt
+    sid = source_id()
+    if not force and library_id() == sid:
+        return LIB_PATH
     nvcc = os.environ.get("NVCC", "nvcc")
-    cmd = [nvcc, *NVCC_FLAGS, "-o", LIB_PATH, *SOURCES]
+    tmp = LIB_PATH + ".tmp"
+    cmd = [nvcc, *NVCC_FLAGS, f"-DPF_BUILD_ID=\"{sid}\"", "-o", tmp, *SOURCES]
     if verbose:
         print(" ".join(cmd))
     subprocess.check_call(cmd)
+    os.replace(tmp, LIB_PATH)
     return LIB_PATH
+
+
+def build_id() -> str:
+    """pf_build_id() of the loaded library."""
+    return lib().pf_build_id().decode()
 
 
 # ------------------------------------------------------------------ ctypes mirrors
@@ -182,11 +218,17 @@ def lib() -> ctypes.CDLL:
     if not os.path.exists(LIB_PATH):
         raise RuntimeError(f"{LIB_PATH} is not built; run __graft_entry__.build() "
                            "(there is no CPU fallback)")
+    if not os.environ.get("PF_LIB"):
+        want, have = source_id(), library_id()
+        if have != want:
+            raise RuntimeError(f"{LIB_PATH} was built from other sources (build id {have}, "
+                               f"tree {want}); run __graft_entry__.build()")
     L = ctypes.CDLL(LIB_PATH)
     vp, i64, i32, u64, dbl = (ctypes.c_void_p, ctypes.c_int64, ctypes.c_int32,
                               ctypes.c_uint64, ctypes.c_double)
     L.pf_abi_version.restype = ctypes.c_int
     L.pf_last_error.restype = ctypes.c_char_p
+    L.pf_build_id.restype = ctypes.c_char_p
     L.pf_device_sm_count.restype = ctypes.c_int
     acc = [vp, vp, vp, vp, vp, vp, vp, i64, vp, vp, vp, i64, i64, i32, i32, i32,
            vp, vp, vp, vp, vp, vp]
@@ -222,7 +264,8 @@ def lib() -> ctypes.CDLL:
     L.pf_begin_frame_checked.argtypes = [vp, vp, i64, i32, dbl, dbl, i32, vp, vp, vp, i64, vp,
                                          vp]
     for name in EXPORTS[3:]:
-        getattr(L, name).restype = ctypes.c_int
+        if name != "pf_build_id":
+            getattr(L, name).restype = ctypes.c_int
     _lib = L
     return L
 

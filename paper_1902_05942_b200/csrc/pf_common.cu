@@ -54,9 +54,18 @@ int sm_count() {
 
 }  // namespace pf
 
+#ifndef PF_BUILD_ID
+#define PF_BUILD_ID "unversioned-----"
+#endif
+// The tree's source id (paper_1902_05942_b200/_lib.py: source_id), embedded so the
+// loader can read it from the file without loading it.
+static const char kBuildTag[] = "PF_BUILD_ID=" PF_BUILD_ID;
+
 extern "C" {
 
 int pf_abi_version(void) { return PF_ABI_VERSION; }
+
+const char *pf_build_id(void) { return kBuildTag + 12; }
 
 const char *pf_last_error(void) { return pf::g_last_error.c_str(); }
 

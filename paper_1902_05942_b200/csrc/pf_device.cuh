@@ -663,6 +663,9 @@ __device__ __forceinline__ uint64_t ld_acquire(const uint64_t *p) {
 __device__ __forceinline__ void st_release(uint64_t *p, uint64_t v) {
     asm volatile("st.release.gpu.global.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
 }
+__device__ __forceinline__ int64_t ld_acquire_i64(const int64_t *p) {
+    return static_cast<int64_t>(ld_acquire(reinterpret_cast<const uint64_t *>(p)));
+}
 __device__ __forceinline__ int64_t ld_relaxed_i64(const int64_t *p) {
     return static_cast<int64_t>(ld_relaxed(reinterpret_cast<const uint64_t *>(p)));
 }
@@ -698,7 +701,13 @@ struct InsertResult {
     int32_t probe_len;
     uint64_t victim_tag;
     int64_t victim_touch;
+    bool counted;    // the key's weight is already in counts[slot] (pinned / evicted / claimed)
 };
+
+// Live count of a cell an evictor owns: counts[s] is CAS'd 0 -> kEvictMark before the
+// wipe and moved back to the incoming key's weight after the new tag is published, so a
+// prober whose count add returns a negative value knows the cell is going away.
+constexpr int64_t kEvictMark = INT64_MIN / 2;
 
 // Wipe an evicted cell (src/_native.pyx:170-183): live + history sums, counts, delta.
 __device__ __forceinline__ void zero_cell(const pf_table &t, int64_t s) {
@@ -714,85 +723,176 @@ __device__ __forceinline__ void zero_cell(const pf_table &t, int64_t s) {
     st_relaxed_u64(t.deltas + s, 0ull);
 }
 
-// Eviction (cold path, out of line): CAS the victim's exact tag to BUSY, wipe the
-// cell, publish the new tag.  Returns the victim's last_touch, or INT64_MIN when the
-// victim changed before the CAS.
+// Eviction (cold path, out of line).  The evictor CASes the victim's exact tag to BUSY
+// (probers that meet BUSY wait), then takes the victim's live count 0 -> kEvictMark.
+// A prober that pinned the cell first (pin_cell) made the count nonzero: the CAS fails
+// and the evictor restores the tag.  Otherwise no prober can pin it any more (a count
+// add returns a negative value and backs off), the cell is wiped, the new tag is
+// published (release), and the count moves from the mark to the incoming key's weight
+// in one add (stray pin attempts undo their own adds, so they net to zero).  Returns
+// the victim's last_touch, or INT64_MIN when the victim changed or was pinned first
+// (the caller re-probes).
 static __device__ __noinline__ int64_t evict_cell(const pf_table &t, int64_t victim,
-                                                  uint64_t victim_tag, uint64_t incoming) {
+                                                  uint64_t victim_tag, uint64_t incoming,
+                                                  uint64_t weight) {
     uint64_t *vp = t.tags + victim;
-    const uint64_t old = atomicCAS(reinterpret_cast<unsigned long long *>(vp), victim_tag,
-                                   kBusyTag);
-    if (old != victim_tag)
+    if (atomicCAS(reinterpret_cast<unsigned long long *>(vp), victim_tag, kBusyTag) != victim_tag)
         return INT64_MIN;
+    __threadfence();
+    unsigned long long *cp = reinterpret_cast<unsigned long long *>(t.counts + victim);
+    if (atomicCAS(cp, 0ull, static_cast<unsigned long long>(kEvictMark)) != 0ull) {
+        st_release(vp, victim_tag);  // pinned by an accumulate since we read it
+        return INT64_MIN;
+    }
     const int64_t touch = ld_relaxed_i64(t.last_touch + victim);
-    zero_cell(t, victim);
+    uint64_t *sums = static_cast<uint64_t *>(t.sums);
+    uint64_t *hsums = static_cast<uint64_t *>(t.hist_sums);
+#pragma unroll
+    for (int c = 0; c < 3; ++c) {  // zero_cell minus the live count, which the mark holds
+        st_relaxed_u64(sums + 3 * victim + c, 0ull);
+        st_relaxed_u64(hsums + 3 * victim + c, 0ull);
+    }
+    st_relaxed_u64(t.hist_counts + victim, 0ull);
+    st_relaxed_u64(t.deltas + victim, 0ull);
     __threadfence();
     st_release(vp, incoming);
+    __threadfence();
+    atomicAdd(cp, static_cast<unsigned long long>(-kEvictMark) + weight);
     return touch;
 }
 
+// Pin a matched cell that an eviction could take (age >= evict_min_age): add the
+// key's weight to its live count, then confirm the tag (once no eviction holds it
+// BUSY) is still the one matched.  A negative old count (an evictor holds the mark) or
+// a changed tag (an eviction finished between the probe's load and the add) undoes
+// the add; the caller re-probes.
+static __device__ __noinline__ bool pin_cell(const pf_table &t, int64_t s, uint64_t tag,
+                                             uint64_t weight) {
+    unsigned long long *cp = reinterpret_cast<unsigned long long *>(t.counts + s);
+    const long long old = static_cast<long long>(atomicAdd(cp, weight));
+    if (old >= 0) {
+        __threadfence();
+        if (wait_not_busy(t.tags + s, ld_relaxed(t.tags + s)) == tag) return true;
+    }
+    atomicAdd(cp, static_cast<unsigned long long>(-static_cast<long long>(weight)));
+    return false;
+}
+
+// Claim an EMPTY slot when evict_min_age == 0 (fresh cells are eviction candidates):
+// EMPTY -> BUSY, count the weight, then publish, so no evictor ever sees the new key
+// with a zero live count -- which a sequential caller never could.  Returns the tag
+// that held the slot (EMPTY when this key claimed it).
+static __device__ __noinline__ uint64_t claim_counted(const pf_table &t, int64_t s,
+                                                      uint64_t incoming, uint64_t weight) {
+    uint64_t *tp = t.tags + s;
+    const uint64_t old = atomicCAS(reinterpret_cast<unsigned long long *>(tp), kEmptyTag, kBusyTag);
+    if (old != kEmptyTag) return old;
+    atomicAdd(reinterpret_cast<unsigned long long *>(t.counts + s), weight);
+    __threadfence();
+    st_release(tp, incoming);
+    return kEmptyTag;
+}
+
 // Probe / claim / evict for one key (src/_native.pyx:209-247) on the live table.
-// Concurrency: a claim is one 64-bit CAS of the whole tag (EMPTY -> FRESH|fp); an
-// eviction CASes the victim's exact tag to BUSY, wipes the cell, then publishes
-// FRESH|fp with release order, so no accumulate lands in a half-wiped cell.  A lost
-// victim CAS re-probes the window (what a sequential caller would see) instead of
-// the reference's racy give-up.
+// Concurrency (every outcome is one a sequential caller could see):
+// - a claim is one 64-bit CAS of the whole tag (EMPTY -> FRESH|fp);
+// - an eviction CASes the victim's exact tag to BUSY, takes its live count (evict_cell),
+//   wipes the cell and publishes FRESH|fp, so no accumulate lands in a half-wiped cell;
+// - a match on a cell an eviction could take (age >= evict_min_age) pins it first
+//   (pin_cell), so the cell cannot be wiped between the match and the adds.  Matches on
+//   younger cells -- every cell touched in the last evict_min_age frames, the common
+//   case -- need no pin: their tags cannot change inside a frame.
+// A lost victim or pin re-probes the window instead of the reference's racy give-up.
 // `home_tag` is the caller's early (prefetched) load of tags[home]; it only seeds the
-// first probe of the first attempt and is re-read after any contention.
+// first probe of the first attempt and is re-read after any contention.  `weight` is
+// what the caller adds to the live count; r.counted says the protocol already added it.
 __device__ __forceinline__ InsertResult probe_insert(const pf_table &t, uint64_t idx, uint32_t fp,
-                                                     uint64_t home_tag) {
+                                                     uint64_t home_tag, uint64_t weight) {
     const uint64_t mask = static_cast<uint64_t>(t.capacity) - 1;
     const uint64_t home = idx & mask;
     const uint64_t want = static_cast<uint64_t>(fp);
     const uint64_t incoming = (kFresh << 32) | want;
+    const uint64_t min_age = static_cast<uint64_t>(t.evict_min_age);
     InsertResult r;
     r.slot = -1;
     r.status = 2;
     r.probe_len = t.probe_limit;
     r.victim_tag = 0;
     r.victim_touch = 0;
+    r.counted = false;
     for (int attempt = 0; attempt < 64; ++attempt) {
         int64_t victim = -1;
         uint64_t victim_tag = 0;
+        bool retry = false, reread = false;
         for (int j = 0; j < t.probe_limit; ++j) {
             const uint64_t s = (home + static_cast<uint64_t>(j)) & mask;
-            uint64_t tag = (attempt == 0 && j == 0) ? home_tag : ld_relaxed(t.tags + s);
+            uint64_t tag = (attempt == 0 && j == 0 && !reread) ? home_tag : ld_relaxed(t.tags + s);
+            reread = false;
             tag = wait_not_busy(t.tags + s, tag);
             if (tag == kEmptyTag) {
-                const uint64_t old = atomicCAS(reinterpret_cast<unsigned long long *>(t.tags + s),
-                                               kEmptyTag, incoming);
-                if (old == kEmptyTag || (old & kFpMask) == want) {
+                uint64_t old;
+                if (min_age == 0) {
+                    old = claim_counted(t, static_cast<int64_t>(s), incoming, weight);
+                    if (old == kEmptyTag) r.counted = true;
+                    else old = wait_not_busy(t.tags + s, old);
+                } else {
+                    old = atomicCAS(reinterpret_cast<unsigned long long *>(t.tags + s), kEmptyTag,
+                                    incoming);
+                }
+                if (old == kEmptyTag) {
                     r.slot = static_cast<int64_t>(s);
                     r.status = 0;
                     r.probe_len = j + 1;
                     return r;
                 }
-                continue;  // lost the claim to a different key (src/_native.pyx:221-222)
+                if ((old & kFpMask) != want)
+                    continue;  // lost the claim to a different key (src/_native.pyx:221-222)
+                tag = old;     // lost it to the same key: a match
             }
             if ((tag & kFpMask) == want) {
+                if (((tag >> 32) & kAgeMask) >= min_age) {
+                    if (!pin_cell(t, static_cast<int64_t>(s), tag, weight)) {
+                        retry = true;
+                        break;
+                    }
+                    r.counted = true;
+                }
                 r.slot = static_cast<int64_t>(s);
                 r.status = 0;
                 r.probe_len = j + 1;
                 return r;
             }
             const uint64_t age = (tag >> 32) & kAgeMask;
-            if (age >= static_cast<uint64_t>(t.evict_min_age) &&
-                ld_relaxed_i64(t.counts + s) == 0) {
-                if (victim < 0 || tag > victim_tag) {
+            if (age >= min_age) {
+                // A candidate needs a consistent (tag, live count) snapshot: a negative
+                // count is an eviction in flight (its new key may be ours), a changed
+                // tag a torn read.  Either way wait for the slot to settle and look at
+                // it again, so every prober of a key sees the same candidates and the
+                // same victim -- two lanes of one key can never evict two cells.
+                const int64_t c = ld_acquire_i64(t.counts + s);
+                if (c < 0 || ld_relaxed(t.tags + s) != tag) {
+                    while (ld_acquire_i64(t.counts + s) < 0) __nanosleep(32);
+                    reread = true;
+                    --j;
+                    continue;
+                }
+                if (c == 0 && (victim < 0 || tag > victim_tag)) {
                     victim = static_cast<int64_t>(s);
                     victim_tag = tag;
                 }
             }
         }
+        if (retry) continue;
         if (victim < 0)
             return r;  // status 2, no mutation
-        const int64_t touch = evict_cell(t, victim, victim_tag, incoming);
+        const int64_t touch = evict_cell(t, victim, victim_tag, incoming, weight);
         if (touch != INT64_MIN) {
             r.victim_touch = touch;
             r.slot = victim;
             r.status = 1;
             r.probe_len = t.probe_limit;
             r.victim_tag = victim_tag;
+            r.counted = true;
             return r;
         }
         // window changed under us: re-probe

@@ -188,8 +188,8 @@ insert_frame_kernel(pf_config cfg, pf_vertices v, pf_table fine, pf_table coarse
         const CellHash h = tb == 0 ? hf : hc;
         const uint64_t home_tag = tb == 0 ? ht_f : ht_c;
         const LaneInsert r = ((PF_FRAME_MERGE >> tb) & 1)
-            ? warp_insert<FIXED>(t, valid, h.index, h.fp, val, frame, home_tag)
-            : lane_insert<FIXED>(t, valid, h.index, h.fp, qval, val, frame, home_tag);
+            ? warp_insert<FIXED>(t, valid, h.index, h.fp, val, frame, home_tag, true, false)
+            : lane_insert<FIXED>(t, valid, h.index, h.fp, qval, val, frame, home_tag, false);
         warp_count(bs, tb == 0 ? PF_STAT_PROBE_FAILURES : PF_STAT_COARSE_PROBE_FAILURES,
                    valid && r.status == 2);
         warp_count(bs, tb == 0 ? PF_STAT_EVICTIONS : PF_STAT_COARSE_EVICTIONS,
@@ -261,17 +261,50 @@ __device__ __forceinline__ Effective fine_effective(const ResolveArgs &a, int64_
     return effective_at(a.fine, s, mode, a.cfg.ema_alpha, a.cfg.delta_max);
 }
 
+constexpr int64_t kNoTouch = INT64_MIN;  // touch_frame of a sweep without deferred touches
+
 // VoxelTable.effective of every occupied fine slot, once per resolve: lookups then
-// read one sector instead of the five SoA sectors of a slot's state.
+// read one sector instead of the five SoA sectors of a slot's state.  The same sweep
+// finishes the frame insert's deferred last_touch stores (touch_frame != kNoTouch): every cell
+// an accumulate reached this frame has a live count > 0 (begin_frame zeroed them), so
+// last_touch = frame there leaves the table byte-identical to the reference's
+// per-vertex store (src/_native.pyx:257) at a fraction of its L2 traffic.  Blocks
+// [0, nb_fine) sweep the fine table, the rest the coarse table (touch only).
 __global__ void __launch_bounds__(kThreads)
-effective_records_kernel(pf_table t, int mode, double ema, double delta_max, ulonglong4 *rec) {
+effective_records_kernel(pf_table t, int mode, double ema, double delta_max, ulonglong4 *rec,
+                         pf_table coarse, int has_coarse, int64_t touch_frame,
+                         unsigned nb_fine) {
     __shared__ SweepSmem<kThreads> q;
+    if (blockIdx.x >= nb_fine) {
+        const int64_t blk = blockIdx.x - nb_fine, nblk = gridDim.x - nb_fine;
+        for_each_occupied<kThreads>(coarse.tags, coarse.capacity, q, blk, nblk,
+                                    [&](int64_t s, uint64_t) {
+            if (ld_relaxed_i64(coarse.counts + s) > 0) coarse.last_touch[s] = touch_frame;
+        });
+        return;
+    }
     const bool fixed = t.sum_mode == PF_SUM_FIXED;
     const bool as_int = eff_is_int(t, mode);
-    for_each_occupied<kThreads>(t.tags, t.capacity, q, [&](int64_t s, uint64_t) {
-        rec[s] = pack_effective(effective_of(load_cell(t, s, true), fixed, mode, ema, delta_max),
-                                as_int);
+    for_each_occupied<kThreads>(t.tags, t.capacity, q, blockIdx.x, nb_fine,
+                                [&](int64_t s, uint64_t) {
+        const CellState cs = load_cell(t, s, true);
+        if (rec != nullptr) rec[s] = pack_effective(effective_of(cs, fixed, mode, ema, delta_max), as_int);
+        if (touch_frame != kNoTouch && cs.counts > 0) t.last_touch[s] = touch_frame;
     });
+}
+
+// Launch the sweep above (records and / or deferred touches); no-op when neither.
+static int launch_post_insert(const char *fn, const pf_table &fine, const pf_table *coarse,
+                              const pf_config &kc, uint64_t *eff_records, int64_t touch_frame,
+                              cudaStream_t st) {
+    if (eff_records == nullptr && touch_frame == kNoTouch) return PF_OK;
+    const unsigned nf = sweep_blocks<kThreads>(fine.capacity, sm_count());
+    const bool tc = coarse != nullptr && touch_frame != kNoTouch;
+    const unsigned nc = tc ? sweep_blocks<kThreads>(coarse->capacity, sm_count()) : 0u;
+    effective_records_kernel<<<nf + nc, kThreads, 0, st>>>(
+        fine, kc.temporal_mode, kc.ema_alpha, kc.delta_max,
+        reinterpret_cast<ulonglong4 *>(eff_records), tc ? *coarse : fine, tc, touch_frame, nf);
+    return check_launch(fn);
 }
 
 // The fine lookup key of one vertex: jitter stream 3 when jitter is on
@@ -692,14 +725,15 @@ static int launch_rungs(const char *fn, const ResolveArgs &a, int64_t n, bool ha
 
 using namespace pf;
 
-extern "C" {
-
-int pf_insert_frame(const pf_config *cfg, const pf_vertices *v, const pf_table *fine,
-                    const pf_table *coarse, uint64_t stream_base_accum, int64_t frame,
-                    int64_t *stats, pf_evict_event *events, int64_t *event_count,
-                    int64_t event_capacity, const int32_t *abort_flag,
-                    uint64_t stream_base_lookup, uint64_t *lookup_keys, void *stream) {
-    const char *fn = "pf_insert_frame";
+// The fused insert.  Its last_touch stores are deferred to a sweep over the occupied
+// slots: run here unless the caller (pf_filter_frame) folds it into the resolve's
+// effective-record sweep (defer_touch).
+static int insert_frame(const char *fn, const pf_config *cfg, const pf_vertices *v,
+                        const pf_table *fine, const pf_table *coarse, uint64_t stream_base_accum,
+                        int64_t frame, int64_t *stats, pf_evict_event *events,
+                        int64_t *event_count, int64_t event_capacity, const int32_t *abort_flag,
+                        uint64_t stream_base_lookup, uint64_t *lookup_keys, bool defer_touch,
+                        void *stream) {
     if (lookup_keys && fine && fine->capacity > (1ll << 32))
         return fail_arg(fn, "packed lookup keys need a fine capacity <= 2^32");
     if (int rc = validate_vertices(fn, v, cfg)) return rc;
@@ -728,17 +762,19 @@ int pf_insert_frame(const pf_config *cfg, const pf_vertices *v, const pf_table *
         insert_frame_kernel<false><<<g, kThreads, 0, as_stream(stream)>>>(
             kc, *v, *fine, c, coarse != nullptr, stream_base_accum, frame, stats, events,
             event_count, event_capacity, abort_flag, stream_base_lookup, lookup_keys);
-    return check_launch(fn);
+    if (int rc = check_launch(fn)) return rc;
+    return defer_touch ? PF_OK
+                       : launch_post_insert(fn, *fine, coarse, kc, nullptr, frame, as_stream(stream));
 }
 
-int pf_resolve_frame(const pf_config *cfg, const pf_vertices *v, const pf_table *fine,
-                     const pf_table *coarse, uint64_t stream_base_lookup,
-                     uint64_t stream_base_coarse, int64_t spp, const double *base_image,
-                     int64_t n_pixels, double *image, double *flat, int64_t *work,
-                     int64_t *work_count, uint8_t *source, double *chosen, int64_t *stats,
-                     const uint64_t *lookup_keys, uint64_t *eff_records,
-                     int64_t *fallback_keys, void *stream) {
-    const char *fn = "pf_resolve_frame";
+// The resolve phase; touch_frame != kNoTouch also finishes a deferred insert's last_touch.
+static int resolve_frame(const char *fn, const pf_config *cfg, const pf_vertices *v,
+                         const pf_table *fine, const pf_table *coarse, uint64_t stream_base_lookup,
+                         uint64_t stream_base_coarse, int64_t spp, const double *base_image,
+                         int64_t n_pixels, double *image, double *flat, int64_t *work,
+                         int64_t *work_count, uint8_t *source, double *chosen, int64_t *stats,
+                         const uint64_t *lookup_keys, uint64_t *eff_records,
+                         int64_t *fallback_keys, int64_t touch_frame, void *stream) {
     if (int rc = validate_vertices(fn, v, cfg)) return rc;
     pf_config kc;
     if (int rc = prepare_config(fn, cfg, &kc)) return rc;
@@ -778,13 +814,8 @@ int pf_resolve_frame(const pf_config *cfg, const pf_vertices *v, const pf_table 
         a.pixel_base = 0;
         a.seg_mask = ~0ull;
         a.crec = nullptr;
-        if (eff_records != nullptr) {
-            effective_records_kernel<<<sweep_blocks<kThreads>(fine->capacity, sm_count()), kThreads,
-                                       0, st>>>(*fine, kc.temporal_mode, kc.ema_alpha,
-                                                kc.delta_max,
-                                                reinterpret_cast<ulonglong4 *>(eff_records));
-            if (int rc = check_launch(fn)) return rc;
-        }
+        if (int rc = launch_post_insert(fn, *fine, coarse, kc, eff_records, touch_frame, st))
+            return rc;
         if (int rc = launch_rungs(fn, a, v->n, lookup_keys != nullptr, fallback_keys != nullptr, st))
             return rc;
     }
@@ -793,6 +824,31 @@ int pf_resolve_frame(const pf_config *cfg, const pf_vertices *v, const pf_table 
         finalize_image_kernel<<<blocks_for(m, kThreads), kThreads, 0, st>>>(
             base_image, flat, image, m, static_cast<double>(spp));
     return check_launch(fn);
+}
+
+extern "C" {
+
+int pf_insert_frame(const pf_config *cfg, const pf_vertices *v, const pf_table *fine,
+                    const pf_table *coarse, uint64_t stream_base_accum, int64_t frame,
+                    int64_t *stats, pf_evict_event *events, int64_t *event_count,
+                    int64_t event_capacity, const int32_t *abort_flag,
+                    uint64_t stream_base_lookup, uint64_t *lookup_keys, void *stream) {
+    return insert_frame("pf_insert_frame", cfg, v, fine, coarse, stream_base_accum, frame, stats,
+                        events, event_count, event_capacity, abort_flag, stream_base_lookup,
+                        lookup_keys, false, stream);
+}
+
+int pf_resolve_frame(const pf_config *cfg, const pf_vertices *v, const pf_table *fine,
+                     const pf_table *coarse, uint64_t stream_base_lookup,
+                     uint64_t stream_base_coarse, int64_t spp, const double *base_image,
+                     int64_t n_pixels, double *image, double *flat, int64_t *work,
+                     int64_t *work_count, uint8_t *source, double *chosen, int64_t *stats,
+                     const uint64_t *lookup_keys, uint64_t *eff_records,
+                     int64_t *fallback_keys, void *stream) {
+    return resolve_frame("pf_resolve_frame", cfg, v, fine, coarse, stream_base_lookup,
+                         stream_base_coarse, spp, base_image, n_pixels, image, flat, work,
+                         work_count, source, chosen, stats, lookup_keys, eff_records,
+                         fallback_keys, kNoTouch, stream);
 }
 
 int pf_resolve_replica(const pf_config *cfg, const pf_vertices *v, const pf_replica *rp,
@@ -887,15 +943,16 @@ int pf_filter_frame(const pf_config *cfg, const pf_vertices *v, const pf_table *
         return rc;
     // accumulate_phase (fused, flag-guarded) + the resolve phase's lookup keys
     mark(1);
-    if (int rc = pf_insert_frame(cfg, v, fine, coarse, stream_base_accum, frame, b->acc_stats,
-                                 b->events, b->event_count, b->event_capacity, b->bad_flag,
-                                 stream_base_lookup, b->lookup_keys, stream))
+    // (last_touch stores deferred to the resolve's effective-record sweep)
+    if (int rc = insert_frame(fn, cfg, v, fine, coarse, stream_base_accum, frame, b->acc_stats,
+                              b->events, b->event_count, b->event_capacity, b->bad_flag,
+                              stream_base_lookup, b->lookup_keys, true, stream))
         return rc;
     mark(2);
-    const int rc = pf_resolve_frame(cfg, v, fine, coarse, stream_base_lookup, stream_base_coarse,
-                                    spp, base_image, n_pixels, image, b->flat, b->work,
-                                    b->work_count, source, chosen, b->res_stats, b->lookup_keys,
-                                    b->eff_records, b->fallback_keys, stream);
+    const int rc = resolve_frame(fn, cfg, v, fine, coarse, stream_base_lookup, stream_base_coarse,
+                                 spp, base_image, n_pixels, image, b->flat, b->work,
+                                 b->work_count, source, chosen, b->res_stats, b->lookup_keys,
+                                 b->eff_records, b->fallback_keys, frame, stream);
     mark(3);
     return rc;
 }

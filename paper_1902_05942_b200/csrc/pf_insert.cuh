@@ -36,7 +36,7 @@ __device__ __forceinline__ LaneInsert warp_insert_sums(const pf_table &t, bool v
                                                        uint32_t fp, int64_t qsum[3],
                                                        double fsum[3], uint64_t weight,
                                                        int64_t frame, uint64_t home_tag,
-                                                       bool merge = true) {
+                                                       bool merge = true, bool touch = true) {
     const unsigned lane = threadIdx.x & 31u;
     const uint64_t k2 = static_cast<uint64_t>(fp) | (static_cast<uint64_t>(valid) << 32);
     // merge == false: every lane is its own group; lanes with the same key then probe
@@ -82,8 +82,10 @@ __device__ __forceinline__ LaneInsert warp_insert_sums(const pf_table &t, bool v
     r.probe_len = 0;
     r.victim_tag = 0;
     r.victim_touch = 0;
+    r.counted = false;
+    const uint64_t group_weight = WEIGHTED ? weight : static_cast<uint64_t>(__popc(peers));
     if (is_leader) {
-        r = probe_insert(t, idx, fp, home_tag);
+        r = probe_insert(t, idx, fp, home_tag, group_weight);
         if (r.status != 2) {
             const int64_t s = r.slot;
             const uint64_t keep = l2_evict_last();
@@ -95,8 +97,8 @@ __device__ __forceinline__ LaneInsert warp_insert_sums(const pf_table &t, bool v
                 else
                     red_add_f64(static_cast<double *>(t.sums) + 3 * s + c, fsum[c], keep);
             }
-            red_add_u64(t.counts + s, WEIGHTED ? weight : static_cast<uint64_t>(__popc(peers)), keep);
-            st_relaxed_u64(t.last_touch + s, static_cast<uint64_t>(frame));
+            if (!r.counted) red_add_u64(t.counts + s, group_weight, keep);
+            if (touch) st_relaxed_u64(t.last_touch + s, static_cast<uint64_t>(frame));
         }
     }
     LaneInsert out;
@@ -125,7 +127,7 @@ template <bool FIXED>
 __device__ __forceinline__ LaneInsert lane_insert(const pf_table &t, bool valid, uint64_t idx,
                                                   uint32_t fp, const int64_t q[3],
                                                   const double val[3], int64_t frame,
-                                                  uint64_t home_tag) {
+                                                  uint64_t home_tag, bool touch = true) {
     LaneInsert out;
     out.slot = -1;
     out.status = 2;
@@ -135,7 +137,7 @@ __device__ __forceinline__ LaneInsert lane_insert(const pf_table &t, bool valid,
     out.leader = valid;
     out.peers = 1u << (threadIdx.x & 31u);
     if (!valid) return out;
-    const InsertResult r = probe_insert(t, idx, fp, home_tag);
+    const InsertResult r = probe_insert(t, idx, fp, home_tag, 1ull);
     if (r.status != 2) {
         const int64_t s = r.slot;
         const uint64_t keep = l2_evict_last();
@@ -147,8 +149,8 @@ __device__ __forceinline__ LaneInsert lane_insert(const pf_table &t, bool valid,
             else
                 red_add_f64(static_cast<double *>(t.sums) + 3 * s + c, val[c], keep);
         }
-        red_add_u64(t.counts + s, 1ull, keep);
-        st_relaxed_u64(t.last_touch + s, static_cast<uint64_t>(frame));
+        if (!r.counted) red_add_u64(t.counts + s, 1ull, keep);
+        if (touch) st_relaxed_u64(t.last_touch + s, static_cast<uint64_t>(frame));
     }
     out.slot = r.slot;
     out.status = r.status;
@@ -162,7 +164,8 @@ __device__ __forceinline__ LaneInsert lane_insert(const pf_table &t, bool valid,
 template <bool FIXED>
 __device__ __forceinline__ LaneInsert warp_insert(const pf_table &t, bool valid, uint64_t idx,
                                                   uint32_t fp, const double val[3], int64_t frame,
-                                                  uint64_t home_tag, bool merge = true) {
+                                                  uint64_t home_tag, bool merge = true,
+                                                  bool touch = true) {
     int64_t qsum[3];
     double fsum[3];
 #pragma unroll
@@ -170,7 +173,8 @@ __device__ __forceinline__ LaneInsert warp_insert(const pf_table &t, bool valid,
         if (FIXED) qsum[c] = valid ? quantize_fixed(val[c]) : 0;
         else fsum[c] = valid ? val[c] : 0.0;
     }
-    return warp_insert_sums<FIXED, false>(t, valid, idx, fp, qsum, fsum, 1, frame, home_tag, merge);
+    return warp_insert_sums<FIXED, false>(t, valid, idx, fp, qsum, fsum, 1, frame, home_tag, merge,
+                                           touch);
 }
 
 }  // namespace pf

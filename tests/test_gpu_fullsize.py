@@ -1,0 +1,137 @@
+"""Parity at the BASELINE.json configurations, at full size, against the reference.
+
+`tests/golden/fullsize.json` holds SHA-256 digests (oracle/digest.py) of what the
+reference itself produced on each configuration (tests/golden/make_fullsize.py, run
+in the build container against baseline/_ref):
+  cornell256  configs[0]  builtin Cornell box 256 x 256, 1 spp, first hit (65,536 vertices)
+  hd1         configs[1]  SURVEY App. B closed box, 1920 x 1080, first hit (2,073,600)
+  hd4         configs[2]  the same, select_k 1..4 (8,184,972 -- the benchmark's stream)
+  hd1_filter  configs[3]  hd1's stream, 8 frames of temporal_mode "filter", EMA + aging
+
+Each test traces the configuration's stream on the device (csrc/pf_trace.cu), checks
+it against the reference tracer's stream (src/tracer.py:411-461) field by field, then
+runs the fused parallel frame (pf_filter_frame) and requires, bit for bit:
+- the three key sets of every vertex (fine and coarse accumulate keys, stream 2; the
+  lookup keys, stream 3) including the jittered positions;
+- both tables, per key (order-free rows: tag, counts, last_touch, sums, history);
+- per-vertex sources and chosen means;
+- the image: bit-exact for first-hit streams (one vertex per pixel); for the 4-bounce
+  stream the reference's composite (np.add.at in vertex order) restated over the
+  device's chosen means must reproduce the reference image's digest, and the
+  device image (float atomics in arrival order) must be within 1e-12 of it.
+"""
+
+import json
+import os
+
+import numpy as np
+import pytest
+import torch
+
+from oracle.digest import composite, digest, table_digest
+
+pytestmark = pytest.mark.gpu
+
+HERE = os.path.dirname(os.path.abspath(__file__))
+FULL = json.load(open(os.path.join(HERE, "golden", "fullsize.json")))
+STREAM_DT = {"position": np.float64, "normal": np.float64, "omega_r": np.float64,
+             "contribution": np.float64, "throughput": np.float64, "pixel": np.int64,
+             "sample": np.int64, "layer_id": np.int64, "camera_distance": np.float64}
+KEY_DT = {"qx": np.int64, "qy": np.int64, "qz": np.int64, "level": np.int64,
+          "aux": np.uint64, "index": np.uint64, "fingerprint": np.uint32,
+          "jittered": np.float64}
+
+
+def _np(t):
+    return t.cpu().numpy() if isinstance(t, torch.Tensor) else np.asarray(t)
+
+
+def _stream(gpu, name):
+    from paper_1902_05942_b200.scene import closed_box, cornell_box
+    from paper_1902_05942_b200.tracer import TraceOptions, multi_bounce_stream, trace
+    if name == "cornell256":
+        sc = cornell_box(256, 256)
+        tr = trace(sc, 1, 1, TraceOptions(select_k=1))
+        return sc, tr.vertices, tr.base_image
+    sc = closed_box(1920, 1080)
+    vs, base = multi_bounce_stream(sc, 4 if name == "hd4" else 1, 1, rr_start=9)
+    return sc, vs, base
+
+
+def _check_stream(want, vs, base=None):
+    bad = [f for f, dt in STREAM_DT.items()
+           if digest(_np(getattr(vs, f)).astype(dt, copy=False)) != want["stream"][f]]
+    assert not bad, f"traced stream differs from the reference tracer in {bad}"
+    if base is not None:
+        assert digest(_np(base)) == want["base"]
+
+
+def _cfg(gpu, want):
+    c = dict(want["cfg"])
+    return gpu.FilterConfig(**c)
+
+
+def _check_keys(gpu, vs, cfg, seed, want):
+    from paper_1902_05942_b200 import rng
+    from paper_1902_05942_b200.pipeline import vertex_keys
+    sets = {"fine": (rng.STREAM_JITTER_ACCUM, 0),
+            "coarse": (rng.STREAM_JITTER_ACCUM, cfg.coarse_delta),
+            "lookup": (rng.STREAM_JITTER_LOOKUP, 0)}
+    for name, (tag, delta) in sets.items():
+        k = vertex_keys(vs, cfg, seed, tag, delta).numpy()
+        bad = [f for f, dt in KEY_DT.items() if digest(k[f].astype(dt, copy=False)) != want[name][f]]
+        assert not bad, f"{name} keys differ from the reference in {bad}"
+
+
+def _check_frame(gpu, want, state, image, report, vs, base, exact_image):
+    src = _np(report.source)
+    assert np.bincount(src, minlength=4).tolist() == want["source_counts"]
+    assert digest(src) == want["source"]
+    chosen = _np(report.means)
+    assert digest(chosen) == want["chosen"]
+    img = _np(image)
+    if exact_image:
+        assert digest(img) == want["image"]
+    else:
+        ref_img = composite(_np(base), _np(vs.pixel), _np(vs.throughput), chosen, 1)
+        assert digest(ref_img) == want["image"]
+        np.testing.assert_allclose(img, ref_img, rtol=1e-12, atol=1e-300)
+    for t, key in ((state.fine, "fine"), (state.coarse, "coarse")):
+        got = table_digest(t.state())
+        assert got == want[key], f"{key} table: {got} != {want[key]}"
+
+
+@pytest.mark.parametrize("name", ["cornell256", "hd1", "hd4"])
+def test_baseline_config_frame_matches_reference(gpu, name):
+    want = FULL[name]
+    sc, vs, base = _stream(gpu, name)
+    assert len(vs) == want["n"]
+    _check_stream(want, vs, base)
+    cfg = _cfg(gpu, want)
+    fr = want["frames"][0]
+    seed = int(fr["seed"])
+    _check_keys(gpu, vs, cfg, seed, fr["keys"])
+    state = gpu.FrameState.from_config(cfg)
+    image, report, stats = gpu.filter_frame(vs, base, cfg, state, 1, seed)
+    assert stats.probe_failures == fr["probe_failures"]
+    assert stats.coarse_probe_failures == fr["coarse_probe_failures"]
+    _check_frame(gpu, fr, state, image, report, vs, base, exact_image=name != "hd4")
+
+
+def test_filter_mode_sequence_matches_reference(gpu):
+    """configs[3]: 8 consecutive filter-mode frames (EMA blend, generation fold, aging,
+    re-prioritised tags) on the 1080p first-hit stream, with the animated-scene seed
+    schedule; every frame bit-exact against the reference."""
+    want = FULL["hd1_filter"]
+    sc, vs, base = _stream(gpu, "hd1")
+    _check_stream(want, vs)
+    cfg = _cfg(gpu, want)
+    assert cfg.temporal_mode == "filter"
+    state = gpu.FrameState.from_config(cfg)
+    for f, fr in enumerate(want["frames"]):
+        seed = int(fr["seed"])
+        if f == 0:
+            _check_keys(gpu, vs, cfg, seed, fr["keys"])
+        image, report, stats = gpu.filter_frame(vs, base, cfg, state, 1, seed)
+        assert stats.probe_failures == fr["probe_failures"], f
+        _check_frame(gpu, fr, state, image, report, vs, base, exact_image=True)
