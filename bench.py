@@ -44,15 +44,28 @@ WORKLOADS = {
     "hd1": (1920, 1080, 1, "integrate", "configs[1]"),
     "hd-temporal": (1920, 1080, 1, "filter", "configs[3]: EMA blend + aging, one step = one frame"),
     "uhd4": (3840, 2160, 4, "integrate", "configs[4] on one GPU"),
+    # configs[4] as named: ONE 4K frame split into N pixel-row bands (rank r traces rows
+    # [r H/N, (r+1) H/N)), key-sharded C = 2^24 tables, band composite: strong scaling
+    "uhd4-band": (3840, 2160, 4, "integrate", "configs[4]: 4K frame in N row bands"),
 }
 METRIC = "filtered path vertices/sec (insert+query); ms/frame at 1080p 1spp 4 bounces"
 WORKLOAD = "1920x1080 1spp, all vertices of 4-bounce paths (closed Cornell box, synthetic)"
 
 
-def make_stream(kind: str, rank: int = 0, device=None):
+def make_stream(kind: str, rank: int = 0, device=None, world: int = 1, band: bool = False):
     """(stream dict of CUDA tensors, base image) of the benchmark workload for a rank:
-    rank r traces sample r of every pixel (distinct path ids and jitter draws)."""
+    rank r traces sample r of every pixel (distinct path ids and jitter draws); with
+    `band`, rank r traces sample 0 of its pixel-row band and the base image is the band."""
     from paper_1902_05942_b200.streams import closed_box_stream
+    if band and world > 1:
+        from paper_1902_05942_b200.scene import closed_box
+        from paper_1902_05942_b200.tracer import band_stream
+        if H_PIX % world:
+            raise SystemExit(f"--workload uhd4-band needs H={H_PIX} divisible by --gpus")
+        rows = H_PIX // world
+        vs, base = band_stream(closed_box(W_PIX, H_PIX), BOUNCES, 1, rank * rows,
+                               (rank + 1) * rows)
+        return {f: getattr(vs, f).contiguous() for f in FIELDS}, base.contiguous()
     if kind == "synthetic":
         stream, base = closed_box_stream(W_PIX, H_PIX, BOUNCES, 1 + rank, device=device)
         if rank:
@@ -161,14 +174,15 @@ def _peaks():
     return 6650.0, "fallback"
 
 
-def _traffic(kernel: str):
+def _traffic(kernel: str, workload: str, stream: str = "traced"):
     """dram bytes (or, for "<kernel>_inst", warp instructions) per launch from the
-    committed ncu --set full summary, if any."""
+    committed ncu --set full capture OF THIS WORKLOAD (profiles/ncu_traffic.json is keyed
+    by bench workload), else None."""
     p = os.path.join(ROOT, "profiles", "ncu_traffic.json")
-    if os.path.exists(p):
-        with open(p) as fh:
-            return json.load(fh).get(kernel)
-    return None
+    if stream != "traced" or not os.path.exists(p):
+        return None
+    with open(p) as fh:
+        return json.load(fh).get(workload, {}).get(kernel)
 
 
 def _l2_red_peak():
@@ -199,57 +213,86 @@ def workload_text(kind: str) -> str:
             f"temporal_mode {TEMPORAL}")
 
 
-def cpu_reference_frame(sample_stream, base, cfg_kwargs, seed, frame, state):
-    """One frame of the reference's own CPU path (baseline/_ref) or the oracle port."""
-    kind, mod = state["kind"], state["mod"]
-    if kind == "reference":
-        pf = mod
-        cfg = state["cfg"]
-        st = state["state"]
-        if "vs" not in state:  # the reference's own VertexStream type
-            state["vs"] = pf.VertexStream(**{f: getattr(sample_stream, f) for f in FIELDS})
-        sample_stream = state["vs"]
-        st.fine.begin_frame(frame, cfg)
-        st.coarse.begin_frame(frame, cfg)
-        fk, _, _ = pf.pipeline.accumulate_phase(sample_stream, cfg, st, frame, seed,
-                                                threads=os.cpu_count() or 1)
-        pf.pipeline.resolve_phase(sample_stream, cfg, st, frame, seed, 1, base, fk)
-    else:
-        orc = mod
-        orc.filter_frame(sample_stream, state["cfg"], state["state"], frame, seed, 1, base)
+# The benchmark scene, as scene text for the reference's own parser.  The
+# reference arm must not import this repo's package (it loads libpf_b200.so), so the
+# text is restated here; tests/test_bench_cpu.py checks it equals scene.CLOSED_BOX.
+REF_CLOSED_BOX = """\
+camera 2.75 2.75 0.6  2.75 2.75 5.5  0 1 0  1.2 {width} {height}
+material white 0.73 0.73 0.73
+material red 0.65 0.05 0.05
+material green 0.12 0.45 0.15
+material lamp 0 0 0
+quad 0 0 0  0 0 5.5  5.5 0 5.5  5.5 0 0  white
+quad 0 5.5 0  5.5 5.5 0  5.5 5.5 5.5  0 5.5 5.5  white
+quad 0 0 5.5  0 5.5 5.5  5.5 5.5 5.5  5.5 0 5.5  white
+quad 0 0 0  0 5.5 0  0 5.5 5.5  0 0 5.5  red
+quad 5.5 0 0  5.5 0 5.5  5.5 5.5 5.5  5.5 5.5 0  green
+quad 0 0 0  5.5 0 0  5.5 5.5 0  0 5.5 0  white
+quad 1.925 5.49 1.925  3.575 5.49 1.925  3.575 5.49 3.575  1.925 5.49 3.575  lamp emit 17 13 6
+"""
+GOLDEN = 0x9E3779B97F4A7C15
 
 
-def cpu_setup(cfg_kwargs):
-    """Prefer the unmodified reference installed in baseline/_ref; else the oracle port."""
+def reference_module():
+    """The unmodified reference installed in baseline/_ref (native Cython backend), or
+    None.  Imported from its install directory only -- never this repo's package."""
     ref = os.path.join(ROOT, "baseline", "_ref")
-    if os.path.isdir(os.path.join(ref, "pathfilter")):
+    if not os.path.isdir(os.path.join(ref, "pathfilter")):
+        return None
+    if ref not in sys.path:
         sys.path.insert(0, ref)
-        try:
-            import pathfilter
-            import pathfilter.pipeline  # noqa: F401
-            cfg = pathfilter.FilterConfig(**cfg_kwargs)
-            st = pathfilter.FrameState.from_config(cfg)
-            return {"kind": "reference", "mod": pathfilter, "cfg": cfg, "state": st,
-                    "backend": pathfilter.BACKEND}
-        except Exception as exc:  # fall through to the port
-            print(f"bench: reference import failed ({exc}); using the oracle port",
-                  file=sys.stderr)
-    from oracle import pf_oracle
-    cfg = pf_oracle.Config(**{k: v for k, v in cfg_kwargs.items()
-                              if k in pf_oracle.Config.__dataclass_fields__})
-    return {"kind": "port", "mod": pf_oracle, "cfg": cfg, "state": pf_oracle.State.from_config(cfg),
-            "backend": "oracle"}
+    try:
+        import pathfilter
+        import pathfilter.pipeline  # noqa: F401
+        return pathfilter
+    except Exception as exc:  # noqa: BLE001
+        print(f"bench: reference import failed ({exc})", file=sys.stderr)
+        return None
+
+
+def reference_config(ref, scene, temporal):
+    """The reference's FilterConfig for a camera: defaults, capacity next_pow2(2 W H)
+    (src/cli.py:142-143), footprint from the camera (src/keys.py:74-76)."""
+    cam = scene.camera
+    cap = 1 << (2 * cam.width * cam.height - 1).bit_length()
+    return ref.FilterConfig(capacity=cap, temporal_mode=temporal).for_camera(cam.fov, cam.height)
+
+
+def reference_stream(ref, width, height, bounces, threads):
+    """The benchmark stream traced by the REFERENCE's tracer (src/tracer.py:411-461):
+    select_k = 1..bounces at 1 spp, seed 1, rr_start 9, sample += k - 1, concatenated
+    (SURVEY App. B).  Returns (scene, VertexStream, base image of k = 1)."""
+    from pathfilter.scene import parse_scene
+    from pathfilter.tracer import TraceOptions, VertexStream, trace
+    scene = parse_scene(REF_CLOSED_BOX.format(width=width, height=height))
+    parts, base = [], None
+    for k in range(1, bounces + 1):
+        tr = trace(scene, spp=1, seed=1, options=TraceOptions(select_k=k, rr_start=9),
+                   threads=threads)
+        v = tr.vertices
+        v.sample = v.sample + (k - 1)
+        parts.append(v)
+        if base is None:
+            base = tr.base_image
+    return scene, VertexStream.concat(parts), base
+
+
+def reference_frame(ref, vs, base, cfg, state, frame, threads):
+    """One frame of the reference's own CPU path: begin_frame on both tables,
+    accumulate_phase, resolve_phase (src/pipeline.py:321-363 minus the tracer), with the
+    animated-scene seed schedule (src/pipeline.py:329).  Returns seconds."""
+    seed = ref.rng.mix64(1 ^ ((frame * GOLDEN) & 0xFFFFFFFFFFFFFFFF))
+    t0 = time.perf_counter()
+    state.fine.begin_frame(frame, cfg)
+    state.coarse.begin_frame(frame, cfg)
+    fk, _, _ = ref.pipeline.accumulate_phase(vs, cfg, state, frame, seed, threads=threads)
+    ref.pipeline.resolve_phase(vs, cfg, state, frame, seed, 1, base, fk)
+    return time.perf_counter() - t0
 
 
 class _Sub:
     def __len__(self):
         return len(self.pixel)
-
-    def select(self, rows):
-        s = _Sub()
-        for f in FIELDS:
-            setattr(s, f, getattr(self, f)[rows])
-        return s
 
 
 FIELDS = ("position", "normal", "omega_r", "contribution", "throughput", "pixel", "sample",
@@ -263,58 +306,120 @@ def host_sample(stream_np, stride: int):
     return s
 
 
-def cpu_baseline(stream_np, base_np, cfg_kwargs, steps: int, stride: int):
-    setup = cpu_setup(cfg_kwargs)
+def port_baseline(stream_np, base_np, cfg_kwargs, frames: int, stride: int):
+    """Fallback when baseline/_ref is absent: the oracle port (oracle/pf_oracle.py, one
+    thread) on every `stride`-th vertex."""
+    from oracle import pf_oracle
+    cfg = pf_oracle.Config(**{k: v for k, v in cfg_kwargs.items()
+                              if k in pf_oracle.Config.__dataclass_fields__})
+    state = pf_oracle.State.from_config(cfg)
     sample = host_sample(stream_np, stride)
-    n = len(sample.pixel)
     times = []
-    from paper_1902_05942_b200 import rng
-    for f in range(steps):
+    for f in range(frames):
+        seed = pf_oracle.mix64(1 ^ ((f * GOLDEN) & 0xFFFFFFFFFFFFFFFF))
         t0 = time.perf_counter()
-        cpu_reference_frame(sample, base_np, cfg_kwargs, rng.frame_seed(1, f), f, setup)
+        pf_oracle.filter_frame(sample, cfg, state, f, seed, 1, base_np)
         times.append(time.perf_counter() - t0)
-    cores = os.cpu_count() if setup["kind"] == "reference" else 1
-    return setup, n, times, cores
+    return len(sample.pixel), times
+
+
+def cpu_baseline_leg(stream_np, base_np, cfg, frames: int = 2):
+    """cpu_baseline of the b200 arm: the unmodified reference (native backend, every host
+    thread) filtering the FULL frame of the same stream (the device tracer's stream,
+    bit-identical to the reference tracer's -- tests/test_gpu_fullsize.py); the best of
+    `frames` consecutive frames.  Falls back to the oracle port on a stride sample."""
+    ref = reference_module()
+    threads = os.cpu_count() or 1
+    if ref is None:
+        kwargs = dict(capacity=cfg.capacity, footprint_scale=cfg.footprint_scale,
+                      temporal_mode=cfg.temporal_mode)
+        n, times = port_baseline(stream_np, base_np, kwargs, frames, 4)
+        return {"value": n / min(times), "unit": "vertices/s", "cores": 1, "kind": "port",
+                "sample": f"every 4th vertex of the same stream ({n} vertices), oracle port, "
+                          f"best of {frames} frames"}
+    vs = ref.VertexStream(**{f: np.ascontiguousarray(getattr(stream_np, f)) for f in FIELDS})
+    rcfg = ref.FilterConfig(capacity=cfg.capacity, footprint_scale=cfg.footprint_scale,
+                            temporal_mode=cfg.temporal_mode)
+    state = ref.FrameState.from_config(rcfg)
+    times = [reference_frame(ref, vs, base_np, rcfg, state, f, threads) for f in range(frames)]
+    n = len(vs)
+    return {"value": n / min(times), "unit": "vertices/s", "cores": threads,
+            "kind": "reference",
+            "sample": f"the full frame ({n} vertices, C={cfg.capacity} fine+coarse), best of "
+                      f"{frames} consecutive frames, baseline/_ref backend={ref.BACKEND}, "
+                      f"threads={threads} (numpy key build single-threaded)",
+            "frame_s": times}
 
 
 def run_reference_arm(args):
+    """The reference arm: the UNMODIFIED reference (baseline/_ref) on the same workload --
+    its own tracer builds the input, its own accumulate_phase + resolve_phase filter the
+    full frame every step.  This process never imports this repo's package."""
     rank = _env_int("RANK", 0)
     if rank != 0:
         return 0
-    import torch
-    from paper_1902_05942_b200.streams import camera_footprint, stream_to_numpy
-    dev = "cuda" if torch.cuda.is_available() else "cpu"
-    if dev == "cpu" and args.stream != "synthetic":
-        raise SystemExit("the traced stream needs a CUDA device; use --stream synthetic")
-    stream, base = make_stream(args.stream, 0, device=dev)
-    stream_np = stream_to_numpy(stream)
-    base_np = base.cpu().numpy()
-    cap = 1 << (2 * W_PIX * H_PIX - 1).bit_length()
-    cfg_kwargs = dict(capacity=cap, footprint_scale=camera_footprint(H_PIX), temporal_mode=TEMPORAL)
-    stride = 4
-    total = args.warmup + args.steps
-    setup, n, times, cores = cpu_baseline(stream_np, base_np, cfg_kwargs, total, stride)
-    timed = times[args.warmup:] or times
-    per = sum(timed) / len(timed)
+    ref = reference_module()
+    threads = os.cpu_count() or 1
+    if ref is None:
+        print(json.dumps({"impl": "reference", "unavailable":
+                          "baseline/_ref (the reference's install) is missing or does not "
+                          "import"}), flush=True)
+        return 0
+    t0 = time.perf_counter()
+    scene, vs, base = reference_stream(ref, W_PIX, H_PIX, BOUNCES, threads)
+    trace_s = time.perf_counter() - t0
+    cfg = reference_config(ref, scene, TEMPORAL)
+    state = ref.FrameState.from_config(cfg)
+    n = len(vs)
+    # the CPU frame takes seconds: at most two untimed warm-up frames
+    warm = min(args.warmup, 2)
+    for f in range(warm):
+        reference_frame(ref, vs, base, cfg, state, f, threads)
+    times = [reference_frame(ref, vs, base, cfg, state, warm + k, threads)
+             for k in range(args.steps)]
+    per = sum(times) / len(times)
     value = n / per
     line = {
         "impl": "reference", "metric": METRIC, "value": value, "unit": "vertices/s",
         "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
         "ms_per_step": per * 1e3, "higher_is_better": True, "scaling": "weak",
         "vs_baseline": None, "dtype": "f64", "data": "synthetic",
-        "config": {"workload": workload_text(args.stream), "bench_workload": args.workload,
-                   "vertices_per_frame": len(stream_np.pixel),
-                   "sample_vertices_per_step": n, "capacity": cap, "tables": "fine+coarse"},
-        "cpu_baseline": {"value": value, "unit": "vertices/s", "cores": cores,
-                         "kind": setup["kind"],
-                         "sample": f"every {stride}th vertex of the 1080p 4-bounce stream "
-                                   f"({n} vertices, C=2^22 tables), backend={setup['backend']}, "
-                                   "numpy key build single-threaded"},
+        "config": {"workload": workload_text("traced").replace("traced on device",
+                                                               "traced by the reference"),
+                   "bench_workload": args.workload,
+                   "vertices_per_frame": n, "pixels": W_PIX * H_PIX,
+                   "capacity": cfg.capacity, "tables": "fine+coarse",
+                   "temporal_mode": cfg.temporal_mode, "sum_mode": cfg.sum_mode,
+                   "input": f"traced by the reference's own tracer ({threads} threads, "
+                            f"{trace_s:.1f} s, untimed)",
+                   "warmup_run": warm},
+        "cpu_baseline": {"value": value, "unit": "vertices/s", "cores": threads,
+                         "kind": "reference",
+                         "sample": f"the full frame every step ({n} vertices), backend="
+                                   f"{ref.BACKEND}, threads={threads} (numpy key build "
+                                   f"single-threaded)"},
         "e2e": {"value": value, "unit": "vertices/s", "h2d_bytes_per_step": 0,
                 "d2h_bytes_per_step": 0},
+        "frame_s": times,
+        "native_so": sorted({os.path.basename(p) for p in _loaded_libs()}),
     }
     print(json.dumps(line), flush=True)
     return 0
+
+
+def _loaded_libs():
+    """Shared objects this process has mapped that belong to this repo or the reference
+    install (a provenance record: the reference arm must map none of the repo's)."""
+    out = set()
+    try:
+        with open("/proc/self/maps") as fh:
+            for line in fh:
+                p = line.split()[-1] if line.strip() else ""
+                if p.endswith(".so") and p.startswith(ROOT):
+                    out.add(p)
+    except OSError:
+        pass
+    return out
 
 
 def run_b200(args):
@@ -343,10 +448,17 @@ def run_b200(args):
     from paper_1902_05942_b200.streams import stream_to_numpy
 
     cfg = make_config(pf)
-    stream, base = make_stream(args.stream, rank)
+    band = args.workload == "uhd4-band"
+    stream, base = make_stream(args.stream, rank, world=world, band=band)
     vs = pf.VertexStream(**stream)
     n = len(vs)
-    n_pix = W_PIX * H_PIX
+    n_pix = int(base.shape[0]) * int(base.shape[1])   # this rank's pixels
+    composite, pixel_base = ("band", rank * n_pix) if band else ("reduce", 0)
+    n_total = n * world
+    if world > 1:  # vertices of the whole job (band ranks differ)
+        t = torch.tensor([n], dtype=torch.int64, device="cuda")
+        dist.all_reduce(t)
+        n_total = int(t.item())
     if world > 1:
         from paper_1902_05942_b200 import sharded
         state = sharded.ShardedState(cfg, rank, world, agg_capacity=1 << 20)
@@ -363,7 +475,8 @@ def run_b200(args):
         seed = rng.frame_seed(1, f)
         if world > 1:
             sharded.run_dist(sharded.filter_frame_sharded(
-                vs, base, cfg, state, world, seed, composite="reduce", want_means=True,
+                vs, base, cfg, state, 1 if band else world, seed, pixel_base=pixel_base,
+                composite=composite, want_means=True,
                 phase_events=evs))
         else:
             pf.filter_frame(vs, base, cfg, state, 1, seed, want_means=True, phase_events=evs)
@@ -409,7 +522,7 @@ def run_b200(args):
         phases[names[1]].append(e1.elapsed_time(e2))
         phases[names[2]].append(e2.elapsed_time(e3))
     ph = {k: float(np.mean(v)) for k, v in phases.items()}
-    value = n * world * args.steps / t_max
+    value = n_total * args.steps / t_max
     ms_per_step = t_max / args.steps * 1e3
 
     # roofline of the dominant phase kernel (bytes per launch / mean launch time)
@@ -425,14 +538,15 @@ def run_b200(args):
     achieved = kbytes / (kms / 1e3) / 1e9
     roofline = {"bound": "hbm", "kernel": kname, "achieved": achieved, "peak": peak,
                 "peak_kind": peak_kind, "unit": "GB/s", "frac": achieved / peak,
-                "bytes_per_launch": kbytes, "traffic": _traffic(kname)}
+                "bytes_per_launch": kbytes, "traffic": _traffic(kname, args.workload, args.stream)}
 
     # the insert kernel is issue-bound, not HBM-bound: its instruction issue rate against
     # the SMs' peak (148 SMs x 4 schedulers x 1 warp-instruction per clock), with the
     # per-launch instruction count from the committed ncu capture (same workload)
     issue = None
-    inst = _traffic("insert_frame_kernel_inst") if kname == "insert_frame_kernel" else None
-    if inst and args.workload == "hd4" and args.stream == "traced":
+    inst = (_traffic("insert_frame_kernel_inst", args.workload, args.stream)
+            if kname == "insert_frame_kernel" else None)
+    if inst:
         sm_mhz = clocks.summary().get("sm_mhz") or 1965.0
         ipeak = 148 * 4 * sm_mhz * 1e6
         iach = inst / (kms / 1e3)
@@ -441,9 +555,10 @@ def run_b200(args):
     # and its L2 reductions against the sustained random-address RED rate measured by
     # tools/l2atomics.cu on this pool (profiles/r1_l2atomics.log)
     atomics = None
-    reds = _traffic("insert_frame_kernel_red_sectors") if kname == "insert_frame_kernel" else None
+    reds = (_traffic("insert_frame_kernel_red_sectors", args.workload, args.stream)
+            if kname == "insert_frame_kernel" else None)
     red_peak = _l2_red_peak()
-    if reds and red_peak and args.workload == "hd4" and args.stream == "traced":
+    if reds and red_peak:
         rach = reds / (kms / 1e3)
         atomics = {"bound": "l2_atomics", "kernel": kname, "achieved": rach, "peak": red_peak,
                    "unit": "red/s", "frac": rach / red_peak, "red_per_launch": reds}
@@ -451,20 +566,14 @@ def run_b200(args):
     # end to end through the public API with host buffers
     e2e = None
     if not args.no_e2e:
-        e2e = run_e2e(pf, rng, cfg, stream, base, args, n, rank, world)
+        e2e = run_e2e(pf, rng, cfg, stream, base, args, n, rank, world, composite, pixel_base,
+                      n_total)
 
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu:
-        stream_np = stream_to_numpy(stream)
-        kwargs = dict(capacity=cfg.capacity, footprint_scale=cfg.footprint_scale,
-                      temporal_mode=cfg.temporal_mode)
-        stride = 4
-        setup, ns, times, cores = cpu_baseline(stream_np, base.cpu().numpy(), kwargs, 2, stride)
-        cpu = {"value": ns / min(times), "unit": "vertices/s", "cores": cores,
-               "kind": setup["kind"],
-               "sample": f"every {stride}th vertex of the same stream ({ns} vertices, C=2^22 "
-                         f"fine+coarse), best of 2 frames, backend={setup['backend']}"}
+        cpu = cpu_baseline_leg(stream_to_numpy(stream), base.cpu().numpy(), cfg)
 
+    in_bytes = QUERY_BYTES_PER_VERTEX * n + QUERY_BYTES_PER_PIXEL * n_pix
     if rank == 0:
         # single: prologue, insert, effective records, resolve main, fallback keys, pool,
         # finalize.  sharded: begin x2, check, keys, emit, apply, reset, publish x2,
@@ -474,15 +583,18 @@ def run_b200(args):
         line = {
             "metric": METRIC, "value": value, "unit": "vertices/s", "n_gpus": world,
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms_per_step,
-            "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+            "higher_is_better": True, "scaling": "strong" if band else "weak",
+            "vs_baseline": None, "dtype": "f64",
             "data": "synthetic",
             "config": {"workload": workload_text(args.stream), "bench_workload": args.workload,
-                       "vertices_per_frame": n, "pixels": n_pix,
+                       "vertices_per_frame": n_total, "vertices_rank0": n,
+                       "pixels": n_pix * (world if band else 1),
                        "capacity": cfg.capacity, "tables": "fine+coarse",
                        "temporal_mode": cfg.temporal_mode, "sum_mode": cfg.sum_mode,
                        "parallelism": (f"key-sharded tables x{world} (NCCL all-to-all), "
                                        f"1 spp per GPU" if world > 1 else "single"),
-                       "l2": "inputs 1.0 GB per frame > 126 MB L2 (no flush needed)",
+                       "l2": f"inputs {in_bytes / 1e9:.2f} GB per frame > 126 MB L2 "
+                             "(no flush needed)",
                        "outputs": "filtered image + per-vertex source and chosen mean "
                                   "(the reference's ResolveReport)"},
             "phases_ms": ph, "roofline": roofline, "roofline_issue": issue,
@@ -496,7 +608,8 @@ def run_b200(args):
     return 0
 
 
-def run_e2e(pf, rng, cfg, stream, base, args, n, rank=0, world=1):
+def run_e2e(pf, rng, cfg, stream, base, args, n, rank=0, world=1, composite="reduce",
+            pixel_base=0, n_total=None):
     """Same frame through the public API from pinned host buffers: H2D of every
     input the frame reads, the frame, D2H of the filtered image (this rank's rows for
     N > 1) -- all timed; max over ranks.  One GPU: pf.HostFramePipeline, whose copy
@@ -516,7 +629,8 @@ def run_e2e(pf, rng, cfg, stream, base, args, n, rank=0, world=1):
                   "layer_id": torch.zeros_like(stream["pixel"])}
         from paper_1902_05942_b200 import sharded
         state = sharded.ShardedState(cfg, rank, world, agg_capacity=1 << 20)
-        himg = himg[: himg.shape[0] // world]
+        if composite == "reduce":
+            himg = himg[: himg.shape[0] // world]
     else:
         state = pf.FrameState.from_config(cfg)
     h2d = sum(t.numel() * t.element_size() for t in host.values()) + hbase.numel() * 8
@@ -535,7 +649,8 @@ def run_e2e(pf, rng, cfg, stream, base, args, n, rank=0, world=1):
         dbase.copy_(hbase, non_blocking=True)
         vs = pf.VertexStream(**dev, **unused)
         image, _, _ = sharded.run_dist(sharded.filter_frame_sharded(
-            vs, dbase, cfg, state, world, rng.frame_seed(1, f), composite="reduce"))
+            vs, dbase, cfg, state, 1 if composite == "band" else world, rng.frame_seed(1, f),
+            pixel_base=pixel_base, composite=composite))
         himg.copy_(image, non_blocking=True)
 
     for f in range(max(1, min(args.warmup, 3))):
@@ -568,7 +683,8 @@ def run_e2e(pf, rng, cfg, stream, base, args, n, rank=0, world=1):
         copy_t.append(s.elapsed_time(e) / 1e3)
     del big_h, big_d
     per = t / k
-    return {"value": n * world * k / t, "unit": "vertices/s", "h2d_bytes_per_step": h2d,
+    return {"value": (n_total or n * world) * k / t, "unit": "vertices/s",
+            "h2d_bytes_per_step": h2d,
             "d2h_bytes_per_step": d2h, "ms_per_step": per * 1e3, "steps": k,
             "roofline": {"bound": "pcie_h2d", "achieved": h2d / per / 1e9,
                          "peak": h2d / min(copy_t) / 1e9, "unit": "GB/s",
@@ -590,12 +706,60 @@ def main():
     ap.add_argument("--stream", default="traced", choices=["traced", "synthetic"],
                     help="benchmark input: App. B scene traced on device, or the synthetic "
                          "closed-box generator")
+    ap.add_argument("--dry-run", action="store_true",
+                    help="start the ranks, one barrier + all-reduce, print the rank count "
+                         "(tests the launch path; no GPU work)")
     args = ap.parse_args()
     global W_PIX, H_PIX, BOUNCES, TEMPORAL
     W_PIX, H_PIX, BOUNCES, TEMPORAL, _ = WORKLOADS[args.workload]
     if args.impl == "reference":
         return run_reference_arm(args)
+    world = os.environ.get("WORLD_SIZE")
+    if world is None and args.gpus > 1:
+        return spawn_ranks(args.gpus)
+    if int(world or 1) != args.gpus:
+        raise SystemExit(f"bench: --gpus {args.gpus} but WORLD_SIZE={world}: refusing to "
+                         "report a rank count other than the one asked for")
+    if args.dry_run:
+        return dry_run(args)
     return run_b200(args)
+
+
+def spawn_ranks(n: int) -> int:
+    """`bench.py --gpus N` without a launcher: re-execute this command under
+    torch.distributed.run with N local ranks (127.0.0.1 rendezvous, a free port),
+    NCCL_DEBUG=INFO (init lines only) so the rank count is visible in the log."""
+    import socket
+    with socket.socket() as sk:
+        sk.bind(("127.0.0.1", 0))
+        port = sk.getsockname()[1]
+    env = dict(os.environ)
+    env.setdefault("NCCL_DEBUG", "INFO")
+    env.setdefault("NCCL_DEBUG_SUBSYS", "INIT")
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1",
+           f"--nproc-per-node={n}", "--master-addr", "127.0.0.1", f"--master-port={port}",
+           os.path.abspath(__file__), *sys.argv[1:]]
+    return subprocess.call(cmd, env=env)
+
+
+def dry_run(args) -> int:
+    import torch
+    import torch.distributed as dist
+    world = _env_int("WORLD_SIZE", 1)
+    rank = _env_int("RANK", 0)
+    n = world
+    if world > 1:
+        dist.init_process_group("nccl" if torch.cuda.is_available() else "gloo")
+        t = torch.ones(1)
+        if torch.cuda.is_available():
+            torch.cuda.set_device(_env_int("LOCAL_RANK", 0))
+            t = t.cuda()
+        dist.all_reduce(t)
+        n = int(t.item())
+        dist.destroy_process_group()
+    if rank == 0:
+        print(json.dumps({"dry_run": True, "n_gpus": world, "ranks_reduced": n}), flush=True)
+    return 0
 
 
 if __name__ == "__main__":

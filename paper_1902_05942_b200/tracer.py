@@ -209,3 +209,28 @@ def multi_bounce_stream(scene: Scene, bounces: int, seed: int, rr_start: int = 9
         if base is None:
             base = res.base_image
     return concat_streams(streams), base
+
+
+def band_stream(scene: Scene, bounces: int, seed: int, row_lo: int, row_hi: int,
+                rr_start: int = 9, options: TraceOptions | None = None) -> tuple:
+    """multi_bounce_stream restricted to the pixel rows [row_lo, row_hi): the stream of
+    one rank of a frame split into pixel-row bands (the reference's thread split,
+    src/pipeline.py:138-149 / src/tracer.py:429-434, across GPUs).  Concatenating the
+    bands' streams in rank order gives, per select_k, the rows of the whole frame's
+    stream.  Returns (VertexStream, base image rows [row_lo, row_hi) of k = 1)."""
+    scene.validate()
+    W = scene.camera.width
+    _, keep = _device_scene(scene)
+    dev = keep["v0"].device
+    pix = torch.arange(row_lo * W, row_hi * W, dtype=torch.int64, device=dev)
+    streams, base = [], None
+    for k in range(1, bounces + 1):
+        opt = TraceOptions(**{**(options.__dict__ if options else {}), "select_k": k,
+                              "rr_start": rr_start})
+        paths = trace_paths(scene, pix, torch.zeros_like(pix), seed, opt)
+        v = _stream_of(paths)
+        v.sample = v.sample + (k - 1)
+        streams.append(v)
+        if base is None:
+            base = paths["base"].reshape(row_hi - row_lo, W, 3)
+    return concat_streams(streams), base

@@ -108,3 +108,23 @@ def test_traced_stream_keys_equal_reference_keys(gpu):
     want_k = gpu.vertex_keys(ref_vs, cfg, 11)
     for f in ("index", "fingerprint", "level", "qx", "qy", "qz"):
         assert torch.equal(getattr(got_k, f), getattr(want_k, f)), f
+
+
+@pytest.mark.parametrize("world", [2, 4])
+def test_band_stream_is_the_frame_stream_restricted_to_its_rows(gpu, world):
+    """bench --workload uhd4-band: rank r's band_stream equals the whole frame's
+    multi_bounce_stream restricted to the pixels of rows [r H/G, (r+1) H/G), field by
+    field and in order; the band base image is those rows of the frame's base."""
+    from paper_1902_05942_b200.scene import closed_box
+    from paper_1902_05942_b200.tracer import band_stream, multi_bounce_stream
+    w, h = 48, 28
+    sc = closed_box(w, h)
+    full, base = multi_bounce_stream(sc, 4, 1)
+    rows = h // world
+    for r in range(world):
+        vs, b = band_stream(sc, 4, 1, r * rows, (r + 1) * rows)
+        m = (full.pixel >= r * rows * w) & (full.pixel < (r + 1) * rows * w)
+        for f in ("position", "normal", "omega_r", "contribution", "throughput", "pixel",
+                  "sample", "layer_id", "camera_distance"):
+            assert torch.equal(getattr(vs, f), getattr(full, f)[m]), f
+        assert torch.equal(b, base[r * rows:(r + 1) * rows])

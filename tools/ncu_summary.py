@@ -1,7 +1,7 @@
 """Summarise an `ncu --set full` report of one bench frame into profiles/.
 
     python tools/ncu_summary.py gpurun_out/m_full.ncu-rep profiles/r1_ncu_full_summary.json \
-        profiles/ncu_traffic.json
+        profiles/ncu_traffic.json hd4
 
 Writes the per-kernel metric subset (the first JSON) and the insert kernel's DRAM
 traffic, instruction and RED-sector counts that bench.py's roofline objects read (the
@@ -27,7 +27,7 @@ METRICS = ("gpu__time_duration.sum", "dram__bytes_read.sum", "dram__bytes_write.
 SCALE = {"byte": 1.0, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9}
 
 
-def main(rep, out_summary, out_traffic):
+def main(rep, out_summary, out_traffic, workload="hd4"):
     raw = subprocess.run(["ncu", "-i", rep, "--page", "raw", "--csv"], capture_output=True,
                          text=True, check=True).stdout
     rows = list(csv.reader(io.StringIO(raw)))
@@ -56,10 +56,16 @@ def main(rep, out_summary, out_traffic):
                     val("l1tex__m_l1tex2xbar_write_sectors_mem_global_op_red.sum"),
             }
     json.dump(summary, open(out_summary, "w"), indent=1)
-    json.dump(traffic, open(out_traffic, "w"), indent=1)
+    try:
+        merged = json.load(open(out_traffic))
+    except (OSError, ValueError):
+        merged = {}
+    if traffic:
+        merged[workload] = traffic  # keyed by bench workload (bench.py _traffic)
+    json.dump(merged, open(out_traffic, "w"), indent=1)
     for k in summary:
         print(k["Kernel Name"][:40], k.get("gpu__time_duration.sum"), k.get("smsp__inst_executed.sum"))
 
 
 if __name__ == "__main__":
-    main(*sys.argv[1:4])
+    main(*sys.argv[1:5])
