@@ -139,6 +139,12 @@ int pf_device_sm_count(void);
 /* Host only: the config every entry point actually runs with -- `in` plus the
  * library-derived fields (lod_ulps, inv_base_voxel, lod_dist).  Validates thresholds. */
 int pf_prepare_config(const pf_config *in, pf_config *out);
+/* Host only: page-lock (cudaHostRegister) / release a caller-owned host buffer in place,
+ * so the kernel-module drop-in stages numpy tables at DMA rate.  A failed registration
+ * (already registered, not supported) returns PF_ERR_CUDA and leaves no CUDA error
+ * pending; the buffer stays usable as pageable memory. */
+int pf_host_register(void *ptr, int64_t bytes);
+int pf_host_unregister(void *ptr);
 
 /* ---- 1. reference kernel-module ABI ------------------------------------------------ */
 

@@ -35,7 +35,8 @@ EXPORTS = ("pf_abi_version", "pf_last_error", "pf_device_sm_count", "pf_accumula
            "pf_count_occupied", "pf_finalize_image", "pf_shard_keys", "pf_shard_emit",
            "pf_shard_apply", "pf_shard_publish", "pf_replica_update", "pf_shard_reset",
            "pf_resolve_replica", "pf_trace_paths", "pf_sincos", "pf_segment_deltas",
-           "pf_begin_frame_checked", "pf_prepare_config", "pf_build_id")
+           "pf_begin_frame_checked", "pf_prepare_config", "pf_build_id",
+           "pf_host_register", "pf_host_unregister")
 
 _BUILD_TAG = b"PF_BUILD_ID="
 
@@ -260,6 +261,8 @@ def lib() -> ctypes.CDLL:
     L.pf_trace_paths.argtypes = [vp, vp, u64, vp, vp, i64, vp, vp]
     L.pf_sincos.argtypes = [vp, i64, vp, vp, vp]
     L.pf_prepare_config.argtypes = [vp, vp]
+    L.pf_host_register.argtypes = [vp, i64]
+    L.pf_host_unregister.argtypes = [vp]
     L.pf_segment_deltas.argtypes = [vp, vp, i64, vp, vp, dbl, vp, vp]
     L.pf_begin_frame_checked.argtypes = [vp, vp, i64, i32, dbl, dbl, i32, vp, vp, vp, i64, vp,
                                          vp]

@@ -76,4 +76,25 @@ int pf_prepare_config(const pf_config *in, pf_config *out) {
     return pf::prepare_config("pf_prepare_config", in, out);
 }
 
+int pf_host_register(void *ptr, int64_t bytes) {
+    if (ptr == nullptr || bytes <= 0) return pf::fail_arg("pf_host_register", "empty buffer");
+    const cudaError_t e = cudaHostRegister(ptr, static_cast<size_t>(bytes), cudaHostRegisterDefault);
+    if (e != cudaSuccess) {
+        cudaGetLastError();  // not sticky: leave nothing for the next launch check
+        pf::set_error(std::string("pf_host_register: ") + cudaGetErrorString(e));
+        return PF_ERR_CUDA;
+    }
+    return PF_OK;
+}
+
+int pf_host_unregister(void *ptr) {
+    const cudaError_t e = cudaHostUnregister(ptr);
+    if (e != cudaSuccess) {
+        cudaGetLastError();
+        pf::set_error(std::string("pf_host_unregister: ") + cudaGetErrorString(e));
+        return PF_ERR_CUDA;
+    }
+    return PF_OK;
+}
+
 }  // extern "C"

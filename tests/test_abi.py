@@ -66,12 +66,41 @@ def test_cubin_is_sm100a():
     assert "sm_100a" in out
 
 
-def test_struct_layouts():
+MIRRORS = {"PfConfig": "pf_config", "PfVertices": "pf_vertices", "PfTable": "pf_table",
+           "PfKeyOut": "pf_key_out", "PfFrameBuffers": "pf_frame_buffers",
+           "PfShard": "pf_shard", "PfReplica": "pf_replica", "PfScene": "pf_scene",
+           "PfTraceOptions": "pf_trace_options", "PfPathOut": "pf_path_out",
+           "PfEvictEvent": "pf_evict_event"}
+
+
+def test_struct_layouts_match_the_c_compiler(tmp_path):
+    """Every ctypes mirror in _lib.py has the C compiler's sizeof and offsetof for
+    every field of the header's struct (a probe compiled with gcc against
+    include/pathfilter_b200.h), so header/ctypes drift fails here."""
     from paper_1902_05942_b200 import _lib
-    assert ctypes.sizeof(_lib.PfConfig) == 4 * 8 + 32 * 8 + 12 * 4 + 2 * 8 + 8 + 32 * 8
-    assert ctypes.sizeof(_lib.PfVertices) == 10 * 8
-    assert ctypes.sizeof(_lib.PfTable) == 8 * 8 + 4 * 4
-    assert ctypes.sizeof(_lib.PfEvictEvent) == 32
+    lines = ["#include <stddef.h>", "#include <stdio.h>", '#include "pathfilter_b200.h"',
+             "int main(void) {"]
+    want = {}
+    for py, c in MIRRORS.items():
+        cls = getattr(_lib, py)
+        lines.append(f'printf("{c} sizeof %zu\\n", sizeof({c}));')
+        want[(c, "sizeof")] = ctypes.sizeof(cls)
+        for name, _ in cls._fields_:
+            lines.append(f'printf("{c} {name} %zu\\n", offsetof({c}, {name}));')
+            want[(c, name)] = getattr(cls, name).offset
+    lines += ["return 0;", "}"]
+    src = tmp_path / "probe.c"
+    src.write_text("\n".join(lines))
+    exe = tmp_path / "probe"
+    subprocess.run(["gcc", "-std=c11", "-I", os.path.join(ROOT, "include"), str(src), "-o",
+                    str(exe)], check=True)
+    got = {}
+    for ln in subprocess.run([str(exe)], capture_output=True, text=True,
+                             check=True).stdout.splitlines():
+        c, name, v = ln.split()
+        got[(c, name)] = int(v)
+    bad = {k: (got.get(k), v) for k, v in want.items() if got.get(k) != v}
+    assert not bad, f"(C, ctypes) mismatches: {bad}"
 
 
 @pytest.mark.parametrize("fs,sp,bv", [(0.003, 8.0, 0.02), (0.01, 8.0, 0.01), (1e-7, 3.0, 0.5),
