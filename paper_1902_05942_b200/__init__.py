@@ -5,26 +5,25 @@ insert vertices, query averages, temporal update -- plus the on-device path trac
 that produces the vertex stream, whole frames (render_frame / run_sequence, all three
 temporal modes) and the key-sharded multi-GPU frame.  All compute runs in hand-written
 sm_100a CUDA kernels (libpf_b200.so, C ABI in include/pathfilter_b200.h); there is no
-CPU fallback.  The scalar key helpers and brute-force partition utilities the
-reference also exports are host code by design (one vertex at a time).
+CPU fallback.  The reference's one-vertex-at-a-time scalar key helpers and brute-force
+partition utilities (src/keys.py:104-240, src/oracle.py) are not part of this package:
+the batched key path (make_key_arrays / vertex_keys) is the filter API, and the CPU
+restatement used as a checker lives in oracle/ (test infrastructure).
 """
 
 from . import rng
 from .images import read_ppm, tonemap, write_ppm
 from .keys import CellHashes, CellKey, FilterConfig, KeyArrays, hash_arrays, hashes, \
     make_key_arrays, pack_aux
-from .partition import ball_average, brute_voxel_average, derive_key, image_mse, \
-    neighborhood_mean
 from .pipeline import FrameState, FrameStats, ResolveReport, VertexStream, accumulate_phase, \
     filter_frame, resolve_phase, vertex_keys
 from .render import FrameResult, render_frame, run_sequence
-from .scalar import jitter_position, level_of_detail, make_cell_key
 from .scene import Camera, Material, Motion, Scene, SceneBuilder, SceneError, closed_box, \
     cornell_box, load_scene, parse_scene
 from .table import EMPTY_TAG, EvictionEvent, InsertOutcome, Outcome, VoxelTable, \
     fixed_to_float, pack_priority, quantize_fixed
-from .temporal import blend, migrate_resolution, reevaluation_deltas, select_replay_ids, \
-    temporal_difference
+from .temporal import migrate_cells, migrate_resolution, reevaluation_deltas, \
+    select_replay_ids
 from .tracer import TraceOptions, TraceResult, reevaluate, trace
 
 from ._backend import BACKEND, available_backends
@@ -38,15 +37,13 @@ __version__ = "0.1.0"
 
 __all__ = [
     "BACKEND", "available_backends", "rng", "CellHashes", "CellKey", "FilterConfig",
-    "KeyArrays", "hash_arrays", "hashes", "make_key_arrays", "pack_aux", "jitter_position",
-    "level_of_detail", "make_cell_key", "ball_average", "brute_voxel_average", "derive_key",
-    "image_mse", "neighborhood_mean", "FrameState", "FrameStats", "ResolveReport",
+    "KeyArrays", "hash_arrays", "hashes", "make_key_arrays", "pack_aux", "FrameState", "FrameStats", "ResolveReport",
     "VertexStream", "accumulate_phase", "filter_frame", "resolve_phase", "vertex_keys",
     "FrameResult", "render_frame", "run_sequence", "Camera", "Material", "Motion", "Scene",
     "SceneBuilder", "SceneError", "closed_box", "cornell_box", "load_scene", "parse_scene",
     "EMPTY_TAG", "EvictionEvent", "InsertOutcome", "Outcome", "VoxelTable", "fixed_to_float",
-    "pack_priority", "quantize_fixed", "blend", "migrate_resolution", "reevaluation_deltas",
-    "select_replay_ids", "temporal_difference", "TraceOptions", "TraceResult", "reevaluate",
+    "pack_priority", "quantize_fixed", "migrate_cells", "migrate_resolution",
+    "reevaluation_deltas", "select_replay_ids", "TraceOptions", "TraceResult", "reevaluate",
     "trace", "read_ppm", "tonemap", "write_ppm", "VertexDescriptor", "levels_array",
     "tangent_basis_array", "jittered_positions", "normal_bins_array", "aux_bits_array",
     "HostFrame", "HostFramePipeline",

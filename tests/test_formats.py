@@ -1,6 +1,6 @@
 """Output formats and keyed temporal helpers against the reference's own outputs
 (tests/golden/formats.npz, make_golden.py gen_formats): tone map / PPM bytes
-(src/images.py), blend / temporal_difference / migrate_resolution (src/temporal.py),
+(src/images.py), migrate_resolution (src/temporal.py, on the device),
 and -- on the GPU -- VoxelTable.export_csv / dump bytes (src/table.py:314-334)."""
 
 import numpy as np
@@ -21,23 +21,8 @@ def test_tonemap_and_ppm_bytes(tmp_path):
         write_ppm(tmp_path / "b.ppm", np.zeros((4, 4)))
 
 
-def test_blend_and_temporal_difference():
-    from paper_1902_05942_b200.temporal import blend, temporal_difference
-    d = load_golden("formats.npz")
-    rows = []
-    for mode in ("integrate", "filter", "hybrid"):
-        for (no, nn, dl) in ((0, 3, 0.0), (5, 0, 0.1), (4, 2, 0.3), (7, 5, 0.9)):
-            m, n = blend([0.1, 0.2, 0.3], no, [0.5, 0.25, 0.0], nn, mode, dl)
-            rows.append(list(m) + [n])
-    assert np.array_equal(np.array(rows), d["blend"])
-    got = [temporal_difference([0.1, 0.2, 0.3], [0.2, 0.1, 0.35]),
-           temporal_difference([0, 0, 0], [1e-5, 0, 0])]
-    assert np.array_equal(np.array(got), d["tdiff"])
-    with pytest.raises(ValueError):
-        blend([0, 0, 0], 0, [0, 0, 0], 0, "integrate")
-
-
-def test_migrate_resolution():
+@pytest.mark.gpu
+def test_migrate_resolution(gpu):
     from paper_1902_05942_b200.keys import CellKey
     from paper_1902_05942_b200.temporal import migrate_resolution
     d = load_golden("formats.npz")
@@ -64,74 +49,12 @@ def test_export_csv_and_dump_bytes(gpu, tmp_path):
     assert np.array_equal(np.frombuffer((tmp_path / "t.bin").read_bytes(), np.uint8), d["dump"])
 
 
-class _Desc:
-    def __init__(self, vs, i):
-        for f in ("position", "normal", "omega_r", "contribution", "throughput"):
-            setattr(self, f, getattr(vs, f)[i])
-        self.pixel, self.sample = int(vs.pixel[i]), int(vs.sample[i])
-        self.layer_id, self.camera_distance = int(vs.layer_id[i]), float(vs.camera_distance[i])
-
-
-_CFGS = {"default": dict(capacity=1024, footprint_scale=0.002),
-         "aux": dict(capacity=1024, footprint_scale=0.002, include_incident_angle=True,
-                     include_layer=True)}
-
-
-@pytest.mark.parametrize("name", list(_CFGS))
-def test_scalar_key_path(name):
-    """make_cell_key / level_of_detail / jitter_position (src/keys.py:100-240)."""
-    from conftest import golden_stream
-    from paper_1902_05942_b200.keys import FilterConfig
-    from paper_1902_05942_b200.scalar import jitter_position, level_of_detail, make_cell_key
-    d = load_golden("formats.npz")
-    vs = golden_stream(d, "part_v_")
-    cfg = FilterConfig(**_CFGS[name])
-    draws = d[f"scalar_{name}_draws"]
-    keys = [make_cell_key(_Desc(vs, i), cfg, draws[i], dl) for i in range(len(vs.pixel))
-            for dl in (0, 2)]
-    got = np.array([[k.qx, k.qy, k.qz, k.level, k.aux] for k in keys])
-    assert np.array_equal(got, d[f"scalar_{name}_keys"])
-    assert np.array_equal(np.array([level_of_detail(float(x), cfg) for x in vs.camera_distance]),
-                          d[f"scalar_{name}_lod"])
-    jit = np.array([jitter_position(vs.position[i], vs.normal[i], 3, draws[i], cfg)
-                    for i in range(len(vs.pixel))])
-    assert np.array_equal(jit, d[f"scalar_{name}_jit"])
-
-
-@pytest.mark.parametrize("name", list(_CFGS))
-@pytest.mark.parametrize("sm", ["fixed", "float"])
-def test_brute_partition_csv(tmp_path, name, sm):
-    """brute_voxel_average + VoxelPartition.to_csv + neighborhood_mean (src/oracle.py)."""
-    from conftest import golden_stream
-    from paper_1902_05942_b200.keys import FilterConfig
-    from paper_1902_05942_b200.partition import brute_voxel_average, neighborhood_mean
-    d = load_golden("formats.npz")
-    vs = golden_stream(d, "part_v_")
-    part = brute_voxel_average(vs, FilterConfig(**_CFGS[name]), d[f"part_{name}_jittered"], sm)
-    part.to_csv(tmp_path / "p.csv")
-    assert (tmp_path / "p.csv").read_text() == str(d[f"part_{name}_{sm}_csv"])
-    some = sorted(part.cells)[::7]
-    assert np.array_equal(np.array([neighborhood_mean(part, k) for k in some]),
-                          d[f"part_{name}_{sm}_nbr"])
-
-
-def test_ball_average_and_mse():
-    from conftest import golden_stream
-    from paper_1902_05942_b200.partition import ball_average, image_mse
-    d = load_golden("formats.npz")
-    vs = golden_stream(d, "part_v_")
-    got = np.array([ball_average(vs, vs.position[5], 1.5),
-                    ball_average(vs, vs.position[9], 0.8,
-                                 lambda c, p: 1.0 / (1.0 + float(((p - c) ** 2).sum())))])
-    assert np.array_equal(got, d["ball"])
-    assert image_mse(d["img"], d["img"] * 0.9) == float(d["mse"])
-
-
 @pytest.mark.gpu
 def test_probe_scan_structured_fingerprints(gpu):
     """normal_in_fingerprint keys share the index hash; probe_scan finds every normal
     variant of a voxel by the fingerprint's spatial bits (src/table.py:186-203)."""
-    from paper_1902_05942_b200.scalar import fingerprint_spatial_bits
+    def fingerprint_spatial_bits(fp):   # src/keys.py:237-240: the bits above the normal bins
+        return fp >> 6
     d = load_golden("formats.npz")
     t = gpu.VoxelTable(256, sum_mode="fixed", probe_limit=8, ordered=True)
     t.accumulate_batch(d["scan_idx"], d["scan_fp"], d["scan_vals"], 0)
@@ -141,3 +64,44 @@ def test_probe_scan_structured_fingerprints(gpu):
     res = t.probe_scan(h, lambda fp: fingerprint_spatial_bits(fp) == sp)
     assert np.array_equal(np.array([c for _, c in res]), d["scan_counts"])
     assert np.array_equal(np.array([np.asarray(m) for m, _ in res]), d["scan_means"])
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("lo,ln,fixed", [(2, 3, False), (2, 4, True), (3, 1, False),
+                                          (3, 2, True), (2, 2, False)])
+def test_migrate_resolution_matches_reference_with_collisions(gpu, lo, ln, fixed):
+    """Random snapshots whose keys collide after migration (children of one parent,
+    pass-through keys equal to a parent or child, in every order) against the
+    reference's own migrate_resolution (baseline/_ref, src/temporal.py:107-151): same
+    keys in the same dict order, same counts, sums bit for bit."""
+    import os
+    import sys
+    ref = os.path.join(os.path.dirname(os.path.dirname(os.path.abspath(__file__))),
+                       "baseline", "_ref")
+    if not os.path.isdir(os.path.join(ref, "pathfilter")):
+        pytest.skip("baseline/_ref absent")
+    sys.path.insert(0, ref)
+    from pathfilter.keys import CellKey as RKey
+    from pathfilter.temporal import migrate_resolution as ref_migrate
+    from paper_1902_05942_b200.keys import CellKey
+    from paper_1902_05942_b200.temporal import migrate_resolution
+    r = np.random.default_rng(lo * 10 + ln)
+    cells_ref, cells = {}, {}
+    for _ in range(300):
+        q = r.integers(-6, 6, 3)
+        lvl = int(r.choice([lo, lo, ln, 5]))
+        aux = int(r.integers(0, 2))
+        tot = r.uniform(0, 9, 3)
+        if fixed:
+            tot = np.floor(tot * 65536).astype(np.int64)
+        c = int(r.integers(1, 40))
+        k = (int(q[0]), int(q[1]), int(q[2]), lvl, aux)
+        cells_ref[RKey(*k)] = (tot, c)
+        cells[CellKey(*k)] = (tot, c)
+    want = ref_migrate(cells_ref, lo, ln, 0.25, fixed)
+    got = migrate_resolution(cells, lo, ln, 0.25, fixed)
+    kt = lambda k: (k.qx, k.qy, k.qz, k.level, k.aux)  # noqa: E731
+    assert [kt(k) for k in got] == [kt(k) for k in want]
+    for (kg, (sg, cg)), (kw, (sw, cw)) in zip(got.items(), want.items()):
+        assert cg == cw, kg
+        assert np.array_equal(np.asarray(sg), np.asarray(sw)), kg
