@@ -23,7 +23,7 @@
 extern "C" {
 #endif
 
-#define PF_ABI_VERSION 4
+#define PF_ABI_VERSION 5
 
 enum pf_status {
     PF_OK = 0,
@@ -78,7 +78,17 @@ typedef struct pf_vertices {
     int64_t n;
 } pf_vertices;
 
-/* VoxelTable state in the reference SoA layout (src/table.py:96-103). */
+/* VoxelTable state (src/table.py:96-103).  Fields are addressed through strides, in
+ * 8-byte words: slot s's count at counts + s * cnt_stride, its live sums at
+ * sums + s * sum_stride + c * sum_cstride, hist_counts / last_touch / deltas at
+ * ptr + s * cold_stride and hist_sums at hist_sums + s * hsum_stride + c; `tags` is
+ * always dense.  The reference's SoA layout (the kernel-module ABI's caller-owned
+ * arrays) is cnt 1, sum 3 / 1, cold 1, hsum 3.  The device-private VoxelTable keeps
+ * tags and counts dense, the live sums channel-major (sum_stride 1, sum_cstride C: the
+ * insert's three REDs per vertex land in three different lines, which the L2 atomic
+ * units serve in parallel) and the fields only the per-frame sweeps touch in one
+ * 64-byte cold record per slot (cold_stride = hsum_stride = 8: last_touch, hist_count,
+ * delta, pad, hist_sum[3], pad). */
 typedef struct pf_table {
     uint64_t *tags;                 /* [C]   EMPTY = 0xFFFFFFFF00000000 */
     void *sums;                     /* [C][3] int64 (fixed) or float64 (float) */
@@ -92,6 +102,11 @@ typedef struct pf_table {
     int32_t probe_limit;
     int32_t evict_min_age;
     int32_t evict_horizon;
+    int32_t cnt_stride;             /* counts: slot stride                     (SoA: 1) */
+    int32_t sum_stride;             /* sums: slot stride                       (SoA: 3) */
+    int32_t cold_stride;            /* hist_counts, last_touch, deltas         (SoA: 1) */
+    int32_t hsum_stride;            /* hist_sums: slot stride (channels adjacent; SoA: 3) */
+    int64_t sum_cstride;            /* sums: channel stride                    (SoA: 1) */
 } pf_table;
 
 /* KeyArrays (src/keys.py:302-320); every pointer may be NULL (not written). */
@@ -169,6 +184,13 @@ int pf_accumulate_float(uint64_t *tags, double *sums, int64_t *counts, double *h
                         int32_t evict_min_age, int32_t ordered, uint8_t *status,
                         int64_t *slots, uint8_t *probe_len, uint64_t *victim_tags,
                         int64_t *victim_touch, void *stream);
+/* accumulate_batch on a table described by pf_table (any layout: the device-private
+ * interleaved VoxelTable or SoA); sum_mode picks fixed / float, probe_limit and
+ * evict_min_age come from the table.  Outputs as pf_accumulate_fixed. */
+int pf_accumulate_table(const pf_table *t, const uint64_t *idx, const uint32_t *fp,
+                        const double *vals, int64_t n, int64_t frame, int32_t ordered,
+                        uint8_t *status, int64_t *slots, uint8_t *probe_len,
+                        uint64_t *victim_tags, int64_t *victim_touch, void *stream);
 /* src/_native.pyx:275-295 lookup_slots: first matching slot, -1 when absent. */
 int pf_lookup_slots(const uint64_t *tags, int64_t capacity, const uint64_t *idx,
                     const uint32_t *fp, int64_t n, int32_t probe_limit, int64_t *out,

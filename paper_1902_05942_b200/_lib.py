@@ -36,7 +36,7 @@ EXPORTS = ("pf_abi_version", "pf_last_error", "pf_device_sm_count", "pf_accumula
            "pf_shard_apply", "pf_shard_publish", "pf_replica_update", "pf_shard_reset",
            "pf_resolve_replica", "pf_trace_paths", "pf_sincos", "pf_segment_deltas",
            "pf_begin_frame_checked", "pf_prepare_config", "pf_build_id",
-           "pf_host_register", "pf_host_unregister")
+           "pf_host_register", "pf_host_unregister", "pf_accumulate_table")
 
 _BUILD_TAG = b"PF_BUILD_ID="
 
@@ -119,7 +119,10 @@ class PfTable(ctypes.Structure):
                 ("hist_counts", ctypes.c_void_p), ("last_touch", ctypes.c_void_p),
                 ("deltas", ctypes.c_void_p), ("capacity", ctypes.c_int64),
                 ("sum_mode", ctypes.c_int32), ("probe_limit", ctypes.c_int32),
-                ("evict_min_age", ctypes.c_int32), ("evict_horizon", ctypes.c_int32)]
+                ("evict_min_age", ctypes.c_int32), ("evict_horizon", ctypes.c_int32),
+                ("cnt_stride", ctypes.c_int32), ("sum_stride", ctypes.c_int32),
+                ("cold_stride", ctypes.c_int32), ("hsum_stride", ctypes.c_int32),
+                ("sum_cstride", ctypes.c_int64)]
 
 
 class PfKeyOut(ctypes.Structure):
@@ -236,6 +239,7 @@ def lib() -> ctypes.CDLL:
     L.pf_accumulate_fixed.argtypes = acc
     L.pf_accumulate_float.argtypes = acc
     L.pf_lookup_slots.argtypes = [vp, i64, vp, vp, i64, i32, vp, vp]
+    L.pf_accumulate_table.argtypes = [vp, vp, vp, vp, i64, i64, i32, vp, vp, vp, vp, vp, vp]
     L.pf_make_key_arrays.argtypes = [vp, vp, vp, vp, i32, vp, vp]
     L.pf_vertex_keys.argtypes = [vp, vp, u64, i32, vp, vp]
     L.pf_hash_arrays.argtypes = [vp, vp, vp, vp, vp, vp, i64, vp, vp, vp]

@@ -32,6 +32,29 @@ constexpr double kTwoPi = 6.283185307179586;            // 2.0 * math.pi (src/ke
 constexpr double kFixedScale = 65536.0;                 // src/table.py:38
 constexpr int kMaxLevel = 31;                           // src/keys.py:19
 
+// ------------------------------------------------------------------ slot fields
+// Addresses of slot s's fields (pf_table: SoA or the interleaved 128-byte record).
+__device__ __forceinline__ int64_t *cnt_at(const pf_table &t, int64_t s) {
+    return t.counts + s * t.cnt_stride;
+}
+__device__ __forceinline__ int64_t *hcnt_at(const pf_table &t, int64_t s) {
+    return t.hist_counts + s * t.cold_stride;
+}
+__device__ __forceinline__ int64_t *touch_at(const pf_table &t, int64_t s) {
+    return t.last_touch + s * t.cold_stride;
+}
+__device__ __forceinline__ double *delta_at(const pf_table &t, int64_t s) {
+    return t.deltas + s * t.cold_stride;
+}
+// channel c of slot s's live sums / the three adjacent channels of its history sums
+// (raw 64-bit words)
+__device__ __forceinline__ uint64_t *sum_at(const pf_table &t, int64_t s, int c) {
+    return static_cast<uint64_t *>(t.sums) + s * t.sum_stride + c * t.sum_cstride;
+}
+__device__ __forceinline__ uint64_t *hsum_at(const pf_table &t, int64_t s) {
+    return static_cast<uint64_t *>(t.hist_sums) + s * t.hsum_stride;
+}
+
 // ------------------------------------------------------------------ integer helpers
 
 __device__ __forceinline__ uint64_t mix64(uint64_t x) {  // src/rng.py:51-59
@@ -711,16 +734,15 @@ constexpr int64_t kEvictMark = INT64_MIN / 2;
 
 // Wipe an evicted cell (src/_native.pyx:170-183): live + history sums, counts, delta.
 __device__ __forceinline__ void zero_cell(const pf_table &t, int64_t s) {
-    uint64_t *sums = static_cast<uint64_t *>(t.sums);
-    uint64_t *hsums = static_cast<uint64_t *>(t.hist_sums);
+    uint64_t *hsums = hsum_at(t, s);
 #pragma unroll
     for (int c = 0; c < 3; ++c) {
-        st_relaxed_u64(sums + 3 * s + c, 0ull);  // int64 0 and float64 +0.0 share bits
-        st_relaxed_u64(hsums + 3 * s + c, 0ull);
+        st_relaxed_u64(sum_at(t, s, c), 0ull);  // int64 0 and float64 +0.0 share bits
+        st_relaxed_u64(hsums + c, 0ull);
     }
-    st_relaxed_u64(t.counts + s, 0ull);
-    st_relaxed_u64(t.hist_counts + s, 0ull);
-    st_relaxed_u64(t.deltas + s, 0ull);
+    st_relaxed_u64(cnt_at(t, s), 0ull);
+    st_relaxed_u64(hcnt_at(t, s), 0ull);
+    st_relaxed_u64(delta_at(t, s), 0ull);
 }
 
 // Eviction (cold path, out of line).  The evictor CASes the victim's exact tag to BUSY
@@ -739,21 +761,20 @@ static __device__ __noinline__ int64_t evict_cell(const pf_table &t, int64_t vic
     if (atomicCAS(reinterpret_cast<unsigned long long *>(vp), victim_tag, kBusyTag) != victim_tag)
         return INT64_MIN;
     __threadfence();
-    unsigned long long *cp = reinterpret_cast<unsigned long long *>(t.counts + victim);
+    unsigned long long *cp = reinterpret_cast<unsigned long long *>(cnt_at(t, victim));
     if (atomicCAS(cp, 0ull, static_cast<unsigned long long>(kEvictMark)) != 0ull) {
         st_release(vp, victim_tag);  // pinned by an accumulate since we read it
         return INT64_MIN;
     }
-    const int64_t touch = ld_relaxed_i64(t.last_touch + victim);
-    uint64_t *sums = static_cast<uint64_t *>(t.sums);
-    uint64_t *hsums = static_cast<uint64_t *>(t.hist_sums);
+    const int64_t touch = ld_relaxed_i64(touch_at(t, victim));
+    uint64_t *hsums = hsum_at(t, victim);
 #pragma unroll
     for (int c = 0; c < 3; ++c) {  // zero_cell minus the live count, which the mark holds
-        st_relaxed_u64(sums + 3 * victim + c, 0ull);
-        st_relaxed_u64(hsums + 3 * victim + c, 0ull);
+        st_relaxed_u64(sum_at(t, victim, c), 0ull);
+        st_relaxed_u64(hsums + c, 0ull);
     }
-    st_relaxed_u64(t.hist_counts + victim, 0ull);
-    st_relaxed_u64(t.deltas + victim, 0ull);
+    st_relaxed_u64(hcnt_at(t, victim), 0ull);
+    st_relaxed_u64(delta_at(t, victim), 0ull);
     __threadfence();
     st_release(vp, incoming);
     __threadfence();
@@ -768,7 +789,7 @@ static __device__ __noinline__ int64_t evict_cell(const pf_table &t, int64_t vic
 // the add; the caller re-probes.
 static __device__ __noinline__ bool pin_cell(const pf_table &t, int64_t s, uint64_t tag,
                                              uint64_t weight) {
-    unsigned long long *cp = reinterpret_cast<unsigned long long *>(t.counts + s);
+    unsigned long long *cp = reinterpret_cast<unsigned long long *>(cnt_at(t, s));
     const long long old = static_cast<long long>(atomicAdd(cp, weight));
     if (old >= 0) {
         __threadfence();
@@ -787,7 +808,7 @@ static __device__ __noinline__ uint64_t claim_counted(const pf_table &t, int64_t
     uint64_t *tp = t.tags + s;
     const uint64_t old = atomicCAS(reinterpret_cast<unsigned long long *>(tp), kEmptyTag, kBusyTag);
     if (old != kEmptyTag) return old;
-    atomicAdd(reinterpret_cast<unsigned long long *>(t.counts + s), weight);
+    atomicAdd(reinterpret_cast<unsigned long long *>(cnt_at(t, s)), weight);
     __threadfence();
     st_release(tp, incoming);
     return kEmptyTag;
@@ -869,9 +890,9 @@ __device__ __forceinline__ InsertResult probe_insert(const pf_table &t, uint64_t
                 // tag a torn read.  Either way wait for the slot to settle and look at
                 // it again, so every prober of a key sees the same candidates and the
                 // same victim -- two lanes of one key can never evict two cells.
-                const int64_t c = ld_acquire_i64(t.counts + s);
+                const int64_t c = ld_acquire_i64(cnt_at(t, s));
                 if (c < 0 || ld_relaxed(t.tags + s) != tag) {
-                    while (ld_acquire_i64(t.counts + s) < 0) __nanosleep(32);
+                    while (ld_acquire_i64(cnt_at(t, s)) < 0) __nanosleep(32);
                     reread = true;
                     --j;
                     continue;
@@ -943,17 +964,19 @@ struct CellState {
 // read-only path for kernels that never write the table.
 __device__ __forceinline__ CellState load_cell(const pf_table &t, int64_t s, bool ro) {
     CellState c;
-    const unsigned long long *sums = static_cast<const unsigned long long *>(t.sums) + 3 * s;
-    const unsigned long long *hist = static_cast<const unsigned long long *>(t.hist_sums) + 3 * s;
+    const unsigned long long *hist = reinterpret_cast<const unsigned long long *>(hsum_at(t, s));
 #pragma unroll
     for (int k = 0; k < 3; ++k) {
-        c.sums[k] = ro ? __ldg(sums + k) : sums[k];
+        const unsigned long long *sp = reinterpret_cast<const unsigned long long *>(sum_at(t, s, k));
+        c.sums[k] = ro ? __ldg(sp) : *sp;
         c.hist[k] = ro ? __ldg(hist + k) : hist[k];
     }
-    c.counts = ro ? __ldg(t.counts + s) : t.counts[s];
-    c.hist_counts = ro ? __ldg(t.hist_counts + s) : t.hist_counts[s];
-    c.last_touch = ro ? __ldg(t.last_touch + s) : t.last_touch[s];
-    c.delta = ro ? __ldg(t.deltas + s) : t.deltas[s];
+    const int64_t *cp = cnt_at(t, s), *hp = hcnt_at(t, s), *lp = touch_at(t, s);
+    const double *dp = delta_at(t, s);
+    c.counts = ro ? __ldg(cp) : *cp;
+    c.hist_counts = ro ? __ldg(hp) : *hp;
+    c.last_touch = ro ? __ldg(lp) : *lp;
+    c.delta = ro ? __ldg(dp) : *dp;
     return c;
 }
 

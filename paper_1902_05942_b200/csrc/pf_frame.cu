@@ -56,6 +56,15 @@ __device__ __forceinline__ void log_eviction(pf_evict_event *events, int64_t *co
 #ifndef PF_INSERT_PREFETCH
 #define PF_INSERT_PREFETCH 0  // L2 prefetch of the CTA's next vertex tile: 5 us slower now
 #endif
+// How the home-slot tags reach the insert.  0: loaded into registers as each hash
+// exists (the rolled key loop's back-edge then waits for the load: the compiler does
+// not keep a load in flight across it -- at 4K, where the tables miss L2, that wait was
+// the kernel's largest stall).  1: an L2 prefetch as each hash exists (no register, no
+// wait), both tags loaded together after the key loop.  2: as 1, plus L2 prefetches of
+// the count and sums lines the REDs will hit.
+#ifndef PF_TAG_PREFETCH
+#define PF_TAG_PREFETCH 0  // 1: uhd4 insert 4.60 -> 5.13 ms (the prefetches evict table lines)
+#endif
 #ifndef PF_INSERT_MIN_BLOCKS
 #define PF_INSERT_MIN_BLOCKS 3  // 3 x 256 threads per SM: <= 85 registers
 #endif
@@ -165,17 +174,29 @@ insert_frame_kernel(pf_config cfg, pf_vertices v, pf_table fine, pf_table coarse
                 make_key_w(cfg, xk, ks, cfg.jitter, w, set == 1 ? cfg.coarse_delta : 0, jt), ks);
             // home-slot tag loads go out as soon as a hash exists; the next key set's
             // arithmetic hides their L2 latency before warp_insert consumes them
-            if (set == 0) {
-                hf = h;
-                ht_f = ld_relaxed(fine.tags + (h.index & static_cast<uint64_t>(fine.capacity - 1)));
-            } else if (set == 1) {
-                hc = h;
-                ht_c = ld_relaxed(coarse.tags +
-                                  (h.index & static_cast<uint64_t>(coarse.capacity - 1)));
+            if (set < 2) {
+                const pf_table &t = set == 0 ? fine : coarse;
+                const int64_t home = static_cast<int64_t>(h.index & static_cast<uint64_t>(t.capacity - 1));
+                if (set == 0) hf = h;
+                else hc = h;
+                if (PF_TAG_PREFETCH == 0) {
+                    (set == 0 ? ht_f : ht_c) = ld_relaxed(t.tags + home);
+                } else {
+                    prefetch_l2(t.tags + home);
+                    if (PF_TAG_PREFETCH == 2) {
+                        prefetch_l2(cnt_at(t, home));
+                        prefetch_l2(sum_at(t, home, 0));
+                    }
+                }
             } else if (valid) {
                 lk_keys[i] = pack_lookup_key(h);
             }
         }
+    }
+    if (PF_TAG_PREFETCH != 0) {  // both home tags in flight together (L2 hits by now)
+        ht_f = ld_relaxed(fine.tags + (hf.index & static_cast<uint64_t>(fine.capacity - 1)));
+        if (has_coarse)
+            ht_c = ld_relaxed(coarse.tags + (hc.index & static_cast<uint64_t>(coarse.capacity - 1)));
     }
     int64_t qval[3];  // quantised once for both tables
 #pragma unroll
@@ -279,7 +300,7 @@ effective_records_kernel(pf_table t, int mode, double ema, double delta_max, ulo
         const int64_t blk = blockIdx.x - nb_fine, nblk = gridDim.x - nb_fine;
         for_each_occupied<kThreads>(coarse.tags, coarse.capacity, q, blk, nblk,
                                     [&](int64_t s, uint64_t) {
-            if (ld_relaxed_i64(coarse.counts + s) > 0) coarse.last_touch[s] = touch_frame;
+            if (ld_relaxed_i64(cnt_at(coarse, s)) > 0) *touch_at(coarse, s) = touch_frame;
         });
         return;
     }
@@ -289,7 +310,7 @@ effective_records_kernel(pf_table t, int mode, double ema, double delta_max, ulo
                                 [&](int64_t s, uint64_t) {
         const CellState cs = load_cell(t, s, true);
         if (rec != nullptr) rec[s] = pack_effective(effective_of(cs, fixed, mode, ema, delta_max), as_int);
-        if (touch_frame != kNoTouch && cs.counts > 0) t.last_touch[s] = touch_frame;
+        if (touch_frame != kNoTouch && cs.counts > 0) *touch_at(t, s) = touch_frame;
     });
 }
 
@@ -875,6 +896,9 @@ int pf_resolve_replica(const pf_config *cfg, const pf_vertices *v, const pf_repl
     if (v->n == 0) return PF_OK;
     if (cudaMemsetAsync(work_count, 0, sizeof(int64_t), st) != cudaSuccess) return check_launch(fn);
     pf_table view{};
+    view.cnt_stride = view.cold_stride = 1;
+    view.sum_stride = view.hsum_stride = 3;
+    view.sum_cstride = 1;
     view.tags = rp->fine_tags;
     view.capacity = rp->capacity;
     view.sum_mode = rp->sum_mode;

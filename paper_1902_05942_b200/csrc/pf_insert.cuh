@@ -8,6 +8,7 @@ namespace pf {
 
 constexpr unsigned kFull = 0xFFFFFFFFu;
 
+
 // 16.16 fixed point, half up (src/_native.pyx:251-253): floor(v*65536 + 0.5).
 __device__ __forceinline__ int64_t quantize_fixed(double v) {
     return np_floor_i64(dadd(dmul(v, kFixedScale), 0.5));
@@ -92,13 +93,13 @@ __device__ __forceinline__ LaneInsert warp_insert_sums(const pf_table &t, bool v
 #pragma unroll
             for (int c = 0; c < 3; ++c) {
                 if (FIXED)
-                    red_add_u64(static_cast<int64_t *>(t.sums) + 3 * s + c,
+                    red_add_u64(reinterpret_cast<int64_t *>(sum_at(t, s, c)),
                                 static_cast<uint64_t>(qsum[c]), keep);
                 else
-                    red_add_f64(static_cast<double *>(t.sums) + 3 * s + c, fsum[c], keep);
+                    red_add_f64(reinterpret_cast<double *>(sum_at(t, s, c)), fsum[c], keep);
             }
-            if (!r.counted) red_add_u64(t.counts + s, group_weight, keep);
-            if (touch) st_relaxed_u64(t.last_touch + s, static_cast<uint64_t>(frame));
+            if (!r.counted) red_add_u64(cnt_at(t, s), group_weight, keep);
+            if (touch) st_relaxed_u64(touch_at(t, s), static_cast<uint64_t>(frame));
         }
     }
     LaneInsert out;
@@ -144,13 +145,13 @@ __device__ __forceinline__ LaneInsert lane_insert(const pf_table &t, bool valid,
 #pragma unroll
         for (int c = 0; c < 3; ++c) {
             if (FIXED)
-                red_add_u64(static_cast<int64_t *>(t.sums) + 3 * s + c,
+                red_add_u64(reinterpret_cast<int64_t *>(sum_at(t, s, c)),
                             static_cast<uint64_t>(q[c]), keep);
             else
-                red_add_f64(static_cast<double *>(t.sums) + 3 * s + c, val[c], keep);
+                red_add_f64(reinterpret_cast<double *>(sum_at(t, s, c)), val[c], keep);
         }
-        if (!r.counted) red_add_u64(t.counts + s, 1ull, keep);
-        if (touch) st_relaxed_u64(t.last_touch + s, static_cast<uint64_t>(frame));
+        if (!r.counted) red_add_u64(cnt_at(t, s), 1ull, keep);
+        if (touch) st_relaxed_u64(touch_at(t, s), static_cast<uint64_t>(frame));
     }
     out.slot = r.slot;
     out.status = r.status;

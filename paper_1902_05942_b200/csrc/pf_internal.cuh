@@ -37,6 +37,9 @@ inline int validate_table(const char *fn, const pf_table *t) {
         return fail_arg(fn, "table array pointer is NULL");
     if (t->sum_mode != PF_SUM_FIXED && t->sum_mode != PF_SUM_FLOAT)
         return fail_arg(fn, "unknown sum_mode");
+    if (t->cnt_stride < 1 || t->cold_stride < 1 || t->sum_stride < 1 || t->hsum_stride < 3 ||
+        t->sum_cstride < 1 || (t->sum_cstride < 3 && t->sum_stride < 3 * t->sum_cstride))
+        return fail_arg(fn, "bad table strides");
     return PF_OK;
 }
 

@@ -83,7 +83,7 @@ accumulate_ordered_kernel(pf_table t, const uint64_t *__restrict__ idx,
             if (in) {
                 const uint64_t age = (tag >> 32) & kAgeMask;
                 elig = age >= static_cast<uint64_t>(t.evict_min_age) &&
-                       ld_relaxed_i64(t.counts + s) == 0;
+                       ld_relaxed_i64(cnt_at(t, s)) == 0;
             }
             uint64_t best_tag = tag;
             int best_j = elig ? j : INT32_MAX;
@@ -118,7 +118,7 @@ accumulate_ordered_kernel(pf_table t, const uint64_t *__restrict__ idx,
                 status = 1;
                 slot = victim;
                 vt = victim_tag;
-                vtt = ld_relaxed_i64(t.last_touch + victim);
+                vtt = ld_relaxed_i64(touch_at(t, victim));
                 zero_cell(t, victim);
                 st_relaxed_u64(t.tags + victim, (kFresh << 32) | want);
             } else {
@@ -129,16 +129,16 @@ accumulate_ordered_kernel(pf_table t, const uint64_t *__restrict__ idx,
                 for (int c = 0; c < 3; ++c) {
                     const double x = vals[3 * i + c];
                     if (FIXED) {
-                        int64_t *p = static_cast<int64_t *>(t.sums) + 3 * slot + c;
+                        int64_t *p = reinterpret_cast<int64_t *>(sum_at(t, slot, c));
                         st_relaxed_u64(p, static_cast<uint64_t>(ld_relaxed_i64(p) + quantize_fixed(x)));
                     } else {
-                        double *p = static_cast<double *>(t.sums) + 3 * slot + c;
+                        double *p = reinterpret_cast<double *>(sum_at(t, slot, c));
                         const uint64_t bits = ld_relaxed(reinterpret_cast<const uint64_t *>(p));
                         st_relaxed_u64(p, __double_as_longlong(dadd(__longlong_as_double(bits), x)));
                     }
                 }
-                st_relaxed_u64(t.counts + slot, static_cast<uint64_t>(ld_relaxed_i64(t.counts + slot) + 1));
-                st_relaxed_u64(t.last_touch + slot, static_cast<uint64_t>(frame));
+                st_relaxed_u64(cnt_at(t, slot), static_cast<uint64_t>(ld_relaxed_i64(cnt_at(t, slot)) + 1));
+                st_relaxed_u64(touch_at(t, slot), static_cast<uint64_t>(frame));
             }
             if (o.status) o.status[i] = static_cast<uint8_t>(status);
             if (o.slots) o.slots[i] = slot;
@@ -332,18 +332,17 @@ __device__ __forceinline__ int fold_slot(const pf_table &t, int64_t s, uint64_t 
     } else {
         hist[0] = hist[1] = hist[2] = 0;
         hc = 0;
-        t.last_touch[s] = 0;
+        *touch_at(t, s) = 0;
     }
-    unsigned long long *sums = static_cast<unsigned long long *>(t.sums) + 3 * s;
-    unsigned long long *hsum = static_cast<unsigned long long *>(t.hist_sums) + 3 * s;
+    uint64_t *hsum = hsum_at(t, s);
 #pragma unroll
     for (int c = 0; c < 3; ++c) {
-        sums[c] = 0;  // live generation reset (bits of 0.0)
+        *sum_at(t, s, c) = 0;  // live generation reset (bits of 0.0)
         hsum[c] = hist[c];
     }
-    t.counts[s] = 0;
-    t.hist_counts[s] = hc;
-    t.deltas[s] = 0.0;
+    *cnt_at(t, s) = 0;
+    *hcnt_at(t, s) = hc;
+    *delta_at(t, s) = 0.0;
     t.tags[s] = new_tag;
     return cleared ? 1 : 0;
 }
@@ -508,15 +507,11 @@ sincos_kernel(const double *x, int64_t n, double *s, double *c) {
 
 // ------------------------------------------------------------------ host wrappers
 
-static int accumulate_impl(const char *fn, bool fixed, uint64_t *tags, void *sums, int64_t *counts,
-                           void *hist_sums, int64_t *hist_counts, int64_t *last_touch,
-                           double *deltas, int64_t capacity, const uint64_t *idx,
-                           const uint32_t *fp, const double *vals, int64_t n, int64_t frame,
-                           int32_t probe_limit, int32_t evict_min_age, int32_t ordered,
-                           BatchOut o, void *stream) {
-    pf_table t{tags, sums, counts, hist_sums, hist_counts, last_touch, deltas, capacity,
-               fixed ? PF_SUM_FIXED : PF_SUM_FLOAT, probe_limit, evict_min_age, 0};
+static int accumulate_table(const char *fn, const pf_table &t, const uint64_t *idx,
+                            const uint32_t *fp, const double *vals, int64_t n, int64_t frame,
+                            int32_t ordered, BatchOut o, void *stream) {
     if (int rc = validate_table(fn, &t)) return rc;
+    const bool fixed = t.sum_mode == PF_SUM_FIXED;
     if (n < 0) return fail_arg(fn, "negative batch size");
     if (n == 0) return PF_OK;
     if (!idx || !fp || !vals) return fail_arg(fn, "idx/fp/vals is NULL");
@@ -532,11 +527,33 @@ static int accumulate_impl(const char *fn, bool fixed, uint64_t *tags, void *sum
     return check_launch(fn);
 }
 
+// The kernel-module ABI's caller-owned arrays: the reference's SoA layout.
+static int accumulate_impl(const char *fn, bool fixed, uint64_t *tags, void *sums, int64_t *counts,
+                           void *hist_sums, int64_t *hist_counts, int64_t *last_touch,
+                           double *deltas, int64_t capacity, const uint64_t *idx,
+                           const uint32_t *fp, const double *vals, int64_t n, int64_t frame,
+                           int32_t probe_limit, int32_t evict_min_age, int32_t ordered,
+                           BatchOut o, void *stream) {
+    const pf_table t{tags, sums, counts, hist_sums, hist_counts, last_touch, deltas, capacity,
+                     fixed ? PF_SUM_FIXED : PF_SUM_FLOAT, probe_limit, evict_min_age, 0,
+                     1, 3, 1, 3, 1};
+    return accumulate_table(fn, t, idx, fp, vals, n, frame, ordered, o, stream);
+}
+
 }  // namespace pf
 
 using namespace pf;
 
 extern "C" {
+
+int pf_accumulate_table(const pf_table *t, const uint64_t *idx, const uint32_t *fp,
+                        const double *vals, int64_t n, int64_t frame, int32_t ordered,
+                        uint8_t *status, int64_t *slots, uint8_t *probe_len,
+                        uint64_t *victim_tags, int64_t *victim_touch, void *stream) {
+    if (t == nullptr) return fail_arg("pf_accumulate_table", "table is NULL");
+    return accumulate_table("pf_accumulate_table", *t, idx, fp, vals, n, frame, ordered,
+                            BatchOut{status, slots, probe_len, victim_tags, victim_touch}, stream);
+}
 
 int pf_accumulate_fixed(uint64_t *tags, int64_t *sums, int64_t *counts, int64_t *hist_sums,
                         int64_t *hist_counts, int64_t *last_touch, double *deltas,

@@ -1,7 +1,6 @@
 """Device-resident voxel table (src/table.py) over the sm_100a table kernels.
 
-Layout in HBM is the reference's SoA (src/table.py:96-103) so the kernel-module ABI
-(`kernels.py`) and this class share state bit for bit:
+The reference's fields (src/table.py:96-103), with the same values and dtypes:
 
     tags        u64[C]   (stored in an int64 tensor)  prio<<56 | age<<32 | fingerprint
     sums        i64|f64[C,3]   live generation radiance (16.16 fixed point or float)
@@ -11,8 +10,13 @@ Layout in HBM is the reference's SoA (src/table.py:96-103) so the kernel-module 
     last_touch  i64[C]
     deltas      f64[C]
 
-All mutation happens in CUDA kernels; host methods only launch and, where the
-reference API returns host values (statistics, dumps), copy results back.
+Layout in HBM (include/pathfilter_b200.h, pf_table): `tags` and `counts` dense, the
+live `sums` channel-major ([3][C]: a vertex's three radiance REDs go to three lines, which
+the L2 atomic units serve in parallel -- the reference's [C][3] rows put them on one line,
+and every per-slot record layout tried, where the count shares the sums' line, was
+slower still), and the fields only the per-frame sweeps read in one 64-byte cold record
+per slot (last_touch, hist_count, delta, pad, hist_sums[3], pad).  The attributes above
+are strided views; `state()` / `dump()` export the reference's SoA arrays.
 """
 
 from __future__ import annotations
@@ -34,6 +38,7 @@ EMPTY_TAG = 0xFFFFFFFF00000000
 EMPTY_TAG_I64 = EMPTY_TAG - (1 << 64)
 _AGE_MASK = 0xFFFFFE
 _DUMP_MAGIC = b"PFVT\x01"
+COLD_WORDS = 8   # 64-bit words per slot cold record (include/pathfilter_b200.h, pf_table)
 
 
 def quantize_fixed(values) -> np.ndarray:
@@ -90,14 +95,19 @@ class VoxelTable:
         self.evict_min_age = int(evict_min_age)
         # ordered=True reproduces the reference's sequential slot layout exactly
         self.ordered = bool(ordered)
-        sdt = torch.int64 if sum_mode == "fixed" else torch.float64
         self.tags = torch.full((capacity,), EMPTY_TAG_I64, dtype=torch.int64, device=dev)
-        self.sums = torch.zeros((capacity, 3), dtype=sdt, device=dev)
-        self.counts = torch.zeros(capacity, dtype=torch.int64, device=dev)
-        self.hist_sums = torch.zeros((capacity, 3), dtype=sdt, device=dev)
-        self.hist_counts = torch.zeros(capacity, dtype=torch.int64, device=dev)
-        self.last_touch = torch.zeros(capacity, dtype=torch.int64, device=dev)
-        self.deltas = torch.zeros(capacity, dtype=torch.float64, device=dev)
+        z = lambda *shape: torch.zeros(shape, dtype=torch.int64, device=dev)  # noqa: E731
+        as_sum = (lambda x: x) if sum_mode == "fixed" else (lambda x: x.view(torch.float64))
+        # dense tags and counts, channel-major live sums, one 64-byte cold record per slot
+        # (include/pathfilter_b200.h, pf_table); the attributes are views
+        self.counts = z(capacity)
+        self._sums = z(3, capacity)
+        self.sums = as_sum(self._sums.t())
+        self._cold = z(capacity, COLD_WORDS)
+        c = self._cold
+        self.last_touch, self.hist_counts = c[:, 0], c[:, 1]
+        self.deltas = c[:, 2].view(torch.float64)
+        self.hist_sums = as_sum(c[:, 4:7])
         self.frame = 0
         self._events: list[EvictionEvent] = []
         self._pending_events: list = []
@@ -135,6 +145,8 @@ class VoxelTable:
         t.probe_limit = self.probe_limit
         t.evict_min_age = self.evict_min_age
         t.evict_horizon = self.evict_horizon
+        t.cnt_stride, t.sum_stride, t.sum_cstride = 1, 1, self.capacity
+        t.cold_stride = t.hsum_stride = COLD_WORDS
         return t
 
     # -- accumulation ---------------------------------------------------------
@@ -157,13 +169,9 @@ class VoxelTable:
         probe_len = torch.empty(n, dtype=torch.uint8, device=dev)
         vtags = torch.empty(n, dtype=torch.int64, device=dev)
         vtouch = torch.empty(n, dtype=torch.int64, device=dev)
-        fn = "pf_accumulate_fixed" if self.sum_mode == "fixed" else "pf_accumulate_float"
         use_ordered = self.ordered if ordered is None else bool(ordered)
-        _lib.call(fn, self.tags.data_ptr(), self.sums.data_ptr(), self.counts.data_ptr(),
-                  self.hist_sums.data_ptr(), self.hist_counts.data_ptr(),
-                  self.last_touch.data_ptr(), self.deltas.data_ptr(), self.capacity,
-                  idx.data_ptr(), fp.data_ptr(), vals.data_ptr(), n, int(frame),
-                  self.probe_limit, self.evict_min_age, int(use_ordered),
+        _lib.call("pf_accumulate_table", ctypes.byref(self.c_table()), idx.data_ptr(),
+                  fp.data_ptr(), vals.data_ptr(), n, int(frame), int(use_ordered),
                   status.data_ptr(), slots.data_ptr(), probe_len.data_ptr(), vtags.data_ptr(),
                   vtouch.data_ptr(), _lib.stream_handle())
         self._pending_events.append((int(frame), status, slots, vtags, vtouch))
