@@ -534,6 +534,17 @@ __device__ __forceinline__ void prefetch_l2(const void *p) {
     asm volatile("prefetch.global.L2 [%0];" ::"l"(p));
 }
 
+// 16 bytes global -> shared through L2 only (coherent at gpu scope like a relaxed load),
+// tracked by cp.async groups instead of a register scoreboard.
+__device__ __forceinline__ void cp_async_16(void *smem, const void *gmem) {
+    const unsigned s = static_cast<unsigned>(__cvta_generic_to_shared(smem));
+    asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n\tcp.async.commit_group;"
+                 ::"r"(s), "l"(gmem) : "memory");
+}
+__device__ __forceinline__ void cp_async_wait_all() {
+    asm volatile("cp.async.wait_all;" ::: "memory");
+}
+
 __device__ __forceinline__ VertexIn load_vertex(const pf_vertices &v, int64_t i,
                                                 const pf_config &cfg, uint64_t pol) {
     VertexIn x;

@@ -61,9 +61,11 @@ __device__ __forceinline__ void log_eviction(pf_evict_event *events, int64_t *co
 // not keep a load in flight across it -- at 4K, where the tables miss L2, that wait was
 // the kernel's largest stall).  1: an L2 prefetch as each hash exists (no register, no
 // wait), both tags loaded together after the key loop.  2: as 1, plus L2 prefetches of
-// the count and sums lines the REDs will hit.
+// the count and sums lines the REDs will hit.  3: cp.async (L2, 16 bytes: the home
+// tag's aligned pair) into shared memory as each hash exists -- no register, so no
+// back-edge wait -- and one wait_all after the key loop.
 #ifndef PF_TAG_PREFETCH
-#define PF_TAG_PREFETCH 0  // 1: uhd4 insert 4.60 -> 5.13 ms (the prefetches evict table lines)
+#define PF_TAG_PREFETCH 3  // hd4 insert 0.774 -> 0.757 ms; 1: uhd4 4.60 -> 5.13 ms (prefetches evict table lines)
 #endif
 #ifndef PF_INSERT_MIN_BLOCKS
 #define PF_INSERT_MIN_BLOCKS 3  // 3 x 256 threads per SM: <= 85 registers
@@ -83,6 +85,9 @@ insert_frame_kernel(pf_config cfg, pf_vertices v, pf_table fine, pf_table coarse
 #endif
 #if PF_POS_SMEM
     __shared__ double posm[3][kThreads];  // per-thread vertex position
+#endif
+#if PF_TAG_PREFETCH == 3
+    __shared__ __align__(16) uint64_t home_pair[2][kThreads][2];  // fine / coarse home tag pairs
 #endif
 
     if (abort_flag != nullptr && *abort_flag != 0) return;  // invalid input: no mutation
@@ -181,6 +186,10 @@ insert_frame_kernel(pf_config cfg, pf_vertices v, pf_table fine, pf_table coarse
                 else hc = h;
                 if (PF_TAG_PREFETCH == 0) {
                     (set == 0 ? ht_f : ht_c) = ld_relaxed(t.tags + home);
+                } else if (PF_TAG_PREFETCH == 3) {
+#if PF_TAG_PREFETCH == 3
+                    cp_async_16(&home_pair[set][threadIdx.x][0], t.tags + (home & ~int64_t(1)));
+#endif
                 } else {
                     prefetch_l2(t.tags + home);
                     if (PF_TAG_PREFETCH == 2) {
@@ -193,7 +202,12 @@ insert_frame_kernel(pf_config cfg, pf_vertices v, pf_table fine, pf_table coarse
             }
         }
     }
-    if (PF_TAG_PREFETCH != 0) {  // both home tags in flight together (L2 hits by now)
+#if PF_TAG_PREFETCH == 3
+    cp_async_wait_all();
+    ht_f = home_pair[0][threadIdx.x][hf.index & 1];
+    if (has_coarse) ht_c = home_pair[1][threadIdx.x][hc.index & 1];
+#endif
+    if (PF_TAG_PREFETCH == 1 || PF_TAG_PREFETCH == 2) {  // both home tags in flight together
         ht_f = ld_relaxed(fine.tags + (hf.index & static_cast<uint64_t>(fine.capacity - 1)));
         if (has_coarse)
             ht_c = ld_relaxed(coarse.tags + (hc.index & static_cast<uint64_t>(coarse.capacity - 1)));
