@@ -36,7 +36,8 @@ EXPORTS = ("pf_abi_version", "pf_last_error", "pf_device_sm_count", "pf_accumula
            "pf_shard_apply", "pf_shard_publish", "pf_replica_update", "pf_shard_reset",
            "pf_resolve_replica", "pf_trace_paths", "pf_sincos", "pf_segment_deltas",
            "pf_begin_frame_checked", "pf_prepare_config", "pf_build_id",
-           "pf_host_register", "pf_host_unregister", "pf_accumulate_table")
+           "pf_host_register", "pf_host_unregister", "pf_accumulate_table",
+           "pf_set_l2_persisting", "pf_pixel_tiles")
 
 _BUILD_TAG = b"PF_BUILD_ID="
 
@@ -139,7 +140,7 @@ class PfFrameBuffers(ctypes.Structure):
                 ("eff_records", ctypes.c_void_p),
                 ("flat", ctypes.c_void_p), ("work", ctypes.c_void_p),
                 ("work_count", ctypes.c_void_p), ("fallback_keys", ctypes.c_void_p),
-                ("phase_events", ctypes.c_void_p * 4)]
+                ("phase_events", ctypes.c_void_p * 4), ("tiles", ctypes.c_void_p)]
 
 
 class PfShard(ctypes.Structure):
@@ -209,6 +210,7 @@ STAT_BAD_PIXELS = 10
 STAT_SHARD_RECORDS = 11
 STAT_SHARD_REQUESTS = 12
 STAT_HIST_BASE = 16
+TILE_PIXELS, TILE_SEGS = 512, 8  # PF_TILE_PIXELS, PF_TILE_SEGS
 STAT_COUNT = 16 + 256
 
 _lib = None
@@ -267,6 +269,8 @@ def lib() -> ctypes.CDLL:
     L.pf_prepare_config.argtypes = [vp, vp]
     L.pf_host_register.argtypes = [vp, i64]
     L.pf_host_unregister.argtypes = [vp]
+    L.pf_set_l2_persisting.argtypes = [i64, vp]
+    L.pf_pixel_tiles.argtypes = [vp, i64, i64, vp, i64, vp]
     L.pf_segment_deltas.argtypes = [vp, vp, i64, vp, vp, dbl, vp, vp]
     L.pf_begin_frame_checked.argtypes = [vp, vp, i64, i32, dbl, dbl, i32, vp, vp, vp, i64, vp,
                                          vp]
@@ -275,6 +279,22 @@ def lib() -> ctypes.CDLL:
             getattr(L, name).restype = ctypes.c_int
     _lib = L
     return L
+
+
+_l2_done: dict = {}
+
+
+def configure_l2() -> int:
+    """Once per device: set aside L2 for evict_last lines (pf_set_l2_persisting).
+    PF_L2_PERSIST_MB overrides the size (-1: the device maximum, 0: none)."""
+    dev = torch.cuda.current_device()
+    if dev in _l2_done:
+        return _l2_done[dev]
+    mb = int(os.environ.get("PF_L2_PERSIST_MB", "32"))
+    got = ctypes.c_int64(0)
+    call("pf_set_l2_persisting", mb if mb < 0 else mb << 20, ctypes.byref(got))
+    _l2_done[dev] = got.value
+    return got.value
 
 
 def require_cuda() -> torch.device:

@@ -76,6 +76,21 @@ int pf_prepare_config(const pf_config *in, pf_config *out) {
     return pf::prepare_config("pf_prepare_config", in, out);
 }
 
+int pf_set_l2_persisting(int64_t bytes, int64_t *applied) {
+    int dev = 0, maxp = 0;
+    if (cudaGetDevice(&dev) != cudaSuccess ||
+        cudaDeviceGetAttribute(&maxp, cudaDevAttrMaxPersistingL2CacheSize, dev) != cudaSuccess)
+        return pf::check_launch("pf_set_l2_persisting");
+    size_t want = bytes < 0 ? static_cast<size_t>(maxp)
+                            : static_cast<size_t>(bytes < maxp ? bytes : maxp);
+    if (cudaDeviceSetLimit(cudaLimitPersistingL2CacheSize, want) != cudaSuccess)
+        return pf::check_launch("pf_set_l2_persisting");
+    size_t got = 0;
+    cudaDeviceGetLimit(&got, cudaLimitPersistingL2CacheSize);
+    if (applied) *applied = static_cast<int64_t>(got);
+    return PF_OK;
+}
+
 int pf_host_register(void *ptr, int64_t bytes) {
     if (ptr == nullptr || bytes <= 0) return pf::fail_arg("pf_host_register", "empty buffer");
     const cudaError_t e = cudaHostRegister(ptr, static_cast<size_t>(bytes), cudaHostRegisterDefault);

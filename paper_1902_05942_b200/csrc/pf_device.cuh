@@ -505,6 +505,22 @@ __device__ __forceinline__ uint64_t l2_evict_last() {
     asm volatile("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;" : "=l"(p));
     return p;
 }
+__device__ __forceinline__ uint64_t l2_evict_normal() {
+    uint64_t p;
+    asm volatile("createpolicy.fractional.L2::evict_normal.b64 %0, 1.0;" : "=l"(p));
+    return p;
+}
+// Policy for the insert's table REDs / the resolve's composite REDs (0 normal,
+// 1 evict_last, 2 evict_first).
+#ifndef PF_TABLE_RED_POLICY
+#define PF_TABLE_RED_POLICY 1
+#endif
+#ifndef PF_FLAT_POLICY
+#define PF_FLAT_POLICY 1
+#endif
+__device__ __forceinline__ uint64_t l2_policy(int k) {
+    return k == 1 ? l2_evict_last() : k == 2 ? l2_evict_first() : l2_evict_normal();
+}
 __device__ __forceinline__ double ld_stream(const double *p, uint64_t pol) {
     double d;
     asm volatile("ld.global.nc.L1::no_allocate.L2::cache_hint.f64 %0, [%1], %2;"

@@ -89,7 +89,7 @@ __device__ __forceinline__ LaneInsert warp_insert_sums(const pf_table &t, bool v
         r = probe_insert(t, idx, fp, home_tag, group_weight);
         if (r.status != 2) {
             const int64_t s = r.slot;
-            const uint64_t keep = l2_evict_last();
+            const uint64_t keep = l2_policy(PF_TABLE_RED_POLICY);
 #pragma unroll
             for (int c = 0; c < 3; ++c) {
                 if (FIXED)
@@ -141,7 +141,7 @@ __device__ __forceinline__ LaneInsert lane_insert(const pf_table &t, bool valid,
     const InsertResult r = probe_insert(t, idx, fp, home_tag, 1ull);
     if (r.status != 2) {
         const int64_t s = r.slot;
-        const uint64_t keep = l2_evict_last();
+        const uint64_t keep = l2_policy(PF_TABLE_RED_POLICY);
 #pragma unroll
         for (int c = 0; c < 3; ++c) {
             if (FIXED)
