@@ -269,8 +269,6 @@ typedef struct pf_frame_buffers {
     int64_t *fallback_keys;         /* 8 * n, or NULL (see pf_resolve_frame) */
     void *phase_events[4];          /* optional cudaEvent_t recorded at frame start, just
                                        before the insert kernel, after it, at frame end */
-    int64_t *tiles;                 /* pf_pixel_tiles plan of THIS stream whose status word
-                                       was 0, or NULL (the flat-buffer composite) */
 } pf_frame_buffers;
 
 /* One whole frame of the filter -- src/pipeline.py:321-363 (render_frame) minus the
@@ -282,21 +280,6 @@ int pf_filter_frame(const pf_config *cfg, const pf_vertices *v, const pf_table *
                     uint64_t stream_base_lookup, uint64_t stream_base_coarse, int64_t spp,
                     const double *base_image, int64_t n_pixels, double *image, uint8_t *source,
                     double *chosen, const pf_frame_buffers *buffers, void *stream);
-
-/* Pixel-tile plan of a stream for pf_filter_frame's tile-mode resolve: tiles of
- * PF_TILE_PIXELS pixels; a segment is a maximal range of consecutive rows whose pixels lie
- * in one tile and do not decrease (a stream made of a few pixel-ordered runs -- the
- * multi-bounce stream, one run per select_k -- has <= runs segments per tile).
- * plan needs 2 + ceil(n_pixels / PF_TILE_PIXELS) * (2 + 2 * PF_TILE_SEGS) words.
- * plan[0] (read by the host) is 0 when the stream is tileable: every pixel inside
- * [0, n_pixels) and <= PF_TILE_SEGS segments per tile.  Tile mode then resolves each
- * tile in one CTA and writes image = base + (sum over its rows) / spp directly: no
- * composite buffer, memset, L2 reductions or finalize pass. */
-#define PF_TILE_LOG2 9
-#define PF_TILE_PIXELS (1 << PF_TILE_LOG2)
-#define PF_TILE_SEGS 8
-int pf_pixel_tiles(const int64_t *pixel, int64_t n, int64_t n_pixels, int64_t *plan,
-                   int64_t plan_words, void *stream);
 
 /* image = base + flat / spp over n_pixels RGB pixels (the last line of
  * src/pipeline.py:282-283). */

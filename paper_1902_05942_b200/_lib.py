@@ -37,7 +37,7 @@ EXPORTS = ("pf_abi_version", "pf_last_error", "pf_device_sm_count", "pf_accumula
            "pf_resolve_replica", "pf_trace_paths", "pf_sincos", "pf_segment_deltas",
            "pf_begin_frame_checked", "pf_prepare_config", "pf_build_id",
            "pf_host_register", "pf_host_unregister", "pf_accumulate_table",
-           "pf_set_l2_persisting", "pf_pixel_tiles")
+           "pf_set_l2_persisting")
 
 _BUILD_TAG = b"PF_BUILD_ID="
 
@@ -140,7 +140,7 @@ class PfFrameBuffers(ctypes.Structure):
                 ("eff_records", ctypes.c_void_p),
                 ("flat", ctypes.c_void_p), ("work", ctypes.c_void_p),
                 ("work_count", ctypes.c_void_p), ("fallback_keys", ctypes.c_void_p),
-                ("phase_events", ctypes.c_void_p * 4), ("tiles", ctypes.c_void_p)]
+                ("phase_events", ctypes.c_void_p * 4)]
 
 
 class PfShard(ctypes.Structure):
@@ -210,7 +210,6 @@ STAT_BAD_PIXELS = 10
 STAT_SHARD_RECORDS = 11
 STAT_SHARD_REQUESTS = 12
 STAT_HIST_BASE = 16
-TILE_PIXELS, TILE_SEGS = 512, 8  # PF_TILE_PIXELS, PF_TILE_SEGS
 STAT_COUNT = 16 + 256
 
 _lib = None
@@ -270,7 +269,6 @@ def lib() -> ctypes.CDLL:
     L.pf_host_register.argtypes = [vp, i64]
     L.pf_host_unregister.argtypes = [vp]
     L.pf_set_l2_persisting.argtypes = [i64, vp]
-    L.pf_pixel_tiles.argtypes = [vp, i64, i64, vp, i64, vp]
     L.pf_segment_deltas.argtypes = [vp, vp, i64, vp, vp, dbl, vp, vp]
     L.pf_begin_frame_checked.argtypes = [vp, vp, i64, i32, dbl, dbl, i32, vp, vp, vp, i64, vp,
                                          vp]

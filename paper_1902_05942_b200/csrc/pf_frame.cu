@@ -280,10 +280,6 @@ struct ResolveArgs {
     int64_t pixel_base;        // first pixel of flat (0 unless a rank composites a band)
     uint64_t seg_mask;         // probe-window segment (~0: plain table; replica: slice - 1)
     const ulonglong4 *crec;    // per-slot effective records of the coarse table (or NULL)
-    const int64_t *tiles;      // pixel-tile plan (pf_pixel_tiles) in tile mode, else NULL
-    double *image;             // tile mode: the image itself (composite adds x / spp)
-    const double *base_image;  // tile mode: base + tile sum / spp
-    double spp;
 };
 
 // The coarse table's effective value of slot s.
@@ -360,10 +356,7 @@ __device__ __forceinline__ void composite(const ResolveArgs &a, int64_t i, int64
 #pragma unroll
         for (int c = 0; c < 3; ++c) {
             const double tp = ld_stream(a.v.throughput + 3 * i + c, stream);
-            if (a.image != nullptr)  // tile mode: image = base + (tile sum) / spp already
-                red_add_f64(a.image + 3 * pixel + c, ddiv(dmul(tp, chosen[c]), a.spp), keep);
-            else
-                red_add_f64(a.flat + 3 * pixel + c, dmul(tp, chosen[c]), keep);
+            red_add_f64(a.flat + 3 * pixel + c, dmul(tp, chosen[c]), keep);
         }
     }
     if (a.source) a.source[i] = static_cast<uint8_t>(source);
@@ -480,163 +473,6 @@ __global__ void __launch_bounds__(kThreads, PF_RESOLVE_MIN_BLOCKS) resolve_main_
                 atomicAdd(reinterpret_cast<unsigned long long *>(a.stats + PF_STAT_BAD_PIXELS),
                           static_cast<unsigned long long>(__popc(b)));
         }
-    }
-}
-
-// ------------------------------------------------------------------ pixel tiles
-//
-// A stream whose rows come in a few pixel-ordered runs (the multi-bounce stream: one run
-// per select_k) is resolved by pixel tile: CTA t takes every row whose pixel lies in
-// [t T, (t + 1) T), sums their composite terms in shared memory and writes
-// image = base + sum / spp for its T pixels itself -- no flat buffer, no memset, no L2
-// REDs, no finalize pass.  Rows that go to the work list are composited later by the
-// fallback rung, which adds x / spp to the image (one vertex per pixel: bit for bit the
-// reference's base + flat / spp; several: within float reordering, as the RED order
-// already is).
-//
-// Plan (pf_pixel_tiles, once per stream): a segment is a maximal range of consecutive
-// rows with pixels in one tile and non-decreasing.  plan[0] != 0: the stream is not
-// tileable (a pixel outside the image, or a tile with more than kTileSegs segments);
-// tile t at plan + 2 + t * kTileWords holds [start count, end count, kTileSegs starts,
-// kTileSegs ends] in arrival order.
-constexpr int kTileLog2 = PF_TILE_LOG2;
-constexpr int64_t kTilePixels = int64_t(1) << kTileLog2;
-constexpr int kTileSegs = PF_TILE_SEGS;
-constexpr int kTileWords = 2 + 2 * kTileSegs;
-
-__global__ void __launch_bounds__(kThreads) pixel_tiles_kernel(const int64_t *__restrict__ pixel,
-                                                               int64_t n, int64_t n_pixels,
-                                                               int64_t *plan) {
-    const int64_t stride = static_cast<int64_t>(gridDim.x) * blockDim.x;
-    unsigned long long *bad = reinterpret_cast<unsigned long long *>(plan);
-    for (int64_t i = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x; i <= n;
-         i += stride) {
-        const int64_t p = i < n ? __ldg(pixel + i) : -1;
-        if (i < n && (p < 0 || p >= n_pixels)) {
-            atomicOr(bad, 1ull);
-            continue;
-        }
-        const int64_t q = i > 0 ? __ldg(pixel + i - 1) : -1;
-        const bool q_ok = q >= 0 && q < n_pixels;
-        const int64_t t = p >> kTileLog2, tq = q >> kTileLog2;
-        // a segment ends at i (the previous row's) / starts at i (this row's)
-        const bool boundary = i == 0 || i == n || t != tq || p < q;
-        if (!boundary) continue;
-        if (i < n) {
-            int64_t *w = plan + 2 + t * kTileWords;
-            const unsigned long long k = atomicAdd(reinterpret_cast<unsigned long long *>(w), 1ull);
-            if (k < static_cast<unsigned long long>(kTileSegs)) w[2 + k] = i;
-            else atomicOr(bad, 2ull);
-        }
-        if (i > 0 && q_ok) {
-            int64_t *w = plan + 2 + tq * kTileWords;
-            const unsigned long long k = atomicAdd(reinterpret_cast<unsigned long long *>(w + 1), 1ull);
-            if (k < static_cast<unsigned long long>(kTileSegs)) w[2 + kTileSegs + k] = i;
-            else atomicOr(bad, 2ull);
-        }
-    }
-}
-
-// Rung 1 of every row of one pixel tile (see above): resolve_main_kernel's per-row
-// recipe with the composite summed in shared memory.  (Software-pipelining the next
-// pass's stream loads spills at the 64-register cap: resolve 0.338 -> 0.388 ms; at 3
-// CTAs per SM 0.347.)
-#ifndef PF_TILE_MIN_BLOCKS
-#define PF_TILE_MIN_BLOCKS 4
-#endif
-__global__ void __launch_bounds__(kThreads, PF_TILE_MIN_BLOCKS) resolve_tile_kernel(ResolveArgs a) {
-    __shared__ double acc[kTilePixels * 3];
-    __shared__ int64_t seg_start[kTileSegs], seg_len[kTileSegs];
-    __shared__ int n_seg;
-    const pf_config &cfg = a.cfg;
-    const uint64_t stream = l2_evict_first();
-    const uint64_t fmask = static_cast<uint64_t>(a.fine.capacity) - 1;
-    const int64_t t = blockIdx.x;
-    const int64_t p0 = t << kTileLog2;
-    const int64_t np = a.n_pixels - p0 < kTilePixels ? a.n_pixels - p0 : kTilePixels;
-    for (int k = threadIdx.x; k < kTilePixels * 3; k += kThreads) acc[k] = 0.0;
-    if (threadIdx.x == 0) {  // pair the tile's segment starts with their ends (sorted)
-        const int64_t *w = a.tiles + 2 + t * kTileWords;
-        const int ns = static_cast<int>(w[0] < kTileSegs ? w[0] : kTileSegs);
-        int64_t st[kTileSegs], en[kTileSegs];
-        for (int k = 0; k < ns; ++k) {
-            const int64_t x = w[2 + k], y = w[2 + kTileSegs + k];
-            int j = k;
-            while (j > 0 && st[j - 1] > x) { st[j] = st[j - 1]; --j; }
-            st[j] = x;
-            j = k;
-            while (j > 0 && en[j - 1] > y) { en[j] = en[j - 1]; --j; }
-            en[j] = y;
-        }
-        for (int k = 0; k < ns; ++k) {
-            seg_start[k] = st[k];
-            seg_len[k] = en[k] - st[k];
-        }
-        n_seg = ns;
-    }
-    __syncthreads();
-    const int ns = n_seg;
-    int64_t m = 0;
-    for (int k = 0; k < ns; ++k) m += seg_len[k];
-    const bool as_int = eff_is_int(a.fine, cfg.temporal_mode);
-    const bool fixed = a.fine.sum_mode == PF_SUM_FIXED;
-    for (int64_t j0 = 0; j0 < m; j0 += kThreads) {
-        const int64_t j = j0 + threadIdx.x;
-        const bool valid = j < m;
-        int64_t row = a.v.n - 1;  // tail lanes shadow the last vertex
-        if (valid) {
-            int64_t r = j;
-            int k = 0;
-            while (r >= seg_len[k]) { r -= seg_len[k]; ++k; }
-            row = seg_start[k] + r;
-        }
-        const CellHash h = unpack_lookup_key(ld_stream(a.lk_keys + row, stream));
-        const int64_t pixel = ld_stream(a.v.pixel + row, stream);
-        double tp[3];
-#pragma unroll
-        for (int c = 0; c < 3; ++c) tp[c] = ld_stream(a.v.throughput + 3 * row + c, stream);
-        const uint64_t tag = __ldg(reinterpret_cast<const unsigned long long *>(a.fine.tags) +
-                                   (h.index & fmask));
-        int64_t slot;
-        if (tag == kEmptyTag) slot = -1;
-        else if ((tag & kFpMask) == h.fp) slot = static_cast<int64_t>(h.index & fmask);
-        else slot = probe_lookup(a.fine.tags, fmask, a.fine.probe_limit, h.index, h.fp, a.seg_mask);
-        bool fine_ok = false;
-        if (slot >= 0) {
-            const Effective e = fine_effective(a, slot);
-            const double cnt = e.fcnt;
-            if (valid && cnt >= a.thr) {
-                fine_ok = true;
-                double mm[3];
-                const double sums[3] = {eff_sum_f64(e, as_int, 0), eff_sum_f64(e, as_int, 1),
-                                        eff_sum_f64(e, as_int, 2)};
-                row_mean3(sums, cnt, fixed, mm);
-                const int64_t px = pixel - p0;
-#pragma unroll
-                for (int c = 0; c < 3; ++c) atomicAdd(&acc[3 * px + c], dmul(tp[c], mm[c]));
-                if (a.source) a.source[row] = 0;
-                if (a.chosen) {
-#pragma unroll
-                    for (int c = 0; c < 3; ++c) a.chosen[3 * row + c] = mm[c];
-                }
-            }
-        }
-        const bool need = valid && !fine_ok;
-        const unsigned msk = __ballot_sync(kFull, need);
-        if (msk) {
-            unsigned long long wb = 0;
-            const int lane = threadIdx.x & 31;
-            if (lane == __ffs(msk) - 1)
-                wb = atomicAdd(reinterpret_cast<unsigned long long *>(a.work_count),
-                               static_cast<unsigned long long>(__popc(msk)));
-            wb = __shfl_sync(kFull, wb, __ffs(msk) - 1);
-            if (need) a.work[static_cast<int64_t>(wb) + __popc(msk & ((1u << lane) - 1u))] = row;
-        }
-    }
-    __syncthreads();
-    for (int64_t k = threadIdx.x; k < 3 * np; k += kThreads) {
-        const int64_t g = 3 * p0 + k;
-        a.image[g] = dadd(__ldg(a.base_image + g), ddiv(acc[k], a.spp));
     }
 }
 
@@ -893,10 +729,7 @@ finalize_image_kernel(const double *__restrict__ base, const double *__restrict_
 // ladder + composite.
 static int launch_rungs(const char *fn, const ResolveArgs &a, int64_t n, bool have_keys,
                         bool have_fb_keys, cudaStream_t st) {
-    if (a.tiles != nullptr)  // tile mode: one CTA per pixel tile, the image written directly
-        resolve_tile_kernel<<<static_cast<unsigned>((a.n_pixels + kTilePixels - 1) >> kTileLog2),
-                              kThreads, 0, st>>>(a);
-    else if (have_keys)
+    if (have_keys)
         resolve_main_kernel<kResolveKV, true>
             <<<blocks_for(n, kThreads * kResolveKV), kThreads, 0, st>>>(a);
     else
@@ -976,8 +809,7 @@ static int resolve_frame(const char *fn, const pf_config *cfg, const pf_vertices
                          int64_t n_pixels, double *image, double *flat, int64_t *work,
                          int64_t *work_count, uint8_t *source, double *chosen, int64_t *stats,
                          const uint64_t *lookup_keys, uint64_t *eff_records,
-                         int64_t *fallback_keys, int64_t touch_frame, void *stream,
-                         const int64_t *tiles = nullptr) {
+                         int64_t *fallback_keys, int64_t touch_frame, void *stream) {
     if (int rc = validate_vertices(fn, v, cfg)) return rc;
     pf_config kc;
     if (int rc = prepare_config(fn, cfg, &kc)) return rc;
@@ -990,9 +822,7 @@ static int resolve_frame(const char *fn, const pf_config *cfg, const pf_vertices
     if (v->n > 0 && (!v->throughput || !v->contribution || !work || !work_count))
         return fail_arg(fn, "throughput/contribution/work is NULL");
     cudaStream_t st = as_stream(stream);
-    // tile mode (pf_pixel_tiles plan, keys from the insert): the tiles write the image
-    const bool tiled = tiles != nullptr && lookup_keys != nullptr && v->n > 0;
-    if (!tiled && cudaMemsetAsync(flat, 0, sizeof(double) * 3 * n_pixels, st) != cudaSuccess)
+    if (cudaMemsetAsync(flat, 0, sizeof(double) * 3 * n_pixels, st) != cudaSuccess)
         return check_launch(fn);
     if (v->n > 0) {
         if (cudaMemsetAsync(work_count, 0, sizeof(int64_t), st) != cudaSuccess)
@@ -1019,17 +849,13 @@ static int resolve_frame(const char *fn, const pf_config *cfg, const pf_vertices
         a.pixel_base = 0;
         a.seg_mask = ~0ull;
         a.crec = nullptr;
-        a.tiles = tiled ? tiles : nullptr;
-        a.image = tiled ? image : nullptr;
-        a.base_image = base_image;
-        a.spp = static_cast<double>(spp);
         if (int rc = launch_post_insert(fn, *fine, coarse, kc, eff_records, touch_frame, st))
             return rc;
         if (int rc = launch_rungs(fn, a, v->n, lookup_keys != nullptr, fallback_keys != nullptr, st))
             return rc;
     }
     const int64_t m = 3 * n_pixels;
-    if (m > 0 && !tiled)
+    if (m > 0)
         finalize_image_kernel<<<blocks_for(m, kThreads), kThreads, 0, st>>>(
             base_image, flat, image, m, static_cast<double>(spp));
     return check_launch(fn);
@@ -1115,28 +941,7 @@ int pf_resolve_replica(const pf_config *cfg, const pf_vertices *v, const pf_repl
     a.pixel_base = pixel_base;
     a.seg_mask = (1ull << rp->slice_log2) - 1;
     a.crec = reinterpret_cast<const ulonglong4 *>(rp->coarse_records);
-    a.tiles = nullptr;
-    a.image = nullptr;
-    a.base_image = nullptr;
-    a.spp = 1.0;
     return launch_rungs(fn, a, v->n, true, true, st);
-}
-
-int pf_pixel_tiles(const int64_t *pixel, int64_t n, int64_t n_pixels, int64_t *plan,
-                   int64_t plan_words, void *stream) {
-    const char *fn = "pf_pixel_tiles";
-    const int64_t n_tiles = (n_pixels + kTilePixels - 1) >> kTileLog2;
-    if (n < 0 || n_pixels < 0 || (n > 0 && !pixel) || !plan || plan_words < 2 + n_tiles * kTileWords)
-        return fail_arg(fn, "bad pixel array / plan size");
-    cudaStream_t st = as_stream(stream);
-    if (cudaMemsetAsync(plan, 0, sizeof(int64_t) * (2 + n_tiles * kTileWords), st) != cudaSuccess)
-        return check_launch(fn);
-    if (n == 0 || n_pixels == 0) return PF_OK;
-    const int64_t g = (n + kThreads) / kThreads;
-    const int64_t cap = static_cast<int64_t>(sm_count()) * 8;
-    pixel_tiles_kernel<<<static_cast<unsigned>(g < cap ? g : cap), kThreads, 0, st>>>(
-        pixel, n, n_pixels, plan);
-    return check_launch(fn);
 }
 
 int pf_finalize_image(const double *base_image, const double *flat, double *image,
@@ -1185,7 +990,7 @@ int pf_filter_frame(const pf_config *cfg, const pf_vertices *v, const pf_table *
     const int rc = resolve_frame(fn, cfg, v, fine, coarse, stream_base_lookup, stream_base_coarse,
                                  spp, base_image, n_pixels, image, b->flat, b->work,
                                  b->work_count, source, chosen, b->res_stats, b->lookup_keys,
-                                 b->eff_records, b->fallback_keys, frame, stream, b->tiles);
+                                 b->eff_records, b->fallback_keys, frame, stream);
     mark(3);
     return rc;
 }

@@ -12,7 +12,6 @@ coarse voxel -> any neighbourhood / coarse samples -> unfiltered contribution.
 from __future__ import annotations
 
 import ctypes
-import os
 from dataclasses import dataclass, field
 
 import numpy as np
@@ -263,24 +262,6 @@ class FrameState:
         coarse = VoxelTable.from_config(cfg, backend, ordered) if cfg.multi_level else None
         return cls(fine, coarse)
 
-    def pixel_tiles(self, vs, n_pixels: int):
-        """The stream's pf_pixel_tiles plan, or None when the stream is not tileable.
-        Recomputed (one small kernel and one status read) only when the pixel array --
-        its storage, length or in-place version -- or the image size changes; every
-        frame over the same stream reuses it."""
-        px = vs.pixel
-        key = (px.data_ptr(), int(px.numel()), px._version, int(n_pixels))
-        if self.scratch.get("_tiles_key") != key:
-            n_tiles = -(-int(n_pixels) // _lib.TILE_PIXELS)
-            words = 2 + n_tiles * (2 + 2 * _lib.TILE_SEGS)
-            buf = self.buffer("tiles", (words,), torch.int64)
-            _lib.call("pf_pixel_tiles", px.data_ptr(), int(px.numel()), int(n_pixels),
-                      buf.data_ptr(), words, _lib.stream_handle())
-            ok = int(buf[0].item()) == 0 and int(px.numel()) > 0
-            self.scratch["_tiles_key"] = key
-            self.scratch["_tiles_plan"] = buf if ok else None
-        return self.scratch["_tiles_plan"]
-
     def buffer(self, name: str, shape, dtype) -> torch.Tensor:
         """Reusable device scratch (caching allocator friendly, no per-frame memsets)."""
         n = int(np.prod(shape))
@@ -487,9 +468,6 @@ def resolve_phase(vertices, cfg: FilterConfig, state: FrameState, frame: int, se
     return image, report
 
 
-_NO_TILES = os.environ.get("PF_NO_TILES") == "1"   # A/B switch: the flat-buffer composite
-
-
 def _fused_frame(vs: VertexStream, base_image, cfg: FilterConfig, state: FrameState, frame: int,
                  spp: int, seed: int, validate: bool, want_means: bool, phase_events=None):
     n = len(vs)
@@ -520,7 +498,6 @@ def _fused_frame(vs: VertexStream, base_image, cfg: FilterConfig, state: FrameSt
     b.work = state.buffer("work", (max(n, 1),), torch.int64).data_ptr()
     b.work_count = state.buffer("work_count", (1,), torch.int64).data_ptr()
     b.fallback_keys = state.buffer("fallback_keys", (max(n, 1), 8), torch.int64).data_ptr()
-    b.tiles = _lib.ptr(state.pixel_tiles(vs, h * w)) if not _NO_TILES else None
     if phase_events is not None:  # torch.cuda.Events recorded inside the C call
         for k, e in enumerate(phase_events):
             b.phase_events[k] = e.cuda_event

@@ -113,38 +113,3 @@ def test_keys_across_lod_thresholds(gpu, stages, delta):
         assert np.array_equal(k[f], stages[f"near{delta}_{f}"]), f
     assert np.array_equal(k["jittered"], stages[f"near{delta}_jittered"], equal_nan=True)
 
-
-@pytest.mark.parametrize("shuffle", [False, True])
-def test_tile_mode_resolve_equals_flat_composite(gpu, monkeypatch, shuffle):
-    """The tile-mode resolve (pf_pixel_tiles plan; CTA per pixel tile, image written
-    directly) and the flat-buffer composite give identical sources, means and tables and
-    images within float reordering; a shuffled stream is not tileable and takes the
-    flat path."""
-    from paper_1902_05942_b200 import pipeline
-    from paper_1902_05942_b200.scene import closed_box
-    from paper_1902_05942_b200.streams import camera_footprint
-    from paper_1902_05942_b200.tracer import multi_bounce_stream
-    w, h = 200, 120
-    vs, base = multi_bounce_stream(closed_box(w, h), 4, 1)
-    if shuffle:
-        perm = torch.randperm(len(vs), generator=torch.Generator().manual_seed(3)).to(vs.pixel.device)
-        vs = gpu.VertexStream(**{f: getattr(vs, f)[perm] for f in (
-            "position", "normal", "omega_r", "contribution", "throughput", "pixel", "sample",
-            "layer_id", "camera_distance")})
-    cap = 1 << (2 * w * h - 1).bit_length()
-    cfg = gpu.FilterConfig(capacity=cap, footprint_scale=camera_footprint(h))
-    out = {}
-    for tiled in (True, False):
-        monkeypatch.setattr(pipeline, "_NO_TILES", not tiled)
-        state = gpu.FrameState.from_config(cfg)
-        for f in range(3):
-            img, rep, _ = gpu.filter_frame(vs, base, cfg, state, 1, 7 + f)
-        plan = state.pixel_tiles(vs, w * h)
-        out[tiled] = (img.cpu().numpy(), rep.source.cpu().numpy(), rep.means.cpu().numpy(),
-                      state.fine.state(), plan)
-    assert (out[True][4] is None) == shuffle
-    assert np.array_equal(out[True][1], out[False][1])
-    assert np.array_equal(out[True][2], out[False][2])
-    from test_gpu_parity import canon
-    assert canon(out[True][3]) == canon(out[False][3])
-    np.testing.assert_allclose(out[True][0], out[False][0], rtol=1e-12, atol=1e-300)
