@@ -116,6 +116,10 @@ class ShardedState:
         self.entries = torch.empty((n_local, 6), dtype=torch.int64, device=dev)
         self.entry_count = torch.zeros(1, dtype=torch.int64, device=dev)
         self.prev_gathered = None  # (entries [world * stride, 6], counts [world], stride)
+        # every rank's published entry count of the last frame, copied to pinned host
+        # memory behind the frame's gather (read once the next frame's count exchange
+        # has synchronised, i.e. after it has landed)
+        self.prev_entry_counts = torch.zeros(world, dtype=torch.int64).pin_memory()
         self.scratch: dict = {}
         self.regrows = 0
 
@@ -172,7 +176,8 @@ class ShardedState:
 
 
 def _stats_message(st: ShardedState) -> torch.Tensor:
-    """[world, 3] int64 per destination: records, overflow, bad input."""
+    """[world, 3] int64 per destination: records, overflow, bad input (all-gathered: every
+    rank sees the whole [world, world, 3] send matrix)."""
     cols = [st.owner_counts[0], st.overflow.to(torch.int64).expand(st.world),
             st.bad_flag.to(torch.int64).expand(st.world)]
     return torch.stack(cols, dim=1).contiguous()
@@ -236,7 +241,9 @@ def filter_frame_sharded(vertices, base_image, cfg: FilterConfig, st: ShardedSta
     if st.coarse is not None:
         st.coarse.frame = frame
 
-    # ---- insert: pre-aggregated records to their owners
+    # ---- insert: pre-aggregated records to their owners.  The counts go by all-gather, so
+    # every rank knows every rank's incoming record count: with last frame's entry counts
+    # that bounds this frame's published entries, and the publish needs no second sync.
     while True:
         sh = st.c_shard()
         _lib.call("pf_shard_keys", ctypes.byref(cc), ctypes.byref(v), ctypes.byref(sh), has_coarse,
@@ -246,25 +253,27 @@ def filter_frame_sharded(vertices, base_image, cfg: FilterConfig, st: ShardedSta
         _lib.call("pf_shard_emit", ctypes.byref(sh), st.send_records.data_ptr(),
                   st.send_requests.data_ptr(), stream)
         msg = _stats_message(st)
-        recv = yield Exchange(msg, [1] * G, [1] * G)
-        mine, theirs = msg.cpu().numpy(), recv.cpu().numpy()
-        if theirs[:, 2].any():
+        allm = (yield AllGather(msg)).reshape(G, G, 3).cpu().numpy()  # the frame's one sync
+        if allm[:, :, 2].any():
             _lib.call("pf_shard_reset", ctypes.byref(sh), stream)
             raise ValueError("contributions must be finite and non-negative "
                              "(frame rejected on every rank; tables unchanged)")
-        if not theirs[:, 1].any():
+        if not allm[:, 0, 1].any():
             break
-        if mine[0, 1]:  # this rank overflowed: grow and redo its keys
+        if allm[st.rank, 0, 1]:  # this rank overflowed: grow and redo its keys
             st.grow_agg(int(st.n_distinct.item()))
         else:  # a peer overflowed: keep this rank's round, repeat the count exchange
             st.overflow.zero_()
+            msg = _stats_message(st)
             while True:
-                recv = yield Exchange(msg, [1] * G, [1] * G)
-                if not recv.cpu().numpy()[:, 1].any():
+                allm = (yield AllGather(msg)).reshape(G, G, 3).cpu().numpy()
+                if not allm[:, 0, 1].any():
                     break
-            theirs = recv.cpu().numpy()
             break
-    send_rec, recv_rec = mine[:, 0].tolist(), theirs[:, 0].tolist()
+    send_rec = allm[st.rank, :, 0].tolist()
+    recv_rec = allm[:, st.rank, 0].tolist()
+    # published entries of rank r <= its entries last frame + the records it receives
+    bound = int((st.prev_entry_counts.numpy() + allm[:, :, 0].sum(axis=0)).max())
     records = yield Exchange(st.send_records[:sum(send_rec)], send_rec, recv_rec)
     _lib.call("pf_shard_apply", ctypes.byref(sh), ctypes.byref(ft),
               ctypes.byref(ct) if ct is not None else None, records.data_ptr(),
@@ -276,9 +285,10 @@ def filter_frame_sharded(vertices, base_image, cfg: FilterConfig, st: ShardedSta
               ctypes.byref(ct) if ct is not None else None, st.entries.data_ptr(),
               st.entry_count.data_ptr(), stream)
     counts = yield AllGather(st.entry_count)
-    stride = int(counts.max().item()) if counts.numel() else 0
-    # every rank saw the same counts, so all skip an empty gather together
+    stride = min(bound, int(st.entries.shape[0]))  # >= every rank's count; same on all ranks
+    # every rank computed the same bound, so all skip an empty gather together
     gathered = (yield AllGather(st.entries[:stride])) if stride else st.entries[:0]
+    st.prev_entry_counts.copy_(counts, non_blocking=True)
     rp = st.c_replica()
     if st.prev_gathered is not None:
         pg, pc, ps = st.prev_gathered
