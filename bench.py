@@ -84,7 +84,7 @@ def make_stream(kind: str, rank: int = 0, device=None, world: int = 1, band: boo
 INSERT_BYTES_PER_VERTEX = 96      # position 24 + normal 24 + distance 8 + pixel 8 + sample 8 + contribution 24
 QUERY_BYTES_PER_VERTEX = 120      # + throughput 24
 QUERY_BYTES_PER_PIXEL = 48        # base image read 24 + filtered image write 24
-LAUNCHES_PER_STEP = 6             # begin_frame x2, check, insert_frame, resolve main, fallback, finalize -> see count below
+MARK_EVERY = 5                    # timed frames with phase events: 0, 5, 10, ...
 
 _REASON_BITS = {0x1: "gpu_idle", 0x2: "applications_clocks_setting", 0x4: "sw_power_cap",
                 0x8: "hw_slowdown", 0x10: "sync_boost", 0x20: "sw_thermal_slowdown",
@@ -490,10 +490,13 @@ def run_b200(args):
     if world > 1:
         dist.barrier()
     torch.cuda.synchronize()
-    # the phase events of every timed frame, created and materialised (one record each)
-    # before the timed region, so inside it only the C call's own records remain
-    marks = [tuple(ev() for _ in range(4)) for _ in range(args.steps)]
-    for m in marks:
+    # phase events on every MARK_EVERY-th timed frame (4 event records cost a frame
+    # ~17 us: they break the kernels' programmatic-launch overlap), created and
+    # materialised (one record each) before the timed region, so inside it only the C
+    # call's own records remain
+    marked = [k for k in range(args.steps) if k % MARK_EVERY == 0]
+    marks = {k: tuple(ev() for _ in range(4)) for k in marked}
+    for m in marks.values():
         for e in m:
             e.record()
     torch.cuda.synchronize()
@@ -501,7 +504,7 @@ def run_b200(args):
     t_wall0 = time.time()
     start.record()
     for k in range(args.steps):
-        step(args.warmup + k, marks[k])
+        step(args.warmup + k, marks.get(k))
     stop.record()
     torch.cuda.synchronize()
     t_wall1 = time.time()
@@ -517,7 +520,7 @@ def run_b200(args):
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         t_max = float(t.item())
     names = list(phases)
-    for e0, e1, e2, e3 in marks:
+    for e0, e1, e2, e3 in marks.values():
         phases[names[0]].append(e0.elapsed_time(e1))
         phases[names[1]].append(e1.elapsed_time(e2))
         phases[names[2]].append(e2.elapsed_time(e3))
@@ -575,11 +578,11 @@ def run_b200(args):
 
     in_bytes = QUERY_BYTES_PER_VERTEX * n + QUERY_BYTES_PER_PIXEL * n_pix
     if rank == 0:
-        # single: prologue, insert, effective records, resolve main, fallback keys, pool,
-        # finalize.  sharded: begin x2, check, keys, emit, apply, reset, publish x2,
-        # replica clear + write, resolve main, fallback keys, pool, finalize (NCCL kernels
-        # not counted)
-        launches = (7 if world == 1 else 15) * args.steps
+        # single: prologue, insert, zero (flat + work counter), effective records, resolve
+        # main, fallback keys, pool, finalize.  sharded: begin x2, check, keys, emit, apply,
+        # reset, publish x2, replica clear + write, resolve main, fallback keys, pool,
+        # finalize (NCCL kernels not counted)
+        launches = (8 if world == 1 else 15) * args.steps
         line = {
             "metric": METRIC, "value": value, "unit": "vertices/s", "n_gpus": world,
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms_per_step,

@@ -32,6 +32,26 @@ constexpr double kTwoPi = 6.283185307179586;            // 2.0 * math.pi (src/ke
 constexpr double kFixedScale = 65536.0;                 // src/table.py:38
 constexpr int kMaxLevel = 31;                           // src/keys.py:19
 
+// ------------------------------------------------------------------ PDL
+#ifndef PF_PDL
+#define PF_PDL 1
+#endif
+// The chain kernels of a frame (launch_pdl): wait for the previous kernel's completion
+// before reading what it wrote.  Single-wave (persistent) kernels also let the next
+// kernel's CTAs launch into the slots their finished CTAs free; a multi-wave kernel
+// must not (the waiting CTAs would take its later waves' slots), so its dependents
+// launch when its last CTA exits, which still saves the launch gap.
+__device__ __forceinline__ void pdl_wait() {
+#if PF_PDL
+    asm volatile("griddepcontrol.wait;" ::: "memory");
+#endif
+}
+__device__ __forceinline__ void pdl_trigger() {
+#if PF_PDL
+    asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
+#endif
+}
+
 // ------------------------------------------------------------------ slot fields
 // Addresses of slot s's fields (pf_table: SoA or the interleaved 128-byte record).
 __device__ __forceinline__ int64_t *cnt_at(const pf_table &t, int64_t s) {

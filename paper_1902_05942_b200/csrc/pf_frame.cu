@@ -90,10 +90,12 @@ insert_frame_kernel(pf_config cfg, pf_vertices v, pf_table fine, pf_table coarse
     __shared__ __align__(16) uint64_t home_pair[2][kThreads][2];  // fine / coarse home tag pairs
 #endif
 
-    if (abort_flag != nullptr && *abort_flag != 0) return;  // invalid input: no mutation
     stats_init(bs);
     stage_sincos_table(sincos_tab);
     stage_lod_dist(lod_dist, cfg);
+    pdl_wait();
+    pdl_trigger();
+    if (abort_flag != nullptr && *abort_flag != 0) return;  // invalid input: no mutation
     __syncthreads();
     // persistent: each block walks 256-vertex tiles; block counters flush once at exit
     const int64_t tiles = (v.n + kThreads - 1) / kThreads;
@@ -310,6 +312,8 @@ effective_records_kernel(pf_table t, int mode, double ema, double delta_max, ulo
                          pf_table coarse, int has_coarse, int64_t touch_frame,
                          unsigned nb_fine) {
     __shared__ SweepSmem<kThreads> q;
+    pdl_wait();  // multi-wave kernels do not trigger early: waiting dependents would take
+                 // the slots of their later waves
     if (blockIdx.x >= nb_fine) {
         const int64_t blk = blockIdx.x - nb_fine, nblk = gridDim.x - nb_fine;
         for_each_occupied<kThreads>(coarse.tags, coarse.capacity, q, blk, nblk,
@@ -336,9 +340,10 @@ static int launch_post_insert(const char *fn, const pf_table &fine, const pf_tab
     const unsigned nf = sweep_blocks<kThreads>(fine.capacity, sm_count());
     const bool tc = coarse != nullptr && touch_frame != kNoTouch;
     const unsigned nc = tc ? sweep_blocks<kThreads>(coarse->capacity, sm_count()) : 0u;
-    effective_records_kernel<<<nf + nc, kThreads, 0, st>>>(
-        fine, kc.temporal_mode, kc.ema_alpha, kc.delta_max,
-        reinterpret_cast<ulonglong4 *>(eff_records), tc ? *coarse : fine, tc, touch_frame, nf);
+    launch_pdl(effective_records_kernel, dim3(nf + nc), dim3(kThreads), st, fine,
+               kc.temporal_mode, kc.ema_alpha, kc.delta_max,
+               reinterpret_cast<ulonglong4 *>(eff_records), tc ? *coarse : fine,
+               static_cast<int>(tc), touch_frame, nf);
     return check_launch(fn);
 }
 
@@ -377,6 +382,7 @@ template <int KV, bool HAVE_KEYS>
 __global__ void __launch_bounds__(kThreads, PF_RESOLVE_MIN_BLOCKS) resolve_main_kernel(ResolveArgs a) {
     // no CTA counters and no barriers: the fine / fallback row counts follow from the
     // work list (main_row_counts in the next kernel), rows outside the image are rare
+    pdl_wait();
     const pf_config &cfg = a.cfg;
     const uint64_t stream = l2_evict_first(), keep = l2_policy(PF_FLAT_POLICY);
     const uint64_t fmask = static_cast<uint64_t>(a.fine.capacity) - 1;
@@ -493,6 +499,8 @@ __global__ void __launch_bounds__(kThreads) fallback_keys_kernel(ResolveArgs a) 
     __shared__ double lod_dist[32];
     stage_sincos_table(sincos_tab);
     stage_lod_dist(lod_dist, a.cfg);
+    pdl_wait();
+    pdl_trigger();
     __syncthreads();
     const pf_config &cfg = a.cfg;
     const int64_t n_work = *a.work_count;
@@ -531,6 +539,8 @@ __global__ void __launch_bounds__(kThreads) fallback_keys_kernel(ResolveArgs a) 
 __global__ void __launch_bounds__(kThreads) resolve_fallback_kernel(ResolveArgs a) {
     __shared__ BlockStats bs;
     stats_init(bs, false);
+    pdl_wait();
+    pdl_trigger();
     __syncthreads();
     const pf_config &cfg = a.cfg;
     const int lane = threadIdx.x & 31;
@@ -635,6 +645,8 @@ __global__ void __launch_bounds__(kThreads) resolve_pool_kernel(ResolveArgs a) {
     __shared__ BlockStats bs;
     __shared__ PoolSmem ps;
     stats_init(bs, false);
+    pdl_wait();
+    pdl_trigger();
     __syncthreads();
     const pf_config &cfg = a.cfg;
     const int mode = cfg.temporal_mode;
@@ -717,9 +729,23 @@ __global__ void __launch_bounds__(kThreads) resolve_pool_kernel(ResolveArgs a) {
     stats_flush(bs, a.stats, false);
 }
 
+// flat[0, m) = 0 (two words per thread) and *counter = 0: a chain kernel instead of
+// cudaMemsetAsync, which would break the frame's PDL chain.
+__global__ void __launch_bounds__(kThreads) zero_kernel(double *flat, int64_t m, int64_t *counter) {
+    pdl_wait();
+    const int64_t k = 2 * (static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x);
+    if (k + 1 < m) {
+        reinterpret_cast<double2 *>(flat)[k / 2] = make_double2(0.0, 0.0);
+    } else if (k < m) {
+        flat[k] = 0.0;
+    }
+    if (counter != nullptr && k == 0) *counter = 0;
+}
+
 __global__ void __launch_bounds__(kThreads)
 finalize_image_kernel(const double *__restrict__ base, const double *__restrict__ flat,
                       double *__restrict__ image, int64_t n, double spp) {
+    pdl_wait();
     const int64_t k = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
     if (k < n) image[k] = dadd(base[k], ddiv(flat[k], spp));
 }
@@ -730,28 +756,30 @@ finalize_image_kernel(const double *__restrict__ base, const double *__restrict_
 static int launch_rungs(const char *fn, const ResolveArgs &a, int64_t n, bool have_keys,
                         bool have_fb_keys, cudaStream_t st) {
     if (have_keys)
-        resolve_main_kernel<kResolveKV, true>
-            <<<blocks_for(n, kThreads * kResolveKV), kThreads, 0, st>>>(a);
+        launch_pdl(resolve_main_kernel<kResolveKV, true>, dim3(blocks_for(n, kThreads * kResolveKV)),
+                   dim3(kThreads), st, a);
     else
-        resolve_main_kernel<1, false><<<blocks_for(n, kThreads), kThreads, 0, st>>>(a);
+        launch_pdl(resolve_main_kernel<1, false>, dim3(blocks_for(n, kThreads)), dim3(kThreads),
+                   st, a);
     if (int rc = check_launch(fn)) return rc;
     if (have_fb_keys) {
         static const int per_sm = resident_blocks(fallback_keys_kernel, kThreads);
         int64_t kb = (n + kThreads - 1) / kThreads;
         const int64_t kcap = static_cast<int64_t>(sm_count()) * per_sm;
         if (kb > kcap) kb = kcap;
-        fallback_keys_kernel<<<static_cast<unsigned>(kb), kThreads, 0, st>>>(a);
+        launch_pdl(fallback_keys_kernel, dim3(static_cast<unsigned>(kb)), dim3(kThreads), st, a);
         if (int rc = check_launch(fn)) return rc;
         static const int per_sm_pool = resident_blocks(resolve_pool_kernel, kThreads);
         int64_t pb = (n + kPoolRows - 1) / kPoolRows;
         const int64_t pcap = static_cast<int64_t>(sm_count()) * per_sm_pool;
         if (pb > pcap) pb = pcap;
-        resolve_pool_kernel<<<static_cast<unsigned>(pb), kThreads, 0, st>>>(a);
+        launch_pdl(resolve_pool_kernel, dim3(static_cast<unsigned>(pb)), dim3(kThreads), st, a);
     } else {
         int64_t fb_blocks = (n + kWarps - 1) / kWarps;
         const int64_t cap = static_cast<int64_t>(sm_count()) * 8;
         if (fb_blocks > cap) fb_blocks = cap;
-        resolve_fallback_kernel<<<static_cast<unsigned>(fb_blocks), kThreads, 0, st>>>(a);
+        launch_pdl(resolve_fallback_kernel, dim3(static_cast<unsigned>(fb_blocks)), dim3(kThreads),
+                   st, a);
     }
     return check_launch(fn);
 }
@@ -789,14 +817,10 @@ static int insert_frame(const char *fn, const pf_config *cfg, const pf_vertices 
     int64_t cap = static_cast<int64_t>(sm_count()) *
                   (fine->sum_mode == PF_SUM_FIXED ? per_sm_fixed : per_sm_float);
     const unsigned g = static_cast<unsigned>(tiles < cap ? tiles : cap);
-    if (fine->sum_mode == PF_SUM_FIXED)
-        insert_frame_kernel<true><<<g, kThreads, 0, as_stream(stream)>>>(
-            kc, *v, *fine, c, coarse != nullptr, stream_base_accum, frame, stats, events,
-            event_count, event_capacity, abort_flag, stream_base_lookup, lookup_keys);
-    else
-        insert_frame_kernel<false><<<g, kThreads, 0, as_stream(stream)>>>(
-            kc, *v, *fine, c, coarse != nullptr, stream_base_accum, frame, stats, events,
-            event_count, event_capacity, abort_flag, stream_base_lookup, lookup_keys);
+    launch_pdl(fine->sum_mode == PF_SUM_FIXED ? insert_frame_kernel<true> : insert_frame_kernel<false>,
+               dim3(g), dim3(kThreads), as_stream(stream), kc, *v, *fine, c, coarse != nullptr,
+               stream_base_accum, frame, stats, events, event_count, event_capacity, abort_flag,
+               stream_base_lookup, lookup_keys);
     if (int rc = check_launch(fn)) return rc;
     return defer_touch ? PF_OK
                        : launch_post_insert(fn, *fine, coarse, kc, nullptr, frame, as_stream(stream));
@@ -822,11 +846,11 @@ static int resolve_frame(const char *fn, const pf_config *cfg, const pf_vertices
     if (v->n > 0 && (!v->throughput || !v->contribution || !work || !work_count))
         return fail_arg(fn, "throughput/contribution/work is NULL");
     cudaStream_t st = as_stream(stream);
-    if (cudaMemsetAsync(flat, 0, sizeof(double) * 3 * n_pixels, st) != cudaSuccess)
-        return check_launch(fn);
+    // flat = 0 and the work list's counter = 0, as a chain kernel (a memset would break
+    // the PDL chain of the frame)
+    launch_pdl(zero_kernel, dim3(blocks_for(3 * n_pixels / 2 + 1, kThreads)), dim3(kThreads), st,
+               flat, 3 * n_pixels, v->n > 0 ? work_count : nullptr);
     if (v->n > 0) {
-        if (cudaMemsetAsync(work_count, 0, sizeof(int64_t), st) != cudaSuccess)
-            return check_launch(fn);
         ResolveArgs a;
         a.cfg = kc;
         a.v = *v;
@@ -856,8 +880,9 @@ static int resolve_frame(const char *fn, const pf_config *cfg, const pf_vertices
     }
     const int64_t m = 3 * n_pixels;
     if (m > 0)
-        finalize_image_kernel<<<blocks_for(m, kThreads), kThreads, 0, st>>>(
-            base_image, flat, image, m, static_cast<double>(spp));
+        launch_pdl(finalize_image_kernel, dim3(blocks_for(m, kThreads)), dim3(kThreads), st,
+                   static_cast<const double *>(base_image), static_cast<const double *>(flat),
+                   image, m, static_cast<double>(spp));
     return check_launch(fn);
 }
 

@@ -1,6 +1,8 @@
 // Host-side helpers shared by the C-ABI translation units.
 #pragma once
 
+#include <utility>
+
 #include <cuda_runtime.h>
 
 #include <cstdint>
@@ -57,6 +59,29 @@ inline int validate_vertices(const char *fn, const pf_vertices *v, const pf_conf
 }
 
 inline cudaStream_t as_stream(void *s) { return static_cast<cudaStream_t>(s); }
+
+#ifndef PF_PDL
+#define PF_PDL 1
+#endif
+// Launch with programmatic dependent launch (PDL) when PF_PDL: the kernel's CTAs may be
+// scheduled while the previous kernel in the stream drains (each chain kernel triggers
+// its dependents at its start, pdl_trigger) and they wait in pdl_wait until it has
+// completed and its writes are visible -- kernel boundaries lose their launch gap.
+template <typename... KArgs, typename... Args>
+inline void launch_pdl(void (*kernel)(KArgs...), dim3 grid, dim3 block, cudaStream_t st,
+                       Args &&...args) {
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = grid;
+    cfg.blockDim = block;
+    cfg.dynamicSmemBytes = 0;
+    cfg.stream = st;
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    attr[0].val.programmaticStreamSerializationAllowed = 1;
+    cfg.attrs = attr;
+    cfg.numAttrs = PF_PDL ? 1 : 0;
+    cudaLaunchKernelEx(&cfg, kernel, std::forward<Args>(args)...);
+}
 
 // Copy of the caller's config with the derived fields the kernels read: lod_ulps[]
 // packs m_k = (bits(2^k) - bits(T[k])) for k = 1..31 in 4-bit fields.  Thresholds

@@ -427,6 +427,7 @@ frame_prologue_kernel(pf_table fine, pf_table coarse, int jobs, int64_t frame, i
                       int64_t *zero0, int64_t n0, int64_t *zero1, int64_t n1, int64_t *zero2) {
     __shared__ SweepSmem<kThreads> q;
     __shared__ int block_clears;
+    pdl_wait();
     if (blockIdx.x == 0) {
         for (int64_t k = threadIdx.x; k < n0; k += blockDim.x) zero0[k] = 0;
         for (int64_t k = threadIdx.x; k < n1; k += blockDim.x) zero1[k] = 0;
@@ -681,14 +682,11 @@ int frame_prologue(const pf_table *fine, const pf_table *coarse, int64_t frame, 
     const unsigned per_job = sweep_blocks<kThreads>(fine->capacity, sm_count());
     const pf_table c = coarse ? *coarse : *fine;
     const unsigned g = per_job * static_cast<unsigned>(jobs);
-    if (fine->sum_mode == PF_SUM_FIXED)
-        frame_prologue_kernel<true><<<g, kThreads, 0, st>>>(
-            *fine, c, jobs, frame, mode, ema, delta_max, sample_cap, clears_fine, clears_coarse,
-            checking ? vals : nullptr, count, bad, zero0, n0, zero1, n1, zero2);
-    else
-        frame_prologue_kernel<false><<<g, kThreads, 0, st>>>(
-            *fine, c, jobs, frame, mode, ema, delta_max, sample_cap, clears_fine, clears_coarse,
-            checking ? vals : nullptr, count, bad, zero0, n0, zero1, n1, zero2);
+    launch_pdl(fine->sum_mode == PF_SUM_FIXED ? frame_prologue_kernel<true>
+                                              : frame_prologue_kernel<false>,
+               dim3(g), dim3(kThreads), st, *fine, c, jobs, frame, mode, ema, delta_max,
+               sample_cap, clears_fine, clears_coarse, checking ? vals : nullptr, count, bad,
+               zero0, n0, zero1, n1, zero2);
     return check_launch(fn);
 }
 
