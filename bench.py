@@ -444,7 +444,7 @@ def run_b200(args):
     if world > 1:
         dist.barrier()
     import paper_1902_05942_b200 as pf
-    from paper_1902_05942_b200 import rng
+    from paper_1902_05942_b200 import _lib, rng
     from paper_1902_05942_b200.streams import stream_to_numpy
 
     cfg = make_config(pf)
@@ -604,6 +604,8 @@ def run_b200(args):
             "roofline_atomics": atomics, "cpu_baseline": cpu,
             "e2e": e2e,
             "gpu_launches": launches, "clocks": clocks.summary(),
+            "build": {"library": os.path.relpath(_lib.LIB_PATH, ROOT), "build_id": _lib.build_id(),
+                      "tree_id": _lib.source_id()},
         }
         print(json.dumps(line), flush=True)
     if world > 1:
