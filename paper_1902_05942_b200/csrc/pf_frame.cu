@@ -632,13 +632,25 @@ __global__ void __launch_bounds__(kThreads) resolve_fallback_kernel(ResolveArgs 
 // probes run 3-4 per thread back to back (independent loads in flight), the found
 // cells' effective values land in shared memory, and one thread per row then pools
 // them in (dx, dy, dz) order, runs the coarse rung and the ladder and composites.
-constexpr int kPoolRows = 32;
+#ifndef PF_POOL_ROWS
+#define PF_POOL_ROWS 32
+#endif
+constexpr int kPoolRows = PF_POOL_ROWS;
 constexpr int kPoolCells = 27 * kPoolRows;
 
 struct PoolSmem {
     int64_t key[kPoolRows][8];
     uint64_t word[kPoolCells][4];   // sum x3 (int64 or float64 bits), count (same dtype)
     uint8_t found[kPoolCells];
+    // per row, fetched in the probe phase by the CTA's last warp (so the serial per-row
+    // phase does no global round trips): the coarse cell's effective value, the row's
+    // contribution (the unfiltered rung), pixel and throughput (the composite)
+    Effective coarse[kPoolRows];
+    uint8_t coarse_found[kPoolRows];
+    double contrib[kPoolRows][3];
+    double tp[kPoolRows][3];
+    int64_t pixel[kPoolRows];
+    int64_t row[kPoolRows];
 };
 
 __global__ void __launch_bounds__(kThreads) resolve_pool_kernel(ResolveArgs a) {
@@ -660,10 +672,35 @@ __global__ void __launch_bounds__(kThreads) resolve_pool_kernel(ResolveArgs a) {
          base += static_cast<int64_t>(gridDim.x) * kPoolRows) {
         const int rows = static_cast<int>(n_work - base < kPoolRows ? n_work - base : kPoolRows);
         {  // stage the pass's key records (8 words per row)
-            const int r = threadIdx.x >> 3, k = threadIdx.x & 7;
-            if (r < rows) ps.key[r][k] = a.fb_keys[8 * (base + r) + k];
+            for (int q = threadIdx.x; q < 8 * rows; q += kThreads)
+                ps.key[q >> 3][q & 7] = a.fb_keys[8 * base + q];
         }
         __syncthreads();
+        {  // the CTA's last warps: each lane one row's coarse rung and composite inputs
+            const int r = kThreads - 1 - static_cast<int>(threadIdx.x);
+            if (r < rows) {
+                const int64_t row = a.work[base + r];
+                ps.row[r] = row;
+                ps.pixel[r] = __ldg(a.v.pixel + row);
+#pragma unroll
+                for (int c = 0; c < 3; ++c) {
+                    ps.contrib[r][c] = __ldg(a.v.contribution + 3 * row + c);
+                    ps.tp[r][c] = __ldg(a.v.throughput + 3 * row + c);
+                }
+                bool found = false;
+                if (a.has_coarse) {
+                    const int64_t cs = probe_lookup(a.coarse.tags, static_cast<uint64_t>(a.coarse.capacity) - 1,
+                                                    a.coarse.probe_limit,
+                                                    static_cast<uint64_t>(ps.key[r][5]),
+                                                    static_cast<uint32_t>(ps.key[r][6]), a.seg_mask);
+                    if (cs >= 0) {
+                        found = true;
+                        ps.coarse[r] = coarse_effective(a, cs);
+                    }
+                }
+                ps.coarse_found[r] = found;
+            }
+        }
         for (int p = threadIdx.x; p < 27 * rows; p += kThreads) {
             const int r = p / 27, j = p - 27 * (p / 27);
             const CellHash h = cell_hash(ps.key[r][0] + neighbour_dx(j), ps.key[r][1] + neighbour_dy(j),
@@ -685,8 +722,7 @@ __global__ void __launch_bounds__(kThreads) resolve_pool_kernel(ResolveArgs a) {
         __syncthreads();
         if (threadIdx.x < rows) {
             const int r = threadIdx.x;
-            const int64_t w = base + r;
-            const int64_t row = a.work[w];
+            const int64_t row = ps.row[r];
             Pool pool{{0, 0, 0}, 0, {0.0, 0.0, 0.0}, 0.0};
             for (int j = 0; j < 27; ++j) {  // numpy's order for the float64 pools
                 const int p = 27 * r + j;
@@ -699,28 +735,27 @@ __global__ void __launch_bounds__(kThreads) resolve_pool_kernel(ResolveArgs a) {
                 if (int_cnt) pool.icnt += static_cast<int64_t>(ps.word[p][3]);
                 else pool.fcnt = dadd(pool.fcnt, __longlong_as_double(ps.word[p][3]));
             }
-            const bool ok_n = (int_cnt ? static_cast<double>(pool.icnt) : pool.fcnt) >= a.thr;
-            bool coarse_found = false;
-            Effective ce{};
-            if (!ok_n && a.has_coarse) {
-                const int64_t s = probe_lookup(a.coarse.tags, static_cast<uint64_t>(a.coarse.capacity) - 1,
-                                               a.coarse.probe_limit,
-                                               static_cast<uint64_t>(ps.key[r][5]),
-                                               static_cast<uint32_t>(ps.key[r][6]), a.seg_mask);
-                if (s >= 0) {
-                    coarse_found = true;
-                    ce = coarse_effective(a, s);
-                }
-            }
             double contrib[3], ch[3];
 #pragma unroll
-            for (int c = 0; c < 3; ++c) contrib[c] = __ldg(a.v.contribution + 3 * row + c);
-            const int src = ladder_choose(pool, as_int, mode, fixed, a.thr, coarse_found, ce,
+            for (int c = 0; c < 3; ++c) contrib[c] = ps.contrib[r][c];
+            const bool cf = ps.coarse_found[r];
+            const Effective ce = cf ? ps.coarse[r] : Effective{};
+            const int src = ladder_choose(pool, as_int, mode, fixed, a.thr, cf, ce,
                                           eff_is_int(a.coarse, mode), contrib, ch);
-            const int64_t pixel = __ldg(a.v.pixel + row);
-            composite(a, row, pixel, ch, src);
-            if (!(pixel - a.pixel_base >= 0 && pixel - a.pixel_base < a.n_pixels))
-                atomicAdd(&bs.v[PF_STAT_BAD_PIXELS], 1u);
+            const int64_t pixel = ps.pixel[r] - a.pixel_base;
+            const uint64_t keep = l2_policy(PF_FLAT_POLICY);
+            const bool in_image = pixel >= 0 && pixel < a.n_pixels;
+            if (in_image) {
+#pragma unroll
+                for (int c = 0; c < 3; ++c)
+                    red_add_f64(a.flat + 3 * pixel + c, dmul(ps.tp[r][c], ch[c]), keep);
+            }
+            if (a.source) a.source[row] = static_cast<uint8_t>(src);
+            if (a.chosen) {
+#pragma unroll
+                for (int c = 0; c < 3; ++c) a.chosen[3 * row + c] = ch[c];
+            }
+            if (!in_image) atomicAdd(&bs.v[PF_STAT_BAD_PIXELS], 1u);
             atomicAdd(&bs.v[PF_STAT_SOURCE_FINE + src], 1u);
         }
         __syncthreads();
