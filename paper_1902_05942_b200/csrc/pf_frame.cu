@@ -53,20 +53,13 @@ __device__ __forceinline__ void log_eviction(pf_evict_event *events, int64_t *co
 #define PF_POS_SMEM 1  // the position too (0.784 -> 0.775 ms)
 #endif
 
-#ifndef PF_INSERT_PREFETCH
-#define PF_INSERT_PREFETCH 0  // L2 prefetch of the CTA's next vertex tile: 5 us slower now
-#endif
-// How the home-slot tags reach the insert.  0: loaded into registers as each hash
-// exists (the rolled key loop's back-edge then waits for the load: the compiler does
-// not keep a load in flight across it -- at 4K, where the tables miss L2, that wait was
-// the kernel's largest stall).  1: an L2 prefetch as each hash exists (no register, no
-// wait), both tags loaded together after the key loop.  2: as 1, plus L2 prefetches of
-// the count and sums lines the REDs will hit.  3: cp.async (L2, 16 bytes: the home
-// tag's aligned pair) into shared memory as each hash exists -- no register, so no
-// back-edge wait -- and one wait_all after the key loop.
-#ifndef PF_TAG_PREFETCH
-#define PF_TAG_PREFETCH 3  // hd4 insert 0.774 -> 0.757 ms; 1: uhd4 4.60 -> 5.13 ms (prefetches evict table lines)
-#endif
+// The home-slot tags reach the insert by cp.async (L2, 16 bytes: the home tag's aligned
+// pair) into shared memory as each hash exists, and one wait_all after the key loop.  A
+// register load there is waited for at the rolled key loop's back-edge (the compiler
+// does not keep a load in flight across it; at 4K, where the tables miss L2, that wait
+// was the kernel's largest stall): hd4 insert 0.774 -> 0.757 ms.  L2 prefetches instead
+// evict table lines (uhd4 4.60 -> 5.13 ms), as did an L2 prefetch of each CTA's next
+// vertex tile (+5 us).  DESIGN.md 4.
 #ifndef PF_INSERT_MIN_BLOCKS
 #define PF_INSERT_MIN_BLOCKS 3  // 3 x 256 threads per SM: <= 85 registers
 #endif
@@ -86,9 +79,7 @@ insert_frame_kernel(pf_config cfg, pf_vertices v, pf_table fine, pf_table coarse
 #if PF_POS_SMEM
     __shared__ double posm[3][kThreads];  // per-thread vertex position
 #endif
-#if PF_TAG_PREFETCH == 3
     __shared__ __align__(16) uint64_t home_pair[2][kThreads][2];  // fine / coarse home tag pairs
-#endif
 
     stats_init(bs);
     stage_sincos_table(sincos_tab);
@@ -108,24 +99,6 @@ insert_frame_kernel(pf_config cfg, pf_vertices v, pf_table fine, pf_table coarse
     CellHash hf{0ull, 0u}, hc{0ull, 0u};
     uint64_t ht_f = 0, ht_c = 0;
     {
-        // warm L2 with the next tile of this CTA (one line per thread per array)
-        {
-            const int64_t nxt = (tile + gridDim.x) * kThreads;
-            const int64_t lines3 = 3 * kThreads * 8 / 128, lines1 = kThreads * 8 / 128;
-            const int k = threadIdx.x;
-            if (PF_INSERT_PREFETCH && nxt < v.n) {
-                if (k < lines3) {
-                    prefetch_l2(reinterpret_cast<const char *>(v.position + 3 * nxt) + 128 * k);
-                    prefetch_l2(reinterpret_cast<const char *>(v.normal + 3 * nxt) + 128 * k);
-                    prefetch_l2(reinterpret_cast<const char *>(v.contribution + 3 * nxt) + 128 * k);
-                } else if (k < lines3 + lines1) {
-                    const int64_t o = 128 * (k - lines3);
-                    prefetch_l2(reinterpret_cast<const char *>(v.camera_distance + nxt) + o);
-                    prefetch_l2(reinterpret_cast<const char *>(v.pixel + nxt) + o);
-                    prefetch_l2(reinterpret_cast<const char *>(v.sample + nxt) + o);
-                }
-            }
-        }
         const uint64_t stream = l2_evict_first();
         const VertexIn x = load_vertex(v, i, cfg, stream);
 #pragma unroll
@@ -179,41 +152,22 @@ insert_frame_kernel(pf_config cfg, pf_vertices v, pf_table fine, pf_table coarse
 #endif
             const CellHash h = key_hash(
                 make_key_w(cfg, xk, ks, cfg.jitter, w, set == 1 ? cfg.coarse_delta : 0, jt), ks);
-            // home-slot tag loads go out as soon as a hash exists; the next key set's
+            // home-slot tag copies go out as soon as a hash exists; the next key set's
             // arithmetic hides their L2 latency before warp_insert consumes them
             if (set < 2) {
                 const pf_table &t = set == 0 ? fine : coarse;
                 const int64_t home = static_cast<int64_t>(h.index & static_cast<uint64_t>(t.capacity - 1));
                 if (set == 0) hf = h;
                 else hc = h;
-                if (PF_TAG_PREFETCH == 0) {
-                    (set == 0 ? ht_f : ht_c) = ld_relaxed(t.tags + home);
-                } else if (PF_TAG_PREFETCH == 3) {
-#if PF_TAG_PREFETCH == 3
-                    cp_async_16(&home_pair[set][threadIdx.x][0], t.tags + (home & ~int64_t(1)));
-#endif
-                } else {
-                    prefetch_l2(t.tags + home);
-                    if (PF_TAG_PREFETCH == 2) {
-                        prefetch_l2(cnt_at(t, home));
-                        prefetch_l2(sum_at(t, home, 0));
-                    }
-                }
+                cp_async_16(&home_pair[set][threadIdx.x][0], t.tags + (home & ~int64_t(1)));
             } else if (valid) {
                 lk_keys[i] = pack_lookup_key(h);
             }
         }
     }
-#if PF_TAG_PREFETCH == 3
     cp_async_wait_all();
     ht_f = home_pair[0][threadIdx.x][hf.index & 1];
     if (has_coarse) ht_c = home_pair[1][threadIdx.x][hc.index & 1];
-#endif
-    if (PF_TAG_PREFETCH == 1 || PF_TAG_PREFETCH == 2) {  // both home tags in flight together
-        ht_f = ld_relaxed(fine.tags + (hf.index & static_cast<uint64_t>(fine.capacity - 1)));
-        if (has_coarse)
-            ht_c = ld_relaxed(coarse.tags + (hc.index & static_cast<uint64_t>(coarse.capacity - 1)));
-    }
     int64_t qval[3];  // quantised once for both tables
 #pragma unroll
     for (int c = 0; c < 3; ++c) qval[c] = FIXED ? quantize_fixed(val[c]) : 0;
