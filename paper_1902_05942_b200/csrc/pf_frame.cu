@@ -264,10 +264,21 @@ constexpr int64_t kNoTouch = INT64_MIN;  // touch_frame of a sweep without defer
 __global__ void __launch_bounds__(kThreads)
 effective_records_kernel(pf_table t, int mode, double ema, double delta_max, ulonglong4 *rec,
                          pf_table coarse, int has_coarse, int64_t touch_frame,
-                         unsigned nb_fine) {
+                         unsigned nb_fine, double *flat, int64_t flat_words, int64_t *counter) {
     __shared__ SweepSmem<kThreads> q;
     pdl_wait();  // multi-wave kernels do not trigger early: waiting dependents would take
                  // the slots of their later waves
+    // the resolve's composite buffer and work counter start at zero (in this launch rather
+    // than a memset, which would break the frame's PDL chain)
+    if (flat != nullptr) {
+        double2 *f2 = reinterpret_cast<double2 *>(flat);
+        const int64_t pairs = flat_words / 2;
+        for (int64_t k = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x; k < pairs;
+             k += static_cast<int64_t>(gridDim.x) * blockDim.x)
+            f2[k] = make_double2(0.0, 0.0);
+        if (blockIdx.x == 0 && threadIdx.x == 0 && (flat_words & 1)) flat[flat_words - 1] = 0.0;
+    }
+    if (counter != nullptr && blockIdx.x == 0 && threadIdx.x == 0) *counter = 0;
     if (blockIdx.x >= nb_fine) {
         const int64_t blk = blockIdx.x - nb_fine, nblk = gridDim.x - nb_fine;
         for_each_occupied<kThreads>(coarse.tags, coarse.capacity, q, blk, nblk,
@@ -286,18 +297,21 @@ effective_records_kernel(pf_table t, int mode, double ema, double delta_max, ulo
     });
 }
 
-// Launch the sweep above (records and / or deferred touches); no-op when neither.
+// Launch the sweep above (records and / or deferred touches, and the zeroing of the
+// composite buffer / work counter when given); no-op when there is nothing to do.
 static int launch_post_insert(const char *fn, const pf_table &fine, const pf_table *coarse,
                               const pf_config &kc, uint64_t *eff_records, int64_t touch_frame,
-                              cudaStream_t st) {
-    if (eff_records == nullptr && touch_frame == kNoTouch) return PF_OK;
+                              cudaStream_t st, double *flat = nullptr, int64_t flat_words = 0,
+                              int64_t *counter = nullptr) {
+    if (eff_records == nullptr && touch_frame == kNoTouch && flat == nullptr && counter == nullptr)
+        return PF_OK;
     const unsigned nf = sweep_blocks<kThreads>(fine.capacity, sm_count());
     const bool tc = coarse != nullptr && touch_frame != kNoTouch;
     const unsigned nc = tc ? sweep_blocks<kThreads>(coarse->capacity, sm_count()) : 0u;
     launch_pdl(effective_records_kernel, dim3(nf + nc), dim3(kThreads), st, fine,
                kc.temporal_mode, kc.ema_alpha, kc.delta_max,
                reinterpret_cast<ulonglong4 *>(eff_records), tc ? *coarse : fine,
-               static_cast<int>(tc), touch_frame, nf);
+               static_cast<int>(tc), touch_frame, nf, flat, flat_words, counter);
     return check_launch(fn);
 }
 
@@ -835,11 +849,10 @@ static int resolve_frame(const char *fn, const pf_config *cfg, const pf_vertices
     if (v->n > 0 && (!v->throughput || !v->contribution || !work || !work_count))
         return fail_arg(fn, "throughput/contribution/work is NULL");
     cudaStream_t st = as_stream(stream);
-    // flat = 0 and the work list's counter = 0, as a chain kernel (a memset would break
-    // the PDL chain of the frame)
-    launch_pdl(zero_kernel, dim3(blocks_for(3 * n_pixels / 2 + 1, kThreads)), dim3(kThreads), st,
-               flat, 3 * n_pixels, v->n > 0 ? work_count : nullptr);
-    if (v->n > 0) {
+    if (v->n == 0) {  // only the image: base + 0 / spp
+        launch_pdl(zero_kernel, dim3(blocks_for(3 * n_pixels / 2 + 1, kThreads)), dim3(kThreads),
+                   st, flat, 3 * n_pixels, static_cast<int64_t *>(nullptr));
+    } else {
         ResolveArgs a;
         a.cfg = kc;
         a.v = *v;
@@ -862,7 +875,9 @@ static int resolve_frame(const char *fn, const pf_config *cfg, const pf_vertices
         a.pixel_base = 0;
         a.seg_mask = ~0ull;
         a.crec = nullptr;
-        if (int rc = launch_post_insert(fn, *fine, coarse, kc, eff_records, touch_frame, st))
+        // flat = 0 and the work counter = 0 ride on the effective-record sweep
+        if (int rc = launch_post_insert(fn, *fine, coarse, kc, eff_records, touch_frame, st, flat,
+                                        3 * n_pixels, work_count))
             return rc;
         if (int rc = launch_rungs(fn, a, v->n, lookup_keys != nullptr, fallback_keys != nullptr, st))
             return rc;
