@@ -430,6 +430,10 @@ def run_b200(args):
     world = _env_int("WORLD_SIZE", 1)
     local = _env_int("LOCAL_RANK", 0)
     if world > 1:
+        # NCCL's init lines (rank count per communicator) in the log, however the ranks
+        # were launched
+        os.environ.setdefault("NCCL_DEBUG", "INFO")
+        os.environ.setdefault("NCCL_DEBUG_SUBSYS", "INIT")
         # PF_BENCH_BACKEND=gloo + PF_BENCH_ONE_DEVICE=1: exercise the N-rank code path on a
         # single GPU (exchanges through host memory, no kernel waits on another rank);
         # numbers from such a run are not multi-GPU measurements
