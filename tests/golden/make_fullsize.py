@@ -13,6 +13,8 @@ Configurations (BASELINE.json `configs`):
   hd1_filter  configs[3]: hd1's stream, 8 frames of temporal_mode "filter" with the
               animated-scene seed schedule mix64(1 ^ f*G) and begin_frame(f) each frame
               (src/pipeline.py:329-333)
+  hd1_filter64  configs[3] as named: the same for 64 frames (tables digested at frames
+              0, 7, 15, 31, 47, 63; sources, means and image every frame)
 
 Everything digested is produced by the reference's own code path (trace,
 vertex_keys, accumulate_phase, resolve_phase, VoxelTable); this script only hashes it
@@ -81,9 +83,11 @@ def box_stream(w, h, ks):
     return scene, VertexStream.concat(parts), base
 
 
-def filter_frames(scene, vs, base, frames=1, mode="integrate", animated=False):
+def filter_frames(scene, vs, base, frames=1, mode="integrate", animated=False,
+                  table_frames=None):
     """begin_frame + accumulate_phase + resolve_phase per frame (render_frame minus the
-    tracer, src/pipeline.py:321-363) on a fresh FrameState."""
+    tracer, src/pipeline.py:321-363) on a fresh FrameState.  table_frames: the frames
+    whose tables are digested (default: all)."""
     h, w = base.shape[:2]
     cfg = FilterConfig(capacity=next_pow2(2 * w * h), temporal_mode=mode).for_camera(
         scene.camera.fov, scene.camera.height)
@@ -102,13 +106,12 @@ def filter_frames(scene, vs, base, frames=1, mode="integrate", animated=False):
                "source_counts": np.bincount(report.source, minlength=4).tolist(),
                "chosen": digest(report.means), "image": digest(image),
                "probe_failures": int(stats.probe_failures),
-               "coarse_probe_failures": int(stats.coarse_probe_failures),
-               "fine": table_digest({k: getattr(state.fine, k) for k in
-                                     ("tags", "sums", "counts", "hist_sums", "hist_counts",
-                                      "last_touch", "deltas")}),
-               "coarse": table_digest({k: getattr(state.coarse, k) for k in
-                                       ("tags", "sums", "counts", "hist_sums", "hist_counts",
-                                        "last_touch", "deltas")})}
+               "coarse_probe_failures": int(stats.coarse_probe_failures)}
+        if table_frames is None or f in table_frames:
+            for name, t in (("fine", state.fine), ("coarse", state.coarse)):
+                rec[name] = table_digest({k: getattr(t, k) for k in
+                                          ("tags", "sums", "counts", "hist_sums", "hist_counts",
+                                           "last_touch", "deltas")})
         # the composite restated over the reference's own chosen means reproduces its image
         assert digest(composite(base, vs.pixel, vs.throughput, report.means, 1)) == rec["image"]
         if f == 0:
@@ -148,6 +151,13 @@ def main():
             res["hd1_filter"] = {"n": len(vs), "stream": stream_digests(vs),
                                  **filter_frames(scene, vs, base, frames=8, mode="filter",
                                                  animated=True)}
+    if want("hd1_filter64"):
+        print("hd1_filter64", flush=True)
+        scene, vs, base = box_stream(1920, 1080, [1])
+        res["hd1_filter64"] = {"n": len(vs), "stream": stream_digests(vs),
+                               **filter_frames(scene, vs, base, frames=64, mode="filter",
+                                               animated=True,
+                                               table_frames={0, 7, 15, 31, 47, 63})}
     if want("hd4"):
         print("hd4", flush=True)
         scene, vs, base = box_stream(1920, 1080, [1, 2, 3, 4])

@@ -176,3 +176,28 @@ def test_uhd4_frame_properties(gpu):
     assert np.array_equal(packed >> np.uint64(32), lk["fingerprint"].astype(np.uint64))
     assert np.array_equal(packed & np.uint64(0xFFFFFFFF),
                           lk["index"].astype(np.uint64) & np.uint64(0xFFFFFFFF))
+
+
+def test_filter_mode_64_frames_matches_reference(gpu):
+    """configs[3] as named: 64 filter-mode frames (EMA blend, generation fold, aging,
+    horizon clears, re-prioritised tags) of the 1080p first-hit stream with the animated
+    seed schedule -- every frame's sources, chosen means and image bit-exact, both tables
+    per key at frames 0, 7, 15, 31, 47, 63."""
+    want = FULL.get("hd1_filter64")
+    if want is None:
+        pytest.skip("hd1_filter64 digests not generated (tests/golden/make_fullsize.py)")
+    sc, vs, base = _stream(gpu, "hd1")
+    _check_stream(want, vs)
+    cfg = _cfg(gpu, want)
+    state = gpu.FrameState.from_config(cfg)
+    for f, fr in enumerate(want["frames"]):
+        image, report, stats = gpu.filter_frame(vs, base, cfg, state, 1, int(fr["seed"]))
+        assert stats.probe_failures == fr["probe_failures"], f
+        src = _np(report.source)
+        assert digest(src) == fr["source"], f
+        assert digest(_np(report.means)) == fr["chosen"], f
+        assert digest(_np(image)) == fr["image"], f
+        for t, key in ((state.fine, "fine"), (state.coarse, "coarse")):
+            if key in fr:
+                assert table_digest(t.state()) == fr[key], (f, key)
+    assert len(want["frames"]) == 64
