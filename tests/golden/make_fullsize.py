@@ -13,6 +13,8 @@ Configurations (BASELINE.json `configs`):
   hd1_filter  configs[3]: hd1's stream, 8 frames of temporal_mode "filter" with the
               animated-scene seed schedule mix64(1 ^ f*G) and begin_frame(f) each frame
               (src/pipeline.py:329-333)
+  hd4_seq     the benchmark's frame sequence: configs[2]'s stream, 4 integrate-mode
+              frames with the animated seed schedule bench.py uses (tables at frames 0, 3)
   hd1_filter64  configs[3] as named: the same for 64 frames (tables digested at frames
               0, 7, 15, 31, 47, 63; sources, means and image every frame)
 
@@ -158,6 +160,12 @@ def main():
                                **filter_frames(scene, vs, base, frames=64, mode="filter",
                                                animated=True,
                                                table_frames={0, 7, 15, 31, 47, 63})}
+    if want("hd4_seq"):
+        print("hd4_seq", flush=True)
+        scene, vs, base = box_stream(1920, 1080, [1, 2, 3, 4])
+        res["hd4_seq"] = {"n": len(vs), "stream": stream_digests(vs), "base": digest(base),
+                          **filter_frames(scene, vs, base, frames=4, animated=True,
+                                          table_frames={0, 3})}
     if want("hd4"):
         print("hd4", flush=True)
         scene, vs, base = box_stream(1920, 1080, [1, 2, 3, 4])

@@ -201,3 +201,31 @@ def test_filter_mode_64_frames_matches_reference(gpu):
             if key in fr:
                 assert table_digest(t.state()) == fr[key], (f, key)
     assert len(want["frames"]) == 64
+
+
+def test_benchmark_frame_sequence_matches_reference(gpu):
+    """The frames bench.py times: configs[2]'s 8,184,972-vertex stream, integrate mode,
+    the animated seed schedule (rng.frame_seed), 4 consecutive frames on one FrameState
+    (history folds, re-prioritised tags) -- sources and means bit-exact every frame, the
+    image within 1e-12 of the reference composite, both tables per key at frames 0, 3."""
+    want = FULL.get("hd4_seq")
+    if want is None:
+        pytest.skip("hd4_seq digests not generated (tests/golden/make_fullsize.py)")
+    from paper_1902_05942_b200 import rng
+    sc, vs, base = _stream(gpu, "hd4")
+    assert len(vs) == want["n"]
+    cfg = _cfg(gpu, want)
+    state = gpu.FrameState.from_config(cfg)
+    for f, fr in enumerate(want["frames"]):
+        assert int(fr["seed"]) == rng.frame_seed(1, f)
+        image, report, stats = gpu.filter_frame(vs, base, cfg, state, 1, int(fr["seed"]))
+        assert stats.probe_failures == fr["probe_failures"], f
+        assert digest(_np(report.source)) == fr["source"], f
+        chosen = _np(report.means)
+        assert digest(chosen) == fr["chosen"], f
+        ref_img = composite(_np(base), _np(vs.pixel), _np(vs.throughput), chosen, 1)
+        assert digest(ref_img) == fr["image"], f
+        np.testing.assert_allclose(_np(image), ref_img, rtol=1e-12, atol=1e-300)
+        for t, key in ((state.fine, "fine"), (state.coarse, "coarse")):
+            if key in fr:
+                assert table_digest(t.state()) == fr[key], (f, key)
