@@ -23,7 +23,7 @@
 extern "C" {
 #endif
 
-#define PF_ABI_VERSION 5
+#define PF_ABI_VERSION 6
 
 enum pf_status {
     PF_OK = 0,
@@ -137,6 +137,13 @@ enum pf_stat_slot {
     PF_STAT_COUNT = 16 + 256
 };
 
+/* The resolve's work list (rows that leave the fine rung) is PF_WORK_LISTS lists, one
+ * per group of resolve blocks (256 rows each), so its append counters are not one hot
+ * L2 atomic: work needs PF_WORK_ROWS(n) entries and work_count PF_WORK_LISTS. */
+#define PF_WORK_LISTS 64
+#define PF_WORK_ROWS(n) \
+    ((((((n) + 255) / 256) + PF_WORK_LISTS - 1) / PF_WORK_LISTS) * PF_WORK_LISTS * 256)
+
 /* Eviction event record (src/table.py:72-77, 137-141). */
 typedef struct pf_evict_event {
     int64_t vertex;                 /* row in the batch */
@@ -233,7 +240,8 @@ int pf_insert_frame(const pf_config *cfg, const pf_vertices *v, const pf_table *
 
 /* Fused resolve_phase (src/pipeline.py:207-283): lookup keys, fine rung, 3x3x3
  * neighbourhood, coarse rung, ladder, composite.  flat: float64[n_pixels][3]
- * scratch; work: int64 scratch of n entries plus work_count (int64[1]);
+ * scratch; work: int64 scratch of PF_WORK_ROWS(n) entries plus work_count
+ * (int64[PF_WORK_LISTS]);
  * image = base_image + flat/spp.  source (u8[n]) and chosen (f64[n][3]) may be NULL.
  * lookup_keys: the packed keys pf_insert_frame emitted for the same vertices and
  * stream_base_lookup, or NULL to build them here.
@@ -264,8 +272,8 @@ typedef struct pf_frame_buffers {
     uint64_t *lookup_keys;          /* n: packed lookup keys handed from insert to resolve */
     uint64_t *eff_records;          /* 4 * fine->capacity */
     double *flat;                   /* [n_pixels][3] */
-    int64_t *work;                  /* n */
-    int64_t *work_count;            /* 1 */
+    int64_t *work;                  /* PF_WORK_ROWS(n) */
+    int64_t *work_count;            /* PF_WORK_LISTS */
     int64_t *fallback_keys;         /* 8 * n, or NULL (see pf_resolve_frame) */
     void *phase_events[4];          /* optional cudaEvent_t recorded at frame start, just
                                        before the insert kernel, after it, at frame end */
@@ -367,7 +375,8 @@ int pf_shard_reset(const pf_shard *sh, void *stream);
 /* resolve_phase (src/pipeline.py:207-283) of this rank's vertices against a replica:
  * the fine rung from lookup_keys (pf_shard_keys), the neighbourhood and
  * coarse rungs, the ladder, the composite into flat (pixels [pixel_base, pixel_base +
- * n_pixels), zeroed here).  work: n int64, fallback_keys: 8 * n int64 scratch. */
+ * n_pixels), zeroed here).  work: PF_WORK_ROWS(n) int64 (+ work_count[PF_WORK_LISTS]),
+ * fallback_keys: 8 * n int64 scratch. */
 int pf_resolve_replica(const pf_config *cfg, const pf_vertices *v, const pf_replica *replica,
                        uint64_t stream_base_lookup, uint64_t stream_base_coarse,
                        const uint64_t *lookup_keys, double *flat,

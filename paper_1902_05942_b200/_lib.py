@@ -210,6 +210,13 @@ STAT_BAD_PIXELS = 10
 STAT_SHARD_RECORDS = 11
 STAT_SHARD_REQUESTS = 12
 STAT_HIST_BASE = 16
+WORK_LISTS = 64  # PF_WORK_LISTS
+
+
+def work_rows(n: int) -> int:
+    """PF_WORK_ROWS(n): entries of the resolve's work-list buffer for n vertices."""
+    blocks = (int(n) + 255) // 256
+    return max((blocks + WORK_LISTS - 1) // WORK_LISTS * WORK_LISTS * 256, 1)
 STAT_COUNT = 16 + 256
 
 _lib = None

@@ -18,6 +18,14 @@ constexpr int kResolveKV = PF_RESOLVE_KV;
 #endif  // vertices per thread in resolve_main
 constexpr int kWarps = kThreads / 32;
 
+// Rows per work list: resolve_main block b (kThreads * kResolveKV rows) appends to list
+// b % PF_WORK_LISTS, so a list holds at most ceil(blocks / PF_WORK_LISTS) blocks' rows.
+inline int64_t work_list_capacity(int64_t n) {
+    const int64_t rows = static_cast<int64_t>(kThreads) * kResolveKV;
+    const int64_t blocks = (n + rows - 1) / rows;
+    return (blocks + PF_WORK_LISTS - 1) / PF_WORK_LISTS * rows;
+}
+
 __device__ __forceinline__ void log_eviction(pf_evict_event *events, int64_t *count, int64_t cap,
                                              int64_t vertex, const LaneInsert &r) {
     if (events == nullptr || count == nullptr) return;
@@ -223,8 +231,9 @@ struct ResolveArgs {
     uint64_t h0_lookup;
     uint64_t h0_coarse;
     double *flat;
-    int64_t *work;
-    int64_t *work_count;
+    int64_t *work;             // PF_WORK_LISTS lists of wcap rows each
+    int64_t *work_count;       // [PF_WORK_LISTS]
+    int64_t wcap;
     uint8_t *source;
     double *chosen;
     int64_t *stats;
@@ -278,7 +287,7 @@ effective_records_kernel(pf_table t, int mode, double ema, double delta_max, ulo
             f2[k] = make_double2(0.0, 0.0);
         if (blockIdx.x == 0 && threadIdx.x == 0 && (flat_words & 1)) flat[flat_words - 1] = 0.0;
     }
-    if (counter != nullptr && blockIdx.x == 0 && threadIdx.x == 0) *counter = 0;
+    if (counter != nullptr && blockIdx.x == 0 && threadIdx.x < PF_WORK_LISTS) counter[threadIdx.x] = 0;
     if (blockIdx.x >= nb_fine) {
         const int64_t blk = blockIdx.x - nb_fine, nblk = gridDim.x - nb_fine;
         for_each_occupied<kThreads>(coarse.tags, coarse.capacity, q, blk, nblk,
@@ -434,11 +443,16 @@ __global__ void __launch_bounds__(kThreads, PF_RESOLVE_MIN_BLOCKS) resolve_main_
         if (m) {
             unsigned long long wb = 0;
             const int lane = threadIdx.x & 31;
+            // one of PF_WORK_LISTS lists per block (by block index): a single counter
+            // hit by every warp with a low-count row was a hot L2 atomic
+            const int list = static_cast<int>(blockIdx.x) & (PF_WORK_LISTS - 1);
             if (lane == __ffs(m) - 1)
-                wb = atomicAdd(reinterpret_cast<unsigned long long *>(a.work_count),
+                wb = atomicAdd(reinterpret_cast<unsigned long long *>(a.work_count + list),
                                static_cast<unsigned long long>(__popc(m)));
             wb = __shfl_sync(kFull, wb, __ffs(m) - 1);
-            if (need) a.work[static_cast<int64_t>(wb) + __popc(m & ((1u << lane) - 1u))] = row[k];
+            if (need)
+                a.work[list * a.wcap + static_cast<int64_t>(wb) + __popc(m & ((1u << lane) - 1u))] =
+                    row[k];
         }
         const bool bad = valid[k] && fine_ok && !(pixel[k] >= 0 && pixel[k] < a.n_pixels);
         if (__any_sync(kFull, bad)) {
@@ -448,6 +462,33 @@ __global__ void __launch_bounds__(kThreads, PF_RESOLVE_MIN_BLOCKS) resolve_main_
                           static_cast<unsigned long long>(__popc(b)));
         }
     }
+}
+
+// The resolve's work lists as one sequence: a CTA loads the PF_WORK_LISTS counts into
+// shared memory once; entry w of the sequence is row work_row(w).
+struct WorkLists {
+    int64_t start[PF_WORK_LISTS + 1];  // prefix sums of the list counts
+};
+__device__ __forceinline__ int64_t load_work_lists(const ResolveArgs &a, WorkLists &wl) {
+    if (threadIdx.x == 0) {
+        int64_t acc = 0;
+        for (int j = 0; j < PF_WORK_LISTS; ++j) {
+            wl.start[j] = acc;
+            acc += a.work_count[j];
+        }
+        wl.start[PF_WORK_LISTS] = acc;
+    }
+    __syncthreads();
+    return wl.start[PF_WORK_LISTS];
+}
+__device__ __forceinline__ int64_t work_row(const ResolveArgs &a, const WorkLists &wl, int64_t w) {
+    int lo = 0, hi = PF_WORK_LISTS;  // the list j with start[j] <= w < start[j + 1]
+    while (hi - lo > 1) {
+        const int mid = (lo + hi) >> 1;
+        if (wl.start[mid] <= w) lo = mid;
+        else hi = mid;
+    }
+    return a.work[lo * a.wcap + (w - wl.start[lo])];
 }
 
 // resolve_main's row counters, once per resolve: every row it saw either took the fine
@@ -467,14 +508,15 @@ __global__ void __launch_bounds__(kThreads) fallback_keys_kernel(ResolveArgs a) 
     __shared__ double lod_dist[32];
     stage_sincos_table(sincos_tab);
     stage_lod_dist(lod_dist, a.cfg);
+    __shared__ WorkLists wl;
     pdl_wait();
     pdl_trigger();
     __syncthreads();
     const pf_config &cfg = a.cfg;
-    const int64_t n_work = *a.work_count;
+    const int64_t n_work = load_work_lists(a, wl);
     for (int64_t w = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x; w < n_work;
          w += static_cast<int64_t>(gridDim.x) * blockDim.x) {
-        const int64_t row = a.work[w];
+        const int64_t row = work_row(a, wl, w);
         const VertexIn x = load_vertex(a.v, row, cfg);
         const KeyShared ks = key_shared(cfg, x, lod_dist);
         double du = 0.0, dv = 0.0, cdu = 0.0, cdv = 0.0;
@@ -506,13 +548,14 @@ __global__ void __launch_bounds__(kThreads) fallback_keys_kernel(ResolveArgs a) 
 // float64 pools), then runs the coarse rung, the ladder and the composite.
 __global__ void __launch_bounds__(kThreads) resolve_fallback_kernel(ResolveArgs a) {
     __shared__ BlockStats bs;
+    __shared__ WorkLists wl;
     stats_init(bs, false);
     pdl_wait();
     pdl_trigger();
     __syncthreads();
     const pf_config &cfg = a.cfg;
     const int lane = threadIdx.x & 31;
-    const int64_t n_work = *a.work_count;
+    const int64_t n_work = load_work_lists(a, wl);
     if (blockIdx.x == 0 && threadIdx.x == 0) main_row_counts(a, n_work);
     const int64_t warp0 = static_cast<int64_t>(blockIdx.x) * kWarps + (threadIdx.x >> 5);
     const int64_t nwarps = static_cast<int64_t>(gridDim.x) * kWarps;
@@ -521,7 +564,7 @@ __global__ void __launch_bounds__(kThreads) resolve_fallback_kernel(ResolveArgs 
     const bool fixed = a.fine.sum_mode == PF_SUM_FIXED;
     const uint64_t fmask = static_cast<uint64_t>(a.fine.capacity) - 1;
     for (int64_t w = warp0; w < n_work; w += nwarps) {
-        const int64_t row = a.work[w];
+        const int64_t row = work_row(a, wl, w);
         // the row's lookup key: from fallback_keys_kernel (lanes 0..7 load the record),
         // else rebuilt by lane 0; broadcast to the 27 probing lanes
         int64_t kq[3] = {0, 0, 0}, klev = 0, kaux = 0, krec = 0;
@@ -634,7 +677,8 @@ __global__ void __launch_bounds__(kThreads) resolve_pool_kernel(ResolveArgs a) {
     const bool int_cnt = mode == PF_INTEGRATE;
     const bool fixed = a.fine.sum_mode == PF_SUM_FIXED;
     const uint64_t fmask = static_cast<uint64_t>(a.fine.capacity) - 1;
-    const int64_t n_work = *a.work_count;
+    __shared__ WorkLists wl;
+    const int64_t n_work = load_work_lists(a, wl);
     if (blockIdx.x == 0 && threadIdx.x == 0) main_row_counts(a, n_work);
     for (int64_t base = static_cast<int64_t>(blockIdx.x) * kPoolRows; base < n_work;
          base += static_cast<int64_t>(gridDim.x) * kPoolRows) {
@@ -647,7 +691,7 @@ __global__ void __launch_bounds__(kThreads) resolve_pool_kernel(ResolveArgs a) {
         {  // the CTA's last warps: each lane one row's coarse rung and composite inputs
             const int r = kThreads - 1 - static_cast<int>(threadIdx.x);
             if (r < rows) {
-                const int64_t row = a.work[base + r];
+                const int64_t row = work_row(a, wl, base + r);
                 ps.row[r] = row;
                 ps.pixel[r] = __ldg(a.v.pixel + row);
 #pragma unroll
@@ -864,6 +908,7 @@ static int resolve_frame(const char *fn, const pf_config *cfg, const pf_vertices
         a.flat = flat;
         a.work = work;
         a.work_count = work_count;
+        a.wcap = work_list_capacity(v->n);
         a.source = source;
         a.chosen = chosen;
         a.stats = stats;
@@ -937,7 +982,8 @@ int pf_resolve_replica(const pf_config *cfg, const pf_vertices *v, const pf_repl
     if (cudaMemsetAsync(flat, 0, sizeof(double) * 3 * n_pixels, st) != cudaSuccess)
         return check_launch(fn);
     if (v->n == 0) return PF_OK;
-    if (cudaMemsetAsync(work_count, 0, sizeof(int64_t), st) != cudaSuccess) return check_launch(fn);
+    if (cudaMemsetAsync(work_count, 0, sizeof(int64_t) * PF_WORK_LISTS, st) != cudaSuccess)
+        return check_launch(fn);
     pf_table view{};
     view.cnt_stride = view.cold_stride = 1;
     view.sum_stride = view.hsum_stride = 3;
@@ -959,6 +1005,7 @@ int pf_resolve_replica(const pf_config *cfg, const pf_vertices *v, const pf_repl
     a.flat = flat;
     a.work = work;
     a.work_count = work_count;
+    a.wcap = work_list_capacity(v->n);
     a.source = source;
     a.chosen = chosen;
     a.stats = stats;

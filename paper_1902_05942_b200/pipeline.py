@@ -442,8 +442,8 @@ def resolve_phase(vertices, cfg: FilterConfig, state: FrameState, frame: int, se
     chosen = torch.empty((n, 3), dtype=torch.float64, device=dev) if want_means else None
     image = torch.empty_like(base)
     flat = state.buffer("flat", (h * w, 3), torch.float64)
-    work = state.buffer("work", (max(n, 1),), torch.int64)
-    work_count = state.buffer("work_count", (1,), torch.int64)
+    work = state.buffer("work", (_lib.work_rows(n),), torch.int64)
+    work_count = state.buffer("work_count", (_lib.WORK_LISTS,), torch.int64)
     counters = torch.zeros(_lib.STAT_COUNT, dtype=torch.int64, device=dev)
     v, keep = vs.c_struct()
     ft = state.fine.c_table()
@@ -495,8 +495,8 @@ def _fused_frame(vs: VertexStream, base_image, cfg: FilterConfig, state: FrameSt
     b.lookup_keys = lk_keys.data_ptr()
     b.eff_records = state.buffer("eff_records", (state.fine.capacity, 4), torch.int64).data_ptr()
     b.flat = state.buffer("flat", (h * w, 3), torch.float64).data_ptr()
-    b.work = state.buffer("work", (max(n, 1),), torch.int64).data_ptr()
-    b.work_count = state.buffer("work_count", (1,), torch.int64).data_ptr()
+    b.work = state.buffer("work", (_lib.work_rows(n),), torch.int64).data_ptr()
+    b.work_count = state.buffer("work_count", (_lib.WORK_LISTS,), torch.int64).data_ptr()
     b.fallback_keys = state.buffer("fallback_keys", (max(n, 1), 8), torch.int64).data_ptr()
     if phase_events is not None:  # torch.cuda.Events recorded inside the C call
         for k, e in enumerate(phase_events):

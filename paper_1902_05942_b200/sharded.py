@@ -304,8 +304,8 @@ def filter_frame_sharded(vertices, base_image, cfg: FilterConfig, st: ShardedSta
     source = torch.empty(n, dtype=torch.uint8, device=dev)
     chosen = torch.empty((n, 3), dtype=torch.float64, device=dev) if want_means else None
     flat = st.buffer("flat", (n_pix, 3), torch.float64)
-    work = st.buffer("work", (max(n, 1),), torch.int64)
-    work_count = st.buffer("work_count", (1,), torch.int64)
+    work = st.buffer("work", (_lib.work_rows(n),), torch.int64)
+    work_count = st.buffer("work_count", (_lib.WORK_LISTS,), torch.int64)
     fb_keys = st.buffer("fallback_keys", (max(n, 1), 8), torch.int64)
     _lib.call("pf_resolve_replica", ctypes.byref(cc), ctypes.byref(v), ctypes.byref(rp),
               lookup_seed, coarse_seed, lk_keys.data_ptr(), flat.data_ptr(),

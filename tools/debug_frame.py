@@ -22,7 +22,7 @@ want = d[f"{mode}_source"]
 bad = np.nonzero(src != want)[0]
 print("mismatch rows", len(bad), "of", len(src), "mine", np.bincount(src, minlength=4),
       "gold", np.bincount(want, minlength=4))
-work_n = int(state.scratch["work_count"][0].item())
+work_n = int(state.scratch["work_count"].sum().item())
 work = state.scratch["work"][:6 * work_n].view(-1, 6).cpu().numpy()
 print("work rows", work_n, "fallback stat", int(report.counters[9].item()),
       "unique rows", len(np.unique(work[:, 0])))
