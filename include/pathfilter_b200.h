@@ -249,8 +249,8 @@ int pf_insert_frame(const pf_config *cfg, const pf_vertices *v, const pf_table *
  * fine table's effective (sum, count) is computed once per occupied slot into one
  * 32-byte record that every lookup then reads.
  * fallback_keys (may be NULL): scratch of 8 * n int64; when given, the lookup key and
- * coarse hash of every row that leaves the fine rung are built one row per thread
- * before the 3x3x3 pool instead of by one lane per row. */
+ * coarse slot of every row that leaves the fine rung are built (and probed) one row per
+ * thread before the 3x3x3 pool instead of by one lane per row. */
 int pf_resolve_frame(const pf_config *cfg, const pf_vertices *v, const pf_table *fine,
                      const pf_table *coarse, uint64_t stream_base_lookup,
                      uint64_t stream_base_coarse, int64_t spp, const double *base_image,

@@ -971,13 +971,14 @@ __device__ __forceinline__ InsertResult probe_insert(const pf_table &t, uint64_t
 // lookup_slots for one key (src/_native.pyx:285-294).  seg_mask (default: the whole
 // table) confines the probe window to the aligned segment of size seg_mask + 1 that holds
 // the home slot -- the layout of a replica of owner-sliced tables (pf_resolve_replica).
+// `first` > 0 resumes a probe whose earlier window slots the caller already checked.
 __device__ __forceinline__ int64_t probe_lookup(const uint64_t *tags, uint64_t mask,
                                                 int probe_limit, uint64_t idx, uint32_t fp,
-                                                uint64_t seg_mask = ~0ull) {
+                                                uint64_t seg_mask = ~0ull, int first = 0) {
     const uint64_t home = idx & mask;
     const uint64_t sm = seg_mask & mask;
     const uint64_t seg = home & ~sm;
-    for (int j = 0; j < probe_limit; ++j) {
+    for (int j = first; j < probe_limit; ++j) {
         const uint64_t s = seg | ((home + static_cast<uint64_t>(j)) & sm);
         const uint64_t tag = __ldg(reinterpret_cast<const unsigned long long *>(tags + s));
         if (tag == kEmptyTag)

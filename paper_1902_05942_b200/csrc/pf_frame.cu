@@ -241,7 +241,7 @@ struct ResolveArgs {
     const uint64_t *lk_keys;   // precomputed packed lookup keys (or NULL)
     const ulonglong4 *rec;     // per-slot effective records of the fine table (or NULL)
     int64_t n_pixels;          // flat holds pixels [pixel_base, pixel_base + n_pixels)
-    int64_t *fb_keys;          // [work row][8] lookup key + coarse hash (or NULL)
+    int64_t *fb_keys;          // [work row][8] lookup key, coarse slot, row, pixel (or NULL)
     int64_t pixel_base;        // first pixel of flat (0 unless a rank composites a band)
     uint64_t seg_mask;         // probe-window segment (~0: plain table; replica: slice - 1)
     const ulonglong4 *crec;    // per-slot effective records of the coarse table (or NULL)
@@ -500,9 +500,10 @@ __device__ __forceinline__ void main_row_counts(const ResolveArgs &a, int64_t n_
               static_cast<unsigned long long>(a.v.n - n_work));
 }
 
-// The work rows' lookup keys (q, level, aux; stream 3) and coarse hashes, one row per
-// thread -- the FP64 key recipe runs SIMT-wide instead of on one lane of a warp.
-// Record per row: q0, q1, q2, level, aux, coarse index, coarse fp, unused.
+// The work rows' lookup keys (q, level, aux; stream 3) and coarse slots, one row per
+// thread -- the FP64 key recipe and the coarse probe run SIMT-wide instead of on the
+// pool's critical path.  Record per work row: q0, q1, q2, level, aux, coarse slot (-1:
+// absent), row, pixel.
 __global__ void __launch_bounds__(kThreads) fallback_keys_kernel(ResolveArgs a) {
     __shared__ double2 sincos_tab[220];
     __shared__ double lod_dist[32];
@@ -533,13 +534,16 @@ __global__ void __launch_bounds__(kThreads) fallback_keys_kernel(ResolveArgs a) 
         }
         double jt[3];
         const CellKey k = make_key(cfg, x, ks, cfg.jitter, du, dv, 0, jt);
-        CellHash hc{0ull, 0u};
-        if (a.has_coarse)
-            hc = key_hash(make_key(cfg, x, ks, cfg.jitter, cdu, cdv, cfg.coarse_delta, jt), ks);
+        int64_t cslot = -1;  // the coarse rung's slot: probed here, where rows run SIMT-wide
+        if (a.has_coarse) {
+            const CellHash hc =
+                key_hash(make_key(cfg, x, ks, cfg.jitter, cdu, cdv, cfg.coarse_delta, jt), ks);
+            cslot = probe_lookup(a.coarse.tags, static_cast<uint64_t>(a.coarse.capacity) - 1,
+                                 a.coarse.probe_limit, hc.index, hc.fp, a.seg_mask);
+        }
         longlong4 *o = reinterpret_cast<longlong4 *>(a.fb_keys + 8 * w);
         o[0] = make_longlong4(k.q[0], k.q[1], k.q[2], k.level);
-        o[1] = make_longlong4(static_cast<long long>(k.aux), static_cast<long long>(hc.index),
-                              static_cast<long long>(hc.fp), 0);
+        o[1] = make_longlong4(static_cast<long long>(k.aux), cslot, row, x.pixel);
     }
 }
 
@@ -565,17 +569,9 @@ __global__ void __launch_bounds__(kThreads) resolve_fallback_kernel(ResolveArgs 
     const uint64_t fmask = static_cast<uint64_t>(a.fine.capacity) - 1;
     for (int64_t w = warp0; w < n_work; w += nwarps) {
         const int64_t row = work_row(a, wl, w);
-        // the row's lookup key: from fallback_keys_kernel (lanes 0..7 load the record),
-        // else rebuilt by lane 0; broadcast to the 27 probing lanes
-        int64_t kq[3] = {0, 0, 0}, klev = 0, kaux = 0, krec = 0;
-        if (a.fb_keys != nullptr) {
-            if (lane < 8) krec = a.fb_keys[8 * w + lane];
-            kq[0] = __shfl_sync(kFull, static_cast<long long>(krec), 0);
-            kq[1] = __shfl_sync(kFull, static_cast<long long>(krec), 1);
-            kq[2] = __shfl_sync(kFull, static_cast<long long>(krec), 2);
-            klev = __shfl_sync(kFull, static_cast<long long>(krec), 3);
-            kaux = __shfl_sync(kFull, static_cast<long long>(krec), 4);
-        } else if (lane == 0) {
+        // the row's lookup key, built by lane 0 and broadcast to the 27 probing lanes
+        int64_t kq[3] = {0, 0, 0}, klev = 0, kaux = 0;
+        if (lane == 0) {
             const CellKey k = lookup_key(a, row).first;
             kq[0] = k.q[0];
             kq[1] = k.q[1];
@@ -608,13 +604,7 @@ __global__ void __launch_bounds__(kThreads) resolve_fallback_kernel(ResolveArgs 
         bool coarse_found = false;
         Effective ce{};
         if (!ok_n && a.has_coarse) {
-            CellHash h;
-            if (a.fb_keys != nullptr) {
-                h.index = static_cast<uint64_t>(a.fb_keys[8 * w + 5]);
-                h.fp = static_cast<uint32_t>(a.fb_keys[8 * w + 6]);
-            } else {
-                h = vertex_key(cfg, a.v, a.h0_coarse, row, cfg.coarse_delta).second;
-            }
+            const CellHash h = vertex_key(cfg, a.v, a.h0_coarse, row, cfg.coarse_delta).second;
             const int64_t s = probe_lookup(a.coarse.tags, static_cast<uint64_t>(a.coarse.capacity) - 1,
                                            a.coarse.probe_limit, h.index, h.fp, a.seg_mask);
             if (s >= 0) {
@@ -639,19 +629,24 @@ __global__ void __launch_bounds__(kThreads) resolve_fallback_kernel(ResolveArgs 
 }
 
 // Rungs 2-5 with the neighbourhood probes spread over the whole CTA: a pass takes
-// kPoolRows work rows (keys from fallback_keys_kernel), their 27 x kPoolRows cell
-// probes run 3-4 per thread back to back (independent loads in flight), the found
-// cells' effective values land in shared memory, and one thread per row then pools
-// them in (dx, dy, dz) order, runs the coarse rung and the ladder and composites.
+// kPoolRows work rows (keys, coarse slots, rows and pixels from fallback_keys_kernel),
+// their 27 x kPoolRows cell probes run 3-4 per thread with all home tags, then all
+// records, in flight together (records by cp.async into shared memory), the last warp
+// fetches the rows' coarse records and composite inputs meanwhile, and the rows are
+// then pooled (kLanesPerRow threads per row for integer pools; one, in (dx, dy, dz)
+// order, for float64 pools), laddered and composited.
 #ifndef PF_POOL_ROWS
 #define PF_POOL_ROWS 32
 #endif
 constexpr int kPoolRows = PF_POOL_ROWS;
 constexpr int kPoolCells = 27 * kPoolRows;
+constexpr int kLanesPerRow = kThreads / kPoolRows;  // the per-row phase's threads per row
+static_assert(kLanesPerRow >= 1 && kLanesPerRow <= 32 && (kLanesPerRow & (kLanesPerRow - 1)) == 0,
+              "rows of the pool's per-row phase must tile warps");
 
 struct PoolSmem {
     int64_t key[kPoolRows][8];
-    uint64_t word[kPoolCells][4];   // sum x3 (int64 or float64 bits), count (same dtype)
+    alignas(16) uint64_t word[kPoolCells][4];  // sum x3 (int64 or float64 bits), count (float64)
     uint8_t found[kPoolCells];
     // per row, fetched in the probe phase by the CTA's last warp (so the serial per-row
     // phase does no global round trips): the coarse cell's effective value, the row's
@@ -664,7 +659,10 @@ struct PoolSmem {
     int64_t row[kPoolRows];
 };
 
-__global__ void __launch_bounds__(kThreads) resolve_pool_kernel(ResolveArgs a) {
+#ifndef PF_POOL_MIN_BLOCKS
+#define PF_POOL_MIN_BLOCKS 3
+#endif
+__global__ void __launch_bounds__(kThreads, PF_POOL_MIN_BLOCKS) resolve_pool_kernel(ResolveArgs a) {
     __shared__ BlockStats bs;
     __shared__ PoolSmem ps;
     stats_init(bs, false);
@@ -688,54 +686,109 @@ __global__ void __launch_bounds__(kThreads) resolve_pool_kernel(ResolveArgs a) {
                 ps.key[q >> 3][q & 7] = a.fb_keys[8 * base + q];
         }
         __syncthreads();
-        {  // the CTA's last warps: each lane one row's coarse rung and composite inputs
+        {  // the CTA's last warp: each lane one row's coarse rung and composite inputs, one
+           // round trip beside the probes (slot, row and pixel come with the key record)
             const int r = kThreads - 1 - static_cast<int>(threadIdx.x);
             if (r < rows) {
-                const int64_t row = work_row(a, wl, base + r);
+                const int64_t cs = ps.key[r][5], row = ps.key[r][6];
                 ps.row[r] = row;
-                ps.pixel[r] = __ldg(a.v.pixel + row);
+                ps.pixel[r] = ps.key[r][7];
 #pragma unroll
                 for (int c = 0; c < 3; ++c) {
                     ps.contrib[r][c] = __ldg(a.v.contribution + 3 * row + c);
                     ps.tp[r][c] = __ldg(a.v.throughput + 3 * row + c);
                 }
-                bool found = false;
-                if (a.has_coarse) {
-                    const int64_t cs = probe_lookup(a.coarse.tags, static_cast<uint64_t>(a.coarse.capacity) - 1,
-                                                    a.coarse.probe_limit,
-                                                    static_cast<uint64_t>(ps.key[r][5]),
-                                                    static_cast<uint32_t>(ps.key[r][6]), a.seg_mask);
-                    if (cs >= 0) {
-                        found = true;
-                        ps.coarse[r] = coarse_effective(a, cs);
-                    }
-                }
-                ps.coarse_found[r] = found;
+                if (cs >= 0) ps.coarse[r] = coarse_effective(a, cs);
+                ps.coarse_found[r] = cs >= 0;
             }
         }
-        for (int p = threadIdx.x; p < 27 * rows; p += kThreads) {
-            const int r = p / 27, j = p - 27 * (p / 27);
-            const CellHash h = cell_hash(ps.key[r][0] + neighbour_dx(j), ps.key[r][1] + neighbour_dy(j),
-                                         ps.key[r][2] + neighbour_dz(j), ps.key[r][3],
-                                         static_cast<uint64_t>(ps.key[r][4]), 0, 0u);
-            const int64_t s = probe_lookup(a.fine.tags, fmask, a.fine.probe_limit, h.index, h.fp,
-                                           a.seg_mask);
-            ps.found[p] = s >= 0;
-            if (s >= 0) {
-                const Effective e = fine_effective(a, s);
+        {  // this thread's probes p = threadIdx.x + u * kThreads: every home tag, then
+           // every found cell's record, each batch issued back to back
+            constexpr int kPP = (kPoolCells + kThreads - 1) / kThreads;
+            const int np = 27 * rows;
+            uint64_t home[kPP], tg[kPP];
+            uint32_t fp[kPP];
 #pragma unroll
-                for (int c = 0; c < 3; ++c)
-                    ps.word[p][c] = as_int ? static_cast<uint64_t>(e.isum[c])
-                                           : static_cast<uint64_t>(__double_as_longlong(e.fsum[c]));
-                ps.word[p][3] = int_cnt ? static_cast<uint64_t>(e.icnt)
-                                        : static_cast<uint64_t>(__double_as_longlong(e.fcnt));
+            for (int u = 0; u < kPP; ++u) {
+                const int p = static_cast<int>(threadIdx.x) + u * kThreads;
+                tg[u] = kEmptyTag;
+                if (p < np) {
+                    const int r = p / 27, j = p - 27 * (p / 27);
+                    const CellHash h = cell_hash(ps.key[r][0] + neighbour_dx(j),
+                                                 ps.key[r][1] + neighbour_dy(j),
+                                                 ps.key[r][2] + neighbour_dz(j), ps.key[r][3],
+                                                 static_cast<uint64_t>(ps.key[r][4]), 0, 0u);
+                    home[u] = h.index;
+                    fp[u] = h.fp;
+                    tg[u] = __ldg(reinterpret_cast<const unsigned long long *>(a.fine.tags) +
+                                  (h.index & fmask));
+                }
+            }
+            int64_t slot[kPP];
+#pragma unroll
+            for (int u = 0; u < kPP; ++u) {
+                const int p = static_cast<int>(threadIdx.x) + u * kThreads;
+                slot[u] = -1;
+                if (p < np && tg[u] != kEmptyTag) {
+                    slot[u] = (tg[u] & kFpMask) == static_cast<uint64_t>(fp[u])
+                                  ? static_cast<int64_t>(home[u] & fmask)
+                                  : probe_lookup(a.fine.tags, fmask, a.fine.probe_limit, home[u],
+                                                 fp[u], a.seg_mask, 1);
+                }
+            }
+            if (a.rec != nullptr) {  // records straight into shared memory (cp.async)
+#pragma unroll
+                for (int u = 0; u < kPP; ++u) {
+                    const int p = static_cast<int>(threadIdx.x) + u * kThreads;
+                    if (p < np) ps.found[p] = slot[u] >= 0;
+                    if (slot[u] >= 0) {
+                        const uint64_t *rp = reinterpret_cast<const uint64_t *>(a.rec + slot[u]);
+                        cp_async_16(&ps.word[p][0], rp);
+                        cp_async_16(&ps.word[p][2], rp + 2);
+                    }
+                }
+                cp_async_wait_all();
+            } else {
+#pragma unroll
+                for (int u = 0; u < kPP; ++u) {
+                    const int p = static_cast<int>(threadIdx.x) + u * kThreads;
+                    if (p < np) ps.found[p] = slot[u] >= 0;
+                    if (slot[u] >= 0) {
+                        const Effective e = fine_effective(a, slot[u]);
+#pragma unroll
+                        for (int c = 0; c < 3; ++c)
+                            ps.word[p][c] = as_int ? static_cast<uint64_t>(e.isum[c])
+                                                   : static_cast<uint64_t>(__double_as_longlong(e.fsum[c]));
+                        ps.word[p][3] = static_cast<uint64_t>(__double_as_longlong(e.fcnt));
+                    }
+                }
             }
         }
         __syncthreads();
-        if (threadIdx.x < rows) {
-            const int r = threadIdx.x;
-            const int64_t row = ps.row[r];
-            Pool pool{{0, 0, 0}, 0, {0.0, 0.0, 0.0}, 0.0};
+        // kLanesPerRow threads per row: integer pools (order-free) are summed over the
+        // 27 cells in parallel and reduced by shuffles; float64 pools keep numpy's
+        // (dx, dy, dz) order on the row's first lane, which then runs the ladder
+        const int r = static_cast<int>(threadIdx.x) / kLanesPerRow;
+        const int sub = static_cast<int>(threadIdx.x) % kLanesPerRow;
+        Pool pool{{0, 0, 0}, 0, {0.0, 0.0, 0.0}, 0.0};
+        if (as_int && int_cnt) {
+            if (r < rows) {
+                for (int j = sub; j < 27; j += kLanesPerRow) {
+                    const int p = 27 * r + j;
+                    if (!ps.found[p]) continue;
+#pragma unroll
+                    for (int c = 0; c < 3; ++c) pool.isum[c] += static_cast<int64_t>(ps.word[p][c]);
+                    pool.icnt += static_cast<int64_t>(__longlong_as_double(ps.word[p][3]));
+                }
+            }
+#pragma unroll
+            for (int off = kLanesPerRow / 2; off > 0; off >>= 1) {
+#pragma unroll
+                for (int c = 0; c < 3; ++c)
+                    pool.isum[c] += __shfl_xor_sync(kFull, static_cast<long long>(pool.isum[c]), off);
+                pool.icnt += __shfl_xor_sync(kFull, static_cast<long long>(pool.icnt), off);
+            }
+        } else if (r < rows && sub == 0) {
             for (int j = 0; j < 27; ++j) {  // numpy's order for the float64 pools
                 const int p = 27 * r + j;
                 if (!ps.found[p]) continue;
@@ -744,9 +797,13 @@ __global__ void __launch_bounds__(kThreads) resolve_pool_kernel(ResolveArgs a) {
                     if (as_int) pool.isum[c] += static_cast<int64_t>(ps.word[p][c]);
                     else pool.fsum[c] = dadd(pool.fsum[c], __longlong_as_double(ps.word[p][c]));
                 }
-                if (int_cnt) pool.icnt += static_cast<int64_t>(ps.word[p][3]);
+                // count: float64 bits (the record's word; integral in integrate mode)
+                if (int_cnt) pool.icnt += static_cast<int64_t>(__longlong_as_double(ps.word[p][3]));
                 else pool.fcnt = dadd(pool.fcnt, __longlong_as_double(ps.word[p][3]));
             }
+        }
+        if (r < rows && sub == 0) {
+            const int64_t row = ps.row[r];
             double contrib[3], ch[3];
 #pragma unroll
             for (int c = 0; c < 3; ++c) contrib[c] = ps.contrib[r][c];
