@@ -340,4 +340,6 @@ def ptr(t) -> int | None:
 
 
 def stream_handle() -> int:
-    return torch.cuda.current_stream().cuda_stream
+    """cudaStream_t of torch's current stream on the current device (the raw accessor:
+    torch.cuda.current_stream() costs several microseconds per frame call)."""
+    return torch._C._cuda_getCurrentRawStream(torch._C._cuda_getDevice())

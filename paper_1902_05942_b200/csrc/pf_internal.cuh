@@ -103,6 +103,14 @@ inline int prepare_config(const char *fn, const pf_config *in, pf_config *out) {
     // over the (monotone) bit patterns of non-negative doubles.  make_key skips the exact
     // LOD of the jittered distance when the jitter cannot reach the next threshold.
     const double c = in->c_lod;
+    // the bisection (32 x ~63 steps) runs once per distinct (c_lod, thresholds): a frame
+    // loop passes the same config every call
+    thread_local double memo_c = std::numeric_limits<double>::quiet_NaN();
+    thread_local double memo_t[32], memo_d[32];
+    if (c == memo_c && std::memcmp(memo_t, in->lod_threshold, sizeof(memo_t)) == 0) {
+        std::memcpy(out->lod_dist, memo_d, sizeof(memo_d));
+        return PF_OK;
+    }
     for (int k = 0; k < 32; ++k) {
         double dk = std::numeric_limits<double>::quiet_NaN();
         if (c > 0.0 && c < std::numeric_limits<double>::infinity()) {
@@ -121,6 +129,9 @@ inline int prepare_config(const char *fn, const pf_config *in, pf_config *out) {
         }
         out->lod_dist[k] = dk;
     }
+    memo_c = c;
+    std::memcpy(memo_t, in->lod_threshold, sizeof(memo_t));
+    std::memcpy(memo_d, out->lod_dist, sizeof(memo_d));
     return PF_OK;
 }
 

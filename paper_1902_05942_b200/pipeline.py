@@ -14,6 +14,8 @@ from __future__ import annotations
 import ctypes
 from dataclasses import dataclass, field
 
+import math
+
 import numpy as np
 import torch
 
@@ -263,13 +265,22 @@ class FrameState:
         return cls(fine, coarse)
 
     def buffer(self, name: str, shape, dtype) -> torch.Tensor:
-        """Reusable device scratch (caching allocator friendly, no per-frame memsets)."""
-        n = int(np.prod(shape))
+        """Reusable device scratch (caching allocator friendly, no per-frame memsets).
+        The shaped view is cached too: a frame asks for the same nine buffers each call."""
+        shape = tuple(int(d) for d in shape) if isinstance(shape, (tuple, list)) else (int(shape),)
+        views = self.scratch.setdefault("_views", {})
+        hit = views.get(name)
+        if hit is not None and hit[0] == shape and hit[1] == dtype and \
+                hit[2] is self.scratch.get(name):
+            return hit[3]
+        n = math.prod(shape)
         b = self.scratch.get(name)
         if b is None or b.numel() < n or b.dtype != dtype:
             b = torch.empty(max(n, 1), dtype=dtype, device=device())
             self.scratch[name] = b
-        return b[:n].view(*shape) if n else b[:0]
+        v = b[:n].view(*shape) if n else b[:0]
+        views[name] = (shape, dtype, b, v)
+        return v
 
 
 class LazyKeyArrays:
@@ -378,10 +389,11 @@ def accumulate_phase(vertices, cfg: FilterConfig, state: FrameState, frame: int,
 
 
 def _register_event_drain(state: FrameState, frame: int, events: torch.Tensor,
-                          ev_count: torch.Tensor, parity: int):
+                          ev_count: torch.Tensor, parity: int) -> torch.cuda.Event:
     """Queue the eviction log of this frame: its count goes to pinned host memory
     without a sync; the rows are read before the device buffer (one of two, by frame
-    parity) is reused two frames later."""
+    parity) is reused two frames later.  Returns the event that marks the copy (and
+    every copy queued before it) landed."""
     host = state.pinned_count(parity)
     host.copy_(ev_count, non_blocking=True)
     done = torch.cuda.Event()
@@ -405,6 +417,7 @@ def _register_event_drain(state: FrameState, frame: int, events: torch.Tensor,
         return out
 
     state.fine._add_pending_events(drain, parity)
+    return done
 
 
 def _accumulate_ordered(vs, cfg, state, frame, seed, stats, fine_keys, coarse_keys):
@@ -518,26 +531,27 @@ def _fused_frame(vs: VertexStream, base_image, cfg: FilterConfig, state: FrameSt
     if state.coarse is not None:
         state.coarse.frame = frame
     state.lookup_keys = (vs, lookup_seed, cc, lk_keys[:n])
-    if n:
-        _register_event_drain(state, frame, events, ev_count, parity)
     stats = FrameStats(frame=frame, n_vertices=n, counters=acc)
     report = ResolveReport(source, image, chosen)
     report.counters = res
     fine_keys = LazyKeyArrays(vs, cfg, seed, rng.STREAM_JITTER_ACCUM, 0)
     coarse_keys = (LazyKeyArrays(vs, cfg, seed, rng.STREAM_JITTER_ACCUM, cfg.coarse_delta)
                    if state.coarse is not None else None)
-    if flag is not None and n:
-        if validate == "sync":
-            raise_if_bad(flag)
-        else:  # deferred: queue the flag read, raise when it has landed
-            key = f"_pinned_flag{parity}"
-            if key not in state.scratch:
-                state.scratch[key] = torch.empty(1, dtype=torch.int32).pin_memory()
-            host = state.scratch[key]
-            host.copy_(flag, non_blocking=True)
-            done = torch.cuda.Event()
-            done.record()
-            state.pending_validation.append((host, done, frame, parity))
+    flag_host = None
+    if flag is not None and n and validate != "sync":
+        # deferred: queue the flag read, raise when it has landed (the eviction count's
+        # event below marks both copies)
+        key = f"_pinned_flag{parity}"
+        if key not in state.scratch:
+            state.scratch[key] = torch.empty(1, dtype=torch.int32).pin_memory()
+        flag_host = state.scratch[key]
+        flag_host.copy_(flag, non_blocking=True)
+    if n:
+        done = _register_event_drain(state, frame, events, ev_count, parity)
+        if flag_host is not None:
+            state.pending_validation.append((flag_host, done, frame, parity))
+    if flag is not None and n and validate == "sync":
+        raise_if_bad(flag)
     return image, report, stats, fine_keys, coarse_keys
 
 

@@ -69,3 +69,14 @@ def test_gpus_flag_must_match_world_size():
                          capture_output=True, text=True, timeout=120, cwd=ROOT, env=env)
     assert out.returncode != 0
     assert "refusing" in out.stderr
+
+
+def test_table_bench_point_lines():
+    """paper_1902_05942_b200.bench mirrors src/bench.py's BenchPoint / spread."""
+    from paper_1902_05942_b200.bench import BenchPoint, spread
+    a = BenchPoint("b200", 100_000, 131072, 1e-4, 2e-5, 1.5e-5)
+    b = BenchPoint("b200", 1_000_000, 1 << 20, 4e-4, 1e-4, 5e-5)
+    assert a.line().startswith("backend=b200 n=100000 capacity=131072 accumulate_s=0.0001")
+    assert "per_vertex_ns=1.2" in a.line() and "device_per_vertex_ns=0.150" in a.line()
+    assert abs(spread([a, b]) - 1.2 / 0.5) < 1e-9
+    assert abs(spread([a, b], device=True) - 0.15 / 0.05) < 1e-9
