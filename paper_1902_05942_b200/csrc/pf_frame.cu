@@ -273,19 +273,29 @@ constexpr int64_t kNoTouch = INT64_MIN;  // touch_frame of a sweep without defer
 __global__ void __launch_bounds__(kThreads)
 effective_records_kernel(pf_table t, int mode, double ema, double delta_max, ulonglong4 *rec,
                          pf_table coarse, int has_coarse, int64_t touch_frame,
-                         unsigned nb_fine, double *flat, int64_t flat_words, int64_t *counter) {
+                         unsigned nb_fine, double *flat, int64_t flat_words, int64_t *counter,
+                         const double *flat_init) {
     __shared__ SweepSmem<kThreads> q;
     pdl_wait();  // multi-wave kernels do not trigger early: waiting dependents would take
                  // the slots of their later waves
     // the resolve's composite buffer and work counter start at zero (in this launch rather
-    // than a memset, which would break the frame's PDL chain)
+    // than a memset, which would break the frame's PDL chain); with flat_init the buffer
+    // starts at flat_init + 0.0 instead (the image itself at spp = 1, see resolve_frame)
     if (flat != nullptr) {
         double2 *f2 = reinterpret_cast<double2 *>(flat);
+        const double2 *i2 = reinterpret_cast<const double2 *>(flat_init);
         const int64_t pairs = flat_words / 2;
         for (int64_t k = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x; k < pairs;
-             k += static_cast<int64_t>(gridDim.x) * blockDim.x)
-            f2[k] = make_double2(0.0, 0.0);
-        if (blockIdx.x == 0 && threadIdx.x == 0 && (flat_words & 1)) flat[flat_words - 1] = 0.0;
+             k += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+            double2 v = make_double2(0.0, 0.0);
+            if (i2 != nullptr) {
+                const double2 b = __ldg(i2 + k);
+                v = make_double2(dadd(b.x, 0.0), dadd(b.y, 0.0));
+            }
+            f2[k] = v;
+        }
+        if (blockIdx.x == 0 && threadIdx.x == 0 && (flat_words & 1))
+            flat[flat_words - 1] = flat_init ? dadd(flat_init[flat_words - 1], 0.0) : 0.0;
     }
     if (counter != nullptr && blockIdx.x == 0 && threadIdx.x < PF_WORK_LISTS) counter[threadIdx.x] = 0;
     if (blockIdx.x >= nb_fine) {
@@ -311,7 +321,7 @@ effective_records_kernel(pf_table t, int mode, double ema, double delta_max, ulo
 static int launch_post_insert(const char *fn, const pf_table &fine, const pf_table *coarse,
                               const pf_config &kc, uint64_t *eff_records, int64_t touch_frame,
                               cudaStream_t st, double *flat = nullptr, int64_t flat_words = 0,
-                              int64_t *counter = nullptr) {
+                              int64_t *counter = nullptr, const double *flat_init = nullptr) {
     if (eff_records == nullptr && touch_frame == kNoTouch && flat == nullptr && counter == nullptr)
         return PF_OK;
     const unsigned nf = sweep_blocks<kThreads>(fine.capacity, sm_count());
@@ -320,7 +330,7 @@ static int launch_post_insert(const char *fn, const pf_table &fine, const pf_tab
     launch_pdl(effective_records_kernel, dim3(nf + nc), dim3(kThreads), st, fine,
                kc.temporal_mode, kc.ema_alpha, kc.delta_max,
                reinterpret_cast<ulonglong4 *>(eff_records), tc ? *coarse : fine,
-               static_cast<int>(tc), touch_frame, nf, flat, flat_words, counter);
+               static_cast<int>(tc), touch_frame, nf, flat, flat_words, counter, flat_init);
     return check_launch(fn);
 }
 
@@ -937,7 +947,8 @@ static int resolve_frame(const char *fn, const pf_config *cfg, const pf_vertices
                          int64_t n_pixels, double *image, double *flat, int64_t *work,
                          int64_t *work_count, uint8_t *source, double *chosen, int64_t *stats,
                          const uint64_t *lookup_keys, uint64_t *eff_records,
-                         int64_t *fallback_keys, int64_t touch_frame, void *stream) {
+                         int64_t *fallback_keys, int64_t touch_frame, void *stream,
+                         bool fold_base = false) {
     if (int rc = validate_vertices(fn, v, cfg)) return rc;
     pf_config kc;
     if (int rc = prepare_config(fn, cfg, &kc)) return rc;
@@ -977,12 +988,23 @@ static int resolve_frame(const char *fn, const pf_config *cfg, const pf_vertices
         a.pixel_base = 0;
         a.seg_mask = ~0ull;
         a.crec = nullptr;
-        // flat = 0 and the work counter = 0 ride on the effective-record sweep
-        if (int rc = launch_post_insert(fn, *fine, coarse, kc, eff_records, touch_frame, st, flat,
-                                        3 * n_pixels, work_count))
+        // At spp = 1 (fold_base) the composite goes straight into the image, which
+        // starts at base + 0.0: image = base + flat / 1 without the finalize pass.  A pixel
+        // with one vertex gets RN(base + c) as the reference does (and base + 0.0 with
+        // none); with several, the float sums' order changes as it already does with
+        // the order of the composite REDs.
+        const bool fold = fold_base && spp == 1 &&
+                          ((reinterpret_cast<uintptr_t>(image) |
+                            reinterpret_cast<uintptr_t>(base_image)) & 15) == 0;
+        if (fold) a.flat = image;
+        // flat = 0 (or base) and the work counter = 0 ride on the effective-record sweep
+        if (int rc = launch_post_insert(fn, *fine, coarse, kc, eff_records, touch_frame, st,
+                                        a.flat, 3 * n_pixels, work_count,
+                                        fold ? base_image : nullptr))
             return rc;
         if (int rc = launch_rungs(fn, a, v->n, lookup_keys != nullptr, fallback_keys != nullptr, st))
             return rc;
+        if (fold) return check_launch(fn);
     }
     const int64_t m = 3 * n_pixels;
     if (m > 0)
@@ -1123,7 +1145,7 @@ int pf_filter_frame(const pf_config *cfg, const pf_vertices *v, const pf_table *
     const int rc = resolve_frame(fn, cfg, v, fine, coarse, stream_base_lookup, stream_base_coarse,
                                  spp, base_image, n_pixels, image, b->flat, b->work,
                                  b->work_count, source, chosen, b->res_stats, b->lookup_keys,
-                                 b->eff_records, b->fallback_keys, frame, stream);
+                                 b->eff_records, b->fallback_keys, frame, stream, true);
     mark(3);
     return rc;
 }
