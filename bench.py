@@ -582,11 +582,12 @@ def run_b200(args):
 
     in_bytes = QUERY_BYTES_PER_VERTEX * n + QUERY_BYTES_PER_PIXEL * n_pix
     if rank == 0:
-        # single: prologue, insert, effective records (+ flat / work-counter zeroing),
-        # resolve main, fallback keys, pool, finalize.  sharded: begin x2, check, keys, emit, apply,
-        # reset, publish x2, replica clear + write, resolve main, fallback keys, pool,
-        # finalize (NCCL kernels not counted)
-        launches = (7 if world == 1 else 15) * args.steps
+        # single: prologue, insert, effective records (+ image = base / work-counter
+        # init), resolve main, fallback keys, pool (spp = 1: the composite lands in the
+        # image, no finalize).  sharded: begin x2, check, keys, emit, apply, reset,
+        # publish x2, replica clear + write, resolve main, fallback keys, pool, finalize
+        # (NCCL kernels not counted)
+        launches = (6 if world == 1 else 15) * args.steps
         line = {
             "metric": METRIC, "value": value, "unit": "vertices/s", "n_gpus": world,
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms_per_step,
@@ -617,7 +618,7 @@ def run_b200(args):
                            "table_layout": "dense tags and counts, channel-major live sums, "
                                            "64-byte cold records; 32 MB L2 set-aside for "
                                            "evict_last table / composite lines",
-                           "kernel_chain": "7 kernels per frame with programmatic dependent "
+                           "kernel_chain": "6 kernels per frame with programmatic dependent "
                                            "launch"}},
             "phases_ms": ph, "roofline": roofline, "roofline_issue": issue,
             "roofline_atomics": atomics, "cpu_baseline": cpu,

@@ -365,6 +365,9 @@ __device__ __forceinline__ void composite(const ResolveArgs &a, int64_t i, int64
 #ifndef PF_RESOLVE_MIN_BLOCKS
 #define PF_RESOLVE_MIN_BLOCKS 4  // 4 x 256 threads per SM: <= 64 registers
 #endif
+#ifndef PF_RESOLVE_SPEC
+#define PF_RESOLVE_SPEC 1  // the home slot's record loaded beside its tag
+#endif
 template <int KV, bool HAVE_KEYS>
 __global__ void __launch_bounds__(kThreads, PF_RESOLVE_MIN_BLOCKS) resolve_main_kernel(ResolveArgs a) {
     // no CTA counters and no barriers: the fine / fallback row counts follow from the
@@ -403,6 +406,14 @@ __global__ void __launch_bounds__(kThreads, PF_RESOLVE_MIN_BLOCKS) resolve_main_
 #pragma unroll
     for (int k = 0; k < KV; ++k) tag[k] = __ldg(reinterpret_cast<const unsigned long long *>(
                                       a.fine.tags) + (h[k].index & fmask));
+#if PF_RESOLVE_SPEC
+    // the home slot's record in flight beside its tag (most keys sit at home)
+    ulonglong4 srec[KV];
+    if (a.rec != nullptr) {
+#pragma unroll
+        for (int k = 0; k < KV; ++k) srec[k] = load_record(a.rec, static_cast<int64_t>(h[k].index & fmask));
+    }
+#endif
     int64_t slot[KV];
 #pragma unroll
     for (int k = 0; k < KV; ++k) {
@@ -415,6 +426,11 @@ __global__ void __launch_bounds__(kThreads, PF_RESOLVE_MIN_BLOCKS) resolve_main_
     Effective ef[KV];
 #pragma unroll
     for (int k = 0; k < KV; ++k) {
+#if PF_RESOLVE_SPEC
+        if (slot[k] >= 0 && a.rec != nullptr && slot[k] == static_cast<int64_t>(h[k].index & fmask))
+            ef[k] = unpack_effective(srec[k], eff_is_int(a.fine, cfg.temporal_mode));
+        else
+#endif
         if (slot[k] >= 0) ef[k] = fine_effective(a, slot[k]);
 #if !PF_RESOLVE_HOIST
         pixel[k] = ld_stream(a.v.pixel + row[k], stream) - a.pixel_base;
