@@ -666,14 +666,31 @@ __device__ __forceinline__ void jitter_dir(double u, double v, const double t1[3
     for (int c = 0; c < 3; ++c) w[c] = dadd(dmul(u, t1[c]), dmul(v, t2[c]));
 }
 
+#ifndef PF_STEP_TABLE
+#define PF_STEP_TABLE 1
+#endif
+// Per-level {step, RN(1/step)} = {base_voxel * 2^l, rbv * 2^-l} for l = 0..31 (every level
+// of a finite distance), staged in shared memory by the key kernels: one LDS.128 instead
+// of two exponent builds and products per use.
+__device__ __forceinline__ void stage_level_steps(double2 *smem, const pf_config &cfg) {
+    if (threadIdx.x < 32) {
+        const int64_t l = threadIdx.x;
+        smem[l] = make_double2(voxel_step(cfg.base_voxel, l), dmul(cfg.inv_base_voxel, pow2i(-l)));
+    }
+}
+
 // make_key_arrays for one vertex and one level_delta (src/keys.py:342-359), given the
-// jitter direction w (jitter_dir; ignored when jit = 0).
+// jitter direction w (jitter_dir; ignored when jit = 0).  steps: stage_level_steps'
+// table (or NULL).
 __device__ __forceinline__ CellKey make_key_w(const pf_config &cfg, const VertexIn &x,
                                               const KeyShared &ks, int jit, const double w[3],
-                                              int32_t level_delta, double jittered[3]) {
+                                              int32_t level_delta, double jittered[3],
+                                              const double2 *steps = nullptr) {
     int64_t lv = clamp_level(ks.lv0, level_delta);
+    const bool tab = PF_STEP_TABLE && steps != nullptr;
     if (jit) {
-        const double step = voxel_step(cfg.base_voxel, lv);
+        const double step = tab && static_cast<uint64_t>(lv) < 32u ? steps[lv].x
+                                                                  : voxel_step(cfg.base_voxel, lv);
         double d2 = 0.0;
 #pragma unroll
         for (int c = 0; c < 3; ++c) jittered[c] = dadd(x.pos[c], dmul(w[c], step));
@@ -690,8 +707,15 @@ __device__ __forceinline__ CellKey make_key_w(const pf_config &cfg, const Vertex
 #pragma unroll
         for (int c = 0; c < 3; ++c) jittered[c] = x.pos[c];
     }
-    const double step = voxel_step(cfg.base_voxel, lv);
-    const double rstep = dmul(ks.rbv, pow2i(-lv));
+    double step, rstep;
+    if (tab && static_cast<uint64_t>(lv) < 32u) {
+        const double2 sr = steps[lv];
+        step = sr.x;
+        rstep = sr.y;
+    } else {
+        step = voxel_step(cfg.base_voxel, lv);
+        rstep = dmul(ks.rbv, pow2i(-lv));
+    }
     CellKey k;
     // IEEE x / step (not a reciprocal multiply: base_voxel is inexact), via Markstein
     double qd[3];
@@ -707,10 +731,11 @@ __device__ __forceinline__ CellKey make_key_w(const pf_config &cfg, const Vertex
 // jit = 0 disables jitter; (u, v) are the disc offsets.
 __device__ __forceinline__ CellKey make_key(const pf_config &cfg, const VertexIn &x,
                                             const KeyShared &ks, int jit, double u, double v,
-                                            int32_t level_delta, double jittered[3]) {
+                                            int32_t level_delta, double jittered[3],
+                                            const double2 *steps = nullptr) {
     double w[3] = {0.0, 0.0, 0.0};
     if (jit) jitter_dir(u, v, ks.frame.t1, ks.frame.t2, w);
-    return make_key_w(cfg, x, ks, jit, w, level_delta, jittered);
+    return make_key_w(cfg, x, ks, jit, w, level_delta, jittered, steps);
 }
 
 __device__ __forceinline__ CellHash key_hash(const CellKey &k, const KeyShared &ks) {

@@ -88,10 +88,12 @@ insert_frame_kernel(pf_config cfg, pf_vertices v, pf_table fine, pf_table coarse
     __shared__ double posm[3][kThreads];  // per-thread vertex position
 #endif
     __shared__ __align__(16) uint64_t home_pair[2][kThreads][2];  // fine / coarse home tag pairs
+    __shared__ double2 lvsteps[32];
 
     stats_init(bs);
     stage_sincos_table(sincos_tab);
     stage_lod_dist(lod_dist, cfg);
+    stage_level_steps(lvsteps, cfg);
     pdl_wait();
     pdl_trigger();
     if (abort_flag != nullptr && *abort_flag != 0) return;  // invalid input: no mutation
@@ -159,7 +161,8 @@ insert_frame_kernel(pf_config cfg, pf_vertices v, pf_table fine, pf_table coarse
             const VertexIn &xk = x;
 #endif
             const CellHash h = key_hash(
-                make_key_w(cfg, xk, ks, cfg.jitter, w, set == 1 ? cfg.coarse_delta : 0, jt), ks);
+                make_key_w(cfg, xk, ks, cfg.jitter, w, set == 1 ? cfg.coarse_delta : 0, jt,
+                           lvsteps), ks);
             // home-slot tag copies go out as soon as a hash exists; the next key set's
             // arithmetic hides their L2 latency before warp_insert consumes them
             if (set < 2) {
@@ -533,8 +536,10 @@ __device__ __forceinline__ void main_row_counts(const ResolveArgs &a, int64_t n_
 __global__ void __launch_bounds__(kThreads) fallback_keys_kernel(ResolveArgs a) {
     __shared__ double2 sincos_tab[220];
     __shared__ double lod_dist[32];
+    __shared__ double2 lvsteps[32];
     stage_sincos_table(sincos_tab);
     stage_lod_dist(lod_dist, a.cfg);
+    stage_level_steps(lvsteps, a.cfg);
     __shared__ WorkLists wl;
     pdl_wait();
     pdl_trigger();
@@ -559,11 +564,11 @@ __global__ void __launch_bounds__(kThreads) fallback_keys_kernel(ResolveArgs a) 
             }
         }
         double jt[3];
-        const CellKey k = make_key(cfg, x, ks, cfg.jitter, du, dv, 0, jt);
+        const CellKey k = make_key(cfg, x, ks, cfg.jitter, du, dv, 0, jt, lvsteps);
         int64_t cslot = -1;  // the coarse rung's slot: probed here, where rows run SIMT-wide
         if (a.has_coarse) {
             const CellHash hc =
-                key_hash(make_key(cfg, x, ks, cfg.jitter, cdu, cdv, cfg.coarse_delta, jt), ks);
+                key_hash(make_key(cfg, x, ks, cfg.jitter, cdu, cdv, cfg.coarse_delta, jt, lvsteps), ks);
             cslot = probe_lookup(a.coarse.tags, static_cast<uint64_t>(a.coarse.capacity) - 1,
                                  a.coarse.probe_limit, hc.index, hc.fp, a.seg_mask);
         }
