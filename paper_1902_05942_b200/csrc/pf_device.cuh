@@ -52,6 +52,18 @@ __device__ __forceinline__ void pdl_trigger() {
 #endif
 }
 
+// Kernel parameters the key / insert loops (and the shard apply) address dynamically (the fine or the coarse
+// table by key set) stay in parameter space: without __grid_constant__ the compiler
+// copies every such struct to local memory at entry and the loops read it back with LDL.
+#ifndef PF_GRID_CONSTANT
+#define PF_GRID_CONSTANT 1
+#endif
+#if PF_GRID_CONSTANT
+#define PF_GRID_CONST __grid_constant__
+#else
+#define PF_GRID_CONST
+#endif
+
 // ------------------------------------------------------------------ slot fields
 // Addresses of slot s's fields (pf_table: SoA or the interleaved 128-byte record).
 __device__ __forceinline__ int64_t *cnt_at(const pf_table &t, int64_t s) {

@@ -74,7 +74,9 @@ __device__ __forceinline__ void log_eviction(pf_evict_event *events, int64_t *co
 
 template <bool FIXED>
 __global__ void __launch_bounds__(kThreads, PF_INSERT_MIN_BLOCKS)
-insert_frame_kernel(pf_config cfg, pf_vertices v, pf_table fine, pf_table coarse, int has_coarse,
+insert_frame_kernel(const PF_GRID_CONST pf_config cfg, const PF_GRID_CONST pf_vertices v,
+                    const PF_GRID_CONST pf_table fine, const PF_GRID_CONST pf_table coarse,
+                    int has_coarse,
                     uint64_t h0, int64_t frame, int64_t *stats, pf_evict_event *events,
                     int64_t *event_count, int64_t event_cap, const int32_t *abort_flag,
                     uint64_t h0_lookup, uint64_t *lk_keys) {

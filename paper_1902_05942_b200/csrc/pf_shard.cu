@@ -316,7 +316,8 @@ __device__ __forceinline__ uint64_t local_index(const ShardK &k, uint64_t home) 
 
 template <bool FIXED>
 __global__ void __launch_bounds__(kT)
-shard_apply_kernel(ShardK k, pf_table fine, pf_table coarse, int has_coarse, const int64_t *rec,
+shard_apply_kernel(ShardK k, const PF_GRID_CONST pf_table fine, const PF_GRID_CONST pf_table coarse,
+                   int has_coarse, const int64_t *rec,
                    int64_t n, int64_t frame, int64_t *stats) {
     __shared__ BlockStats bs;
     stats_init(bs);
