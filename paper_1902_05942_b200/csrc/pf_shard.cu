@@ -174,11 +174,13 @@ __device__ __forceinline__ int64_t warp_agg_insert(const ShardK &k, OwnerCounts 
 
 template <bool FIXED>
 __global__ void __launch_bounds__(kT, PF_SHARD_KEYS_MIN_BLOCKS)
-shard_keys_kernel(pf_config cfg, pf_vertices v, ShardK k, int has_coarse, uint64_t h0,
+shard_keys_kernel(const PF_GRID_CONST pf_config cfg, const PF_GRID_CONST pf_vertices v,
+                  const PF_GRID_CONST ShardK k, int has_coarse, uint64_t h0,
                   uint64_t h0_lookup, const int32_t *abort_flag, uint64_t *lk_keys) {
     __shared__ OwnerCounts oc;
     __shared__ double2 sincos_tab[220];
     __shared__ double lod_dist[32];
+    __shared__ double2 lvsteps[32];
 #if PF_SHARD_PARK
     __shared__ double park[9][kT];  // t1, t2, position per thread
 #endif
@@ -186,6 +188,7 @@ shard_keys_kernel(pf_config cfg, pf_vertices v, ShardK k, int has_coarse, uint64
     owner_init(oc, k.s.world);
     stage_sincos_table(sincos_tab);
     stage_lod_dist(lod_dist, cfg);
+    stage_level_steps(lvsteps, cfg);
     __syncthreads();
     const int64_t tiles = (v.n + kT - 1) / kT;
     for (int64_t tile = blockIdx.x; tile < tiles; tile += gridDim.x) {
@@ -241,7 +244,8 @@ shard_keys_kernel(pf_config cfg, pf_vertices v, ShardK k, int has_coarse, uint64
             const VertexIn &xk = x;
 #endif
             const CellHash h = key_hash(
-                make_key_w(cfg, xk, ks, cfg.jitter, w, set == 1 ? cfg.coarse_delta : 0, jt), ks);
+                make_key_w(cfg, xk, ks, cfg.jitter, w, set == 1 ? cfg.coarse_delta : 0, jt,
+                           lvsteps), ks);
             if (set < 2) {
                 const uint64_t key = agg_key(set, h.index & k.home_mask, h.fp);
                 int64_t qs[3] = {q[0], q[1], q[2]};

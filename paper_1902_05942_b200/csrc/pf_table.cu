@@ -22,7 +22,7 @@ struct BatchOut {
 // Parallel batch insert (src/_native.pyx:186-258 semantics, warp-merged atomics).
 template <bool FIXED>
 __global__ void __launch_bounds__(kThreads)
-accumulate_kernel(pf_table t, const uint64_t *__restrict__ idx, const uint32_t *__restrict__ fp,
+accumulate_kernel(const PF_GRID_CONST pf_table t, const uint64_t *__restrict__ idx, const uint32_t *__restrict__ fp,
                   const double *__restrict__ vals, int64_t n, int64_t frame, BatchOut o) {
     const int64_t i = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
     const bool valid = i < n;

@@ -28,6 +28,9 @@ def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--worlds", default="1,2,4,8")
     ap.add_argument("--frames", type=int, default=5)
+    ap.add_argument("--repeat", type=int, default=3,
+                    help="timed runs per point; the fastest is reported (the loopback's "
+                         "host work between the ranks' kernels makes single runs noisy)")
     ap.add_argument("--width", type=int, default=1920)
     ap.add_argument("--height", type=int, default=1080)
     ap.add_argument("--stream", default="traced", choices=["traced", "synthetic"])
@@ -51,14 +54,18 @@ def main():
         for f in range(2):
             fn(f)
         torch.cuda.synchronize()
-        s, e = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-        t0 = time.perf_counter()
-        s.record()
-        for f in range(frames):
-            fn(10 + f)
-        e.record()
-        torch.cuda.synchronize()
-        return s.elapsed_time(e) / frames, (time.perf_counter() - t0) * 1e3 / frames
+        best = None
+        for rep in range(max(1, args.repeat)):
+            s, e = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            t0 = time.perf_counter()
+            s.record()
+            for f in range(frames):
+                fn(10 + rep * frames + f)
+            e.record()
+            torch.cuda.synchronize()
+            r = (s.elapsed_time(e) / frames, (time.perf_counter() - t0) * 1e3 / frames)
+            best = r if best is None or r[0] < best[0] else best
+        return best
 
     from paper_1902_05942_b200.scene import closed_box
     from paper_1902_05942_b200.tracer import multi_bounce_stream
