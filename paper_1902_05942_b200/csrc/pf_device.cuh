@@ -589,6 +589,13 @@ __device__ __forceinline__ void cp_async_16(void *smem, const void *gmem) {
     asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n\tcp.async.commit_group;"
                  ::"r"(s), "l"(gmem) : "memory");
 }
+// 8-byte global -> shared copy (L1-allocating .ca: .cg takes only 16 bytes) with an L2
+// policy, committed as its own group
+__device__ __forceinline__ void cp_async_8_hint(void *smem, const void *gmem, uint64_t pol) {
+    const unsigned s = static_cast<unsigned>(__cvta_generic_to_shared(smem));
+    asm volatile("cp.async.ca.shared.global.L2::cache_hint [%0], [%1], 8, %2;\n\tcp.async.commit_group;"
+                 ::"r"(s), "l"(gmem), "l"(pol) : "memory");
+}
 __device__ __forceinline__ void cp_async_wait_all() {
     asm volatile("cp.async.wait_all;" ::: "memory");
 }

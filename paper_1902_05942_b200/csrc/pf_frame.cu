@@ -373,8 +373,16 @@ __device__ __forceinline__ void composite(const ResolveArgs &a, int64_t i, int64
 #ifndef PF_RESOLVE_SPEC
 #define PF_RESOLVE_SPEC 1  // the home slot's record loaded beside its tag
 #endif
+#ifndef PF_RESOLVE_STAGE
+#define PF_RESOLVE_STAGE 1  // composite stream words staged in shared memory by cp.async
+#endif
+#ifndef PF_RESOLVE_KEYS_MIN_BLOCKS
+#define PF_RESOLVE_KEYS_MIN_BLOCKS 5  // with the insert's keys and staging: <= 48 registers
+#endif
 template <int KV, bool HAVE_KEYS>
-__global__ void __launch_bounds__(kThreads, PF_RESOLVE_MIN_BLOCKS) resolve_main_kernel(ResolveArgs a) {
+__global__ void __launch_bounds__(kThreads, HAVE_KEYS ? PF_RESOLVE_KEYS_MIN_BLOCKS
+                                                      : PF_RESOLVE_MIN_BLOCKS)
+resolve_main_kernel(ResolveArgs a) {
     // no CTA counters and no barriers: the fine / fallback row counts follow from the
     // work list (main_row_counts in the next kernel), rows outside the image are rare
     pdl_wait();
@@ -399,7 +407,17 @@ __global__ void __launch_bounds__(kThreads, PF_RESOLVE_MIN_BLOCKS) resolve_main_
             h[k] = lookup_key(a, row[k]).second;
         }
     }
-#if PF_RESOLVE_HOIST
+#if PF_RESOLVE_STAGE
+    // the composite's stream words go to shared memory by cp.async beside the key load:
+    // in flight through the key -> tag -> record chain without holding registers
+    static_assert(KV == 1, "staged resolve is one row per thread");
+    __shared__ int64_t stg_pix[kThreads];
+    __shared__ double stg_tp[3][kThreads];
+    cp_async_8_hint(&stg_pix[threadIdx.x], a.v.pixel + row[0], stream);
+#pragma unroll
+    for (int c = 0; c < 3; ++c)
+        cp_async_8_hint(&stg_tp[c][threadIdx.x], a.v.throughput + 3 * row[0] + c, stream);
+#elif PF_RESOLVE_HOIST
     // the composite's stream loads depend on nothing: in flight beside the key loads
 #pragma unroll
     for (int k = 0; k < KV; ++k) {
@@ -437,12 +455,18 @@ __global__ void __launch_bounds__(kThreads, PF_RESOLVE_MIN_BLOCKS) resolve_main_
         else
 #endif
         if (slot[k] >= 0) ef[k] = fine_effective(a, slot[k]);
-#if !PF_RESOLVE_HOIST
+#if !PF_RESOLVE_HOIST && !PF_RESOLVE_STAGE
         pixel[k] = ld_stream(a.v.pixel + row[k], stream) - a.pixel_base;
 #pragma unroll
         for (int c = 0; c < 3; ++c) tp[k][c] = ld_stream(a.v.throughput + 3 * row[k] + c, stream);
 #endif
     }
+#if PF_RESOLVE_STAGE
+    cp_async_wait_all();
+    pixel[0] = stg_pix[threadIdx.x] - a.pixel_base;
+#pragma unroll
+    for (int c = 0; c < 3; ++c) tp[0][c] = stg_tp[c][threadIdx.x];
+#endif
     const bool as_int = eff_is_int(a.fine, cfg.temporal_mode);
     const bool fixed = a.fine.sum_mode == PF_SUM_FIXED;
 #pragma unroll
