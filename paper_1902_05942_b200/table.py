@@ -256,21 +256,23 @@ class VoxelTable:
         return mean, int(self.counts[s])
 
     def probe_scan(self, h: CellHashes, accept) -> list:
-        """All occupied window slots whose fingerprint satisfies `accept` (src/table.py:186-203)."""
+        """All occupied window slots whose fingerprint satisfies `accept` (src/table.py:186-203).
+        The window's tags and counts come back in one gather; `accept` is the caller's
+        Python predicate, so the filter runs on the host; the accepted slots' means are one
+        device call."""
         mask = self.capacity - 1
         home = int(h.index) & mask
         window = [(home + j) & mask for j in range(self.probe_limit)]
         w = torch.tensor(window, dtype=torch.int64, device=self.tags.device)
         tags = u64_numpy(self.tags[w])
         cnts = self.counts[w].cpu().numpy()
-        out = []
-        for j, s in enumerate(window):
-            fp = int(tags[j]) & 0xFFFFFFFF
-            if fp == 0 or cnts[j] == 0:
-                continue
-            if accept(fp):
-                out.append((self.mean_at(np.array([s]))[0].cpu().numpy(), int(cnts[j])))
-        return out
+        hits = [j for j in range(len(window))
+                if (int(tags[j]) & 0xFFFFFFFF) != 0 and cnts[j] != 0
+                and accept(int(tags[j]) & 0xFFFFFFFF)]
+        if not hits:
+            return []
+        means = self.mean_at(np.array([window[j] for j in hits])).cpu().numpy()
+        return [(means[k], int(cnts[j])) for k, j in enumerate(hits)]
 
     def effective(self, mode: str, ema_alpha: float = 0.8, delta_max: float = 0.5):
         """Temporally blended (sum, count) per slot (src/table.py:205-238)."""
