@@ -23,7 +23,7 @@
 extern "C" {
 #endif
 
-#define PF_ABI_VERSION 6
+#define PF_ABI_VERSION 7
 
 enum pf_status {
     PF_OK = 0,
@@ -277,6 +277,15 @@ typedef struct pf_frame_buffers {
     int64_t *fallback_keys;         /* 8 * n, or NULL (see pf_resolve_frame) */
     void *phase_events[4];          /* optional cudaEvent_t recorded at frame start, just
                                        before the insert kernel, after it, at frame end */
+    /* Occupied-slot lists (optional).  occ_out[0] / occ_out[1] (int32[fine / coarse
+     * capacity]) receive the slots occupied when this frame ends and occ_count_out
+     * (int64[2], zeroed here) their counts.  A later frame may pass them back as occ_in /
+     * occ_count_in ONLY if nothing changed either table in between: its begin_frame then
+     * folds exactly those slots instead of sweeping the tag arrays.  NULL: sweep. */
+    int32_t *occ_in[2];
+    const int64_t *occ_count_in;
+    int32_t *occ_out[2];
+    int64_t *occ_count_out;
 } pf_frame_buffers;
 
 /* One whole frame of the filter -- src/pipeline.py:321-363 (render_frame) minus the

@@ -140,7 +140,9 @@ class PfFrameBuffers(ctypes.Structure):
                 ("eff_records", ctypes.c_void_p),
                 ("flat", ctypes.c_void_p), ("work", ctypes.c_void_p),
                 ("work_count", ctypes.c_void_p), ("fallback_keys", ctypes.c_void_p),
-                ("phase_events", ctypes.c_void_p * 4)]
+                ("phase_events", ctypes.c_void_p * 4),
+                ("occ_in", ctypes.c_void_p * 2), ("occ_count_in", ctypes.c_void_p),
+                ("occ_out", ctypes.c_void_p * 2), ("occ_count_out", ctypes.c_void_p)]
 
 
 class PfShard(ctypes.Structure):

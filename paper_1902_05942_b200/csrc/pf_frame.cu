@@ -275,11 +275,26 @@ constexpr int64_t kNoTouch = INT64_MIN;  // touch_frame of a sweep without defer
 // last_touch = frame there leaves the table byte-identical to the reference's
 // per-vertex store (src/_native.pyx:257) at a fraction of its L2 traffic.  Blocks
 // [0, nb_fine) sweep the fine table, the rest the coarse table (touch only).
+// Append slot s to an occupied-slot list (opportunistic warp aggregation over the lanes
+// that reach this call together).
+__device__ __forceinline__ void occ_append(int32_t *list, int64_t *count, int64_t s) {
+    const unsigned m = __activemask();
+    const int lane = threadIdx.x & 31;
+    const int leader = __ffs(m) - 1;
+    unsigned long long base = 0;
+    if (lane == leader)
+        base = atomicAdd(reinterpret_cast<unsigned long long *>(count),
+                         static_cast<unsigned long long>(__popc(m)));
+    base = __shfl_sync(m, base, leader);
+    list[base + __popc(m & ((1u << lane) - 1u))] = static_cast<int32_t>(s);
+}
+
 __global__ void __launch_bounds__(kThreads)
-effective_records_kernel(pf_table t, int mode, double ema, double delta_max, ulonglong4 *rec,
-                         pf_table coarse, int has_coarse, int64_t touch_frame,
-                         unsigned nb_fine, double *flat, int64_t flat_words, int64_t *counter,
-                         const double *flat_init) {
+effective_records_kernel(const PF_GRID_CONST pf_table t, int mode, double ema, double delta_max,
+                         ulonglong4 *rec, const PF_GRID_CONST pf_table coarse, int has_coarse,
+                         int64_t touch_frame, unsigned nb_fine, double *flat, int64_t flat_words,
+                         int64_t *counter, const double *flat_init, int32_t *occ_fine,
+                         int32_t *occ_coarse, int64_t *occ_n) {
     __shared__ SweepSmem<kThreads> q;
     pdl_wait();  // multi-wave kernels do not trigger early: waiting dependents would take
                  // the slots of their later waves
@@ -308,6 +323,7 @@ effective_records_kernel(pf_table t, int mode, double ema, double delta_max, ulo
         for_each_occupied<kThreads>(coarse.tags, coarse.capacity, q, blk, nblk,
                                     [&](int64_t s, uint64_t) {
             if (ld_relaxed_i64(cnt_at(coarse, s)) > 0) *touch_at(coarse, s) = touch_frame;
+            if (occ_coarse != nullptr) occ_append(occ_coarse, occ_n + 1, s);
         });
         return;
     }
@@ -318,6 +334,7 @@ effective_records_kernel(pf_table t, int mode, double ema, double delta_max, ulo
         const CellState cs = load_cell(t, s, true);
         if (rec != nullptr) rec[s] = pack_effective(effective_of(cs, fixed, mode, ema, delta_max), as_int);
         if (touch_frame != kNoTouch && cs.counts > 0) *touch_at(t, s) = touch_frame;
+        if (occ_fine != nullptr) occ_append(occ_fine, occ_n, s);
     });
 }
 
@@ -326,7 +343,9 @@ effective_records_kernel(pf_table t, int mode, double ema, double delta_max, ulo
 static int launch_post_insert(const char *fn, const pf_table &fine, const pf_table *coarse,
                               const pf_config &kc, uint64_t *eff_records, int64_t touch_frame,
                               cudaStream_t st, double *flat = nullptr, int64_t flat_words = 0,
-                              int64_t *counter = nullptr, const double *flat_init = nullptr) {
+                              int64_t *counter = nullptr, const double *flat_init = nullptr,
+                              int32_t *occ_fine = nullptr, int32_t *occ_coarse = nullptr,
+                              int64_t *occ_n = nullptr) {
     if (eff_records == nullptr && touch_frame == kNoTouch && flat == nullptr && counter == nullptr)
         return PF_OK;
     const unsigned nf = sweep_blocks<kThreads>(fine.capacity, sm_count());
@@ -335,7 +354,8 @@ static int launch_post_insert(const char *fn, const pf_table &fine, const pf_tab
     launch_pdl(effective_records_kernel, dim3(nf + nc), dim3(kThreads), st, fine,
                kc.temporal_mode, kc.ema_alpha, kc.delta_max,
                reinterpret_cast<ulonglong4 *>(eff_records), tc ? *coarse : fine,
-               static_cast<int>(tc), touch_frame, nf, flat, flat_words, counter, flat_init);
+               static_cast<int>(tc), touch_frame, nf, flat, flat_words, counter, flat_init,
+               occ_n ? occ_fine : nullptr, occ_n && tc ? occ_coarse : nullptr, occ_n);
     return check_launch(fn);
 }
 
@@ -995,7 +1015,8 @@ static int resolve_frame(const char *fn, const pf_config *cfg, const pf_vertices
                          int64_t *work_count, uint8_t *source, double *chosen, int64_t *stats,
                          const uint64_t *lookup_keys, uint64_t *eff_records,
                          int64_t *fallback_keys, int64_t touch_frame, void *stream,
-                         bool fold_base = false) {
+                         bool fold_base = false, int32_t *const *occ_out = nullptr,
+                         int64_t *occ_count_out = nullptr) {
     if (int rc = validate_vertices(fn, v, cfg)) return rc;
     pf_config kc;
     if (int rc = prepare_config(fn, cfg, &kc)) return rc;
@@ -1047,7 +1068,9 @@ static int resolve_frame(const char *fn, const pf_config *cfg, const pf_vertices
         // flat = 0 (or base) and the work counter = 0 ride on the effective-record sweep
         if (int rc = launch_post_insert(fn, *fine, coarse, kc, eff_records, touch_frame, st,
                                         a.flat, 3 * n_pixels, work_count,
-                                        fold ? base_image : nullptr))
+                                        fold ? base_image : nullptr,
+                                        occ_count_out ? occ_out[0] : nullptr,
+                                        occ_count_out ? occ_out[1] : nullptr, occ_count_out))
             return rc;
         if (int rc = launch_rungs(fn, a, v->n, lookup_keys != nullptr, fallback_keys != nullptr, st))
             return rc;
@@ -1171,6 +1194,14 @@ int pf_filter_frame(const pf_config *cfg, const pf_vertices *v, const pf_table *
         if (b->phase_events[k]) cudaEventRecord(static_cast<cudaEvent_t>(b->phase_events[k]), st);
     };
     mark(0);
+    if (b->occ_count_in != nullptr && (!b->occ_in[0] || (coarse && !b->occ_in[1])))
+        return fail_arg(fn, "occ_count_in without the occupied-slot lists");
+    if (b->occ_count_in != nullptr && b->occ_count_in == b->occ_count_out)
+        return fail_arg(fn, "occ_count_in and occ_count_out must be different buffers");
+    // the lists this frame leaves behind (written by the effective-record sweep, which
+    // runs only with a non-empty stream)
+    const bool occ_out = b->occ_count_out != nullptr && b->occ_out[0] != nullptr &&
+                         (!coarse || b->occ_out[1] != nullptr) && v->n > 0;
     // prologue in one launch: generation fold on both tables (src/pipeline.py:331-333),
     // the input check and the counter resets, side by side over the grid
     if (b->bad_flag && cudaMemsetAsync(b->bad_flag, 0, sizeof(int32_t), st) != cudaSuccess)
@@ -1179,7 +1210,8 @@ int pf_filter_frame(const pf_config *cfg, const pf_vertices *v, const pf_table *
                                 cfg->delta_max, cfg->sample_cap, b->horizon_clears_fine,
                                 b->horizon_clears_coarse, v->n > 0 ? v->contribution : nullptr,
                                 3 * v->n, b->bad_flag, b->acc_stats, PF_STAT_COUNT, b->res_stats,
-                                PF_STAT_COUNT, b->event_count, st))
+                                PF_STAT_COUNT, b->event_count, st, b->occ_in[0], b->occ_in[1],
+                                b->occ_count_in, occ_out ? b->occ_count_out : nullptr))
         return rc;
     // accumulate_phase (fused, flag-guarded) + the resolve phase's lookup keys
     mark(1);
@@ -1192,7 +1224,9 @@ int pf_filter_frame(const pf_config *cfg, const pf_vertices *v, const pf_table *
     const int rc = resolve_frame(fn, cfg, v, fine, coarse, stream_base_lookup, stream_base_coarse,
                                  spp, base_image, n_pixels, image, b->flat, b->work,
                                  b->work_count, source, chosen, b->res_stats, b->lookup_keys,
-                                 b->eff_records, b->fallback_keys, frame, stream, true);
+                                 b->eff_records, b->fallback_keys, frame, stream, true,
+                                 occ_out ? b->occ_out : nullptr,
+                                 occ_out ? b->occ_count_out : nullptr);
     mark(3);
     return rc;
 }

@@ -135,13 +135,16 @@ inline int prepare_config(const char *fn, const pf_config *in, pf_config *out) {
     return PF_OK;
 }
 
-// pf_filter_frame's prologue in one launch (pf_table.cu): begin_frame on both tables,
-// the input check (vals/bad may be NULL) and the zeroing of three counter arrays.
+// pf_filter_frame's prologue in one launch (pf_table.cu): begin_frame on both tables
+// (over the occupied-slot lists occ_* when given, else a tag sweep), the input check
+// (vals/bad may be NULL) and the zeroing of the counter arrays (zero3: int64[2]).
 int frame_prologue(const pf_table *fine, const pf_table *coarse, int64_t frame, int32_t mode,
                    double ema, double delta_max, int32_t sample_cap, int64_t *clears_fine,
                    int64_t *clears_coarse, const double *vals, int64_t count, int32_t *bad,
                    int64_t *zero0, int64_t n0, int64_t *zero1, int64_t n1, int64_t *zero2,
-                   cudaStream_t st);
+                   cudaStream_t st, const int32_t *occ_fine = nullptr,
+                   const int32_t *occ_coarse = nullptr, const int64_t *occ_n = nullptr,
+                   int64_t *zero3 = nullptr);
 
 inline unsigned blocks_for(int64_t n, int threads) {
     return static_cast<unsigned>((n + threads - 1) / threads);

@@ -421,10 +421,13 @@ selftest_division_kernel(uint64_t seed, int64_t n, double base_voxel, unsigned l
 // the three sweeps run side by side; block 0 also clears the frame's counters.
 template <bool FIXED>
 __global__ void __launch_bounds__(kThreads)
-frame_prologue_kernel(pf_table fine, pf_table coarse, int jobs, int64_t frame, int mode,
+frame_prologue_kernel(const PF_GRID_CONST pf_table fine, const PF_GRID_CONST pf_table coarse,
+                      int jobs, int64_t frame, int mode,
                       double ema, double delta_max, int32_t sample_cap, int64_t *clears_fine,
                       int64_t *clears_coarse, const double *vals, int64_t count, int32_t *bad,
-                      int64_t *zero0, int64_t n0, int64_t *zero1, int64_t n1, int64_t *zero2) {
+                      int64_t *zero0, int64_t n0, int64_t *zero1, int64_t n1, int64_t *zero2,
+                      const int32_t *occ_fine, const int32_t *occ_coarse, const int64_t *occ_n,
+                      int64_t *zero3) {
     __shared__ SweepSmem<kThreads> q;
     __shared__ int block_clears;
     pdl_wait();
@@ -432,6 +435,7 @@ frame_prologue_kernel(pf_table fine, pf_table coarse, int jobs, int64_t frame, i
         for (int64_t k = threadIdx.x; k < n0; k += blockDim.x) zero0[k] = 0;
         for (int64_t k = threadIdx.x; k < n1; k += blockDim.x) zero1[k] = 0;
         if (zero2 && threadIdx.x == 0) *zero2 = 0;
+        if (zero3 && threadIdx.x < 2) zero3[threadIdx.x] = 0;
     }
     const int job = static_cast<int>(blockIdx.x % jobs);
     const int64_t blk = blockIdx.x / jobs, nblk = gridDim.x / jobs;
@@ -461,9 +465,23 @@ frame_prologue_kernel(pf_table fine, pf_table coarse, int jobs, int64_t frame, i
     const pf_table &t = job == 0 ? fine : coarse;
     if (threadIdx.x == 0) block_clears = 0;
     int cleared = 0;
-    for_each_occupied<kThreads>(t.tags, t.capacity, q, blk, nblk, [&](int64_t s, uint64_t tag) {
-        cleared += fold_slot<FIXED>(t, s, tag, frame, mode, ema, delta_max, sample_cap);
-    });
+    const int32_t *occ = job == 0 ? occ_fine : occ_coarse;
+    if (occ != nullptr) {
+        // the slots occupied when the previous frame ended (its effective-record sweep's
+        // list; the host passes it only when nothing touched the tables since): exactly
+        // the slots the tag sweep would find, without reading the tag arrays
+        const int64_t m = occ_n[job == 0 ? 0 : 1];
+        for (int64_t d = blk * blockDim.x + threadIdx.x; d < m; d += nblk * blockDim.x) {
+            const int64_t s = occ[d];
+            const uint64_t tag = ld_relaxed(t.tags + s);
+            if (tag != kEmptyTag)
+                cleared += fold_slot<FIXED>(t, s, tag, frame, mode, ema, delta_max, sample_cap);
+        }
+    } else {
+        for_each_occupied<kThreads>(t.tags, t.capacity, q, blk, nblk, [&](int64_t s, uint64_t tag) {
+            cleared += fold_slot<FIXED>(t, s, tag, frame, mode, ema, delta_max, sample_cap);
+        });
+    }
     if (cleared) atomicAdd(&block_clears, cleared);
     __syncthreads();
     int64_t *clears = job == 0 ? clears_fine : clears_coarse;
@@ -669,7 +687,8 @@ int frame_prologue(const pf_table *fine, const pf_table *coarse, int64_t frame, 
                    double ema, double delta_max, int32_t sample_cap, int64_t *clears_fine,
                    int64_t *clears_coarse, const double *vals, int64_t count, int32_t *bad,
                    int64_t *zero0, int64_t n0, int64_t *zero1, int64_t n1, int64_t *zero2,
-                   cudaStream_t st) {
+                   cudaStream_t st, const int32_t *occ_fine, const int32_t *occ_coarse,
+                   const int64_t *occ_n, int64_t *zero3) {
     const char *fn = "pf_filter_frame";
     if (int rc = validate_table(fn, fine)) return rc;
     if (coarse) {
@@ -686,7 +705,8 @@ int frame_prologue(const pf_table *fine, const pf_table *coarse, int64_t frame, 
                                               : frame_prologue_kernel<false>,
                dim3(g), dim3(kThreads), st, *fine, c, jobs, frame, mode, ema, delta_max,
                sample_cap, clears_fine, clears_coarse, checking ? vals : nullptr, count, bad,
-               zero0, n0, zero1, n1, zero2);
+               zero0, n0, zero1, n1, zero2, occ_n ? occ_fine : nullptr,
+               occ_n && coarse ? occ_coarse : nullptr, occ_n, zero3);
     return check_launch(fn);
 }
 

@@ -481,6 +481,17 @@ def resolve_phase(vertices, cfg: FilterConfig, state: FrameState, frame: int, se
     return image, report
 
 
+def _table_key(t: VoxelTable):
+    """Changes whenever the table may have changed: a C call on it (c_table), or an
+    in-place torch write to any of its storages (tensor version counters)."""
+    return (t.tags.data_ptr(), t.__dict__.get("_c_calls", 0), t.tags._version,
+            t.counts._version, t._sums._version, t._cold._version)
+
+
+def _occ_key(state: FrameState):
+    return (_table_key(state.fine), _table_key(state.coarse) if state.coarse is not None else None)
+
+
 def _fused_frame(vs: VertexStream, base_image, cfg: FilterConfig, state: FrameState, frame: int,
                  spp: int, seed: int, validate: bool, want_means: bool, phase_events=None):
     n = len(vs)
@@ -514,6 +525,23 @@ def _fused_frame(vs: VertexStream, base_image, cfg: FilterConfig, state: FrameSt
     if phase_events is not None:  # torch.cuda.Events recorded inside the C call
         for k, e in enumerate(phase_events):
             b.phase_events[k] = e.cuda_event
+    # occupied-slot lists: the frame writes the slots occupied at its end into one of two
+    # list buffers; the next frame's begin_frame folds exactly those slots (no tag sweep)
+    # if nothing touched the tables in between (same key), else it sweeps
+    prev = state.scratch.get("_occ_prev")
+    use_in = prev is not None and prev[0] == _occ_key(state)
+    out_idx = 1 - prev[1] if prev is not None else 0
+    cap_c = state.coarse.capacity if state.coarse is not None else 1
+
+    def occ_bufs(i):
+        return (state.buffer(f"occ_fine{i}", (state.fine.capacity,), torch.int32),
+                state.buffer(f"occ_coarse{i}", (cap_c,), torch.int32),
+                state.buffer(f"occ_n{i}", (2,), torch.int64))
+    of, oc, on = occ_bufs(out_idx)
+    b.occ_out[0], b.occ_out[1], b.occ_count_out = of.data_ptr(), oc.data_ptr(), on.data_ptr()
+    if use_in:
+        inf, inc, inn = occ_bufs(prev[1])
+        b.occ_in[0], b.occ_in[1], b.occ_count_in = inf.data_ptr(), inc.data_ptr(), inn.data_ptr()
     v, keep = vs.c_struct()
     ft = state.fine.c_table()
     ct = state.coarse.c_table() if state.coarse is not None else None
@@ -527,6 +555,11 @@ def _fused_frame(vs: VertexStream, base_image, cfg: FilterConfig, state: FrameSt
               image.data_ptr(), source.data_ptr(), _lib.ptr(chosen), ctypes.byref(b),
               _lib.stream_handle())
     del keep
+    # the lists describe the tables as this call left them (none without an effective sweep)
+    if n:
+        state.scratch["_occ_prev"] = (_occ_key(state), out_idx)
+    else:
+        state.scratch.pop("_occ_prev", None)
     state.fine.frame = frame
     if state.coarse is not None:
         state.coarse.frame = frame

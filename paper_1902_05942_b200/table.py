@@ -123,6 +123,9 @@ class VoxelTable:
     # -- C view ---------------------------------------------------------------
 
     def c_table(self) -> _lib.PfTable:
+        # every C call that may write the table goes through here: the count lets a frame
+        # know the table is exactly as the previous frame left it (pipeline._occ_key)
+        self.__dict__["_c_calls"] = self.__dict__.get("_c_calls", 0) + 1
         key = (self.tags.data_ptr(), self.probe_limit, self.evict_min_age, self.evict_horizon)
         cached = self.__dict__.get("_c_cache")
         if cached is not None and cached[0] == key:

@@ -11,8 +11,8 @@ cols = [c for c in h if c.startswith("stall_") and "Not Issued" not in c]
 tot = {c: 0 for c in cols}
 lines = []
 for r in rows[2:]:
-    if len(r) < len(h):
-        continue
+    if len(r) < len(h) or r[0] == "Address" or not r[ix["Warp Stall Sampling (All Samples)"]].isdigit():
+        continue  # short rows, repeated headers (one block per kernel instance)
     s = int(r[ix["Warp Stall Sampling (All Samples)"]] or 0)
     for c in cols:
         tot[c] += int(r[ix[c]] or 0)
