@@ -570,6 +570,18 @@ def run_b200(args):
         atomics = {"bound": "l2_atomics", "kernel": kname, "achieved": rach, "peak": red_peak,
                    "unit": "red/s", "frac": rach / red_peak, "red_per_launch": reds}
 
+    # per-rank bytes of a frame (world > 1): the algorithmic HBM bytes of this rank's
+    # vertices and pixels, and what crossed the interconnect in the last timed frame
+    comm = None
+    if world > 1 and getattr(state, "last_comm", None) is not None:
+        c = {k: int(v) for k, v in state.last_comm.items()}
+        t = torch.tensor([sum(c.values())], dtype=torch.float64, device="cuda")
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        comm = {"rank0_bytes_per_frame": c, "rank0_total": sum(c.values()),
+                "max_rank_total": int(t.item()),
+                "hbm_algorithmic_bytes_per_rank": INSERT_BYTES_PER_VERTEX * n +
+                QUERY_BYTES_PER_VERTEX * n + QUERY_BYTES_PER_PIXEL * n_pix}
+
     # end to end through the public API with host buffers
     e2e = None
     if not args.no_e2e:
@@ -620,7 +632,7 @@ def run_b200(args):
                                            "evict_last table / composite lines",
                            "kernel_chain": "6 kernels per frame with programmatic dependent "
                                            "launch"}},
-            "phases_ms": ph, "roofline": roofline, "roofline_issue": issue,
+            "phases_ms": ph, "roofline": roofline, "roofline_issue": issue, "comm": comm,
             "roofline_atomics": atomics, "cpu_baseline": cpu,
             "e2e": e2e,
             "gpu_launches": launches, "clocks": clocks.summary(),

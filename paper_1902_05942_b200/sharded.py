@@ -116,6 +116,7 @@ class ShardedState:
         self.entries = torch.empty((n_local, 6), dtype=torch.int64, device=dev)
         self.entry_count = torch.zeros(1, dtype=torch.int64, device=dev)
         self.prev_gathered = None  # (entries [world * stride, 6], counts [world], stride)
+        self.last_comm = None  # interconnect bytes of the last frame (filter_frame_sharded)
         # every rank's published entry count of the last frame, copied to pinned host
         # memory behind the frame's gather (read once the next frame's count exchange
         # has synchronised, i.e. after it has landed)
@@ -272,6 +273,12 @@ def filter_frame_sharded(vertices, base_image, cfg: FilterConfig, st: ShardedSta
             break
     send_rec = allm[st.rank, :, 0].tolist()
     recv_rec = allm[:, st.rank, 0].tolist()
+    # this rank's interconnect bytes of the frame (what leaves / arrives over NVLink; the
+    # self-addressed share of the all-to-all stays on the device)
+    rec_b = st.send_records.element_size() * int(st.send_records[:1].numel())
+    comm = {"count_allgather": msg.numel() * msg.element_size() * (G - 1),
+            "records_sent": rec_b * (sum(send_rec) - send_rec[st.rank]),
+            "records_received": rec_b * (sum(recv_rec) - recv_rec[st.rank])}
     # published entries of rank r <= its entries last frame + the records it receives
     bound = int((st.prev_entry_counts.numpy() + allm[:, :, 0].sum(axis=0)).max())
     records = yield Exchange(st.send_records[:sum(send_rec)], send_rec, recv_rec)
@@ -288,6 +295,8 @@ def filter_frame_sharded(vertices, base_image, cfg: FilterConfig, st: ShardedSta
     stride = min(bound, int(st.entries.shape[0]))  # >= every rank's count; same on all ranks
     # every rank computed the same bound, so all skip an empty gather together
     gathered = (yield AllGather(st.entries[:stride])) if stride else st.entries[:0]
+    ent_b = st.entries.element_size() * int(st.entries[:1].numel())
+    comm["entries_allgather"] = ent_b * stride * (G - 1) + counts.element_size() * (G - 1)
     st.prev_entry_counts.copy_(counts, non_blocking=True)
     rp = st.c_replica()
     if st.prev_gathered is not None:
@@ -318,12 +327,15 @@ def filter_frame_sharded(vertices, base_image, cfg: FilterConfig, st: ShardedSta
         band_flat = yield ReduceScatter(flat)
         rows = H // G
         base_band = base[st.rank * rows:(st.rank + 1) * rows]
+        # ring reduce-scatter: (G - 1) / G of the buffer leaves each rank
+        comm["image_reduce_scatter"] = flat.numel() * flat.element_size() * (G - 1) // G
     else:
         band_flat, base_band = flat, base
     image = torch.empty_like(base_band)
     _lib.call("pf_finalize_image", base_band.data_ptr(), band_flat.data_ptr(), image.data_ptr(),
               int(base_band.shape[0] * base_band.shape[1]), int(spp), stream)
     mark(3)
+    st.last_comm = comm
     st.fine.frame = frame
     if st.coarse is not None:
         st.coarse.frame = frame
