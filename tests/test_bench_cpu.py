@@ -80,3 +80,35 @@ def test_table_bench_point_lines():
     assert "per_vertex_ns=1.2" in a.line() and "device_per_vertex_ns=0.150" in a.line()
     assert abs(spread([a, b]) - 1.2 / 0.5) < 1e-9
     assert abs(spread([a, b], device=True) - 0.15 / 0.05) < 1e-9
+
+
+def test_occupied_list_key_invalidation():
+    """pipeline._occ_key changes on every C-call view of a table (c_table) and on any
+    in-place tensor write, so the occupied-slot lists are only reused untouched."""
+    import types
+
+    import torch
+
+    from paper_1902_05942_b200.pipeline import _occ_key, _table_key
+
+    def fake():
+        t = types.SimpleNamespace(tags=torch.zeros(8, dtype=torch.int64),
+                                  counts=torch.zeros(8, dtype=torch.int64),
+                                  _sums=torch.zeros(3, 8, dtype=torch.int64),
+                                  _cold=torch.zeros(8, 8, dtype=torch.int64))
+        return t
+    fine, coarse = fake(), fake()
+    state = types.SimpleNamespace(fine=fine, coarse=coarse)
+    k0 = _occ_key(state)
+    assert _occ_key(state) == k0
+    fine.__dict__["_c_calls"] = 1          # what VoxelTable.c_table() does
+    k1 = _occ_key(state)
+    assert k1 != k0
+    coarse._cold[3, 2] = 5                 # e.g. set_deltas / a user write
+    assert _occ_key(state) != k1
+    k2 = _occ_key(state)
+    fine._sums.t()[2] = 1                  # a write through a view bumps the base
+    assert _occ_key(state) != k2
+    assert _table_key(fine)[0] == fine.tags.data_ptr()
+    state.coarse = None
+    assert _occ_key(state)[1] is None
