@@ -10,7 +10,12 @@ ix = {k: h.index(k) for k in h}
 cols = [c for c in h if c.startswith("stall_") and "Not Issued" not in c]
 tot = {c: 0 for c in cols}
 lines = []
+seen = set()
 for r in rows[2:]:
+    if r and r[0] in seen:
+        continue  # the export can list an instruction twice
+    if r:
+        seen.add(r[0])
     if len(r) < len(h) or r[0] == "Address" or not r[ix["Warp Stall Sampling (All Samples)"]].isdigit():
         continue  # short rows, repeated headers (one block per kernel instance)
     s = int(r[ix["Warp Stall Sampling (All Samples)"]] or 0)
